@@ -1,0 +1,412 @@
+/* eks_oracle.c — plain, slow, single-threaded fp64 CPU oracle for the
+ * s-step enlarged CG methods of arXiv:1804.10629.
+ *
+ * TEST INFRASTRUCTURE ONLY (see eks_oracle.h).  Shares no code with the
+ * CUDA product.  Build: gcc -O2 -ffp-contract=off -fPIC -shared.
+ *
+ * The routines follow the paper's algorithm boxes step by step:
+ *   s-step SRE-CG2  Alg 3
+ *   s-step SRE-CG   Alg 4, window of 2 blocks
+ *   s-step MSDO-CG  Alg 6
+ *   A-orthonormalization = CGS2 against the window + A-CholQR
+ * Readings of silent/ambiguous points (R1..R27) are listed in DESIGN.md.
+ *
+ * Parity status: every routine here is pinned by tests/test_oracle_*.py
+ * (closed forms, textbook CG, dense direct solves, paper table cells).
+ */
+#include "eks_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------ */
+/* Small helpers                                                             */
+/* ------------------------------------------------------------------------ */
+
+/* Neumaier-compensated running sum. */
+typedef struct { double s, c; } ksum;
+static void ks_add(ksum* k, double v) {
+  double t = k->s + v;
+  if (fabs(k->s) >= fabs(v)) k->c += (k->s - t) + v;
+  else k->c += (v - t) + k->s;
+  k->s = t;
+}
+static double ks_val(const ksum* k) { return k->s + k->c; }
+
+static double* dalloc(size_t count) {
+  double* p = (double*)calloc(count ? count : 1, sizeof(double));
+  if (!p) abort();
+  return p;
+}
+
+static double norm2(int64_t n, const double* v) {
+  ksum k = {0, 0};
+  for (int64_t i = 0; i < n; ++i) ks_add(&k, v[i] * v[i]);
+  return sqrt(ks_val(&k));
+}
+
+/* ------------------------------------------------------------------------ */
+/* T(r) — P:41 (§2), P:311-312 (proof of Theorem 1: r = T(r)·1_t)            */
+/* ------------------------------------------------------------------------ */
+void or_split(int64_t n, int t, const double* r, double* Z) {
+  /* Domains D_d = [floor(d n / t), floor((d+1) n / t)) (reading R1). */
+  memset(Z, 0, sizeof(double) * (size_t)n * (size_t)t);
+  for (int d = 0; d < t; ++d) {
+    int64_t lo = (int64_t)d * n / t, hi = (int64_t)(d + 1) * n / t;
+    for (int64_t i = lo; i < hi; ++i) Z[i * t + d] = r[i];
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Y = A X — P:54 ("W_k = AW_{k-1}"); fixed ascending fma order (R20)        */
+/* ------------------------------------------------------------------------ */
+void or_spmm(const or_csr* A, int t, const double* X, double* Y) {
+  for (int64_t i = 0; i < A->n; ++i) {
+    for (int c = 0; c < t; ++c) {
+      double acc = 0.0;
+      for (int64_t p = A->row_ptr[i]; p < A->row_ptr[i + 1]; ++p)
+        acc = fma(A->val[p], X[(int64_t)A->col[p] * t + c], acc);
+      Y[i * t + c] = acc;
+    }
+  }
+}
+
+/* C = Xᵀ Y, compensated over rows. */
+void or_xty(int64_t n, int p, const double* X, int q, const double* Y, double* C) {
+  for (int a = 0; a < p; ++a)
+    for (int b = 0; b < q; ++b) {
+      ksum k = {0, 0};
+      for (int64_t i = 0; i < n; ++i) ks_add(&k, X[i * p + a] * Y[i * q + b]);
+      C[a * q + b] = ks_val(&k);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Cholesky B = RᵀR — A-CholQR's factorization ("A-CholQR"; R4, R6)   */
+/* Column-by-column, left-to-right sums, no fma (compiled -ffp-contract=off). */
+/* ------------------------------------------------------------------------ */
+int or_chol(int t, const double* B, double* R) {
+  double bmax = 0.0;
+  for (int i = 0; i < t; ++i)
+    for (int j = i; j < t; ++j)
+      if (fabs(B[i * t + j]) > bmax) bmax = fabs(B[i * t + j]);
+  double thr = (double)t * ldexp(1.0, -52) * bmax;
+  memset(R, 0, sizeof(double) * (size_t)t * (size_t)t);
+  for (int k = 0; k < t; ++k) {
+    double d = B[k * t + k];
+    for (int i = 0; i < k; ++i) d = d - R[i * t + k] * R[i * t + k];
+    if (!(d > thr)) return OR_BREAKDOWN;
+    double rkk = sqrt(d);
+    R[k * t + k] = rkk;
+    for (int j = k + 1; j < t; ++j) {
+      double v = B[k * t + j];
+      for (int i = 0; i < k; ++i) v = v - R[i * t + k] * R[i * t + j];
+      R[k * t + j] = v / rkk;
+    }
+  }
+  return OR_OK;
+}
+
+/* W = Z R⁻¹ row by row: w R = z  ⇒  w_j = (z_j − Σ_{i<j} w_i R_ij) / R_jj. */
+static void rsolve_rows(int64_t n, int t, const double* R, const double* Z, double* W) {
+  for (int64_t r = 0; r < n; ++r) {
+    const double* z = Z + r * t;
+    double* w = W + r * t;
+    for (int j = 0; j < t; ++j) {
+      double v = z[j];
+      for (int i = 0; i < j; ++i) v = v - w[i] * R[i * t + j];
+      w[j] = v / R[j * t + j];
+    }
+  }
+}
+
+/* Rᵀ a = g (forward substitution on the lower-triangular Rᵀ). */
+static void rtsolve_vec(int t, const double* R, const double* g, double* a) {
+  for (int j = 0; j < t; ++j) {
+    double v = g[j];
+    for (int i = 0; i < j; ++i) v = v - R[i * t + j] * a[i];
+    a[j] = v / R[j * t + j];
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* CGS2 in the A-inner product — P:198 ("A-orthonormalized against all the   */
+/* previously computed vectors using CGS2"); reading R3.         */
+/* ------------------------------------------------------------------------ */
+static void cgs_pass_from_AZ(int64_t n, int t, int nq, const double* const* Q,
+                             const double* const* AQ_or_null, const double* AZ_or_Z,
+                             double* Z, double* C) {
+  /* C_q = Q_qᵀ (A Z)  [definition]   or   C_q = (A Q_q)ᵀ Z  [mirror]. */
+  for (int q = 0; q < nq; ++q) {
+    const double* left = AQ_or_null ? AQ_or_null[q] : Q[q];
+    or_xty(n, t, left, t, AZ_or_Z, C + (size_t)q * t * t);
+  }
+  /* Z = Z − Q C, per row: z_c −= Σ_q Σ_a Q_q[row][a] C_q[a][c]. */
+  for (int64_t r = 0; r < n; ++r)
+    for (int c = 0; c < t; ++c) {
+      double acc = 0.0;
+      for (int q = 0; q < nq; ++q)
+        for (int a = 0; a < t; ++a) acc += Q[q][r * t + a] * C[((size_t)q * t + a) * t + c];
+      Z[r * t + c] -= acc;
+    }
+}
+
+void or_cgs2(const or_csr* A, int t, int nq, const double* const* Q, double* Z,
+             double* C1, double* C2) {
+  int64_t n = A->n;
+  double* AZ = dalloc((size_t)n * t);
+  double* Cbuf = dalloc((size_t)nq * t * t);
+  for (int pass = 0; pass < 2; ++pass) {
+    or_spmm(A, t, Z, AZ);
+    cgs_pass_from_AZ(n, t, nq, Q, NULL, AZ, Z, Cbuf);
+    double* dst = pass == 0 ? C1 : C2;
+    if (dst) memcpy(dst, Cbuf, sizeof(double) * (size_t)nq * t * t);
+  }
+  free(AZ);
+  free(Cbuf);
+}
+
+/* ------------------------------------------------------------------------ */
+/* A-CholQR — P:198; reading R4                                       */
+/* ------------------------------------------------------------------------ */
+int or_acholqr(const or_csr* A, int t, const double* Z, double* W, double* R, double* Bout) {
+  int64_t n = A->n;
+  double* AZ = dalloc((size_t)n * t);
+  double* B = dalloc((size_t)t * t);
+  or_spmm(A, t, Z, AZ);
+  or_xty(n, t, Z, t, AZ, B);
+  for (int i = 0; i < t; ++i)
+    for (int j = 0; j < i; ++j) B[i * t + j] = 0.0; /* upper triangle only (R4) */
+  if (Bout) memcpy(Bout, B, sizeof(double) * (size_t)t * t);
+  int st = or_chol(t, B, R);
+  if (st == OR_OK) rsolve_rows(n, t, R, Z, W);
+  free(AZ);
+  free(B);
+  return st;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Block list (the Q of Alg 3/6 or the 2-block window of Alg 4)              */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int count, cap;
+  double** W;   /* A-orthonormal blocks */
+  double** AW;  /* mirror mode: cached A·W */
+} blist;
+
+static void bl_push(blist* L, double* W, double* AW) {
+  if (L->count == L->cap) {
+    L->cap = L->cap ? 2 * L->cap : 8;
+    L->W = (double**)realloc(L->W, sizeof(double*) * (size_t)L->cap);
+    L->AW = (double**)realloc(L->AW, sizeof(double*) * (size_t)L->cap);
+  }
+  L->W[L->count] = W;
+  L->AW[L->count] = AW;
+  L->count++;
+}
+
+static void bl_free(blist* L) {
+  for (int i = 0; i < L->count; ++i) { free(L->W[i]); free(L->AW[i]); }
+  free(L->W);
+  free(L->AW);
+}
+
+/* Window for the next block: SRE-CG → the last min(2, #) blocks (Alg 4,
+ * P:182/"against W_{j-2} and W_{j-1}"; R11); SRE-CG2 and MSDO-CG →
+ * all of Q (Alg 3; Alg 6). */
+static int window_start(const blist* L, int method) {
+  if (method == OR_SRE_CG) return L->count > 2 ? L->count - 2 : 0;
+  return 0;
+}
+
+/* SRE-CG keeps only the last 2 blocks: drop older ones to bound memory. */
+static void bl_trim(blist* L, int method) {
+  if (method != OR_SRE_CG) return;
+  while (L->count > 2) {
+    free(L->W[0]);
+    free(L->AW[0]);
+    memmove(L->W, L->W + 1, sizeof(double*) * (size_t)(L->count - 1));
+    memmove(L->AW, L->AW + 1, sizeof(double*) * (size_t)(L->count - 1));
+    L->count--;
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Solver — Alg 3 / Alg 4 / Alg 6                                            */
+/* ------------------------------------------------------------------------ */
+int or_solve(const or_csr* A, const double* b, double* x, int method, int s, int t,
+             double eps, int kmax, int mode, or_report* rep, or_iter_cb cb, void* user) {
+  int64_t n = A->n;
+  if (s < 1 || t < 1 || t > n || !(eps >= 0.0) || method < 0 || method > 2) return OR_BADARG;
+  size_t blk = (size_t)n * (size_t)t;
+
+  double* r = dalloc((size_t)n);
+  double* tmp = dalloc((size_t)n);
+  double* u = dalloc((size_t)n);
+  /* r_0 = b − A x_0 ; rho_0 = ||r_0||_2  (line 1 of every algorithm box) */
+  or_spmm(A, 1, x, tmp);
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - tmp[i];
+  double rho0 = norm2(n, r), rho = rho0;
+  if (rep) {
+    rep->rho0 = rho0;
+    rep->breakdown_block = -1;
+    if (rep->rho_history) rep->rho_history[0] = rho0;
+  }
+
+  blist Q = {0, 0, NULL, NULL};
+  double** V = (double**)calloc((size_t)s, sizeof(double*));
+  double** AV = (double**)calloc((size_t)s, sizeof(double*));
+  double* alpha = dalloc((size_t)s * t);
+  double* R = dalloc((size_t)t * t);
+  double* B = dalloc((size_t)t * t);
+  double* g = dalloc((size_t)t);
+  double* Cb = NULL;
+  int status = OR_OK, k = 1, gblock = 0;
+  double* rnew = dalloc((size_t)n);
+
+  /* while (rho > eps*rho0 and k < kmax)   — P:146 / P:177 / P:329 (R7) */
+  while (rho > eps * rho0 && k < kmax) {
+    memcpy(rnew, r, sizeof(double) * (size_t)n);
+    int ok = 1;
+    for (int i = 0; i < s; ++i) {
+      double* Z = dalloc(blk);
+      /* Seed block: T(r_{k-1}) for MSDO-CG every k (Alg 6) and for
+       * SRE-CG/SRE-CG2 at k=1 (Alg 3, Alg 4); otherwise the next
+       * power A·W_{j-1}. */
+      if (i == 0 && (method == OR_MSDO_CG || k == 1)) {
+        or_split(n, t, r, Z);
+      } else {
+        const double* Wprev = Q.W[Q.count - 1];
+        if (mode == OR_MODE_MIRROR) memcpy(Z, Q.AW[Q.count - 1], sizeof(double) * blk);
+        else or_spmm(A, t, Wprev, Z);
+      }
+      int w0 = window_start(&Q, method), nq = Q.count - w0;
+      double* W = dalloc(blk);
+      double* AW = NULL;
+      if (mode == OR_MODE_DEFINITION) {
+        /* "A-orthonormalize W against Q" (CGS2), then "A-orthonormalize W" (A-CholQR). */
+        if (nq > 0) or_cgs2(A, t, nq, (const double* const*)(Q.W + w0), Z, NULL, NULL);
+        int st = or_acholqr(A, t, Z, W, R, NULL);
+        if (st != OR_OK) { status = OR_BREAKDOWN; free(Z); free(W); ok = 0; break; }
+        AW = dalloc(1);
+      } else {
+        /* Mirror of the GPU algebra: C = (AQ)ᵀZ with cached AQ, one SpMM of Z2,
+         * AW = (A Z2) R⁻¹, alpha_b = R⁻ᵀ (Z2ᵀ r_{k-1}). Equal to the definition in
+         * exact arithmetic (A symmetric, reading R24). */
+        if (nq > 0) {
+          Cb = (double*)realloc(Cb, sizeof(double) * (size_t)nq * t * t);
+          for (int pass = 0; pass < 2; ++pass)
+            cgs_pass_from_AZ(n, t, nq, (const double* const*)(Q.W + w0),
+                             (const double* const*)(Q.AW + w0), Z, Z, Cb);
+        }
+        double* AZ = dalloc(blk);
+        or_spmm(A, t, Z, AZ);
+        or_xty(n, t, Z, t, AZ, B);
+        for (int a = 0; a < t; ++a)
+          for (int c = 0; c < a; ++c) B[a * t + c] = 0.0;
+        if (or_chol(t, B, R) != OR_OK) { status = OR_BREAKDOWN; free(Z); free(W); free(AZ); ok = 0; break; }
+        AW = dalloc(blk);
+        rsolve_rows(n, t, R, Z, W);
+        rsolve_rows(n, t, R, AZ, AW);
+        or_xty(n, t, Z, 1, r, g);
+        rtsolve_vec(t, R, g, alpha + (size_t)i * t);
+        free(AZ);
+      }
+      free(Z);
+      V[i] = W;
+      AV[i] = AW;
+      bl_push(&Q, W, AW);
+      gblock++;
+    }
+    if (!ok) {
+      if (rep) rep->breakdown_block = gblock;
+      /* blocks already pushed belong to Q; nothing else to release here */
+      break;
+    }
+    if (mode == OR_MODE_DEFINITION) {
+      /* alpha~ = Vᵀ r_{k-1};  x_k = x_{k-1} + V alpha~;  r_k = r_{k-1} − A V alpha~
+       * (Alg 3, Alg 4, Alg 6).  Reading R9:
+       * u = V alpha~ first, then r −= A·u. */
+      for (int i = 0; i < s; ++i) or_xty(n, t, V[i], 1, r, alpha + (size_t)i * t);
+      for (int64_t row = 0; row < n; ++row) {
+        double acc = 0.0;
+        for (int i = 0; i < s; ++i)
+          for (int c = 0; c < t; ++c) acc += V[i][row * t + c] * alpha[(size_t)i * t + c];
+        u[row] = acc;
+      }
+      or_spmm(A, 1, u, tmp);
+      for (int64_t row = 0; row < n; ++row) { x[row] += u[row]; r[row] -= tmp[row]; }
+    } else {
+      for (int i = 0; i < s; ++i)
+        for (int64_t row = 0; row < n; ++row) {
+          double dx = 0.0, dr = 0.0;
+          for (int c = 0; c < t; ++c) {
+            dx += V[i][row * t + c] * alpha[(size_t)i * t + c];
+            dr += AV[i][row * t + c] * alpha[(size_t)i * t + c];
+          }
+          x[row] += dx;
+          rnew[row] -= dr;
+        }
+      memcpy(r, rnew, sizeof(double) * (size_t)n);
+    }
+    rho = norm2(n, r);  /* rho = ||r_k||_2, the recursive residual (R8) */
+    if (cb) {
+      int st = s * t;
+      double* Vc = dalloc((size_t)n * st);
+      for (int i = 0; i < s; ++i)
+        for (int64_t row = 0; row < n; ++row)
+          for (int c = 0; c < t; ++c) Vc[row * st + i * t + c] = V[i][row * t + c];
+      cb(user, k, n, st, Vc, alpha, x, r, rho);
+      free(Vc);
+    }
+    if (rep && rep->rho_history) rep->rho_history[k] = rho;
+    k = k + 1;
+    bl_trim(&Q, method);
+  }
+
+  if (rep) {
+    rep->outer_iters = k - 1;
+    rep->rho = rho;
+    rep->converged = rho <= eps * rho0;
+    or_spmm(A, 1, x, tmp);
+    for (int64_t i = 0; i < n; ++i) tmp[i] = b[i] - tmp[i];
+    double nb = norm2(n, b);
+    rep->true_relres = nb > 0 ? norm2(n, tmp) / nb : 0.0;
+  }
+  if (status == OR_OK && !(rho <= eps * rho0)) status = OR_MAXITER;
+  if (rep) rep->status = status;
+  bl_free(&Q);
+  free(V); free(AV); free(alpha); free(R); free(B); free(g); free(Cb);
+  free(r); free(tmp); free(u); free(rnew);
+  return status;
+}
+
+/* ------------------------------------------------------------------------ */
+/* cfg5 basis sweep (reading R27): Alg 4 lines 178-188 with T(r0) replaced  */
+/* by a given start block; no update, no convergence test.                   */
+/* ------------------------------------------------------------------------ */
+int or_basis_sweep(const or_csr* A, int t, const double* X0, int nblocks, double* W_last) {
+  int64_t n = A->n;
+  size_t blk = (size_t)n * t;
+  double* R = dalloc((size_t)t * t);
+  blist Q = {0, 0, NULL, NULL};
+  int status = OR_OK;
+  for (int j = 0; j < nblocks; ++j) {
+    double* Z = dalloc(blk);
+    if (j == 0) memcpy(Z, X0, sizeof(double) * blk);
+    else or_spmm(A, t, Q.W[Q.count - 1], Z);
+    int w0 = window_start(&Q, OR_SRE_CG), nq = Q.count - w0;
+    if (nq > 0) or_cgs2(A, t, nq, (const double* const*)(Q.W + w0), Z, NULL, NULL);
+    double* W = dalloc(blk);
+    int st = or_acholqr(A, t, Z, W, R, NULL);
+    free(Z);
+    if (st != OR_OK) { free(W); status = st; break; }
+    bl_push(&Q, W, dalloc(1));
+    bl_trim(&Q, OR_SRE_CG);
+  }
+  if (status == OR_OK) memcpy(W_last, Q.W[Q.count - 1], sizeof(double) * blk);
+  bl_free(&Q);
+  free(R);
+  return status;
+}

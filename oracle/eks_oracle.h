@@ -1,0 +1,87 @@
+/* eks_oracle.h — CPU reference ("oracle") for the s-step enlarged CG hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load or call this code.
+ * The product (paper_1804_10629_b200/, libeks.so) never links, imports or
+ * executes it, and this tree shares no source, header, table or helper with
+ * the CUDA path.
+ *
+ * Plain single-threaded C99, fp64, no BLAS, no OpenMP, built with
+ * -O2 -ffp-contract=off (reading R20).  Every routine cites the
+ * PAPER.md passage it follows ("P:<line>", section / algorithm).
+ *
+ * Layout: every n×t block is ROW-MAJOR (row i's t values contiguous).
+ */
+#ifndef EKS_ORACLE_H
+#define EKS_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int64_t n;
+  const int64_t* row_ptr;  /* n+1, row_ptr[0] == 0 */
+  const int32_t* col;      /* nnz, ascending within a row */
+  const double* val;       /* nnz */
+} or_csr;
+
+enum { OR_SRE_CG = 0, OR_SRE_CG2 = 1, OR_MSDO_CG = 2 };
+enum { OR_OK = 0, OR_BREAKDOWN = 7, OR_MAXITER = 8, OR_BADARG = 1 };
+enum { OR_MODE_DEFINITION = 0, OR_MODE_MIRROR = 1 };
+
+/* Per-outer-iteration hook for the invariant pins (tests only).
+ * V is the n×(s·t) basis of this outer iteration, row-major; alpha = Vᵀr_{k-1};
+ * x, r are x_k, r_k after the update. */
+typedef void (*or_iter_cb)(void* user, int k, int64_t n, int st, const double* V,
+                           const double* alpha, const double* x, const double* r, double rho);
+
+typedef struct {
+  int outer_iters;      /* loop bodies executed (= k-1 at exit, P:146 / reading R7) */
+  int converged;        /* rho <= eps*rho0 */
+  int status;           /* OR_OK / OR_BREAKDOWN / OR_MAXITER */
+  int breakdown_block;  /* global block index of the failed Cholesky, or -1 */
+  double rho0, rho, true_relres;
+  double* rho_history;  /* caller-owned, capacity kmax+1, may be NULL */
+} or_report;
+
+/* T(r): Z[i][d] = r[i] if i in D_d else 0, D_d = [floor(d n/t), floor((d+1) n/t)).
+ * P:41 (§2, "T(r_0) is an operator that splits r_0 into t vectors"). */
+void or_split(int64_t n, int t, const double* r, double* Z);
+
+/* Y = A·X (n×t), accumulation p ascending from 0.0 with fma (reading R20).
+ * P:54 (§3.1, "W_k = AW_{k-1}"). */
+void or_spmm(const or_csr* A, int t, const double* X, double* Y);
+
+/* C = Xᵀ Y (p×q, row-major), X n×p, Y n×q, Neumaier-compensated sums over rows. */
+void or_xty(int64_t n, int p, const double* X, int q, const double* Y, double* C);
+
+/* Cholesky B = RᵀR (t×t, R upper, row-major), only B's upper triangle read.
+ * Breakdown (returns OR_BREAKDOWN) when a pivot d_k <= t·2^-52·max|B_ij| (reading R6). */
+int or_chol(int t, const double* B, double* R);
+
+/* CGS2 "A-orthonormalize Z against Q" (reading R3):
+ * twice { C = Qᵀ(A·Z) ; Z = Z − Q·C }.  Q is given as nq blocks of n×t.
+ * C1, C2 (nq·t × t, row-major) receive the two passes' coefficients (may be NULL). */
+void or_cgs2(const or_csr* A, int t, int nq, const double* const* Q, double* Z,
+             double* C1, double* C2);
+
+/* A-CholQR "A-orthonormalize W" (reading R4):
+ * B = upper(Zᵀ(A·Z)), B = RᵀR, W = Z·R⁻¹ (row-wise forward substitution). */
+int or_acholqr(const or_csr* A, int t, const double* Z, double* W, double* R, double* B);
+
+/* Solve with s-step SRE-CG (Alg 4), SRE-CG2 (Alg 3) or
+ * MSDO-CG (Alg 6).  x holds x0 on entry, x_k on exit. */
+int or_solve(const or_csr* A, const double* b, double* x, int method, int s, int t,
+             double eps, int kmax, int mode, or_report* rep, or_iter_cb cb, void* user);
+
+/* s-step SRE-CG basis sweep only (cfg5, reading R27): starting block X0 (n×t)
+ * is A-orthonormalized, then nblocks-1 further blocks W=A-orth(A·W_prev) against
+ * the last min(2,#) blocks.  Writes the last block to W_last.  Returns status. */
+int or_basis_sweep(const or_csr* A, int t, const double* X0, int nblocks, double* W_last);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
