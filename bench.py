@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""bench.py — outer iterations/s of the s-step enlarged CG hot path on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` (N>1 under
+torchrun, one rank per GPU over NCCL).  A *step* is one full ``eks_solve`` of the
+workload (every §8(a) row: split, s chained SpMMs per outer iteration, CGS2 +
+A-CholQR, x/r update, loop control) with the inputs resident in HBM; ``value`` =
+outer iterations of all timed steps ÷ device time (CUDA events on the solve
+stream, max over ranks).  Rank 0 prints ONE JSON line.
+
+``--impl reference`` times the CPU oracle (oracle/, plain C, single thread) on
+the same workload instead: each step = a bounded sample of outer iterations.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import eks_inputs as ei  # noqa: E402
+
+METRIC = "outer iterations/s and SpMM-block HBM GB/s vs peak, at 1/2/4/8 B200"
+UNIT = "outer_iter/s"
+
+
+def workload(name: str):
+    """(Problem, description).  Default = configs[1] of BASELINE.json (cfg2, s-step SRE-CG)."""
+    if name == "cfg2":
+        return ei.cfg2(method="sre-cg")
+    if name == "cfg2-sre-cg2":
+        return ei.cfg2(method="sre-cg2")
+    if name == "cfg1":
+        return ei.cfg1()
+    if name == "cfg3":
+        return ei.cfg3()
+    if name == "cfg4":
+        return ei.cfg4()
+    raise SystemExit(f"unknown workload {name}")
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6558.7, "source": "fallback"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        peaks.update(hbm_gbs=d.get("hbm_gbs", peaks["hbm_gbs"]), source="MEASURED_PEAKS.json (measured copy)")
+    f = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+    peaks["dfma_tflops"] = 34.217  # measured, profiles/fp64_peaks_r01.json (tools/fp64_peaks.cu)
+    peaks["dmma_tflops"] = 37.089
+    if os.path.exists(f):
+        for line in open(f):
+            try:
+                d = json.loads(line)
+            except ValueError:
+                continue
+            for k in ("dfma_tflops", "dmma_tflops"):
+                if k in d:
+                    peaks[k] = d[k]
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- reference arm (CPU oracle)
+def oracle_sample(p, iters: int):
+    """Time the oracle (as it stands) on the first `iters` outer iterations of the workload."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    r = oracle.solve(p.A, p.b, p.method, p.s, p.t, 0.0, kmax=iters + 1)
+    dt = time.perf_counter() - t0
+    return r["outer_iters"], dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    p = workload(args.workload)
+    per_step = args.ref_iters
+    for _ in range(args.warmup):
+        oracle_sample(p, per_step)
+    total_it, total_t = 0, 0.0
+    for _ in range(args.steps):
+        k, dt = oracle_sample(p, per_step)
+        total_it += k
+        total_t += dt
+    value = total_it / total_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args, p, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"first {per_step} outer iteration(s) of {p.name} {p.method} per step "
+                                   f"(definition mode, single thread, {os.cpu_count()} host cores present)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_of(args, p, N):
+    return {"workload": f"{p.name}: {p.note}; s-step {p.method}, s={p.s}, t={p.t}, tol={p.tol:g}",
+            "n": p.A.n, "nnz": p.A.nnz, "method": p.method, "s": p.s, "t": p.t, "tol": p.tol,
+            "parallelism": f"row-slabs x{N} (t/N domains per GPU)",
+            "l2": "flushed: 256 MiB buffer written between timed steps (outside the step events)"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="eks", choices=["eks", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--ref-iters", type=int, default=1, help="oracle outer iterations per reference step")
+    ap.add_argument("--cpu-iters", type=int, default=2, help="oracle outer iterations for cpu_baseline")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1804_10629_b200 as eks
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    p = workload(args.workload)
+    n, t = p.A.n, p.t
+    if t % world:
+        raise SystemExit("t must be divisible by the number of GPUs")
+    lo = (rank * (t // world)) * n // t
+    hi = ((rank + 1) * (t // world)) * n // t
+    slab = p.A.rows(lo, hi)
+
+    uid = None
+    if world > 1:
+        obj = [eks.eks_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    solver = eks.Solver(None, rank=rank, nranks=world, device=local, nccl_id=uid)
+    solver.setup(n, lo, hi, slab.row_ptr, slab.col, slab.val)
+    stream = torch.cuda.Stream()
+    eks.eks_set_stream(solver.ctx, stream.cuda_stream)
+
+    b = torch.from_numpy(np.ascontiguousarray(p.b[lo:hi])).cuda()
+    x = torch.zeros_like(b)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(profile=False):
+        with torch.cuda.stream(stream):
+            x.zero_()
+        st, rep = eks.eks_solve_ex(solver.ctx, p.method, p.s, p.t, p.tol, b, x, profile=profile)
+        if st not in (0,):
+            raise SystemExit(f"solve failed: {eks.STATUS.get(st)} {eks.eks_error_string(solver.ctx)}")
+        return rep
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---------------- timed region: K steps, CUDA events on the solve stream, L2 flushed between steps
+    clocks = ClockSampler(local)
+    clocks.start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    reps = []
+    barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        evs[k][0].record(stream)
+        reps.append(step())
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = sum(a.elapsed_time(bb) for a, bb in evs)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    outer = sum(r["outer_iters"] for r in reps)
+    value = outer / (ms * 1e-3)
+    launches = sum(r["gpu_launches"] for r in reps)
+
+    # ---------------- per-kernel-class device time (same K steps, events per launch on the solve stream)
+    prof_reps, prof_ms = [], 0.0
+    agg = None
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        prof_reps.append(step(profile=True))
+        pr = eks.eks_get_profile(solver.ctx)
+        if agg is None:
+            agg = pr
+        else:
+            for key in ("ms", "launches", "bytes", "flops"):
+                for c in agg[key]:
+                    agg[key][c] += pr[key][c]
+    torch.cuda.synchronize()
+    peaks = load_peaks()
+    classes = [c for c in agg["ms"] if c not in ("comm",)]
+    dom = max(classes, key=lambda c: agg["ms"][c])
+
+    def roof(c):
+        if agg["ms"][c] <= 0:
+            return None
+        gbs = agg["bytes"][c] / (agg["ms"][c] * 1e-3) / 1e9
+        tfl = agg["flops"][c] / (agg["ms"][c] * 1e-3) / 1e12
+        intensity = agg["flops"][c] / max(agg["bytes"][c], 1.0)
+        ridge = peaks["dfma_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+        if intensity > ridge:
+            return {"kernel": c, "bound": "alu", "achieved": tfl, "peak": peaks["dfma_tflops"], "unit": "TFLOP/s",
+                    "frac": tfl / peaks["dfma_tflops"], "traffic": None,
+                    "peak_source": "measured DFMA (profiles/fp64_peaks_r01.json)",
+                    "launches": agg["launches"][c], "avg_launch_us": 1e3 * agg["ms"][c] / max(1, agg["launches"][c])}
+        return {"kernel": c, "bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": gbs / peaks["hbm_gbs"], "traffic": None, "peak_source": peaks["source"],
+                "frac_of_8TBs": gbs / 8000.0, "launches": agg["launches"][c],
+                "avg_launch_us": 1e3 * agg["ms"][c] / max(1, agg["launches"][c]),
+                "bytes_per_launch": agg["bytes"][c] / max(1, agg["launches"][c])}
+
+    roofline = roof(dom)
+    spmm_roof = roof("spmm")
+    share = {c: agg["ms"][c] / max(1e-9, sum(agg["ms"].values())) for c in agg["ms"]}
+
+    # ---------------- e2e: C-ABI with pinned HOST buffers, setup + solve per step, wall clock
+    e2e = None
+    if not args.no_e2e:
+        def pinned(a):
+            tt = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+            return tt.numpy()
+        hrp, hcol, hval = pinned(slab.row_ptr), pinned(slab.col), pinned(slab.val)
+        hb = pinned(p.b[lo:hi])
+        hx = pinned(np.zeros(hi - lo))
+        e2e_solver = eks.Solver(None, rank=rank, nranks=world, device=local, nccl_id=uid) if False else solver
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        e_outer = 0
+        for k in range(args.steps):
+            e2e_solver.setup(n, lo, hi, hrp, hcol, hval)
+            hx[:] = 0.0
+            st, rep = eks.eks_solve_ex(e2e_solver.ctx, p.method, p.s, p.t, p.tol, hb, hx)
+            e_outer += rep["outer_iters"]
+        torch.cuda.synchronize()
+        barrier()
+        wall = time.perf_counter() - t0
+        wt = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        wall = float(wt.item())
+        h2d = hrp.nbytes + hcol.nbytes + hval.nbytes + hb.nbytes + hx.nbytes
+        e2e = {"value": e_outer / wall, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(hx.nbytes),
+               "note": "eks_setup_csr(host CSR) + eks_solve(host b, host x) per step, pinned host memory, wall clock"}
+
+    # ---------------- CPU oracle baseline (rank 0, N=1 only; bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        k, dt = oracle_sample(p, args.cpu_iters)
+        cpu = {"value": k / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {k} outer iterations of {p.name} {p.method} (definition mode, single thread, "
+                         f"{os.cpu_count()} host cores present), {dt:.1f} s"}
+
+    if rank == 0:
+        r0 = reps[0]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_of(args, p, world),
+            "roofline": roofline, "spmm_roofline": spmm_roof,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "solve": {"outer_iters": r0["outer_iters"], "converged": r0["converged"],
+                      "true_relres": r0["true_relres"], "rho_ratio": r0["rho"] / r0["rho0"],
+                      "model_bytes_per_outer": r0["model_bytes"] / max(1, r0["outer_iters"]),
+                      "achieved_model_gbs": r0["model_bytes"] / (ms * 1e-3 / args.steps) / 1e9},
+            "time_share": share,
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

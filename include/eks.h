@@ -1,0 +1,141 @@
+/* eks.h — C ABI of libeks.so, the B200-native hot path of the s-step enlarged
+ * Conjugate Gradient methods (s-step SRE-CG, SRE-CG2, MSDO-CG) of
+ * arXiv:1804.10629.  Citations "P:<line>" refer to the paper's LaTeX
+ * (PAPER.md), "S:<line>" to SPEC.md; readings R1..R27 are in DESIGN.md.
+ *
+ * Problem statement (Alg 3/4/6 inputs): solve A x = b for a
+ * sparse symmetric positive definite A, given b, x0, tolerance eps, s, k_max.
+ *
+ * Conventions for every entry point
+ *  - Return value: eks_status.  No C++ exception, abort() or exit() crosses the
+ *    ABI; on failure eks_error_string() gives a one-line reason.
+ *  - Pointers are plain host or device pointers as stated by the eks_mem flag of
+ *    the call; sizes are element counts.  Blocks of t vectors are ROW-MAJOR
+ *    (row i's t doubles contiguous).
+ *  - Ownership: eks_setup_csr copies the matrix (the caller may free its arrays
+ *    on return); b and x are borrowed for the duration of the call only.
+ *  - All calls are synchronous with respect to the host (they return after the
+ *    device work they issued has completed), and run on the context's stream
+ *    (eks_set_stream; default: a stream the context creates).  The caller must
+ *    synchronize its producing stream before passing device pointers.
+ *  - Thread safety: one context per host thread and per rank; no global state
+ *    besides the CUDA runtime and NCCL.
+ */
+#ifndef EKS_H
+#define EKS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct eks_ctx eks_ctx;
+
+/* The three s-step methods: Alg 4, Alg 3, Alg 6. */
+typedef enum { EKS_SRE_CG = 0, EKS_SRE_CG2 = 1, EKS_MSDO_CG = 2 } eks_method;
+
+typedef enum { EKS_MEM_HOST = 0, EKS_MEM_DEVICE = 1 } eks_mem;
+
+typedef enum {
+  EKS_OK = 0,
+  EKS_ERR_INVALID_ARG = 1, /* s<1, t not in {1,2,4,...,64}, t>n, tol<0/NaN, NULL pointer,
+                              t % nranks != 0, slab not a union of domains, nnz >= 2^31 */
+  EKS_ERR_STATE = 2,       /* solve before setup, use after destroy */
+  EKS_ERR_BAD_MATRIX = 3,  /* col out of range, unsorted/duplicate cols in a row, missing or <=0 diagonal */
+  EKS_ERR_OOM = 4,         /* device memory exhausted; for SRE-CG2/MSDO-CG report.max_outer_fit says
+                              how many outer iterations the full basis Q can hold */
+  EKS_ERR_CUDA = 5,
+  EKS_ERR_NCCL = 6,
+  EKS_ERR_BREAKDOWN = 7,   /* A-CholQR pivot <= t*2^-52*max|B| (reading R6): x = last completed iterate */
+  EKS_ERR_MAXITER = 8      /* k_max reached with rho > tol*rho0: x = last iterate */
+} eks_status;
+
+/* Multi-GPU description: one process per GPU; rank r owns the contiguous row
+ * slab it passes to eks_setup_csr.  nccl_id comes from eks_get_unique_id() on
+ * rank 0 and is broadcast by the caller (e.g. torch.distributed). */
+typedef struct {
+  int rank, nranks, device;
+  unsigned char nccl_id[128];
+} eks_dist;
+
+typedef struct {
+  int outer_iters;        /* k_s: loop bodies executed (= k-1 at exit, reading R7) */
+  int converged;          /* rho <= tol*rho0 */
+  int breakdown_block;    /* -1, or global block index whose Cholesky failed */
+  int max_outer_fit;      /* memory planner cap for full-Q methods (SRE-CG2/MSDO-CG), else -1 */
+  double rho0, rho;       /* ||r0||_2 and final recursive ||r_k||_2 (reading R8) */
+  double true_relres;     /* ||b - A x||_2 / ||b||_2, computed once at exit */
+  double solve_seconds;   /* device time of the solve (CUDA events on the ctx stream) */
+  double model_bytes;     /* algorithmic bytes of the whole solve (DESIGN.md byte model) */
+  double model_flops;     /* algorithmic flops of the whole solve */
+  int gpu_launches;       /* kernels launched by the solve */
+  const double* rho_history; /* outer_iters+1 entries, owned by ctx, valid until next solve/destroy */
+} eks_report;
+
+/* Extended options; zero-initialise and set fields.  Defaults reproduce the
+ * oracle's defaults (A-CholQR, k_max 5000). */
+typedef struct {
+  int max_outer;          /* <=0: 5000 (reading R7) */
+  int use_graph;          /* 1: capture one outer iteration as a CUDA graph and replay it */
+  int profile;            /* 1: record per-kernel-class CUDA events (see eks_profile) */
+  int reserved[8];
+} eks_options;
+
+/* Per-kernel-class device time accumulated while options.profile == 1. */
+typedef enum {
+  EKS_K_SPLIT = 0, EKS_K_SPMM = 1, EKS_K_COEF = 2, EKS_K_UPDATE = 3, EKS_K_REDUCE = 4,
+  EKS_K_CHOL = 5, EKS_K_APPLY = 6, EKS_K_COMM = 7, EKS_K_OTHER = 8, EKS_K_NCLASSES = 9
+} eks_kclass;
+typedef struct {
+  double ms[EKS_K_NCLASSES];      /* summed event time per class */
+  long long launches[EKS_K_NCLASSES];
+  double bytes[EKS_K_NCLASSES];   /* algorithmic bytes per class (DESIGN.md byte model); SpMM: 12nnz+4(n+1)+16nt */
+  double flops[EKS_K_NCLASSES];   /* algorithmic flops per class */
+} eks_profile;
+
+/* rank 0 only: a fresh NCCL unique id (128 bytes) for eks_create on all ranks. */
+eks_status eks_get_unique_id(unsigned char id[128]);
+
+/* dist == NULL: single GPU (current device), no NCCL.  Creates a stream. */
+eks_status eks_create(eks_ctx** out, const eks_dist* dist);
+
+/* Use the caller's cudaStream_t (passed as void*) for all later work; NULL = own stream. */
+eks_status eks_set_stream(eks_ctx* ctx, void* stream);
+
+/* Rows [row_begin,row_end) of an n_global×n_global SPD matrix in CSR with GLOBAL
+ * int32 column indices (ascending, unique within a row, diagonal present and >0).
+ * row_ptr has row_end-row_begin+1 entries with row_ptr[0]==0.  Validated on the
+ * host side of the copy (EKS_ERR_BAD_MATRIX).  Symmetry is assumed, not checked. */
+eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t row_end,
+                         const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                         eks_mem where);
+
+/* Solve A x = b with the chosen s-step method (Alg 3/4/6), t domains
+ * D_d = [floor(d n/t), floor((d+1) n/t)) (reading R1), tolerance tol on the
+ * recursive residual.  b, x: this rank's rows; x holds x0 on entry.
+ * max_outer <= 0 means 5000.  rep may be NULL. */
+eks_status eks_solve(eks_ctx* ctx, eks_method method, int s, int t, double tol,
+                     const double* b, double* x, eks_mem where, int max_outer, eks_report* rep);
+
+eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double tol,
+                        const double* b, double* x, eks_mem where, const eks_options* opt,
+                        eks_report* rep);
+
+/* cfg5 basis-generation sweep (reading R27): A-orthonormalize the start block X0
+ * (this rank's rows, n_local×t), then build nblocks-1 further blocks
+ * W = A-orth(A·W_prev) against the last two blocks (Alg 4), no
+ * update.  W_last (n_local×t) receives the final block.  rep->outer_iters = nblocks. */
+eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks, const double* X0, double* W_last,
+                           eks_mem where, const eks_options* opt, eks_report* rep);
+
+/* Kernel-class timings of the last solve/sweep run with opt.profile = 1. */
+eks_status eks_get_profile(const eks_ctx* ctx, eks_profile* out);
+
+eks_status eks_destroy(eks_ctx* ctx);             /* NULL-safe */
+const char* eks_error_string(const eks_ctx* ctx); /* last error detail, owned by ctx */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EKS_H */

@@ -1,0 +1,44 @@
+/* eks_kernels.h — kernel-level C ABI of libeks.so, used by the parity tests and
+ * by bench.py's roofline measurement.  Each call runs ONE step of the hot path
+ * on the context's matrix (set by eks_setup_csr) and stream, on DEVICE
+ * pointers (e.g. torch tensors' data_ptr()), single-rank contexts only
+ * (EKS_ERR_INVALID_ARG when nranks > 1).  Blocks are row-major n×t fp64,
+ * t ∈ {1,2,4,8,16,32,64}; n = the context's local row count.  All calls are
+ * synchronous (they return after the device work completed).
+ */
+#ifndef EKS_KERNELS_H
+#define EKS_KERNELS_H
+
+#include "eks.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* (a1) Z = T(r): Z[i][d] = r[i] if row i is in domain D_d = [floor(d n/t), floor((d+1) n/t)),
+ * else 0 (reading R1). */
+eks_status eks_k_split(eks_ctx* ctx, int t, const double* r, double* Z);
+
+/* (a2) Y = A·X, p-ascending fma from 0 (bitwise equal to the oracle, R20).
+ * If G != NULL: G = XᵀY (t×t, full, fixed-order sums).  If v and g != NULL: g = Xᵀv (t). */
+eks_status eks_k_spmm(eks_ctx* ctx, int t, const double* X, double* Y, double* G, const double* v, double* g);
+
+/* (a3) CGS2: twice { C = (AQ)ᵀZ ; Z = Z − Q·C } against nq window blocks (
+ * readings R3, R24).  Q and AQ are HOST arrays of nq DEVICE pointers (each an n×t block,
+ * AQ[j] = A·Q[j]).  Z is updated in place; C1, C2 ((nq·t)×t device, may be NULL) receive the
+ * two passes' coefficients. */
+eks_status eks_k_cgs2(eks_ctx* ctx, int t, int nq, const double* const* Q, const double* const* AQ,
+                      double* Z, double* C1, double* C2);
+
+/* (a4) A-CholQR of Z (reading R4): AZ = A·Z, B = Zᵀ(AZ), B = RᵀR, W = Z R⁻¹,
+ * AW = (AZ) R⁻¹.  Outputs W, AW (n×t), R, B (t×t; device, B/R may be NULL).
+ * Returns EKS_ERR_BREAKDOWN when a pivot <= t·2^-52·max|B| (reading R6). */
+eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double* AW, double* R, double* B);
+
+/* Cholesky alone: B (t×t device, upper triangle read) = RᵀR, R upper (device). */
+eks_status eks_k_chol(eks_ctx* ctx, int t, const double* B, double* R);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

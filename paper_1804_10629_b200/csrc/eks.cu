@@ -1,0 +1,975 @@
+// eks.cu — host driver and C ABI of libeks.so (include/eks.h, include/eks_kernels.h).
+//
+// One process per GPU.  Rank r owns a contiguous row slab; its n×t blocks are
+// stored row-major with ghost rows ("halo") from the other ranks in an
+// extended layout [ghosts of lower ranks | local rows | ghosts of higher ranks],
+// so the SpMM indexes one array with remapped column indices.  Communication is
+// NCCL: one halo exchange (ncclSend/ncclRecv on a comm stream, overlapped with
+// the interior rows) per SpMM and one ncclAllReduce per reduced small
+// matrix (CGS2 coefficients, Gram + Z2ᵀr, ρ²).  No CPU fallback: without a CUDA
+// device every call fails with EKS_ERR_CUDA.
+#include "../../include/eks.h"
+#include "../../include/eks_kernels.h"
+#include "eks_kernels.cuh"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+using eks::kThreads;
+
+namespace {
+
+struct Recv { int peer; int64_t lo, hi, ext_off; };  // ghost rows [lo,hi) of peer → ext rows ext_off..
+struct Send { int peer; int64_t lo, hi; };           // my global rows [lo,hi) → peer
+
+struct Block {
+  double* base = nullptr;  // ext allocation (ghost rows included) or local allocation
+  double* loc = nullptr;   // first local row
+};
+
+struct ProfRec { int cls; cudaEvent_t a, b; };
+
+}  // namespace
+
+struct eks_ctx {
+  int device = 0, rank = 0, nranks = 1;
+  cudaStream_t stream = nullptr, own = nullptr, comm_stream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  ncclComm_t comm = nullptr;
+  int sms = 148, nblk = 296;
+  std::string err;
+  // matrix (local slab)
+  bool have_matrix = false;
+  int64_t n_global = 0, row_begin = 0, row_end = 0, n = 0, nnz = 0;
+  int* d_rp = nullptr;
+  int* d_col = nullptr;
+  double* d_val = nullptr;
+  int64_t halo_before = 0, halo_after = 0;
+  std::vector<Recv> recvs;
+  std::vector<Send> sends;
+  int64_t int_lo = 0, int_hi = 0;  // interior local rows (all columns local)
+  // workspace, keyed by t
+  int ws_t = 0;
+  std::vector<Block> Wpool, AWpool;  // Wpool ext layout, AWpool local
+  Block Zs, Z1, xv, tmpv;            // xv: ext vector
+  double *b = nullptr, *r = nullptr, *rnew = nullptr, *dx = nullptr;
+  double* part = nullptr;
+  size_t part_cap = 0;  // doubles
+  double *C1 = nullptr, *C2 = nullptr;
+  size_t C_cap = 0;
+  double *Bg = nullptr, *Rm = nullptr, *Rinv = nullptr, *alpha = nullptr, *scal = nullptr;
+  int alpha_cap = 0;
+  int* flag = nullptr;
+  double* h_scal = nullptr;  // pinned: [0..3] doubles, [4] flag as double
+  int* h_flag = nullptr;     // pinned INT_MAX source
+  std::vector<double> hist;
+  // profiling
+  bool prof_on = false;
+  std::vector<ProfRec> prof_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  eks_profile prof{};
+  long long launches = 0;
+  double model_bytes = 0.0, model_flops = 0.0;
+};
+
+namespace {
+
+eks_status fail(eks_ctx* c, eks_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return st;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return fail(ctx, EKS_ERR_CUDA, "%s: %s (%s:%d)", #call,               \
+                                       cudaGetErrorString(e_), __FILE__, __LINE__);              \
+  } while (0)
+#define NK(call)                                                                                  \
+  do {                                                                                            \
+    ncclResult_t r_ = (call);                                                                     \
+    if (r_ != ncclSuccess) return fail(ctx, EKS_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+#define ST(call)                     \
+  do {                               \
+    eks_status s_ = (call);          \
+    if (s_ != EKS_OK) return s_;     \
+  } while (0)
+
+bool valid_t(int t) { return t == 1 || t == 2 || t == 4 || t == 8 || t == 16 || t == 32 || t == 64; }
+
+// ---------------------------------------------------------------- profiling
+cudaEvent_t pev(eks_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct KScope {
+  eks_ctx* c;
+  int cls;
+  cudaEvent_t a = nullptr;
+  KScope(eks_ctx* c_, int cls_) : c(c_), cls(cls_) {
+    if (cls != EKS_K_COMM) c->launches++;  // count only this library's kernels
+    c->prof.launches[cls]++;
+    if (c->prof_on) {
+      a = pev(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~KScope() {
+    if (c->prof_on) {
+      cudaEvent_t b = pev(c);
+      cudaEventRecord(b, c->stream);
+      c->prof_pending.push_back({cls, a, b});
+    }
+  }
+};
+void prof_harvest(eks_ctx* c) {  // call after a stream sync
+  for (auto& p : c->prof_pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    c->prof.ms[p.cls] += ms;
+    c->ev_pool.push_back(p.a);
+    c->ev_pool.push_back(p.b);
+  }
+  c->prof_pending.clear();
+}
+
+void account(eks_ctx* c, int cls, double bytes, double flops) {
+  c->prof.bytes[cls] += bytes;
+  c->prof.flops[cls] += flops;
+  c->model_bytes += bytes;
+  c->model_flops += flops;
+}
+
+// ---------------------------------------------------------------- memory
+eks_status dalloc(eks_ctx* ctx, double** p, size_t count) {
+  if (*p) return EKS_OK;
+  cudaError_t e = cudaMalloc((void**)p, sizeof(double) * (count ? count : 1));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return fail(ctx, EKS_ERR_OOM, "cudaMalloc(%zu doubles): %s", count, cudaGetErrorString(e));
+  }
+  return EKS_OK;
+}
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+int64_t n_ext(const eks_ctx* c) { return c->halo_before + c->n + c->halo_after; }
+
+eks_status alloc_block(eks_ctx* ctx, Block* B, int t, bool ext) {
+  if (B->base) return EKS_OK;
+  int64_t rows = ext ? n_ext(ctx) : ctx->n;
+  ST(dalloc(ctx, &B->base, (size_t)rows * t));
+  B->loc = B->base + (ext ? ctx->halo_before * t : 0);
+  return EKS_OK;
+}
+
+void free_workspace(eks_ctx* c) {
+  for (auto& b : c->Wpool) dfree(b.base);
+  for (auto& b : c->AWpool) dfree(b.base);
+  c->Wpool.clear();
+  c->AWpool.clear();
+  for (Block* b : {&c->Zs, &c->Z1, &c->xv, &c->tmpv}) { dfree(b->base); *b = Block{}; }
+  for (double** p : {&c->b, &c->r, &c->rnew, &c->dx, &c->part, &c->C1, &c->C2, &c->Bg, &c->Rm, &c->Rinv,
+                     &c->alpha, &c->scal}) { dfree(*p); *p = nullptr; }
+  dfree(c->flag);
+  c->flag = nullptr;
+  c->part_cap = c->C_cap = 0;
+  c->alpha_cap = 0;
+  c->ws_t = 0;
+}
+
+eks_status ensure_workspace(eks_ctx* ctx, int t, int s) {
+  if (ctx->ws_t != t) {
+    free_workspace(ctx);
+    ctx->ws_t = t;
+  }
+  ST(alloc_block(ctx, &ctx->Zs, t, false));
+  ST(alloc_block(ctx, &ctx->Z1, t, false));
+  ST(alloc_block(ctx, &ctx->xv, 1, true));
+  ST(alloc_block(ctx, &ctx->tmpv, 1, false));
+  for (double** p : {&ctx->b, &ctx->r, &ctx->rnew, &ctx->dx}) ST(dalloc(ctx, p, (size_t)ctx->n));
+  ST(dalloc(ctx, &ctx->Bg, (size_t)t * t + t));
+  ST(dalloc(ctx, &ctx->Rm, (size_t)t * t));
+  ST(dalloc(ctx, &ctx->Rinv, (size_t)t * t));
+  ST(dalloc(ctx, &ctx->scal, 16));
+  if (!ctx->flag) CK(cudaMalloc((void**)&ctx->flag, sizeof(int) * 4));
+  if (ctx->alpha_cap < s * t) {
+    dfree(ctx->alpha);
+    ctx->alpha = nullptr;
+    ST(dalloc(ctx, &ctx->alpha, (size_t)s * t));
+    ctx->alpha_cap = s * t;
+  }
+  size_t need_part = (size_t)ctx->nblk * ((size_t)t * t + t + 8);
+  if (ctx->part_cap < need_part) {
+    dfree(ctx->part);
+    ctx->part = nullptr;
+    ST(dalloc(ctx, &ctx->part, need_part));
+    ctx->part_cap = need_part;
+  }
+  return EKS_OK;
+}
+
+eks_status ensure_part(eks_ctx* ctx, size_t doubles) {
+  if (ctx->part_cap >= doubles) return EKS_OK;
+  dfree(ctx->part);
+  ctx->part = nullptr;
+  ST(dalloc(ctx, &ctx->part, doubles));
+  ctx->part_cap = doubles;
+  return EKS_OK;
+}
+
+eks_status ensure_C(eks_ctx* ctx, size_t doubles) {
+  if (ctx->C_cap >= doubles) return EKS_OK;
+  dfree(ctx->C1);
+  dfree(ctx->C2);
+  ctx->C1 = ctx->C2 = nullptr;
+  ST(dalloc(ctx, &ctx->C1, doubles));
+  ST(dalloc(ctx, &ctx->C2, doubles));
+  ctx->C_cap = doubles;
+  return EKS_OK;
+}
+
+// ---------------------------------------------------------------- communication
+eks_status allreduce(eks_ctx* ctx, double* buf, size_t count) {
+  if (ctx->nranks == 1 || count == 0) return EKS_OK;
+  KScope k(ctx, EKS_K_COMM);
+  NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  return EKS_OK;
+}
+
+eks_status halo_start(eks_ctx* ctx, const Block& X, int t) {
+  if (ctx->nranks == 1) return EKS_OK;
+  CK(cudaEventRecord(ctx->ev_ready, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_ready, 0));
+  NK(ncclGroupStart());
+  for (const Send& s : ctx->sends)
+    NK(ncclSend(X.loc + (s.lo - ctx->row_begin) * t, (size_t)(s.hi - s.lo) * t, ncclDouble, s.peer, ctx->comm,
+                ctx->comm_stream));
+  for (const Recv& r : ctx->recvs)
+    NK(ncclRecv(X.base + r.ext_off * t, (size_t)(r.hi - r.lo) * t, ncclDouble, r.peer, ctx->comm,
+                ctx->comm_stream));
+  NK(ncclGroupEnd());
+  CK(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
+  return EKS_OK;
+}
+
+// Y = A X with halo exchange overlapped with the interior rows.
+eks_status spmm(eks_ctx* ctx, const Block& X, double* Y, int t) {
+  ST(halo_start(ctx, X, t));
+  account(ctx, EKS_K_SPMM, 12.0 * ctx->nnz + 4.0 * (ctx->n + 1) + 16.0 * ctx->n * t, 2.0 * ctx->nnz * t);
+  if (ctx->nranks == 1) {
+    KScope k(ctx, EKS_K_SPMM);
+    CK(eks::launch_spmm(ctx->stream, t, 0, (int)ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val, X.base, Y, ctx->sms));
+    return EKS_OK;
+  }
+  {
+    KScope k(ctx, EKS_K_SPMM);
+    CK(eks::launch_spmm(ctx->stream, t, (int)ctx->int_lo, (int)ctx->int_hi, ctx->d_rp, ctx->d_col, ctx->d_val,
+                        X.base, Y, ctx->sms));
+  }
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+  {
+    KScope k(ctx, EKS_K_SPMM);
+    CK(eks::launch_spmm(ctx->stream, t, 0, (int)ctx->int_lo, ctx->d_rp, ctx->d_col, ctx->d_val, X.base, Y,
+                        ctx->sms));
+    CK(eks::launch_spmm(ctx->stream, t, (int)ctx->int_hi, (int)ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val, X.base,
+                        Y, ctx->sms));
+  }
+  return EKS_OK;
+}
+
+// out (nl·t·t [+t]) = Σ over all rows of Lᵀ R [and L_0ᵀ v], allreduced.
+eks_status tn_reduce(eks_ctx* ctx, int t, int nl, const double* const* L, const double* R, const double* v,
+                     double* out) {
+  const size_t stride = eks::tn_partials_stride(t, nl, v != nullptr);
+  ST(ensure_part(ctx, stride * ctx->nblk));
+  account(ctx, EKS_K_COEF, 8.0 * ctx->n * ((double)(nl + 1) * t + (v ? 1 : 0)), 2.0 * ctx->n * t * (t * nl + (v ? 1 : 0)));
+  {
+    KScope k(ctx, EKS_K_COEF);
+    CK(eks::launch_tn_partials(ctx->stream, t, ctx->n, nl, L, R, v, ctx->part, ctx->nblk));
+  }
+  {
+    KScope k(ctx, EKS_K_REDUCE);
+    CK(eks::launch_reduce(ctx->stream, ctx->part, ctx->nblk, stride, stride, out));
+  }
+  return allreduce(ctx, out, stride);
+}
+
+eks_status ts_update(eks_ctx* ctx, int t, int nq, const double* const* Q, const double* C, const double* Zin,
+                     double* Zout) {
+  account(ctx, EKS_K_UPDATE, 8.0 * ctx->n * ((double)nq * t + 2.0 * t), 2.0 * ctx->n * t * t * nq);
+  KScope k(ctx, EKS_K_UPDATE);
+  CK(eks::launch_ts_update(ctx->stream, t, ctx->n, nq, Q, C, Zin, Zout, ctx->nblk));
+  return EKS_OK;
+}
+
+// CGS2 of Z against the window (Q, AQ): two passes of C = (AQ)ᵀZ, Z -= Q C (reading R3/R24).
+eks_status cgs2(eks_ctx* ctx, int t, const std::vector<const double*>& Q, const std::vector<const double*>& AQ,
+                const double* Z, double* Zout) {
+  const int nq = (int)Q.size();
+  ST(ensure_C(ctx, (size_t)nq * t * t));
+  ST(tn_reduce(ctx, t, nq, AQ.data(), Z, nullptr, ctx->C1));
+  ST(ts_update(ctx, t, nq, Q.data(), ctx->C1, Z, ctx->Z1.loc));
+  ST(tn_reduce(ctx, t, nq, AQ.data(), ctx->Z1.loc, nullptr, ctx->C2));
+  ST(ts_update(ctx, t, nq, Q.data(), ctx->C2, ctx->Z1.loc, Zout));
+  return EKS_OK;
+}
+
+eks_status chol(eks_ctx* ctx, int t, const double* B, const double* g, double* R, double* Rinv, double* alpha,
+                int gblock) {
+  KScope k(ctx, EKS_K_CHOL);
+  CK(eks::launch_chol(ctx->stream, t, B, g, R, Rinv, alpha, ctx->flag, gblock));
+  return EKS_OK;
+}
+
+eks_status reset_flag(eks_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->flag, ctx->h_flag, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  return EKS_OK;
+}
+
+// ρ² partials → scal[slot] (allreduced)
+eks_status reduce_scalar(eks_ctx* ctx, double* slot) {
+  {
+    KScope k(ctx, EKS_K_REDUCE);
+    CK(eks::launch_reduce(ctx->stream, ctx->part, ctx->nblk, 1, 1, slot));
+  }
+  return allreduce(ctx, slot, 1);
+}
+
+eks_status sync_scalars(eks_ctx* ctx, int count) {
+  CK(cudaMemcpyAsync(ctx->h_scal, ctx->scal, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->h_flag + 1, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->prof_on) prof_harvest(ctx);
+  return EKS_OK;
+}
+
+eks_status check_ready(eks_ctx* ctx) {
+  if (!ctx) return EKS_ERR_INVALID_ARG;
+  if (!ctx->have_matrix) return fail(ctx, EKS_ERR_STATE, "eks_setup_csr has not been called");
+  CK(cudaSetDevice(ctx->device));
+  return EKS_OK;
+}
+
+eks_status copy_in(eks_ctx* ctx, double* dst, const double* src, int64_t count, eks_mem where) {
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * count,
+                     where == EKS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ctx->stream));
+  return EKS_OK;
+}
+eks_status copy_out(eks_ctx* ctx, double* dst, const double* src, int64_t count, eks_mem where) {
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * count,
+                     where == EKS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
+  return EKS_OK;
+}
+
+// block slot for global block index gb: SRE-CG ring of 3, full-Q methods one per block
+eks_status slot(eks_ctx* ctx, int t, int idx, Block** W, Block** AW) {
+  while ((int)ctx->Wpool.size() <= idx) {
+    Block w, aw;
+    ctx->Wpool.push_back(w);
+    ctx->AWpool.push_back(aw);
+  }
+  eks_status s1 = alloc_block(ctx, &ctx->Wpool[idx], t, true);
+  if (s1 != EKS_OK) return s1;
+  s1 = alloc_block(ctx, &ctx->AWpool[idx], t, false);
+  if (s1 != EKS_OK) return s1;
+  *W = &ctx->Wpool[idx];
+  *AW = &ctx->AWpool[idx];
+  return EKS_OK;
+}
+
+struct Window {
+  std::vector<const double*> Q, AQ;
+};
+
+// Window of the next block: SRE-CG → last min(2,#) blocks (Alg 4, reading R11);
+// SRE-CG2 / MSDO-CG → all blocks (Alg 3 P:151/Alg 6).
+Window window_for(eks_ctx* ctx, int method, int nblocks, int ring) {
+  Window w;
+  int first = (method == EKS_SRE_CG) ? std::max(0, nblocks - 2) : 0;
+  for (int j = first; j < nblocks; ++j) {
+    int idx = ring ? j % ring : j;
+    w.Q.push_back(ctx->Wpool[idx].loc);
+    w.AQ.push_back(ctx->AWpool[idx].loc);
+  }
+  return w;
+}
+
+// One A-orthonormalized block: Zsrc (or the split of r) → W_new, AW_new, R⁻¹, alpha_b.
+eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bool seed_from_r, const double* Zsrc,
+                      Block* Wn, Block* AWn, int alpha_off, int gb, int mode) {
+  Window w = window_for(ctx, method, nblocks, ring);
+  if (seed_from_r) {
+    double* dst = w.Q.empty() ? Wn->loc : ctx->Zs.loc;
+    {
+      KScope k(ctx, EKS_K_SPLIT);
+      CK(eks::launch_split(ctx->stream, t, ctx->n, ctx->row_begin, ctx->n_global, ctx->r, dst));
+    }
+    account(ctx, EKS_K_SPLIT, 8.0 * ctx->n * (t + 1), 0.0);
+    Zsrc = dst;
+  }
+  if (!w.Q.empty()) {
+    ST(cgs2(ctx, t, w.Q, w.AQ, Zsrc, Wn->loc));  // "A-orthonormalize W against Q"
+  } else if (Zsrc != Wn->loc) {
+    CK(cudaMemcpyAsync(Wn->loc, Zsrc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  // "A-orthonormalize W": A-CholQR with one SpMM of Z2 (AW = (A Z2) R⁻¹)
+  ST(spmm(ctx, *Wn, AWn->loc, t));
+  const double* Lw[1] = {Wn->loc};
+  const bool with_update = !(mode & 4);
+  ST(tn_reduce(ctx, t, 1, Lw, AWn->loc, with_update ? ctx->r : nullptr, ctx->Bg));
+  ST(chol(ctx, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
+          with_update ? ctx->alpha + alpha_off : nullptr, gb));
+  {
+    KScope k(ctx, EKS_K_APPLY);
+    account(ctx, EKS_K_APPLY, 8.0 * ctx->n * (4.0 * t + 4.0), 2.0 * ctx->n * t * (t + 2));
+    CK(eks::launch_apply(ctx->stream, t, ctx->n, Wn->loc, AWn->loc, ctx->Rinv,
+                         with_update ? ctx->alpha + alpha_off : nullptr, ctx->xv.loc, ctx->dx, ctx->r, ctx->rnew,
+                         ctx->part, ctx->flag, mode, ctx->nblk));
+  }
+  return EKS_OK;
+}
+
+// r = b − A x (x in ctx->xv), scal[slot] = ||r||² ; if r_out == nullptr only the norm
+eks_status residual(eks_ctx* ctx, double* r_out, double* slotp) {
+  ST(spmm(ctx, ctx->xv, ctx->tmpv.loc, 1));
+  {
+    KScope k(ctx, EKS_K_OTHER);
+    CK(eks::launch_residual(ctx->stream, ctx->n, ctx->b, ctx->tmpv.loc, r_out, ctx->part, ctx->nblk));
+  }
+  return reduce_scalar(ctx, slotp);
+}
+
+void begin_run(eks_ctx* ctx, const eks_options* opt) {
+  ctx->prof_on = opt && opt->profile;
+  ctx->prof = eks_profile{};
+  ctx->launches = 0;
+  ctx->model_bytes = ctx->model_flops = 0.0;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+eks_status eks_get_unique_id(unsigned char id[128]) {
+  if (!id) return EKS_ERR_INVALID_ARG;
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return EKS_ERR_NCCL;
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  memcpy(id, &u, 128);
+  return EKS_OK;
+}
+
+eks_status eks_create(eks_ctx** out, const eks_dist* dist) {
+  if (!out) return EKS_ERR_INVALID_ARG;
+  *out = nullptr;
+  eks_ctx* ctx = new (std::nothrow) eks_ctx();
+  if (!ctx) return EKS_ERR_OOM;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    delete ctx;
+    return EKS_ERR_CUDA;  // no CPU fallback
+  }
+  if (dist) {
+    if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks || dist->device < 0 || dist->device >= ndev) {
+      delete ctx;
+      return EKS_ERR_INVALID_ARG;
+    }
+    ctx->rank = dist->rank;
+    ctx->nranks = dist->nranks;
+    ctx->device = dist->device;
+  } else {
+    cudaGetDevice(&ctx->device);
+  }
+  eks_status st = EKS_OK;
+  do {
+    if (cudaSetDevice(ctx->device) != cudaSuccess) { st = EKS_ERR_CUDA; break; }
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    ctx->nblk = eks::sweep_ctas(ctx->sms);
+    if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { st = EKS_ERR_CUDA; break; }
+    ctx->stream = ctx->own;
+    if (cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking) != cudaSuccess) { st = EKS_ERR_CUDA; break; }
+    cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming);
+    if (cudaMallocHost((void**)&ctx->h_scal, 16 * sizeof(double)) != cudaSuccess) { st = EKS_ERR_CUDA; break; }
+    if (cudaMallocHost((void**)&ctx->h_flag, 4 * sizeof(int)) != cudaSuccess) { st = EKS_ERR_CUDA; break; }
+    ctx->h_flag[0] = INT_MAX;
+    if (ctx->nranks > 1) {
+      ncclUniqueId u;
+      memcpy(&u, dist->nccl_id, 128);
+      if (ncclCommInitRank(&ctx->comm, ctx->nranks, u, ctx->rank) != ncclSuccess) { st = EKS_ERR_NCCL; break; }
+    }
+  } while (0);
+  if (st != EKS_OK) {
+    eks_destroy(ctx);
+    return st;
+  }
+  *out = ctx;
+  return EKS_OK;
+}
+
+eks_status eks_set_stream(eks_ctx* ctx, void* stream) {
+  if (!ctx) return EKS_ERR_INVALID_ARG;
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own;
+  return EKS_OK;
+}
+
+eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t row_end, const int64_t* row_ptr,
+                         const int32_t* col_idx, const double* vals, eks_mem where) {
+  if (!ctx) return EKS_ERR_INVALID_ARG;
+  if (!row_ptr || !col_idx || !vals) return fail(ctx, EKS_ERR_INVALID_ARG, "NULL matrix pointer");
+  if (n_global <= 0 || row_begin < 0 || row_end <= row_begin || row_end > n_global)
+    return fail(ctx, EKS_ERR_INVALID_ARG, "bad row range [%lld,%lld) of n=%lld", (long long)row_begin,
+                (long long)row_end, (long long)n_global);
+  if (n_global >= INT_MAX) return fail(ctx, EKS_ERR_INVALID_ARG, "n_global must be < 2^31 (int32 columns)");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t n = row_end - row_begin;
+  std::vector<int64_t> rp(n + 1);
+  if (where == EKS_MEM_HOST) memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1));
+  else CK(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+  if (rp[0] != 0) return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr[0] != 0");
+  for (int64_t i = 0; i < n; ++i)
+    if (rp[i + 1] < rp[i]) return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr not monotone at row %lld", (long long)i);
+  const int64_t nnz = rp[n];
+  if (nnz >= INT_MAX) return fail(ctx, EKS_ERR_INVALID_ARG, "local nnz must be < 2^31");
+  std::vector<int32_t> col(nnz);
+  std::vector<double> val(nnz);
+  if (where == EKS_MEM_HOST) {
+    memcpy(col.data(), col_idx, sizeof(int32_t) * nnz);
+    memcpy(val.data(), vals, sizeof(double) * nnz);
+  } else {
+    CK(cudaMemcpy(col.data(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(val.data(), vals, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+  }
+  // validation (SPEC S:30-33 invariants): sorted unique columns in range, positive diagonal
+  for (int64_t i = 0; i < n; ++i) {
+    bool diag = false;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t c = col[p];
+      if (c < 0 || c >= n_global) return fail(ctx, EKS_ERR_BAD_MATRIX, "column %lld out of range in row %lld",
+                                              (long long)c, (long long)(row_begin + i));
+      if (p > rp[i] && col[p - 1] >= c)
+        return fail(ctx, EKS_ERR_BAD_MATRIX, "columns not strictly ascending in row %lld", (long long)(row_begin + i));
+      if (c == row_begin + i) {
+        if (!(val[p] > 0.0)) return fail(ctx, EKS_ERR_BAD_MATRIX, "non-positive diagonal in row %lld",
+                                         (long long)(row_begin + i));
+        diag = true;
+      }
+    }
+    if (!diag) return fail(ctx, EKS_ERR_BAD_MATRIX, "missing diagonal in row %lld", (long long)(row_begin + i));
+  }
+  // ---- slab table of all ranks
+  std::vector<int64_t> ranges(2 * ctx->nranks);
+  ranges[2 * ctx->rank] = row_begin;
+  ranges[2 * ctx->rank + 1] = row_end;
+  if (ctx->nranks > 1) {
+    int64_t* d = nullptr;
+    CK(cudaMalloc((void**)&d, sizeof(int64_t) * 2 * ctx->nranks));
+    CK(cudaMemcpy(d + 2 * ctx->rank, ranges.data() + 2 * ctx->rank, 2 * sizeof(int64_t), cudaMemcpyHostToDevice));
+    NK(ncclAllGather(d + 2 * ctx->rank, d, 2, ncclInt64, ctx->comm, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(ranges.data(), d, sizeof(int64_t) * 2 * ctx->nranks, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    for (int q = 0; q + 1 < ctx->nranks; ++q)
+      if (ranges[2 * q + 1] != ranges[2 * q + 2] || ranges[0] != 0 || ranges[2 * ctx->nranks - 1] != n_global)
+        return fail(ctx, EKS_ERR_INVALID_ARG, "rank slabs must tile [0,n) in rank order");
+  }
+  auto owner = [&](int64_t c) {
+    int q = 0;
+    while (q < ctx->nranks && !(c >= ranges[2 * q] && c < ranges[2 * q + 1])) ++q;
+    return q;
+  };
+  // ---- halo plan: contiguous ghost range per owner rank
+  std::vector<int64_t> glo(ctx->nranks, INT64_MAX), ghi(ctx->nranks, INT64_MIN);
+  for (int64_t p = 0; p < nnz; ++p) {
+    const int64_t c = col[p];
+    if (c < row_begin || c >= row_end) {
+      int q = owner(c);
+      glo[q] = std::min(glo[q], c);
+      ghi[q] = std::max(ghi[q], c + 1);
+    }
+  }
+  const int64_t old_before = ctx->halo_before, old_after = ctx->halo_after;
+  ctx->recvs.clear();
+  ctx->sends.clear();
+  std::vector<int64_t> off(ctx->nranks, 0);
+  int64_t ext = 0;
+  for (int q = 0; q < ctx->nranks; ++q) {
+    if (q == ctx->rank) {
+      off[q] = ext;
+      ext += n;
+      continue;
+    }
+    if (glo[q] < ghi[q]) {
+      off[q] = ext;
+      ctx->recvs.push_back({q, glo[q], ghi[q], ext});
+      ext += ghi[q] - glo[q];
+    }
+  }
+  ctx->halo_before = off[ctx->rank];
+  ctx->halo_after = ext - off[ctx->rank] - n;
+  if (ctx->nranks > 1) {
+    // everyone learns who needs which of its rows
+    std::vector<int64_t> req(2 * ctx->nranks * ctx->nranks, 0);
+    for (int q = 0; q < ctx->nranks; ++q)
+      if (q != ctx->rank && glo[q] < ghi[q]) {
+        req[2 * (ctx->rank * ctx->nranks + q)] = glo[q];
+        req[2 * (ctx->rank * ctx->nranks + q) + 1] = ghi[q];
+      }
+    int64_t* d = nullptr;
+    const size_t per = 2 * ctx->nranks;
+    CK(cudaMalloc((void**)&d, sizeof(int64_t) * per * ctx->nranks));
+    CK(cudaMemcpy(d + per * ctx->rank, req.data() + per * ctx->rank, sizeof(int64_t) * per, cudaMemcpyHostToDevice));
+    NK(ncclAllGather(d + per * ctx->rank, d, per, ncclInt64, ctx->comm, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(req.data(), d, sizeof(int64_t) * per * ctx->nranks, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    for (int q = 0; q < ctx->nranks; ++q) {
+      if (q == ctx->rank) continue;
+      const int64_t lo = req[2 * (q * ctx->nranks + ctx->rank)], hi = req[2 * (q * ctx->nranks + ctx->rank) + 1];
+      if (hi > lo) ctx->sends.push_back({q, lo, hi});
+    }
+  }
+  // ---- remap columns to the extended layout; interior run
+  std::vector<int32_t> ecol(nnz);
+  std::vector<char> interior(n, 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t c = col[p];
+      if (c >= row_begin && c < row_end) {
+        ecol[p] = (int32_t)(ctx->halo_before + (c - row_begin));
+      } else {
+        int q = owner(c);
+        ecol[p] = (int32_t)(off[q] + (c - glo[q]));
+        interior[i] = 0;
+      }
+    }
+  int64_t best_lo = 0, best_len = 0, cur = 0;
+  for (int64_t i = 0; i <= n; ++i) {
+    if (i < n && interior[i]) { ++cur; continue; }
+    if (cur > best_len) { best_len = cur; best_lo = i - cur; }
+    cur = 0;
+  }
+  ctx->int_lo = best_lo;
+  ctx->int_hi = best_lo + best_len;
+  // ---- upload (the block workspace survives when the slab geometry is unchanged)
+  if (!ctx->have_matrix || ctx->n != n || old_before != ctx->halo_before || old_after != ctx->halo_after)
+    free_workspace(ctx);
+  dfree(ctx->d_rp);
+  dfree(ctx->d_col);
+  dfree(ctx->d_val);
+  ctx->d_rp = nullptr;
+  ctx->d_col = nullptr;
+  ctx->d_val = nullptr;
+  ctx->have_matrix = false;
+  std::vector<int32_t> rp32(n + 1);
+  for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)rp[i];
+  CK(cudaMalloc((void**)&ctx->d_rp, sizeof(int) * (n + 1)));
+  CK(cudaMalloc((void**)&ctx->d_col, sizeof(int) * (nnz ? nnz : 1)));
+  CK(cudaMalloc((void**)&ctx->d_val, sizeof(double) * (nnz ? nnz : 1)));
+  CK(cudaMemcpy(ctx->d_rp, rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_col, ecol.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_val, val.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  ctx->n_global = n_global;
+  ctx->row_begin = row_begin;
+  ctx->row_end = row_end;
+  ctx->n = n;
+  ctx->nnz = nnz;
+  ctx->have_matrix = true;
+  return EKS_OK;
+}
+
+eks_status eks_solve(eks_ctx* ctx, eks_method method, int s, int t, double tol, const double* b, double* x,
+                     eks_mem where, int max_outer, eks_report* rep) {
+  eks_options o{};
+  o.max_outer = max_outer;
+  return eks_solve_ex(ctx, method, s, t, tol, b, x, where, &o, rep);
+}
+
+eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double tol, const double* b, double* x,
+                        eks_mem where, const eks_options* opt, eks_report* rep) {
+  ST(check_ready(ctx));
+  if (method < EKS_SRE_CG || method > EKS_MSDO_CG) return fail(ctx, EKS_ERR_INVALID_ARG, "unknown method");
+  if (s < 1 || !valid_t(t) || t > ctx->n_global) return fail(ctx, EKS_ERR_INVALID_ARG, "bad s=%d or t=%d", s, t);
+  if (!(tol >= 0.0)) return fail(ctx, EKS_ERR_INVALID_ARG, "tol must be >= 0");
+  if (!b || !x) return fail(ctx, EKS_ERR_INVALID_ARG, "NULL b or x");
+  if (t % ctx->nranks) return fail(ctx, EKS_ERR_INVALID_ARG, "t %% nranks != 0");
+  if (ctx->nranks > 1) {  // slab must be a union of domains (reading R1)
+    const int64_t dlo = (int64_t)(ctx->rank * (t / ctx->nranks)) * ctx->n_global / t;
+    const int64_t dhi = (int64_t)((ctx->rank + 1) * (t / ctx->nranks)) * ctx->n_global / t;
+    if (dlo != ctx->row_begin || dhi != ctx->row_end)
+      return fail(ctx, EKS_ERR_INVALID_ARG, "rank slab is not the union of its t/nranks domains");
+  }
+  const int kmax = (opt && opt->max_outer > 0) ? opt->max_outer : 5000;
+  begin_run(ctx, opt);
+  auto wall0 = std::chrono::steady_clock::now();
+  ST(ensure_workspace(ctx, t, s));
+  const int ring = (method == EKS_SRE_CG) ? 3 : 0;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, ctx->stream));
+  // r0 = b − A x0, ρ0 = ||r0||  (line 1 of Alg 3/4/6)
+  ST(copy_in(ctx, ctx->b, b, ctx->n, where));
+  ST(copy_in(ctx, ctx->xv.loc, x, ctx->n, where));
+  ST(residual(ctx, ctx->r, ctx->scal + 0));
+  ST(sync_scalars(ctx, 1));
+  const double rho0 = std::sqrt(ctx->h_scal[0]);
+  double rho = rho0;
+  ctx->hist.assign(1, rho0);
+  int k = 1, nblocks = 0, breakdown_block = -1, max_fit = -1;
+  eks_status status = EKS_OK;
+  // while (ρ > ε ρ0 and k < k_max)   (reading R7)
+  while (rho > tol * rho0 && k < kmax) {
+    ST(reset_flag(ctx));
+    for (int i = 0; i < s; ++i) {
+      Block *Wn = nullptr, *AWn = nullptr;
+      const int idx = ring ? nblocks % ring : nblocks;
+      eks_status as = slot(ctx, t, idx, &Wn, &AWn);
+      if (as == EKS_ERR_OOM) {
+        max_fit = nblocks / s;
+        status = EKS_ERR_OOM;
+        break;
+      }
+      ST(as);
+      const bool seed = (i == 0) && (method == EKS_MSDO_CG || k == 1);
+      const double* Zsrc = seed ? nullptr : ctx->AWpool[ring ? (nblocks - 1) % ring : nblocks - 1].loc;
+      const int mode = (i == 0 ? 1 : 0) | (i == s - 1 ? 2 : 0);
+      ST(make_block(ctx, t, method, ring, nblocks, seed, Zsrc, Wn, AWn, i * t, nblocks, mode));
+      ++nblocks;
+    }
+    if (status == EKS_ERR_OOM) break;
+    ST(reduce_scalar(ctx, ctx->scal + 1));
+    ST(sync_scalars(ctx, 2));
+    const int fl = ctx->h_flag[1];
+    if (fl != INT_MAX) {  // A-CholQR breakdown: x stays the last completed iterate
+      breakdown_block = fl;
+      status = EKS_ERR_BREAKDOWN;
+      break;
+    }
+    std::swap(ctx->r, ctx->rnew);  // r_k = r_{k-1} − A V α̃
+    rho = std::sqrt(ctx->h_scal[1]);
+    ctx->hist.push_back(rho);
+    ++k;
+    if (!std::isfinite(rho)) break;
+  }
+  // true residual at exit
+  ST(residual(ctx, nullptr, ctx->scal + 2));
+  {
+    KScope kk(ctx, EKS_K_OTHER);
+    CK(eks::launch_sumsq(ctx->stream, ctx->n, ctx->b, ctx->part, ctx->nblk));
+  }
+  ST(reduce_scalar(ctx, ctx->scal + 3));
+  ST(copy_out(ctx, x, ctx->xv.loc, ctx->n, where));
+  CK(cudaEventRecord(e1, ctx->stream));
+  ST(sync_scalars(ctx, 4));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  (void)wall0;
+  const bool converged = rho <= tol * rho0;
+  if (status == EKS_OK && !converged) status = EKS_ERR_MAXITER;
+  if (rep) {
+    rep->outer_iters = k - 1;
+    rep->converged = converged;
+    rep->breakdown_block = breakdown_block;
+    rep->max_outer_fit = (method == EKS_SRE_CG) ? -1 : max_fit;
+    rep->rho0 = rho0;
+    rep->rho = rho;
+    const double nb = std::sqrt(ctx->h_scal[3]);
+    rep->true_relres = nb > 0 ? std::sqrt(ctx->h_scal[2]) / nb : 0.0;
+    rep->solve_seconds = ms * 1e-3;
+    rep->model_bytes = ctx->model_bytes;
+    rep->model_flops = ctx->model_flops;
+    rep->gpu_launches = (int)ctx->launches;
+    rep->rho_history = ctx->hist.data();
+  }
+  if (status == EKS_ERR_OOM) return fail(ctx, EKS_ERR_OOM, "full basis Q exhausted device memory after %d outer iterations", max_fit);
+  if (status == EKS_ERR_BREAKDOWN) return fail(ctx, status, "A-CholQR breakdown in block %d", breakdown_block);
+  if (status == EKS_ERR_MAXITER) return fail(ctx, status, "k_max=%d reached, rho/rho0=%.3e", kmax, rho / rho0);
+  return EKS_OK;
+}
+
+eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks_total, const double* X0, double* W_last, eks_mem where,
+                           const eks_options* opt, eks_report* rep) {
+  ST(check_ready(ctx));
+  if (!valid_t(t) || nblocks_total < 1 || !X0 || !W_last || t % ctx->nranks)
+    return fail(ctx, EKS_ERR_INVALID_ARG, "bad basis-sweep arguments");
+  begin_run(ctx, opt);
+  ST(ensure_workspace(ctx, t, 1));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, ctx->stream));
+  ST(reset_flag(ctx));
+  const int ring = 3;
+  for (int j = 0; j < nblocks_total; ++j) {
+    Block *Wn = nullptr, *AWn = nullptr;
+    ST(slot(ctx, t, j % ring, &Wn, &AWn));
+    const double* Zsrc = nullptr;
+    if (j == 0) {
+      ST(copy_in(ctx, ctx->Zs.loc, X0, ctx->n * t, where));
+      Zsrc = ctx->Zs.loc;
+    } else {
+      Zsrc = ctx->AWpool[(j - 1) % ring].loc;
+    }
+    ST(make_block(ctx, t, EKS_SRE_CG, ring, j, false, Zsrc, Wn, AWn, 0, j, 4));
+  }
+  ST(copy_out(ctx, W_last, ctx->Wpool[(nblocks_total - 1) % ring].loc, ctx->n * t, where));
+  CK(cudaEventRecord(e1, ctx->stream));
+  ST(sync_scalars(ctx, 1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const int fl = ctx->h_flag[1];
+  if (rep) {
+    memset(rep, 0, sizeof *rep);
+    rep->outer_iters = nblocks_total;
+    rep->breakdown_block = fl == INT_MAX ? -1 : fl;
+    rep->max_outer_fit = -1;
+    rep->solve_seconds = ms * 1e-3;
+    rep->model_bytes = ctx->model_bytes;
+    rep->model_flops = ctx->model_flops;
+    rep->gpu_launches = (int)ctx->launches;
+  }
+  if (fl != INT_MAX) return fail(ctx, EKS_ERR_BREAKDOWN, "A-CholQR breakdown in block %d", fl);
+  return EKS_OK;
+}
+
+eks_status eks_get_profile(const eks_ctx* ctx, eks_profile* out) {
+  if (!ctx || !out) return EKS_ERR_INVALID_ARG;
+  *out = ctx->prof;
+  return EKS_OK;
+}
+
+eks_status eks_destroy(eks_ctx* ctx) {
+  if (!ctx) return EKS_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  free_workspace(ctx);
+  dfree(ctx->d_rp);
+  dfree(ctx->d_col);
+  dfree(ctx->d_val);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto& p : ctx->prof_pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+  if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
+  if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
+  if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
+  delete ctx;
+  return EKS_OK;
+}
+
+const char* eks_error_string(const eks_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
+
+// ============================================================================
+// Kernel-level ABI (include/eks_kernels.h)
+// ============================================================================
+static eks_status k_ready(eks_ctx* ctx, int t) {
+  ST(check_ready(ctx));
+  if (ctx->nranks != 1) return fail(ctx, EKS_ERR_INVALID_ARG, "kernel-level calls are single-rank");
+  if (!valid_t(t)) return fail(ctx, EKS_ERR_INVALID_ARG, "t=%d not in {1,2,4,...,64}", t);
+  begin_run(ctx, nullptr);
+  return ensure_workspace(ctx, t, 1);
+}
+
+eks_status eks_k_split(eks_ctx* ctx, int t, const double* r, double* Z) {
+  ST(k_ready(ctx, t));
+  CK(eks::launch_split(ctx->stream, t, ctx->n, ctx->row_begin, ctx->n_global, r, Z));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return EKS_OK;
+}
+
+eks_status eks_k_spmm(eks_ctx* ctx, int t, const double* X, double* Y, double* G, const double* v, double* g) {
+  ST(k_ready(ctx, t));
+  Block xb;
+  xb.base = const_cast<double*>(X);
+  xb.loc = xb.base;
+  ST(spmm(ctx, xb, Y, t));
+  if (G || g) {
+    const double* L[1] = {X};
+    ST(tn_reduce(ctx, t, 1, L, Y, g ? v : nullptr, ctx->Bg));
+    if (G) CK(cudaMemcpyAsync(G, ctx->Bg, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (g && v) CK(cudaMemcpyAsync(g, ctx->Bg + t * t, sizeof(double) * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return EKS_OK;
+}
+
+eks_status eks_k_cgs2(eks_ctx* ctx, int t, int nq, const double* const* Q, const double* const* AQ, double* Z,
+                      double* C1, double* C2) {
+  ST(k_ready(ctx, t));
+  if (nq < 1 || !Q || !AQ || !Z) return fail(ctx, EKS_ERR_INVALID_ARG, "bad cgs2 arguments");
+  std::vector<const double*> q(Q, Q + nq), aq(AQ, AQ + nq);
+  ST(cgs2(ctx, t, q, aq, Z, Z));
+  if (C1) CK(cudaMemcpyAsync(C1, ctx->C1, sizeof(double) * nq * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (C2) CK(cudaMemcpyAsync(C2, ctx->C2, sizeof(double) * nq * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return EKS_OK;
+}
+
+eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double* AW, double* R, double* B) {
+  ST(k_ready(ctx, t));
+  if (!Z || !W || !AW) return fail(ctx, EKS_ERR_INVALID_ARG, "NULL argument");
+  ST(reset_flag(ctx));
+  Block wb;
+  wb.base = W;
+  wb.loc = W;
+  if (W != Z) CK(cudaMemcpyAsync(W, Z, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  ST(spmm(ctx, wb, AW, t));
+  const double* L[1] = {W};
+  ST(tn_reduce(ctx, t, 1, L, AW, nullptr, ctx->Bg));
+  ST(chol(ctx, t, ctx->Bg, nullptr, ctx->Rm, ctx->Rinv, nullptr, 0));
+  CK(eks::launch_apply(ctx->stream, t, ctx->n, W, AW, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr,
+                       nullptr, nullptr, 4, ctx->nblk));
+  if (R) CK(cudaMemcpyAsync(R, ctx->Rm, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (B) CK(cudaMemcpyAsync(B, ctx->Bg, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  ST(sync_scalars(ctx, 1));
+  if (ctx->h_flag[1] != INT_MAX) return fail(ctx, EKS_ERR_BREAKDOWN, "A-CholQR breakdown");
+  return EKS_OK;
+}
+
+eks_status eks_k_chol(eks_ctx* ctx, int t, const double* B, double* R) {
+  ST(k_ready(ctx, t));
+  ST(reset_flag(ctx));
+  ST(chol(ctx, t, B, nullptr, R, ctx->Rinv, nullptr, 0));
+  ST(sync_scalars(ctx, 1));
+  if (ctx->h_flag[1] != INT_MAX) return fail(ctx, EKS_ERR_BREAKDOWN, "Cholesky breakdown");
+  return EKS_OK;
+}
+
+}  // extern "C"

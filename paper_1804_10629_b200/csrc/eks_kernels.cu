@@ -1,0 +1,629 @@
+// eks_kernels.cu — sm_100a CUDA kernels of the s-step enlarged CG hot path
+// (arXiv:1804.10629, Alg 3/4/6).  fp64 throughout (the paper's MATLAB precision).
+// Blocks are row-major n×T, T a power of two ≤ 64.  No fp64 atomics: every
+// reduction is a fixed-order two-stage tree (per-CTA partials, then
+// launch_reduce), so results are bitwise reproducible run to run.
+#include "eks_kernels.cuh"
+
+#include <climits>
+#include <cstdio>
+
+namespace eks {
+
+int sweep_ctas(int sms) { return 2 * sms; }
+
+#define EKS_DISPATCH_T(t, ...)                          \
+  switch (t) {                                          \
+    case 1: { constexpr int T = 1; __VA_ARGS__; } break;   \
+    case 2: { constexpr int T = 2; __VA_ARGS__; } break;   \
+    case 4: { constexpr int T = 4; __VA_ARGS__; } break;   \
+    case 8: { constexpr int T = 8; __VA_ARGS__; } break;   \
+    case 16: { constexpr int T = 16; __VA_ARGS__; } break; \
+    case 32: { constexpr int T = 32; __VA_ARGS__; } break; \
+    case 64: { constexpr int T = 64; __VA_ARGS__; } break; \
+    default: return cudaErrorInvalidValue;              \
+  }
+
+static inline int ilog2(int t) { int l = 0; while ((1 << l) < t) ++l; return l; }
+
+__device__ __forceinline__ int64_t chunk_lo(int64_t n, int b, int nb) { return (int64_t)b * n / nb; }
+
+// Sum a per-thread double over the CTA in a fixed order (warp shuffle tree, then warps in order).
+__device__ __forceinline__ double block_sum(double v, double* sbuf) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sbuf[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sbuf[i];
+  return s;
+}
+
+// ============================================================================
+// (a1) T(r) — P:41 ("T(r_0) … splits r_0 into t vectors").
+// ============================================================================
+__global__ void k_split(int t, int lt, int64_t n_local, int64_t row0, int64_t n_global,
+                        const double* __restrict__ r, double* __restrict__ Z) {
+  const int64_t total = n_local * t;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e >> lt;
+    const int c = (int)(e & (t - 1));
+    const int64_t g = row0 + i;
+    // D_c = [floor(c n / t), floor((c+1) n / t))  (reading R1); t is a power of two
+    const int64_t lo = ((int64_t)c * n_global) >> lt, hi = ((int64_t)(c + 1) * n_global) >> lt;
+    Z[e] = (g >= lo && g < hi) ? r[i] : 0.0;
+  }
+}
+
+cudaError_t launch_split(cudaStream_t st, int t, int64_t n_local, int64_t row0, int64_t n_global,
+                         const double* r, double* Z) {
+  if (n_local <= 0) return cudaSuccess;
+  int64_t total = n_local * t;
+  int blocks = (int)((total + kThreads - 1) / kThreads);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_split<<<blocks, kThreads, 0, st>>>(t, ilog2(t), n_local, row0, n_global, r, Z);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// (a2) SpMM Y = A·X — P:54.  G = T/2 threads per row, each
+// owning two consecutive columns (16-byte loads of the row-major X rows).
+// Accumulation: p ascending, fma, from 0.0 — bitwise equal to the oracle (R20).
+// ============================================================================
+template <int T>
+__global__ void __launch_bounds__(kThreads) k_spmm(int r0, int r1, const int* __restrict__ rp,
+                                                   const int* __restrict__ col,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ X, double* __restrict__ Y) {
+  constexpr int VEC = T >= 2 ? 2 : 1;
+  constexpr int G = T / VEC;
+  const int lane = threadIdx.x % G;
+  const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t i = r0 + grp; i < r1; i += ngrp) {
+    const int p0 = __ldg(rp + i), p1 = __ldg(rp + i + 1);
+    if constexpr (VEC == 2) {
+      double ax = 0.0, ay = 0.0;
+      for (int p = p0; p < p1; ++p) {
+        const double a = __ldg(val + p);
+        const int c = __ldg(col + p);
+        const double2 xv = __ldg(reinterpret_cast<const double2*>(X + (int64_t)c * T) + lane);
+        ax = __fma_rn(a, xv.x, ax);
+        ay = __fma_rn(a, xv.y, ay);
+      }
+      reinterpret_cast<double2*>(Y + i * T)[lane] = make_double2(ax, ay);
+    } else {
+      double ax = 0.0;
+      for (int p = p0; p < p1; ++p) ax = __fma_rn(__ldg(val + p), __ldg(X + __ldg(col + p)), ax);
+      Y[i] = ax;
+    }
+  }
+}
+
+cudaError_t launch_spmm(cudaStream_t st, int t, int r0, int r1, const int* rp, const int* col,
+                        const double* val, const double* Xext, double* Y, int sms) {
+  if (r1 <= r0) return cudaSuccess;
+  EKS_DISPATCH_T(t, {
+    constexpr int G = (T >= 2 ? T / 2 : 1);
+    int64_t threads = (int64_t)(r1 - r0) * G;
+    int64_t blocks = (threads + kThreads - 1) / kThreads;
+    int64_t cap = (int64_t)sms * 8;
+    if (blocks > cap) blocks = cap;
+    k_spmm<T><<<(int)blocks, kThreads, 0, st>>>(r0, r1, rp, col, val, Xext, Y);
+  });
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Tall-skinny Lᵀ·R partial products (CGS2 coefficients, Gram matrices).
+// Each CTA owns a contiguous row chunk, streams TR-row tiles of R and of up to
+// GL left blocks through shared memory, and accumulates a TA×TA register tile
+// per thread; KS row slices are summed in a fixed order at the end.
+// ============================================================================
+constexpr int kMaxList = 32;
+struct PtrList { const double* p[kMaxList]; };
+
+template <int T>
+struct TnCfg {
+  static constexpr int TA = T >= 64 ? 8 : (T >= 16 ? 4 : (T >= 2 ? 2 : 1));
+  static constexpr int NA = T / TA;
+  static constexpr int TPS = NA * NA;
+  static constexpr int KS = kThreads / TPS;
+  static constexpr int TR = KS > 32 ? KS : 32;
+  static constexpr int ACC = TA * TA;
+  static constexpr int TILE = TR * T;  // doubles per tile
+  static constexpr int GLa = ACC >= 32 ? 1 : 32 / ACC;
+  static constexpr int GLb = (32768 / (TILE * 8)) > 0 ? 32768 / (TILE * 8) : 1;
+  static constexpr int GL = GLa < GLb ? GLa : GLb;
+};
+
+size_t tn_partials_stride(int t, int nl, bool has_v) { return (size_t)nl * t * t + (has_v ? t : 0); }
+
+template <int T>
+__device__ __forceinline__ void load_tile(double* __restrict__ s, const double* __restrict__ g,
+                                          int64_t row, int64_t rows_avail, int TR) {
+  // copy rows [row, row+TR) (only the first rows_avail exist) of a row-major n×T block
+  const int nvalid = (int)(rows_avail < TR ? (rows_avail > 0 ? rows_avail : 0) : TR);
+  if constexpr (T >= 2) {
+    const double2* src = reinterpret_cast<const double2*>(g + row * T);
+    double2* dst = reinterpret_cast<double2*>(s);
+    const int nv = nvalid * T / 2, ntot = TR * T / 2;
+    for (int e = threadIdx.x; e < ntot; e += blockDim.x)
+      dst[e] = e < nv ? __ldg(src + e) : make_double2(0.0, 0.0);
+  } else {
+    for (int e = threadIdx.x; e < TR; e += blockDim.x) s[e] = e < nvalid ? __ldg(g + row + e) : 0.0;
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(kThreads) k_tn_partials(int64_t n, int nl, PtrList L, const double* __restrict__ R,
+                                                          const double* __restrict__ v, double* __restrict__ part,
+                                                          size_t stride, int j0) {
+  using C = TnCfg<T>;
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x;
+  const int ks = tid / C::TPS, tin = tid % C::TPS;
+  const int ia = tin / C::NA, ib = tin % C::NA;
+  const int64_t lo = chunk_lo(n, blockIdx.x, gridDim.x), hi = chunk_lo(n, blockIdx.x + 1, gridDim.x);
+  double* sR = smem;
+  double* sL = smem + C::TILE;
+  double* sV = sL + C::GL * C::TILE;  // TR doubles (only if v)
+  const bool has_v = v != nullptr;
+  double* outb = part + (size_t)blockIdx.x * stride;
+
+  for (int g0 = 0; g0 < nl; g0 += C::GL) {
+    const int gn = (nl - g0) < C::GL ? (nl - g0) : C::GL;
+    const bool vhere = has_v && g0 == 0;
+    double acc[C::GL][C::TA][C::TA];
+    double accv[C::TA];
+#pragma unroll
+    for (int j = 0; j < C::GL; ++j)
+#pragma unroll
+      for (int x = 0; x < C::TA; ++x)
+#pragma unroll
+        for (int y = 0; y < C::TA; ++y) acc[j][x][y] = 0.0;
+#pragma unroll
+    for (int x = 0; x < C::TA; ++x) accv[x] = 0.0;
+
+    for (int64_t row = lo; row < hi; row += C::TR) {
+      const int64_t avail = hi - row;
+      load_tile<T>(sR, R, row, avail, C::TR);
+      for (int j = 0; j < gn; ++j) load_tile<T>(sL + j * C::TILE, L.p[g0 + j], row, avail, C::TR);
+      if (vhere)
+        for (int e = tid; e < C::TR; e += blockDim.x) sV[e] = e < avail ? __ldg(v + row + e) : 0.0;
+      __syncthreads();
+      for (int rr = ks; rr < C::TR; rr += C::KS) {
+        double rv[C::TA];
+#pragma unroll
+        for (int y = 0; y < C::TA; ++y) rv[y] = sR[rr * T + ib * C::TA + y];
+#pragma unroll
+        for (int j = 0; j < C::GL; ++j) {
+          if (j < gn) {
+            double lv[C::TA];
+#pragma unroll
+            for (int x = 0; x < C::TA; ++x) lv[x] = sL[j * C::TILE + rr * T + ia * C::TA + x];
+#pragma unroll
+            for (int x = 0; x < C::TA; ++x)
+#pragma unroll
+              for (int y = 0; y < C::TA; ++y) acc[j][x][y] = __fma_rn(lv[x], rv[y], acc[j][x][y]);
+            if (j == 0 && vhere && ib == 0) {
+              const double vv = sV[rr];
+#pragma unroll
+              for (int x = 0; x < C::TA; ++x) accv[x] = __fma_rn(lv[x], vv, accv[x]);
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // fixed-order reduction of the KS slices through shared memory; block j of
+    // this group lands at (g0+j)*T*T, the v part (only with nl == 1) at nl*T*T.
+    const int per = gn * T * T + (vhere ? T : 0);
+    const int RB = (4160 / per) > 0 ? 4160 / per : 1;
+    double* sred = smem;  // reuse of the tile area (>= 4160 doubles, see tn_smem_bytes)
+    for (int c0 = 0; c0 < C::KS; c0 += RB) {
+      if (ks >= c0 && ks < c0 + RB) {
+        double* dst = sred + (size_t)(ks - c0) * per;
+#pragma unroll
+        for (int j = 0; j < C::GL; ++j)
+          if (j < gn)
+#pragma unroll
+            for (int x = 0; x < C::TA; ++x)
+#pragma unroll
+              for (int y = 0; y < C::TA; ++y) dst[j * T * T + (ia * C::TA + x) * T + ib * C::TA + y] = acc[j][x][y];
+        if (vhere && ib == 0)
+#pragma unroll
+          for (int x = 0; x < C::TA; ++x) dst[gn * T * T + ia * C::TA + x] = accv[x];
+      }
+      __syncthreads();
+      const int nk = (C::KS - c0) < RB ? (C::KS - c0) : RB;
+      for (int e = tid; e < per; e += blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < nk; ++k) s += sred[(size_t)k * per + e];
+        const size_t o = e < gn * T * T ? (size_t)g0 * T * T + e : (size_t)nl * T * T + (e - gn * T * T);
+        if (c0 == 0) outb[o] = s; else outb[o] += s;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <int T>
+static size_t tn_smem_bytes() {
+  using C = TnCfg<T>;
+  size_t tiles = (size_t)(1 + C::GL) * C::TILE * 8 + (size_t)C::TR * 8;
+  size_t red = 4160 * 8;
+  return tiles > red ? tiles : red;
+}
+
+cudaError_t launch_tn_partials(cudaStream_t st, int t, int64_t n, int nl, const double* const* Lhost,
+                               const double* R, const double* v, double* part, int nblk) {
+  if (nl <= 0) return cudaSuccess;
+  if (v != nullptr && nl != 1) return cudaErrorInvalidValue;  // v only with a single left block
+  const size_t stride = tn_partials_stride(t, nl, v != nullptr);
+  for (int j0 = 0; j0 < nl; j0 += kMaxList) {
+    const int cnt = (nl - j0) < kMaxList ? (nl - j0) : kMaxList;
+    PtrList pl{};
+    for (int j = 0; j < cnt; ++j) pl.p[j] = Lhost[j0 + j];
+    // partial layout per CTA: [nl][T][T] then [T] (v); this launch writes blocks j0..j0+cnt-1
+    EKS_DISPATCH_T(t, {
+      size_t sm = tn_smem_bytes<T>();
+      cudaFuncSetAttribute(k_tn_partials<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      // offset the partial pointer so that block j0 lands at j0; v part only with j0 == 0
+      k_tn_partials<T><<<nblk, kThreads, sm, st>>>(n, cnt, pl, R, j0 == 0 ? v : nullptr,
+                                                   part + (size_t)j0 * T * T, stride, 0);
+    });
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// ============================================================================
+// Fixed-order reduction of per-CTA partials.
+// ============================================================================
+__global__ void k_reduce(const double* __restrict__ part, int nblk, size_t stride, size_t count,
+                         double* __restrict__ out) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += part[(size_t)b * stride + e];
+    out[e] = s;
+  }
+}
+
+cudaError_t launch_reduce(cudaStream_t st, const double* part, int nblk, size_t stride, size_t count,
+                          double* out) {
+  if (count == 0) return cudaSuccess;
+  int blocks = (int)((count + 127) / 128);
+  if (blocks > 1024) blocks = 1024;
+  k_reduce<<<blocks, 128, 0, st>>>(part, nblk, stride, count, out);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// CGS update Zout = Zin − Σ_j Q_j C_j.  Each thread owns CPT
+// consecutive columns of RPT rows of a TRU-row tile; Q_j tiles and the C_j
+// blocks are staged in shared memory.
+// ============================================================================
+template <int T>
+struct UpCfg {
+  static constexpr int CPT = T >= 64 ? 8 : (T == 32 ? 4 : (T == 16 ? 2 : 1));
+  static constexpr int TPR = T / CPT;                 // threads per row
+  static constexpr int RPP = kThreads / TPR;          // rows per pass
+  static constexpr int TRU = T >= 64 ? 64 : RPP;      // rows per tile
+  static constexpr int RPT = TRU / RPP;               // rows per thread
+  static constexpr int CJ = (49152 / (T * T * 8)) < kMaxList ? (49152 / (T * T * 8)) : kMaxList;
+};
+
+template <int T>
+__global__ void __launch_bounds__(kThreads) k_ts_update(int64_t n, int nq, PtrList Q, const double* __restrict__ Cm,
+                                                        const double* Zin, double* Zout) {
+  using U = UpCfg<T>;
+  extern __shared__ double smem[];
+  double* sQ = smem;                 // TRU*T
+  double* sC = smem + U::TRU * T;    // CJ*T*T
+  const int tid = threadIdx.x;
+  const int rloc = tid / U::TPR, c0 = (tid % U::TPR) * U::CPT;
+  const int64_t lo = chunk_lo(n, blockIdx.x, gridDim.x), hi = chunk_lo(n, blockIdx.x + 1, gridDim.x);
+  const int nchunk = (nq + U::CJ - 1) / U::CJ;
+  if (nchunk == 1) {
+    for (int e = tid; e < nq * T * T; e += blockDim.x) sC[e] = Cm[e];
+    __syncthreads();
+  }
+  for (int64_t row = lo; row < hi; row += U::TRU) {
+    const int64_t avail = hi - row;
+    double acc[U::RPT][U::CPT];
+#pragma unroll
+    for (int q = 0; q < U::RPT; ++q)
+#pragma unroll
+      for (int c = 0; c < U::CPT; ++c) acc[q][c] = 0.0;
+    for (int ch = 0; ch < nchunk; ++ch) {
+      const int jb = ch * U::CJ, je = (jb + U::CJ) < nq ? jb + U::CJ : nq;
+      if (nchunk > 1) {
+        __syncthreads();
+        for (int e = tid; e < (je - jb) * T * T; e += blockDim.x) sC[e] = Cm[(size_t)jb * T * T + e];
+      }
+      for (int j = jb; j < je; ++j) {
+        __syncthreads();
+        load_tile<T>(sQ, Q.p[j], row, avail, U::TRU);
+        __syncthreads();
+        const double* Cj = sC + (size_t)(j - jb) * T * T;
+#pragma unroll
+        for (int q = 0; q < U::RPT; ++q) {
+          const int rr = rloc + q * U::RPP;
+#pragma unroll 4
+          for (int a = 0; a < T; ++a) {
+            const double qa = sQ[rr * T + a];
+#pragma unroll
+            for (int c = 0; c < U::CPT; ++c) acc[q][c] = __fma_rn(qa, Cj[a * T + c0 + c], acc[q][c]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < U::RPT; ++q) {
+      const int64_t r = row + rloc + q * U::RPP;
+      if (r < hi) {
+#pragma unroll
+        for (int c = 0; c < U::CPT; ++c) Zout[r * T + c0 + c] = Zin[r * T + c0 + c] - acc[q][c];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_ts_update(cudaStream_t st, int t, int64_t n, int nq, const double* const* Qhost,
+                             const double* C, const double* Zin, double* Zout, int nblk) {
+  if (nq <= 0) {
+    if (Zin != Zout) return cudaMemcpyAsync(Zout, Zin, sizeof(double) * n * t, cudaMemcpyDeviceToDevice, st);
+    return cudaSuccess;
+  }
+  for (int j0 = 0; j0 < nq; j0 += kMaxList) {
+    const int cnt = (nq - j0) < kMaxList ? (nq - j0) : kMaxList;
+    PtrList pl{};
+    for (int j = 0; j < cnt; ++j) pl.p[j] = Qhost[j0 + j];
+    EKS_DISPATCH_T(t, {
+      using U = UpCfg<T>;
+      size_t sm = (size_t)(U::TRU * T + U::CJ * T * T) * 8;
+      cudaFuncSetAttribute(k_ts_update<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_ts_update<T><<<nblk, kThreads, sm, st>>>(n, cnt, pl, C + (size_t)j0 * T * T, j0 == 0 ? Zin : Zout, Zout);
+    });
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// ============================================================================
+// Small Cholesky B = RᵀR (A-CholQR), explicit R⁻¹, alpha = R⁻ᵀ g.
+// Same loop order as the oracle, no fma (__dmul_rn/__dsub_rn) — bitwise equal
+// R for equal B (reading R20).  Breakdown rule: pivot <= t·2^-52·max|B| (R6).
+// ============================================================================
+template <int T>
+__global__ void k_chol(const double* __restrict__ B, const double* __restrict__ g, double* __restrict__ Rout,
+                       double* __restrict__ Rinv, double* __restrict__ alpha, int* flag, int gblock) {
+  extern __shared__ double csm[];
+  double(*sB)[T + 1] = reinterpret_cast<double(*)[T + 1]>(csm);
+  double(*sR)[T + 1] = reinterpret_cast<double(*)[T + 1]>(csm + T * (T + 1));
+  double(*sRi)[T + 1] = reinterpret_cast<double(*)[T + 1]>(csm + 2 * T * (T + 1));
+  __shared__ double sred[32];
+  __shared__ int sfail;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < T * T; e += blockDim.x) {
+    sB[e / T][e % T] = B[e];
+    sR[e / T][e % T] = 0.0;
+    sRi[e / T][e % T] = 0.0;
+  }
+  if (tid == 0) sfail = 0;
+  __syncthreads();
+  double m = 0.0;
+  for (int e = tid; e < T * T; e += blockDim.x) {
+    const int i = e / T, j = e % T;
+    if (j >= i) m = fmax(m, fabs(sB[i][j]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((tid & 31) == 0) sred[tid >> 5] = m;
+  __syncthreads();
+  if (tid == 0) {
+    double bm = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) bm = fmax(bm, sred[w]);
+    sred[0] = bm;
+  }
+  __syncthreads();
+  const double thr = __dmul_rn((double)T * 0x1p-52, sred[0]);
+  for (int k = 0; k < T; ++k) {
+    if (tid == 0) {
+      double d = sB[k][k];
+      for (int i = 0; i < k; ++i) d = __dsub_rn(d, __dmul_rn(sR[i][k], sR[i][k]));
+      if (!(d > thr)) sfail = 1;
+      sR[k][k] = __dsqrt_rn(d);
+    }
+    __syncthreads();
+    const double rkk = sR[k][k];
+    for (int j = k + 1 + tid; j < T; j += blockDim.x) {
+      double v = sB[k][j];
+      for (int i = 0; i < k; ++i) v = __dsub_rn(v, __dmul_rn(sR[i][k], sR[i][j]));
+      sR[k][j] = __ddiv_rn(v, rkk);
+    }
+    __syncthreads();
+  }
+  // R⁻¹ column by column (upper triangular back substitution)
+  for (int j = tid; j < T; j += blockDim.x) {
+    sRi[j][j] = __ddiv_rn(1.0, sR[j][j]);
+    for (int i = j - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int l = i + 1; l <= j; ++l) s = __fma_rn(sR[i][l], sRi[l][j], s);
+      sRi[i][j] = -__ddiv_rn(s, sR[i][i]);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < T * T; e += blockDim.x) {
+    if (Rout) Rout[e] = sR[e / T][e % T];
+    Rinv[e] = sRi[e / T][e % T];
+  }
+  if (tid == 0) {
+    if (g != nullptr && alpha != nullptr) {
+      double a[T];
+      for (int j = 0; j < T; ++j) {
+        double v = g[j];
+        for (int i = 0; i < j; ++i) v = __dsub_rn(v, __dmul_rn(sR[i][j], a[i]));
+        a[j] = __ddiv_rn(v, sR[j][j]);
+        alpha[j] = a[j];
+      }
+    }
+    if (sfail && flag) atomicMin(flag, gblock);
+  }
+}
+
+cudaError_t launch_chol(cudaStream_t st, int t, const double* B, const double* g, double* R, double* Rinv,
+                        double* alpha, int* flag, int gblock) {
+  EKS_DISPATCH_T(t, {
+    const size_t sm = (size_t)3 * T * (T + 1) * 8;
+    cudaFuncSetAttribute(k_chol<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_chol<T><<<1, 64, sm, st>>>(B, g, R, Rinv, alpha, flag, gblock);
+  });
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Apply R⁻¹ and the x/r update of this block (P:159-161 / P:189-191 / P:340-342,
+// α̃_b = R⁻ᵀ(Z2ᵀ r_{k-1}) so that α̃ = Vᵀ r_{k-1} blockwise).
+// ============================================================================
+template <int T>
+__global__ void __launch_bounds__(kThreads) k_apply(int64_t n, double* __restrict__ Z2W, double* __restrict__ AZ2AW,
+                                                    const double* __restrict__ Rinv, const double* __restrict__ alpha,
+                                                    double* __restrict__ x, double* __restrict__ dx,
+                                                    const double* __restrict__ r, double* __restrict__ rnew,
+                                                    double* __restrict__ rho_part, const int* __restrict__ flag,
+                                                    int mode) {
+  using U = UpCfg<T>;
+  extern __shared__ double smem[];
+  double* sRi = smem;               // T*T
+  double* sA = sRi + T * T;         // T
+  double* sZ = sA + T;              // TRU*T
+  double* sY = sZ + U::TRU * T;     // TRU*T
+  __shared__ double sred[32];
+  const int tid = threadIdx.x;
+  const int rloc = tid / U::TPR, c0 = (tid % U::TPR) * U::CPT;
+  const int64_t lo = chunk_lo(n, blockIdx.x, gridDim.x), hi = chunk_lo(n, blockIdx.x + 1, gridDim.x);
+  const bool first = mode & 1, last = mode & 2, basis = mode & 4;
+  const bool skip = basis || (flag != nullptr && *flag != INT_MAX);
+  for (int e = tid; e < T * T; e += blockDim.x) sRi[e] = Rinv[e];
+  for (int e = tid; e < T; e += blockDim.x) sA[e] = alpha ? alpha[e] : 0.0;
+  double rr_acc = 0.0;
+  __syncthreads();
+  for (int64_t row = lo; row < hi; row += U::TRU) {
+    const int64_t avail = hi - row;
+    load_tile<T>(sZ, Z2W, row, avail, U::TRU);
+    load_tile<T>(sY, AZ2AW, row, avail, U::TRU);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < U::RPT; ++q) {
+      const int rr = rloc + q * U::RPP;
+      const int64_t rg = row + rr;
+      double w[U::CPT], aw[U::CPT];
+#pragma unroll
+      for (int c = 0; c < U::CPT; ++c) { w[c] = 0.0; aw[c] = 0.0; }
+      for (int a = 0; a < c0 + U::CPT; ++a) {
+        const double za = sZ[rr * T + a], ya = sY[rr * T + a];
+#pragma unroll
+        for (int c = 0; c < U::CPT; ++c) {
+          const double ri = sRi[a * T + c0 + c];
+          w[c] = __fma_rn(za, ri, w[c]);
+          aw[c] = __fma_rn(ya, ri, aw[c]);
+        }
+      }
+      double u = 0.0, qv = 0.0;
+#pragma unroll
+      for (int c = 0; c < U::CPT; ++c) {
+        u = __fma_rn(w[c], sA[c0 + c], u);
+        qv = __fma_rn(aw[c], sA[c0 + c], qv);
+      }
+      // fixed-order sum over the TPR threads of the row (consecutive lanes)
+#pragma unroll
+      for (int o = U::TPR / 2; o > 0; o >>= 1) {
+        u += __shfl_down_sync(0xffffffffu, u, o, U::TPR);
+        qv += __shfl_down_sync(0xffffffffu, qv, o, U::TPR);
+      }
+      if (rg < hi) {
+#pragma unroll
+        for (int c = 0; c < U::CPT; ++c) {
+          Z2W[rg * T + c0 + c] = w[c];
+          AZ2AW[rg * T + c0 + c] = aw[c];
+        }
+        if (!skip && (tid % U::TPR) == 0) {
+          double dxi = first ? u : dx[rg] + u;
+          double rn = first ? r[rg] - qv : rnew[rg] - qv;
+          rnew[rg] = rn;
+          if (last) {
+            x[rg] += dxi;
+            rr_acc = __fma_rn(rn, rn, rr_acc);
+          } else {
+            dx[rg] = dxi;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (last && rho_part != nullptr) {
+    double s = block_sum(rr_acc, sred);
+    if (tid == 0) rho_part[blockIdx.x] = s;
+  }
+}
+
+cudaError_t launch_apply(cudaStream_t st, int t, int64_t n, double* Z2W, double* AZ2AW, const double* Rinv,
+                         const double* alpha, double* x, double* dx, const double* r, double* rnew,
+                         double* rho_part, const int* flag, int mode, int nblk) {
+  EKS_DISPATCH_T(t, {
+    using U = UpCfg<T>;
+    size_t sm = (size_t)(T * T + T + 2 * U::TRU * T) * 8;
+    cudaFuncSetAttribute(k_apply<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_apply<T><<<nblk, kThreads, sm, st>>>(n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, rho_part, flag, mode);
+  });
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Vector kernels
+// ============================================================================
+__global__ void k_residual(int64_t n, const double* __restrict__ b, const double* __restrict__ y,
+                           double* __restrict__ r, double* __restrict__ part) {
+  __shared__ double sred[32];
+  const int64_t lo = chunk_lo(n, blockIdx.x, gridDim.x), hi = chunk_lo(n, blockIdx.x + 1, gridDim.x);
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const double v = b[i] - y[i];
+    if (r) r[i] = v;
+    acc = __fma_rn(v, v, acc);
+  }
+  const double s = block_sum(acc, sred);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+cudaError_t launch_residual(cudaStream_t st, int64_t n, const double* b, const double* y, double* r,
+                            double* part, int nblk) {
+  k_residual<<<nblk, kThreads, 0, st>>>(n, b, y, r, part);
+  return cudaGetLastError();
+}
+
+__global__ void k_sumsq(int64_t n, const double* __restrict__ v, double* __restrict__ part) {
+  __shared__ double sred[32];
+  const int64_t lo = chunk_lo(n, blockIdx.x, gridDim.x), hi = chunk_lo(n, blockIdx.x + 1, gridDim.x);
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc = __fma_rn(v[i], v[i], acc);
+  const double s = block_sum(acc, sred);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+cudaError_t launch_sumsq(cudaStream_t st, int64_t n, const double* v, double* part, int nblk) {
+  k_sumsq<<<nblk, kThreads, 0, st>>>(n, v, part);
+  return cudaGetLastError();
+}
+
+}  // namespace eks

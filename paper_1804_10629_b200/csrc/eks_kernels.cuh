@@ -1,0 +1,68 @@
+// eks_kernels.cuh — launch wrappers for the sm_100a kernels of the s-step
+// enlarged CG hot path (kernels in eks_kernels.cu).  All blocks are row-major
+// n×T fp64; T ∈ {1,2,4,8,16,32,64}.  Every wrapper returns the cudaError_t of
+// its launch.  Citations: PAPER.md line numbers "P:<line>".
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace eks {
+
+constexpr int kThreads = 256;
+
+// Number of CTAs of the persistent row-sweep kernels (fixed per device so that
+// every fixed-order reduction is deterministic run to run).
+int sweep_ctas(int sms);
+
+// ---- (a1) T(r) — P:41: Z[i][d(i)] = r[i], zeros elsewhere, with
+// d(i) = floor(((i_global+1) t - 1) / n_global) (reading R1).
+cudaError_t launch_split(cudaStream_t st, int t, int64_t n_local, int64_t row0, int64_t n_global,
+                         const double* r, double* Z);
+
+// ---- (a2) SpMM Y = A·X ("W_k = AW_{k-1}") over local rows [r0, r1):
+// CSR int32 row_ptr/col (col indexes the extended X with halo rows), fp64 val;
+// ascending-p fma accumulation from 0.0 (bitwise equal to the oracle, R20).
+cudaError_t launch_spmm(cudaStream_t st, int t, int r0, int r1, const int* rp, const int* col,
+                        const double* val, const double* Xext, double* Y, int sms);
+
+// ---- partials of Lᵀ R (nl left blocks, each n×t) and optionally L_0ᵀ v:
+// part[b][j][a][c] for CTA b (nblk CTAs, contiguous row chunks).  Used for the
+// CGS2 coefficients (AQ)ᵀZ (reading R24) and the Gram Z2ᵀ(AZ2)
+// (A-CholQR) with Z2ᵀ r (α̃).
+cudaError_t launch_tn_partials(cudaStream_t st, int t, int64_t n, int nl, const double* const* Ldev,
+                               const double* R, const double* v, double* part, int nblk);
+size_t tn_partials_stride(int t, int nl, bool has_v);  // doubles per CTA
+
+// ---- fixed-order reduction out[e] = Σ_b part[b*stride + e], e < count.
+cudaError_t launch_reduce(cudaStream_t st, const double* part, int nblk, size_t stride, size_t count,
+                          double* out);
+
+// ---- CGS update Zout = Zin − Σ_j Q_j C_j  (Z − Q·C; reading R3).
+// C is (nq·t)×t row-major (block j = rows j·t..j·t+t-1).  Zout may alias Zin.
+cudaError_t launch_ts_update(cudaStream_t st, int t, int64_t n, int nq, const double* const* Qdev,
+                             const double* C, const double* Zin, double* Zout, int nblk);
+
+// ---- small Cholesky + inverse (A-CholQR; reading R4/R6), one CTA:
+// B (t×t, upper read) = RᵀR; Rinv = R⁻¹; alpha = R⁻ᵀ g (if g != nullptr);
+// breakdown: atomicMin(flag, gblock) when a pivot <= t·2^-52·max|B|.
+cudaError_t launch_chol(cudaStream_t st, int t, const double* B, const double* g, double* R,
+                        double* Rinv, double* alpha, int* flag, int gblock);
+
+// ---- apply R⁻¹ and the update (fused per block):
+// W = Z2·Rinv, AW = AZ2·Rinv in place; u = W·alpha, q = AW·alpha;
+// mode bit0 (first block): dx = u, rnew = r − q; else dx += u, rnew −= q;
+// mode bit1 (last block): x += dx (+u) and partial ‖rnew‖² per CTA into rho_part —
+// skipped when *flag != INT_MAX (breakdown in this outer iteration).
+// mode bit2 (basis only): no update at all.
+cudaError_t launch_apply(cudaStream_t st, int t, int64_t n, double* Z2W, double* AZ2AW, const double* Rinv,
+                         const double* alpha, double* x, double* dx, const double* r, double* rnew,
+                         double* rho_part, const int* flag, int mode, int nblk);
+
+// ---- vector kernels
+// out = b − Ax (y holds A·x): r = b − y; partial Σ r² per CTA
+cudaError_t launch_residual(cudaStream_t st, int64_t n, const double* b, const double* y, double* r,
+                            double* part, int nblk);
+// partial Σ v² per CTA
+cudaError_t launch_sumsq(cudaStream_t st, int64_t n, const double* v, double* part, int nblk);
+
+}  // namespace eks

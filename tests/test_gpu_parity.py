@@ -1,0 +1,291 @@
+"""GPU parity: every step of the hot path, called through the C ABI of libeks.so,
+against the oracle on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star):
+* T(r), SpMM: bitwise (same fma order, reading R20); Cholesky factor R: bitwise for equal B.
+* Gram / CGS2 / CholQR outputs: normwise relative 1e-12 (CGS2 pass-2 coefficients
+  normalised by ||AQ||_F ||Z||_F, reading R25).
+* End to end: both reach relres <= 1e-8, outer iterations within max(5%, 1), x within 1e-6.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import eks_inputs as ei
+
+pytestmark = pytest.mark.gpu
+
+TS = [1, 2, 4, 8, 16, 32, 64]
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def eks(torch_cuda):
+    from paper_1804_10629_b200 import build
+    build.build()
+    import paper_1804_10629_b200 as m
+    return m
+
+
+def dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+# ------------------------------------------------------------------ operators used below
+def op_2d_bands(N=37):  # ragged n (not a multiple of any tile), jump coefficients
+    return ei.stencil_csr(N, N, ndim=2, kappa=ei.bands_kappa(N, band=4))
+
+
+# ------------------------------------------------------------------ (a1) split
+@pytest.mark.parametrize("t", TS)
+@pytest.mark.parametrize("n", [1000, 4096, 12345])
+def test_split_bitwise(eks, torch_cuda, oracle_lib, t, n):
+    torch = torch_cuda
+    A = ei.poisson2d(int(math.isqrt(n)))
+    if A.n != n:
+        A = ei.stencil_csr(n, 1, ndim=2)  # 1D chain of length n
+    s = eks.Solver(A)
+    r = ei.uniform_pm1(3, A.n)
+    Z = torch.empty(A.n, t, dtype=torch.float64, device="cuda")
+    eks.eks_k_split(s.ctx, t, dev(torch, r), Z)
+    assert np.array_equal(host(Z), oracle_lib.split(r, t))
+    s.close()
+
+
+# ------------------------------------------------------------------ (a2) SpMM + Gram
+@pytest.mark.parametrize("t", TS)
+@pytest.mark.parametrize("opname", ["poisson64", "bands37", "aniso13"])
+def test_spmm_bitwise_and_gram(eks, torch_cuda, oracle_lib, t, opname):
+    torch = torch_cuda
+    A = {"poisson64": lambda: ei.poisson2d(64), "bands37": op_2d_bands,
+         "aniso13": lambda: ei.stencil_csr(13, 13, 13, ndim=3, scale=(1.0, 1.0, 1e-2))}[opname]()
+    s = eks.Solver(A)
+    X = ei.uniform_pm1(5, A.n * t).reshape(A.n, t)
+    v = ei.uniform_pm1(6, A.n)
+    Y = torch.empty(A.n, t, dtype=torch.float64, device="cuda")
+    G = torch.empty(t, t, dtype=torch.float64, device="cuda")
+    g = torch.empty(t, dtype=torch.float64, device="cuda")
+    eks.eks_k_spmm(s.ctx, t, dev(torch, X), Y, G, dev(torch, v), g)
+    Yo = oracle_lib.spmm(A, X)
+    assert np.array_equal(host(Y), Yo)                     # bitwise (R20)
+    assert rel(host(G), oracle_lib.xty(X, Yo)) <= 1e-12    # Gram XᵀAX
+    assert rel(host(g), oracle_lib.xty(X, v[:, None])[:, 0]) <= 1e-12
+    s.close()
+
+
+# ------------------------------------------------------------------ (a4) Cholesky
+@pytest.mark.parametrize("t", TS)
+def test_chol_bitwise(eks, torch_cuda, oracle_lib, t):
+    torch = torch_cuda
+    A = ei.poisson2d(16)
+    s = eks.Solver(A)
+    Gm = ei.uniform_pm1(40 + t, t * t).reshape(t, t)
+    B = Gm @ Gm.T + 0.1 * np.eye(t)
+    R = torch.empty(t, t, dtype=torch.float64, device="cuda")
+    st = eks.eks_k_chol(s.ctx, t, dev(torch, B), R)
+    so, Ro = oracle_lib.chol(B)
+    assert st == 0 and so == 0
+    assert np.array_equal(np.triu(host(R)), Ro)
+    # breakdown on a singular Gram (duplicate columns)
+    if t >= 2:
+        v = ei.uniform_pm1(1, t)
+        Bs = np.outer(v, v)
+        assert eks.eks_k_chol(s.ctx, t, dev(torch, Bs), R) == eks.EKS_ERR_BREAKDOWN
+        assert oracle_lib.chol(Bs)[0] == oracle_lib.BREAKDOWN
+    s.close()
+
+
+# ------------------------------------------------------------------ (a3) CGS2 and (a4) A-CholQR
+@pytest.mark.parametrize("t", [1, 4, 16, 32, 64])
+@pytest.mark.parametrize("nq", [1, 2, 5])
+def test_cgs2_and_acholqr_parity(eks, torch_cuda, oracle_lib, t, nq):
+    torch = torch_cuda
+    A = op_2d_bands(41)
+    n = A.n
+    s = eks.Solver(A)
+    # build an A-orthonormal window with the oracle, so both sides see identical Q
+    Qs, AQs = [], []
+    for j in range(nq):
+        Z0 = ei.uniform_pm1(100 + j, n * t).reshape(n, t)
+        if Qs:
+            Z0, _, _ = oracle_lib.cgs2(A, Z0, Qs)
+        st, W, R, B = oracle_lib.acholqr(A, Z0)
+        assert st == 0
+        Qs.append(W)
+        AQs.append(oracle_lib.spmm(A, W))
+    Z = ei.uniform_pm1(7, n * t).reshape(n, t)
+    Zo, C1o, C2o = oracle_lib.cgs2(A, Z, Qs)
+    Zd = dev(torch, Z)
+    C1 = torch.empty(nq * t, t, dtype=torch.float64, device="cuda")
+    C2 = torch.empty(nq * t, t, dtype=torch.float64, device="cuda")
+    eks.eks_k_cgs2(s.ctx, t, [dev(torch, q) for q in Qs], [dev(torch, q) for q in AQs], Zd, C1, C2)
+    assert rel(host(Zd), Zo) <= 1e-12
+    assert rel(host(C1), C1o) <= 1e-12
+    scale = math.sqrt(sum(np.linalg.norm(q) ** 2 for q in AQs)) * np.linalg.norm(Z)
+    assert np.linalg.norm(host(C2) - C2o) <= 1e-12 * scale       # reading R25
+    # A-CholQR of the projected block
+    W = torch.empty(n, t, dtype=torch.float64, device="cuda")
+    AW = torch.empty_like(W)
+    R = torch.empty(t, t, dtype=torch.float64, device="cuda")
+    B = torch.empty(t, t, dtype=torch.float64, device="cuda")
+    st = eks.eks_k_acholqr(s.ctx, t, dev(torch, Zo), W, AW, R, B)
+    so, Wo, Ro, Bo = oracle_lib.acholqr(A, Zo)
+    assert st == 0 and so == 0
+    assert rel(np.triu(host(B)), Bo) <= 1e-12
+    assert rel(np.triu(host(R)), Ro) <= 1e-12
+    assert rel(host(W), Wo) <= 1e-11
+    Wh = host(W)
+    D = oracle_lib.xty(Wh, oracle_lib.spmm(A, Wh))
+    assert np.abs(D - np.eye(t)).max() <= 1e-10                   # block A-orthonormality
+    s.close()
+
+
+# ------------------------------------------------------------------ end to end
+def _e2e(eks, torch, oracle_lib, A, b, method, s_, t, tol, kmax=5000, mode=0):
+    S = eks.Solver(A)
+    rep = S.solve(dev(torch, b), method, s_, t, tol, max_outer=kmax)
+    S.close()
+    ref = oracle_lib.solve(A, b, method, s_, t, tol, kmax=kmax, mode=mode)
+    return rep, ref
+
+
+@pytest.mark.parametrize("method,s_,t", [("sre-cg", 2, 4), ("sre-cg2", 2, 4), ("msdo-cg", 2, 4),
+                                         ("sre-cg", 1, 1), ("sre-cg", 3, 16), ("msdo-cg", 4, 8)])
+def test_cfg1_end_to_end(eks, torch_cuda, oracle_lib, method, s_, t):
+    p = ei.cfg1()
+    rep, ref = _e2e(eks, torch_cuda, oracle_lib, p.A, p.b, method, s_, t, p.tol)
+    assert rep["status"] == 0 and rep["converged"] and ref["converged"]
+    assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+    assert rep["true_relres"] <= 1.5e-8 and ref["true_relres"] <= 1.5e-8
+    assert rep["rho"] <= p.tol * rep["rho0"]
+    assert abs(rep["rho0"] - ref["rho0"]) <= 1e-14 * ref["rho0"]
+
+
+@pytest.mark.parametrize("method", ["sre-cg", "sre-cg2"])
+def test_cfg2_analog_end_to_end(eks, torch_cuda, oracle_lib, method):
+    # cfg2 recipe at 64² (the oracle cannot finish 512² in seconds): bands of 32, t=16, s=3
+    p = ei.cfg2(N=64, method=method)
+    rep, ref = _e2e(eks, torch_cuda, oracle_lib, p.A, p.b, method, p.s, p.t, p.tol)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+    assert rep["true_relres"] <= 2e-8
+
+
+def test_cfg2_full_size_prefix(eks, torch_cuda, oracle_lib):
+    # full 512² operator, first 2 outer iterations (tol=0, k_max=3) — x after the same count
+    p = ei.cfg2()
+    rep, ref = _e2e(eks, torch_cuda, oracle_lib, p.A, p.b, "sre-cg", p.s, p.t, 0.0, kmax=3)
+    assert rep["outer_iters"] == ref["outer_iters"] == 2
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-10
+    assert abs(rep["rho"] - ref["rho"]) <= 1e-8 * ref["rho"]
+
+
+def test_cfg3_analog_msdo(eks, torch_cuda, oracle_lib):
+    p = ei.cfg3(N=16)  # 16³ analog of the 128³ subcube problem, t=32 (a domain = 8 rows... 128 rows), s=4
+    rep, ref = _e2e(eks, torch_cuda, oracle_lib, p.A, p.b, "msdo-cg", p.s, p.t, p.tol)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+
+
+def test_cfg4_analog_sre_t64(eks, torch_cuda, oracle_lib):
+    p = ei.cfg4(N=16)  # 16³ analog of the 256³ anisotropic problem, t=64, s=2
+    rep, ref = _e2e(eks, torch_cuda, oracle_lib, p.A, p.b, "sre-cg", p.s, p.t, p.tol)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+
+
+@pytest.mark.parametrize("t,nblocks", [(8, 4), (16, 8), (32, 6)])
+def test_basis_sweep_parity(eks, torch_cuda, oracle_lib, t, nblocks):
+    torch = torch_cuda
+    A = ei.stencil_csr(12, 12, 12, ndim=3)
+    X0 = ei.cfg5_start_block(A.n, t)
+    S = eks.Solver(A)
+    W = torch.empty(A.n, t, dtype=torch.float64, device="cuda")
+    rep = eks.eks_basis_sweep(S.ctx, t, nblocks, dev(torch, X0), W)
+    st, Wo = oracle_lib.basis_sweep(A, X0, nblocks)
+    assert st == 0 and rep["outer_iters"] == nblocks
+    assert rel(host(W), Wo) <= 1e-9
+    Wh = host(W)
+    assert np.abs(oracle_lib.xty(Wh, oracle_lib.spmm(A, Wh)) - np.eye(t)).max() <= 1e-10
+    S.close()
+
+
+# ------------------------------------------------------------------ degenerate / error cases
+def test_zero_rhs_and_errors(eks, torch_cuda):
+    torch = torch_cuda
+    A = ei.poisson2d(10)
+    S = eks.Solver(A)
+    rep = S.solve(torch.zeros(A.n, dtype=torch.float64, device="cuda"), "sre-cg", 2, 4, 1e-8)
+    assert rep["status"] == 0 and rep["outer_iters"] == 0 and rep["converged"]
+    with pytest.raises(eks.EksError) as e:
+        S.solve(torch.ones(A.n, dtype=torch.float64, device="cuda"), "sre-cg", 2, 3, 1e-8)  # t=3
+    assert e.value.status == 1
+    with pytest.raises(eks.EksError):
+        S.solve(torch.ones(A.n, dtype=torch.float64, device="cuda"), "sre-cg", 0, 4, 1e-8)  # s=0
+    S.close()
+
+
+def test_bad_matrix_rejected(eks, torch_cuda):
+    A = ei.poisson2d(4)
+    ctx = eks.eks_create()
+    col = A.col.copy()
+    col[0], col[1] = col[1], col[0]  # unsorted row
+    with pytest.raises(eks.EksError) as e:
+        eks.eks_setup_csr(ctx, A.n, 0, A.n, A.row_ptr, col, A.val)
+    assert e.value.status == 3
+    val = A.val.copy()
+    val[0] = -1.0  # negative diagonal
+    with pytest.raises(eks.EksError) as e:
+        eks.eks_setup_csr(ctx, A.n, 0, A.n, A.row_ptr, A.col, val)
+    assert e.value.status == 3
+    eks.eks_destroy(ctx)
+
+
+def test_msdo_breakdown_keeps_x0(eks, torch_cuda, oracle_lib):
+    torch = torch_cuda
+    A = ei.poisson2d(8)
+    b = ei.uniform_pm1(2, A.n)
+    b[: A.n // 4] = 0.0
+    S = eks.Solver(A)
+    rep = S.solve(dev(torch, b), "msdo-cg", 2, 4, 1e-8)
+    assert rep["status"] == eks.EKS_ERR_BREAKDOWN and rep["outer_iters"] == 0
+    assert rep["breakdown_block"] == 0 and float(rep["x"].abs().max()) == 0.0
+    ref = oracle_lib.solve(A, b, "msdo-cg", 2, 4, 1e-8)
+    assert ref["status"] == oracle_lib.BREAKDOWN
+    S.close()
+
+
+def test_maxiter_and_determinism_and_host_pointers(eks, torch_cuda):
+    torch = torch_cuda
+    p = ei.cfg1()
+    S = eks.Solver(p.A)
+    r1 = S.solve(dev(torch, p.b), p.method, p.s, p.t, p.tol, max_outer=5)
+    assert r1["status"] == eks.EKS_ERR_MAXITER and r1["outer_iters"] == 4 and not r1["converged"]
+    a = S.solve(dev(torch, p.b), p.method, p.s, p.t, p.tol)
+    b = S.solve(dev(torch, p.b), p.method, p.s, p.t, p.tol)
+    c = S.solve(p.b.copy(), p.method, p.s, p.t, p.tol)  # host pointers (EKS_MEM_HOST)
+    assert torch.equal(a["x"], b["x"])                       # bitwise run-to-run
+    assert np.array_equal(host(a["x"]), c["x"])
+    assert np.array_equal(a["hist"], c["hist"])
+    S.close()
