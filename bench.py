@@ -170,6 +170,7 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=2, help="oracle outer iterations for cpu_baseline")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--max-outer", type=int, default=0, help="cap outer iterations per solve (profiling only)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -217,8 +218,9 @@ def main():
     def step(profile=False):
         with torch.cuda.stream(stream):
             x.zero_()
-        st, rep = eks.eks_solve_ex(solver.ctx, p.method, p.s, p.t, p.tol, b, x, profile=profile)
-        if st not in (0,):
+        st, rep = eks.eks_solve_ex(solver.ctx, p.method, p.s, p.t, p.tol, b, x, profile=profile,
+                                   max_outer=args.max_outer)
+        if st not in ((0, 8) if args.max_outer else (0,)):
             raise SystemExit(f"solve failed: {eks.STATUS.get(st)} {eks.eks_error_string(solver.ctx)}")
         return rep
 

@@ -11,6 +11,7 @@
 #include "../../include/eks.h"
 #include "../../include/eks_kernels.h"
 #include "eks_kernels.cuh"
+#include "eks_sweep.cuh"
 
 #include <nccl.h>
 
@@ -46,7 +47,7 @@ struct eks_ctx {
   cudaStream_t stream = nullptr, own = nullptr, comm_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   ncclComm_t comm = nullptr;
-  int sms = 148, nblk = 296;
+  int sms = 148, nblk = 296, rho_nblk = 296;  // rho_nblk: CTAs that wrote the last scalar partials
   std::string err;
   // matrix (local slab)
   bool have_matrix = false;
@@ -58,6 +59,7 @@ struct eks_ctx {
   std::vector<Recv> recvs;
   std::vector<Send> sends;
   int64_t int_lo = 0, int_hi = 0;  // interior local rows (all columns local)
+  int64_t maxrow = 0;              // longest local CSR row
   // workspace, keyed by t
   int ws_t = 0;
   std::vector<Block> Wpool, AWpool;  // Wpool ext layout, AWpool local
@@ -303,8 +305,36 @@ eks_status spmm(eks_ctx* ctx, const Block& X, double* Y, int t) {
 }
 
 // out (nl·t·t [+t]) = Σ over all rows of Lᵀ R [and L_0ᵀ v], allreduced.
+// out (nl·t·t [+t]) = Σ over all rows of Lᵀ R [and L_0ᵀ v], allreduced over ranks.
 eks_status tn_reduce(eks_ctx* ctx, int t, int nl, const double* const* L, const double* R, const double* v,
                      double* out) {
+  if (v && nl != 1) return fail(ctx, EKS_ERR_INVALID_ARG, "internal: v needs one left block");
+  const size_t total = (size_t)nl * t * t + (v ? t : 0);
+  if (eks::sweep_supported(t)) {
+    const int maxb = eks::sweep_max_blocks(t);
+    for (int j0 = 0; j0 < nl;) {
+      int k = 1;
+      while (2 * k <= maxb && 2 * k <= nl - j0) k *= 2;  // power-of-two chunks of left blocks
+      eks::SweepPtrs P{};
+      for (int j = 0; j < k; ++j) P.l[j] = L[j0 + j];
+      const size_t stride = eks::sweep_part_stride(t, k, v != nullptr);
+      ST(ensure_part(ctx, stride * ctx->nblk));
+      account(ctx, EKS_K_COEF, 8.0 * ctx->n * ((double)(k + 1) * t + (v ? 1 : 0)),
+              2.0 * ctx->n * t * (t * k + (v ? 1 : 0)));
+      {
+        KScope ks(ctx, EKS_K_COEF);
+        CK(eks::launch_sweep(ctx->stream, t, 0, k, v != nullptr, ctx->n, R, nullptr, P, nullptr, v, ctx->part,
+                             ctx->nblk));
+      }
+      {
+        KScope ks(ctx, EKS_K_REDUCE);
+        CK(eks::launch_reduce(ctx->stream, ctx->part, eks::sweep_last_grid(), stride, stride,
+                              out + (size_t)j0 * t * t));
+      }
+      j0 += k;
+    }
+    return allreduce(ctx, out, total);
+  }
   const size_t stride = eks::tn_partials_stride(t, nl, v != nullptr);
   ST(ensure_part(ctx, stride * ctx->nblk));
   account(ctx, EKS_K_COEF, 8.0 * ctx->n * ((double)(nl + 1) * t + (v ? 1 : 0)), 2.0 * ctx->n * t * (t * nl + (v ? 1 : 0)));
@@ -319,12 +349,73 @@ eks_status tn_reduce(eks_ctx* ctx, int t, int nl, const double* const* L, const 
   return allreduce(ctx, out, stride);
 }
 
+// Zout = Zin − Σ_j Q_j C_j  (CGS update)
 eks_status ts_update(eks_ctx* ctx, int t, int nq, const double* const* Q, const double* C, const double* Zin,
                      double* Zout) {
+  if (eks::sweep_supported(t)) {
+    const int maxb = eks::sweep_max_blocks(t);
+    for (int j0 = 0; j0 < nq;) {
+      const int k = std::min(maxb, nq - j0);
+      eks::SweepPtrs P{};
+      for (int j = 0; j < k; ++j) P.q[j] = Q[j0 + j];
+      account(ctx, EKS_K_UPDATE, 8.0 * ctx->n * ((double)k * t + 2.0 * t), 2.0 * ctx->n * t * t * k);
+      KScope ks(ctx, EKS_K_UPDATE);
+      CK(eks::launch_sweep(ctx->stream, t, k, 0, false, ctx->n, j0 == 0 ? Zin : Zout, Zout, P,
+                           C + (size_t)j0 * t * t, nullptr, nullptr, ctx->nblk));
+      j0 += k;
+    }
+    return EKS_OK;
+  }
   account(ctx, EKS_K_UPDATE, 8.0 * ctx->n * ((double)nq * t + 2.0 * t), 2.0 * ctx->n * t * t * nq);
   KScope k(ctx, EKS_K_UPDATE);
   CK(eks::launch_ts_update(ctx->stream, t, ctx->n, nq, Q, C, Zin, Zout, ctx->nblk));
   return EKS_OK;
+}
+
+// Fused CGS pass: Z1 = Z − Q C1 and C2 = (AQ)ᵀ Z1 in one sweep (nq ≤ 2 window of SRE-CG).
+eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, const double* const* AQ,
+                       const double* C1, const double* Z, double* Z1, double* C2) {
+  eks::SweepPtrs P{};
+  for (int j = 0; j < nq; ++j) {
+    P.q[j] = Q[j];
+    P.l[j] = AQ[j];
+  }
+  const size_t stride = eks::sweep_part_stride(t, nq, false);
+  ST(ensure_part(ctx, stride * ctx->nblk));
+  account(ctx, EKS_K_UPDATE, 8.0 * ctx->n * ((double)2 * nq * t + 2.0 * t), 4.0 * ctx->n * t * t * nq);
+  {
+    KScope ks(ctx, EKS_K_UPDATE);
+    CK(eks::launch_sweep(ctx->stream, t, nq, nq, false, ctx->n, Z, Z1, P, C1, nullptr, ctx->part, ctx->nblk));
+  }
+  {
+    KScope ks(ctx, EKS_K_REDUCE);
+    CK(eks::launch_reduce(ctx->stream, ctx->part, eks::sweep_last_grid(), stride, stride, C2));
+  }
+  return allreduce(ctx, C2, stride);
+}
+
+// Y = A·X and out = [XᵀY | Xᵀr] (t·t + t, allreduced): the A-CholQR Gram with the α̃ projection.
+// Single-rank stencil-like matrices (rows ≤ 8 entries) use the fused SpMM+Gram kernel.
+eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const double* r, double* out) {
+  if (ctx->nranks != 1 || !eks::sweep_supported(t) || ctx->maxrow > eks::spmm_gram_max_row()) {
+    ST(spmm(ctx, X, Y, t));
+    const double* L[1] = {X.loc};
+    return tn_reduce(ctx, t, 1, L, Y, r, out);
+  }
+  const size_t stride = eks::sweep_part_stride(t, 1, true);
+  ST(ensure_part(ctx, stride * ctx->nblk));
+  account(ctx, EKS_K_SPMM, 12.0 * ctx->nnz + 4.0 * (ctx->n + 1) + 16.0 * ctx->n * t, 2.0 * ctx->nnz * t);
+  account(ctx, EKS_K_COEF, r ? 8.0 * ctx->n : 0.0, 2.0 * ctx->n * t * (t + 1));  // epilogue: only r is extra traffic
+  {
+    KScope k(ctx, EKS_K_SPMM);
+    CK(eks::launch_spmm_gram(ctx->stream, t, ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val, X.base, X.loc, Y, r,
+                             ctx->part, ctx->nblk));
+  }
+  {
+    KScope k(ctx, EKS_K_REDUCE);
+    CK(eks::launch_reduce(ctx->stream, ctx->part, eks::sweep_last_grid(), stride, stride, out));
+  }
+  return allreduce(ctx, out, stride);
 }
 
 // CGS2 of Z against the window (Q, AQ): two passes of C = (AQ)ᵀZ, Z -= Q C (reading R3/R24).
@@ -332,10 +423,14 @@ eks_status cgs2(eks_ctx* ctx, int t, const std::vector<const double*>& Q, const 
                 const double* Z, double* Zout) {
   const int nq = (int)Q.size();
   ST(ensure_C(ctx, (size_t)nq * t * t));
-  ST(tn_reduce(ctx, t, nq, AQ.data(), Z, nullptr, ctx->C1));
-  ST(ts_update(ctx, t, nq, Q.data(), ctx->C1, Z, ctx->Z1.loc));
-  ST(tn_reduce(ctx, t, nq, AQ.data(), ctx->Z1.loc, nullptr, ctx->C2));
-  ST(ts_update(ctx, t, nq, Q.data(), ctx->C2, ctx->Z1.loc, Zout));
+  ST(tn_reduce(ctx, t, nq, AQ.data(), Z, nullptr, ctx->C1));  // C1 = (AQ)ᵀ Z
+  if (eks::sweep_supported(t) && eks::sweep_fused_supported(t, nq)) {
+    ST(update_coef(ctx, t, nq, Q.data(), AQ.data(), ctx->C1, Z, ctx->Z1.loc, ctx->C2));  // Z1, C2 = (AQ)ᵀ Z1
+  } else {
+    ST(ts_update(ctx, t, nq, Q.data(), ctx->C1, Z, ctx->Z1.loc));
+    ST(tn_reduce(ctx, t, nq, AQ.data(), ctx->Z1.loc, nullptr, ctx->C2));
+  }
+  ST(ts_update(ctx, t, nq, Q.data(), ctx->C2, ctx->Z1.loc, Zout));  // Z2 = Z1 − Q C2
   return EKS_OK;
 }
 
@@ -355,7 +450,7 @@ eks_status reset_flag(eks_ctx* ctx) {
 eks_status reduce_scalar(eks_ctx* ctx, double* slot) {
   {
     KScope k(ctx, EKS_K_REDUCE);
-    CK(eks::launch_reduce(ctx->stream, ctx->part, ctx->nblk, 1, 1, slot));
+    CK(eks::launch_reduce(ctx->stream, ctx->part, ctx->rho_nblk, 1, 1, slot));
   }
   return allreduce(ctx, slot, 1);
 }
@@ -438,18 +533,17 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
     CK(cudaMemcpyAsync(Wn->loc, Zsrc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   // "A-orthonormalize W": A-CholQR with one SpMM of Z2 (AW = (A Z2) R⁻¹)
-  ST(spmm(ctx, *Wn, AWn->loc, t));
-  const double* Lw[1] = {Wn->loc};
   const bool with_update = !(mode & 4);
-  ST(tn_reduce(ctx, t, 1, Lw, AWn->loc, with_update ? ctx->r : nullptr, ctx->Bg));
+  ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg));
   ST(chol(ctx, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
           with_update ? ctx->alpha + alpha_off : nullptr, gb));
   {
     KScope k(ctx, EKS_K_APPLY);
     account(ctx, EKS_K_APPLY, 8.0 * ctx->n * (4.0 * t + 4.0), 2.0 * ctx->n * t * (t + 2));
-    CK(eks::launch_apply(ctx->stream, t, ctx->n, Wn->loc, AWn->loc, ctx->Rinv,
-                         with_update ? ctx->alpha + alpha_off : nullptr, ctx->xv.loc, ctx->dx, ctx->r, ctx->rnew,
-                         ctx->part, ctx->flag, mode, ctx->nblk));
+    auto fn = eks::sweep_supported(t) ? eks::launch_apply_tc : eks::launch_apply;
+    CK(fn(ctx->stream, t, ctx->n, Wn->loc, AWn->loc, ctx->Rinv, with_update ? ctx->alpha + alpha_off : nullptr,
+          ctx->xv.loc, ctx->dx, ctx->r, ctx->rnew, ctx->part, ctx->flag, mode, ctx->nblk));
+    ctx->rho_nblk = eks::sweep_supported(t) ? eks::sweep_last_grid() : ctx->nblk;
   }
   return EKS_OK;
 }
@@ -460,6 +554,7 @@ eks_status residual(eks_ctx* ctx, double* r_out, double* slotp) {
   {
     KScope k(ctx, EKS_K_OTHER);
     CK(eks::launch_residual(ctx->stream, ctx->n, ctx->b, ctx->tmpv.loc, r_out, ctx->part, ctx->nblk));
+    ctx->rho_nblk = ctx->nblk;
   }
   return reduce_scalar(ctx, slotp);
 }
@@ -681,6 +776,8 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   }
   ctx->int_lo = best_lo;
   ctx->int_hi = best_lo + best_len;
+  ctx->maxrow = 0;
+  for (int64_t i = 0; i < n; ++i) ctx->maxrow = std::max<int64_t>(ctx->maxrow, rp[i + 1] - rp[i]);
   // ---- upload (the block workspace survives when the slab geometry is unchanged)
   if (!ctx->have_matrix || ctx->n != n || old_before != ctx->halo_before || old_after != ctx->halo_after)
     free_workspace(ctx);
@@ -787,6 +884,7 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   {
     KScope kk(ctx, EKS_K_OTHER);
     CK(eks::launch_sumsq(ctx->stream, ctx->n, ctx->b, ctx->part, ctx->nblk));
+    ctx->rho_nblk = ctx->nblk;
   }
   ST(reduce_scalar(ctx, ctx->scal + 3));
   ST(copy_out(ctx, x, ctx->xv.loc, ctx->n, where));
@@ -919,10 +1017,9 @@ eks_status eks_k_spmm(eks_ctx* ctx, int t, const double* X, double* Y, double* G
   Block xb;
   xb.base = const_cast<double*>(X);
   xb.loc = xb.base;
-  ST(spmm(ctx, xb, Y, t));
+  if (!(G || g)) ST(spmm(ctx, xb, Y, t));
   if (G || g) {
-    const double* L[1] = {X};
-    ST(tn_reduce(ctx, t, 1, L, Y, g ? v : nullptr, ctx->Bg));
+    ST(spmm_gram(ctx, xb, Y, t, g ? v : nullptr, ctx->Bg));
     if (G) CK(cudaMemcpyAsync(G, ctx->Bg, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
     if (g && v) CK(cudaMemcpyAsync(g, ctx->Bg + t * t, sizeof(double) * t, cudaMemcpyDeviceToDevice, ctx->stream));
   }
@@ -950,12 +1047,11 @@ eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double
   wb.base = W;
   wb.loc = W;
   if (W != Z) CK(cudaMemcpyAsync(W, Z, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
-  ST(spmm(ctx, wb, AW, t));
-  const double* L[1] = {W};
-  ST(tn_reduce(ctx, t, 1, L, AW, nullptr, ctx->Bg));
+  ST(spmm_gram(ctx, wb, AW, t, nullptr, ctx->Bg));
   ST(chol(ctx, t, ctx->Bg, nullptr, ctx->Rm, ctx->Rinv, nullptr, 0));
-  CK(eks::launch_apply(ctx->stream, t, ctx->n, W, AW, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr,
-                       nullptr, nullptr, 4, ctx->nblk));
+  auto fn = eks::sweep_supported(t) ? eks::launch_apply_tc : eks::launch_apply;
+  CK(fn(ctx->stream, t, ctx->n, W, AW, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 4,
+        ctx->nblk));
   if (R) CK(cudaMemcpyAsync(R, ctx->Rm, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
   if (B) CK(cudaMemcpyAsync(B, ctx->Bg, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
   ST(sync_scalars(ctx, 1));

@@ -10,7 +10,9 @@
 
 namespace eks {
 
-int sweep_ctas(int sms) { return 2 * sms; }
+// Upper bound on CTAs (= per-CTA partial slots) of the row-sweep kernels; each
+// launcher uses min(this, SMs × resident CTAs per SM), i.e. one full wave.
+int sweep_ctas(int sms) { return 4 * sms; }
 
 #define EKS_DISPATCH_T(t, ...)                          \
   switch (t) {                                          \
@@ -84,11 +86,52 @@ __global__ void __launch_bounds__(kThreads) k_spmm(int r0, int r1, const int* __
   const int lane = threadIdx.x % G;
   const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
   const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+  constexpr int B = 8;  // entries fetched per batch: all (val, col) loads, then all X gathers in flight
   for (int64_t i = r0 + grp; i < r1; i += ngrp) {
     const int p0 = __ldg(rp + i), p1 = __ldg(rp + i + 1);
     if constexpr (VEC == 2) {
       double ax = 0.0, ay = 0.0;
-      for (int p = p0; p < p1; ++p) {
+      int p = p0;
+      for (; p + B <= p1; p += B) {
+        double a[B];
+        int c[B];
+        double2 xv[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          a[k] = __ldg(val + p + k);
+          c[k] = __ldg(col + p + k);
+        }
+#pragma unroll
+        for (int k = 0; k < B; ++k) xv[k] = __ldg(reinterpret_cast<const double2*>(X + (int64_t)c[k] * T) + lane);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          ax = __fma_rn(a[k], xv[k].x, ax);
+          ay = __fma_rn(a[k], xv[k].y, ay);
+        }
+      }
+      if (p < p1) {  // tail (< B entries; a 5/7-point stencil row lands here entirely)
+        const int m = p1 - p;
+        double a[B];
+        int c[B];
+        double2 xv[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k)
+          if (k < m) {
+            a[k] = __ldg(val + p + k);
+            c[k] = __ldg(col + p + k);
+          }
+#pragma unroll
+        for (int k = 0; k < B; ++k)
+          if (k < m) xv[k] = __ldg(reinterpret_cast<const double2*>(X + (int64_t)c[k] * T) + lane);
+#pragma unroll
+        for (int k = 0; k < B; ++k)
+          if (k < m) {
+            ax = __fma_rn(a[k], xv[k].x, ax);
+            ay = __fma_rn(a[k], xv[k].y, ay);
+          }
+        p = p1;
+      }
+      for (; p < p1; ++p) {
         const double a = __ldg(val + p);
         const int c = __ldg(col + p);
         const double2 xv = __ldg(reinterpret_cast<const double2*>(X + (int64_t)c * T) + lane);
@@ -295,12 +338,40 @@ __global__ void k_reduce(const double* __restrict__ part, int nblk, size_t strid
   }
 }
 
+// 32 consecutive entries per CTA (coalesced), the 8 warps split the CTA partials
+// (warp w takes b ≡ w mod 8, ascending), then warps are combined in order.
+__global__ void __launch_bounds__(256) k_reduce32(const double* __restrict__ part, int nblk, size_t stride,
+                                                  size_t count, double* __restrict__ out) {
+  __shared__ double s[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const size_t e = (size_t)blockIdx.x * 32 + lane;
+  double acc = 0.0;
+  if (e < count) {
+    // 8 independent loads in flight per lane, then summed in ascending b order
+    for (int b0 = w; b0 < nblk; b0 += 64) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int b = b0 + 8 * k;
+        v[k] = b < nblk ? __ldg(part + (size_t)b * stride + e) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc += v[k];
+    }
+  }
+  s[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && e < count) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += s[k][lane];
+    out[e] = t;
+  }
+}
+
 cudaError_t launch_reduce(cudaStream_t st, const double* part, int nblk, size_t stride, size_t count,
                           double* out) {
   if (count == 0) return cudaSuccess;
-  int blocks = (int)((count + 127) / 128);
-  if (blocks > 1024) blocks = 1024;
-  k_reduce<<<blocks, 128, 0, st>>>(part, nblk, stride, count, out);
+  k_reduce32<<<(int)((count + 31) / 32), 256, 0, st>>>(part, nblk, stride, count, out);
   return cudaGetLastError();
 }
 
@@ -466,18 +537,19 @@ __global__ void k_chol(const double* __restrict__ B, const double* __restrict__ 
     if (Rout) Rout[e] = sR[e / T][e % T];
     Rinv[e] = sRi[e / T][e % T];
   }
-  if (tid == 0) {
-    if (g != nullptr && alpha != nullptr) {
-      double a[T];
-      for (int j = 0; j < T; ++j) {
-        double v = g[j];
-        for (int i = 0; i < j; ++i) v = __dsub_rn(v, __dmul_rn(sR[i][j], a[i]));
-        a[j] = __ddiv_rn(v, sR[j][j]);
-        alpha[j] = a[j];
-      }
+  if (g != nullptr && alpha != nullptr) {
+    // alpha = R⁻ᵀ g = Rinvᵀ g: alpha_j = Σ_{i<=j} Rinv[i][j] g_i, one thread per j
+    double* sg = &sB[0][0];  // B is no longer needed
+    __syncthreads();
+    for (int j = tid; j < T; j += blockDim.x) sg[j] = g[j];
+    __syncthreads();
+    for (int j = tid; j < T; j += blockDim.x) {
+      double a = 0.0;
+      for (int i = 0; i <= j; ++i) a = __fma_rn(sRi[i][j], sg[i], a);
+      alpha[j] = a;
     }
-    if (sfail && flag) atomicMin(flag, gblock);
   }
+  if (tid == 0 && sfail && flag) atomicMin(flag, gblock);
 }
 
 cudaError_t launch_chol(cudaStream_t st, int t, const double* B, const double* g, double* R, double* Rinv,
@@ -485,7 +557,8 @@ cudaError_t launch_chol(cudaStream_t st, int t, const double* B, const double* g
   EKS_DISPATCH_T(t, {
     const size_t sm = (size_t)3 * T * (T + 1) * 8;
     cudaFuncSetAttribute(k_chol<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_chol<T><<<1, 64, sm, st>>>(B, g, R, Rinv, alpha, flag, gblock);
+    // one warp for t <= 32 (cheaper barriers on the serial factorization), two for t = 64
+    k_chol<T><<<1, T > 32 ? 64 : 32, sm, st>>>(B, g, R, Rinv, alpha, flag, gblock);
   });
   return cudaGetLastError();
 }
