@@ -129,6 +129,19 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
 eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks, const double* X0, double* W_last,
                            eks_mem where, const eks_options* opt, eks_report* rep);
 
+/* Host-only halo plan that eks_setup_csr uses on every rank (no device, no NCCL;
+ * exported so the multi-rank logic can be tested on CPUs).  Rank r owns rows
+ * [ranges[2r], ranges[2r+1]) (the ranges must tile [0,n) in rank order
+ * "processor i owns D_i"); row_ptr/col are its slab with GLOBAL columns.
+ * Outputs: ext_col[nnz] — columns remapped to the extended layout
+ * [ghost rows of lower ranks | local rows | ghost rows of higher ranks];
+ * need[2*nranks] — the ghost range [lo,hi) received from each rank (0,0: none;
+ * rank q therefore sends rows need_p[2q..2q+1] of its slab to rank p);
+ * geom[4] — halo_before, halo_after, interior_lo, interior_hi (local rows whose
+ * columns are all local, multiplied while the halo is in flight). */
+eks_status eks_plan_halo(int rank, int nranks, const int64_t* ranges, const int64_t* row_ptr,
+                         const int32_t* col, int32_t* ext_col, int64_t* need, int64_t* geom);
+
 /* Kernel-class timings of the last solve/sweep run with opt.profile = 1. */
 eks_status eks_get_profile(const eks_ctx* ctx, eks_profile* out);
 

@@ -79,6 +79,7 @@ def lib():
             "eks_k_cgs2": [vp, i32, i32, vp, vp, vp, vp, vp],
             "eks_k_acholqr": [vp, i32, vp, vp, vp, vp, vp],
             "eks_k_chol": [vp, i32, vp, vp],
+            "eks_plan_halo": [i32, i32, vp, vp, vp, vp, vp, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -92,7 +93,22 @@ def lib():
 
 EXPORTED = ["eks_get_unique_id", "eks_create", "eks_set_stream", "eks_setup_csr", "eks_solve", "eks_solve_ex",
             "eks_basis_sweep", "eks_get_profile", "eks_destroy", "eks_error_string", "eks_k_split", "eks_k_spmm",
-            "eks_k_cgs2", "eks_k_acholqr", "eks_k_chol"]
+            "eks_k_cgs2", "eks_k_acholqr", "eks_k_chol", "eks_plan_halo"]
+
+
+def eks_plan_halo(rank: int, nranks: int, ranges, row_ptr, col):
+    """Host-only halo plan (see include/eks.h).  Returns (ext_col, need[nranks,2], geom dict)."""
+    ranges = np.ascontiguousarray(ranges, np.int64)
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cl = np.ascontiguousarray(col, np.int32)
+    ext = np.empty_like(cl)
+    need = np.zeros(2 * nranks, np.int64)
+    geom = np.zeros(4, np.int64)
+    st = lib().eks_plan_halo(int(rank), int(nranks), _ptr(ranges, np.int64), _ptr(rp, np.int64), _ptr(cl, np.int32),
+                             _ptr(ext, np.int32), _ptr(need, np.int64), _ptr(geom, np.int64))
+    _check(None, st)
+    return ext, need.reshape(nranks, 2), dict(halo_before=int(geom[0]), halo_after=int(geom[1]),
+                                              interior_lo=int(geom[2]), interior_hi=int(geom[3]))
 
 
 def _where(*arrays):

@@ -559,6 +559,88 @@ eks_status residual(eks_ctx* ctx, double* r_out, double* slotp) {
   return reduce_scalar(ctx, slotp);
 }
 
+// ---------------------------------------------------------------- halo plan (host only)
+// Rank `rank` owns rows [ranges[2r], ranges[2r+1]).  For every other rank q the
+// ghost rows it needs are the contiguous range [lo_q, hi_q) spanning all its
+// off-slab column indices owned by q (exact for banded/stencil matrices, a
+// superset otherwise).  Extended layout: ghost ranges of lower ranks, local
+// rows, ghost ranges of higher ranks — so the SpMM reads one array.  The
+// interior run is the longest run of rows with only local columns: it is
+// multiplied while the halo is in flight.
+struct HaloPlan {
+  int64_t halo_before = 0, halo_after = 0, int_lo = 0, int_hi = 0;
+  std::vector<Recv> recvs;
+  std::vector<int64_t> need;  // 2*nranks: [lo,hi) received from each rank (0,0 if none)
+  std::vector<int32_t> ecol;  // columns remapped to the extended layout
+};
+
+void plan_halo(int rank, int nranks, const int64_t* ranges, int64_t n, const int64_t* rp, const int32_t* col,
+               HaloPlan& P) {
+  const int64_t row_begin = ranges[2 * rank], row_end = ranges[2 * rank + 1];
+  const int64_t nnz = rp[n];
+  auto owner = [&](int64_t c) {
+    int q = 0;
+    while (q < nranks && !(c >= ranges[2 * q] && c < ranges[2 * q + 1])) ++q;
+    return q;
+  };
+  std::vector<int64_t> glo(nranks, INT64_MAX), ghi(nranks, INT64_MIN);
+  for (int64_t p = 0; p < nnz; ++p) {
+    const int64_t c = col[p];
+    if (c < row_begin || c >= row_end) {
+      const int q = owner(c);
+      glo[q] = std::min(glo[q], c);
+      ghi[q] = std::max(ghi[q], c + 1);
+    }
+  }
+  P.recvs.clear();
+  P.need.assign(2 * nranks, 0);
+  std::vector<int64_t> off(nranks, 0);
+  int64_t ext = 0;
+  for (int q = 0; q < nranks; ++q) {
+    if (q == rank) {
+      off[q] = ext;
+      ext += n;
+      continue;
+    }
+    if (glo[q] < ghi[q]) {
+      off[q] = ext;
+      P.recvs.push_back({q, glo[q], ghi[q], ext});
+      P.need[2 * q] = glo[q];
+      P.need[2 * q + 1] = ghi[q];
+      ext += ghi[q] - glo[q];
+    }
+  }
+  P.halo_before = off[rank];
+  P.halo_after = ext - off[rank] - n;
+  P.ecol.assign(nnz, 0);
+  std::vector<char> interior(n, 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t c = col[p];
+      if (c >= row_begin && c < row_end) {
+        P.ecol[p] = (int32_t)(P.halo_before + (c - row_begin));
+      } else {
+        const int q = owner(c);
+        P.ecol[p] = (int32_t)(off[q] + (c - glo[q]));
+        interior[i] = 0;
+      }
+    }
+  int64_t best_lo = 0, best_len = 0, cur = 0;
+  for (int64_t i = 0; i <= n; ++i) {
+    if (i < n && interior[i]) {
+      ++cur;
+      continue;
+    }
+    if (cur > best_len) {
+      best_len = cur;
+      best_lo = i - cur;
+    }
+    cur = 0;
+  }
+  P.int_lo = best_lo;
+  P.int_hi = best_lo + best_len;
+}
+
 void begin_run(eks_ctx* ctx, const eks_options* opt) {
   ctx->prof_on = opt && opt->profile;
   ctx->prof = eks_profile{};
@@ -698,48 +780,18 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
       if (ranges[2 * q + 1] != ranges[2 * q + 2] || ranges[0] != 0 || ranges[2 * ctx->nranks - 1] != n_global)
         return fail(ctx, EKS_ERR_INVALID_ARG, "rank slabs must tile [0,n) in rank order");
   }
-  auto owner = [&](int64_t c) {
-    int q = 0;
-    while (q < ctx->nranks && !(c >= ranges[2 * q] && c < ranges[2 * q + 1])) ++q;
-    return q;
-  };
-  // ---- halo plan: contiguous ghost range per owner rank
-  std::vector<int64_t> glo(ctx->nranks, INT64_MAX), ghi(ctx->nranks, INT64_MIN);
-  for (int64_t p = 0; p < nnz; ++p) {
-    const int64_t c = col[p];
-    if (c < row_begin || c >= row_end) {
-      int q = owner(c);
-      glo[q] = std::min(glo[q], c);
-      ghi[q] = std::max(ghi[q], c + 1);
-    }
-  }
+  // ---- halo plan (host-only, also exported as eks_plan_halo for the multi-rank CPU tests)
+  HaloPlan plan;
+  plan_halo(ctx->rank, ctx->nranks, ranges.data(), n, rp.data(), col.data(), plan);
   const int64_t old_before = ctx->halo_before, old_after = ctx->halo_after;
-  ctx->recvs.clear();
+  ctx->recvs = plan.recvs;
   ctx->sends.clear();
-  std::vector<int64_t> off(ctx->nranks, 0);
-  int64_t ext = 0;
-  for (int q = 0; q < ctx->nranks; ++q) {
-    if (q == ctx->rank) {
-      off[q] = ext;
-      ext += n;
-      continue;
-    }
-    if (glo[q] < ghi[q]) {
-      off[q] = ext;
-      ctx->recvs.push_back({q, glo[q], ghi[q], ext});
-      ext += ghi[q] - glo[q];
-    }
-  }
-  ctx->halo_before = off[ctx->rank];
-  ctx->halo_after = ext - off[ctx->rank] - n;
+  ctx->halo_before = plan.halo_before;
+  ctx->halo_after = plan.halo_after;
   if (ctx->nranks > 1) {
     // everyone learns who needs which of its rows
     std::vector<int64_t> req(2 * ctx->nranks * ctx->nranks, 0);
-    for (int q = 0; q < ctx->nranks; ++q)
-      if (q != ctx->rank && glo[q] < ghi[q]) {
-        req[2 * (ctx->rank * ctx->nranks + q)] = glo[q];
-        req[2 * (ctx->rank * ctx->nranks + q) + 1] = ghi[q];
-      }
+    for (int q = 0; q < 2 * ctx->nranks; ++q) req[2 * ctx->rank * ctx->nranks + q] = plan.need[q];
     int64_t* d = nullptr;
     const size_t per = 2 * ctx->nranks;
     CK(cudaMalloc((void**)&d, sizeof(int64_t) * per * ctx->nranks));
@@ -754,28 +806,9 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
       if (hi > lo) ctx->sends.push_back({q, lo, hi});
     }
   }
-  // ---- remap columns to the extended layout; interior run
-  std::vector<int32_t> ecol(nnz);
-  std::vector<char> interior(n, 1);
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-      const int64_t c = col[p];
-      if (c >= row_begin && c < row_end) {
-        ecol[p] = (int32_t)(ctx->halo_before + (c - row_begin));
-      } else {
-        int q = owner(c);
-        ecol[p] = (int32_t)(off[q] + (c - glo[q]));
-        interior[i] = 0;
-      }
-    }
-  int64_t best_lo = 0, best_len = 0, cur = 0;
-  for (int64_t i = 0; i <= n; ++i) {
-    if (i < n && interior[i]) { ++cur; continue; }
-    if (cur > best_len) { best_len = cur; best_lo = i - cur; }
-    cur = 0;
-  }
-  ctx->int_lo = best_lo;
-  ctx->int_hi = best_lo + best_len;
+  const std::vector<int32_t>& ecol = plan.ecol;
+  ctx->int_lo = plan.int_lo;
+  ctx->int_hi = plan.int_hi;
   ctx->maxrow = 0;
   for (int64_t i = 0; i < n; ++i) ctx->maxrow = std::max<int64_t>(ctx->maxrow, rp[i + 1] - rp[i]);
   // ---- upload (the block workspace survives when the slab geometry is unchanged)
@@ -962,6 +995,27 @@ eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks_total, const double*
     rep->gpu_launches = (int)ctx->launches;
   }
   if (fl != INT_MAX) return fail(ctx, EKS_ERR_BREAKDOWN, "A-CholQR breakdown in block %d", fl);
+  return EKS_OK;
+}
+
+eks_status eks_plan_halo(int rank, int nranks, const int64_t* ranges, const int64_t* row_ptr, const int32_t* col,
+                         int32_t* ext_col, int64_t* need, int64_t* geom) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !ranges || !row_ptr || !col || !ext_col || !need || !geom)
+    return EKS_ERR_INVALID_ARG;
+  for (int q = 0; q < nranks; ++q)
+    if (ranges[2 * q] > ranges[2 * q + 1] || (q > 0 && ranges[2 * q] != ranges[2 * q - 1]) || ranges[0] != 0)
+      return EKS_ERR_INVALID_ARG;
+  const int64_t n = ranges[2 * rank + 1] - ranges[2 * rank];
+  for (int64_t p = 0; p < row_ptr[n]; ++p)
+    if (col[p] < 0 || col[p] >= ranges[2 * nranks - 1]) return EKS_ERR_BAD_MATRIX;
+  HaloPlan P;
+  plan_halo(rank, nranks, ranges, n, row_ptr, col, P);
+  memcpy(ext_col, P.ecol.data(), sizeof(int32_t) * P.ecol.size());
+  memcpy(need, P.need.data(), sizeof(int64_t) * P.need.size());
+  geom[0] = P.halo_before;
+  geom[1] = P.halo_after;
+  geom[2] = P.int_lo;
+  geom[3] = P.int_hi;
   return EKS_OK;
 }
 

@@ -1,0 +1,176 @@
+"""Multi-rank logic on CPUs (gloo, world_size 2 and 4): the row-slab partition of
+§8(e), the halo plan that libeks.so builds on every rank (eks_plan_halo, the
+same host code eks_setup_csr runs before its NCCL exchanges), the halo exchange
+protocol (rank q sends rows need_p[q] to rank p), and the allreduce of per-rank
+partial sums.  The distributed SpMM assembled from the plan must be BITWISE the
+global SpMM (same fma order, reading R20); the distributed Gram must equal the
+global one to rounding.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import eks_inputs as ei
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def slab(rank, world, n, t):
+    """Rows of rank `rank`: the union of its t/world domains D_d = [⌊d n/t⌋, ⌊(d+1) n/t⌋) (reading R1)."""
+    per = t // world
+    return (rank * per) * n // t, ((rank + 1) * per) * n // t
+
+
+def _matrix(kind):
+    if kind == "bands2d":
+        return ei.stencil_csr(24, 24, ndim=2, kappa=ei.bands_kappa(24, band=3))
+    if kind == "aniso3d":
+        return ei.stencil_csr(8, 8, 8, ndim=3, scale=(1.0, 1.0, 1e-2))
+    # general sparse SPD: random symmetric pattern + dominant diagonal (non-banded ghost sets)
+    n = 300
+    rng = np.random.default_rng(7)
+    D = np.zeros((n, n))
+    for _ in range(900):
+        i, j = rng.integers(0, n, 2)
+        if i != j:
+            D[i, j] = D[j, i] = -rng.random()
+    D[np.arange(n), np.arange(n)] = np.abs(D).sum(1) + 1.0
+    return ei.csr_from_dense(D)
+
+
+def _worker(rank, world, port, kind, t, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import paper_1804_10629_b200 as eks
+        A = _matrix(kind)
+        n = A.n
+        ranges = np.array([v for r in range(world) for v in slab(r, world, n, t)], np.int64)
+        lo, hi = ranges[2 * rank], ranges[2 * rank + 1]
+        S = A.rows(lo, hi)
+        ext_col, need, geom = eks.eks_plan_halo(rank, world, ranges, S.row_ptr, S.col)
+        # every rank learns every rank's needs (eks_setup_csr: ncclAllGather)
+        need_t = torch.from_numpy(need.copy())
+        all_need = [torch.zeros_like(need_t) for _ in range(world)]
+        dist.all_gather(all_need, need_t)
+        X = ei.uniform_pm1(11, n * t).reshape(n, t)  # same global block on every rank
+        Xloc = X[lo:hi].copy()
+        nloc = hi - lo
+        next_ = geom["halo_before"] + nloc + geom["halo_after"]
+        Xext = np.full((next_, t), np.nan)
+        Xext[geom["halo_before"]:geom["halo_before"] + nloc] = Xloc
+        # halo exchange: rank p sends to q the rows q asked from p; receives its own ghost ranges
+        reqs = []
+        for peer in range(world):
+            if peer == rank:
+                continue
+            a, b = all_need[peer][rank].tolist()
+            if b > a:
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(Xloc[a - lo:b - lo])), dst=peer))
+        off = 0
+        recv_bufs = []
+        for peer in range(world):
+            if peer == rank:
+                off += nloc
+                continue
+            a, b = need[peer].tolist()
+            if b > a:
+                buf = torch.empty((b - a, t), dtype=torch.float64)
+                reqs.append(dist.irecv(buf, src=peer))
+                recv_bufs.append((off, buf))
+                off += b - a
+        for r_ in reqs:
+            r_.wait()
+        for o, buf in recv_bufs:
+            Xext[o:o + buf.shape[0]] = buf.numpy()
+        assert off == next_
+        # local SpMM on the extended layout vs the global SpMM: bitwise
+        Aloc = ei.Csr(nloc, S.row_ptr, ext_col, S.val)
+        Yloc = oracle.spmm(Aloc, Xext)[:nloc]  # the wrapper sizes Y like X; rows past nloc are unused
+        Yglob = oracle.spmm(A, X)[lo:hi]
+        bitwise = bool(np.array_equal(Yloc, Yglob))
+        # interior rows only touch local columns
+        ilo, ihi = geom["interior_lo"], geom["interior_hi"]
+        interior_ok = True
+        for i in range(ilo, ihi):
+            cols = ext_col[S.row_ptr[i]:S.row_ptr[i + 1]]
+            interior_ok &= bool(np.all((cols >= geom["halo_before"]) & (cols < geom["halo_before"] + nloc)))
+        # Gram: per-rank partial XᵀY, allreduced (the stacked ncclAllReduce of §8(e))
+        G = torch.from_numpy(Xloc.T @ Yloc)
+        dist.all_reduce(G)
+        Gref = X.T @ oracle.spmm(A, X)
+        gram_err = float(np.abs(G.numpy() - Gref).max() / np.abs(Gref).max())
+        # max-over-ranks timing aggregation used by bench.py
+        tt = torch.tensor([float(rank + 1)])
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        q.put((rank, bitwise, interior_ok, gram_err, float(tt.item()), int(nloc), geom))
+    except Exception as e:  # report instead of leaving the parent waiting
+        q.put((rank, f"error: {e!r}"))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind,t", [(2, "bands2d", 4), (2, "aniso3d", 8), (4, "bands2d", 8),
+                                          (4, "aniso3d", 4), (2, "general", 4), (4, "general", 8)])
+def test_distributed_spmm_gram_protocol(world, kind, t):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, t, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    errors = [r for r in res if len(r) == 2]
+    for p in procs:
+        p.join(timeout=60)
+        if errors and p.is_alive():
+            p.kill()
+    assert not errors, errors
+    for p in procs:
+        assert p.exitcode == 0
+    res.sort()
+    n = _matrix(kind).n
+    assert sum(r[5] for r in res) == n
+    for rank, bitwise, interior_ok, gram_err, tmax, nloc, geom in res:
+        assert bitwise, (rank, kind)
+        assert interior_ok
+        assert gram_err <= 1e-13
+        assert tmax == float(world)
+        if kind == "bands2d":  # 24-wide grid, ≥ 6 grid rows per slab: the middle rows are interior
+            assert geom["interior_hi"] - geom["interior_lo"] >= nloc - 2 * 24
+    if kind == "bands2d":
+        # first rank has no lower ghosts, last rank no upper ghosts
+        assert res[0][6]["halo_before"] == 0 and res[-1][6]["halo_after"] == 0
+
+
+def test_slabs_are_unions_of_domains():
+    for n, t, world in [(262144, 16, 4), (16777216, 64, 8), (2097152, 32, 2), (4099, 8, 4)]:
+        prev = 0
+        for r in range(world):
+            lo, hi = slab(r, world, n, t)
+            assert lo == prev
+            prev = hi
+            for d in range(r * (t // world), (r + 1) * (t // world)):
+                assert lo <= d * n // t and (d + 1) * n // t <= hi
+        assert prev == n
+
+
+def test_plan_halo_single_rank_is_identity():
+    import paper_1804_10629_b200 as eks
+    A = ei.poisson2d(10)
+    ext, need, geom = eks.eks_plan_halo(0, 1, np.array([0, A.n]), A.row_ptr, A.col)
+    assert np.array_equal(ext, A.col) and not need.any()
+    assert geom == dict(halo_before=0, halo_after=0, interior_lo=0, interior_hi=A.n)
