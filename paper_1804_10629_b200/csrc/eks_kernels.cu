@@ -471,81 +471,81 @@ cudaError_t launch_ts_update(cudaStream_t st, int t, int64_t n, int nq, const do
 
 // ============================================================================
 // Small Cholesky B = RᵀR (A-CholQR), explicit R⁻¹, alpha = R⁻ᵀ g.
-// Same loop order as the oracle, no fma (__dmul_rn/__dsub_rn) — bitwise equal
-// R for equal B (reading R20).  Breakdown rule: pivot <= t·2^-52·max|B| (R6).
+// Right-looking: at step k the trailing entries get B_ij -= R_ki·R_kj (product
+// rounded, then subtracted, no fma), so every entry sees exactly the
+// subtractions of the oracle's left-looking loop in the same order — R is
+// bitwise equal to or_chol for equal B (reading R20), while each step is one
+// parallel sweep instead of a serial dot product.  Breakdown: pivot <= t·2^-52·max|B| (R6).
+// R⁻¹ by the mirrored right-looking backward substitution.
 // ============================================================================
 template <int T>
-__global__ void k_chol(const double* __restrict__ B, const double* __restrict__ g, double* __restrict__ Rout,
-                       double* __restrict__ Rinv, double* __restrict__ alpha, int* flag, int gblock) {
+__global__ void __launch_bounds__(256) k_chol(const double* __restrict__ B, const double* __restrict__ g,
+                                              double* __restrict__ Rout, double* __restrict__ Rinv,
+                                              double* __restrict__ alpha, int* flag, int gblock) {
   extern __shared__ double csm[];
-  double(*sB)[T + 1] = reinterpret_cast<double(*)[T + 1]>(csm);
-  double(*sR)[T + 1] = reinterpret_cast<double(*)[T + 1]>(csm + T * (T + 1));
-  double(*sRi)[T + 1] = reinterpret_cast<double(*)[T + 1]>(csm + 2 * T * (T + 1));
-  __shared__ double sred[32];
+  double(*sA)[T + 1] = reinterpret_cast<double(*)[T + 1]>(csm);                  // trailing matrix
+  double(*sR)[T + 1] = reinterpret_cast<double(*)[T + 1]>(csm + T * (T + 1));      // R
+  double(*sY)[T + 1] = reinterpret_cast<double(*)[T + 1]>(csm + 2 * T * (T + 1));  // R⁻¹
+  __shared__ double sred[8];
+  __shared__ double sg[T];
   __shared__ int sfail;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < T * T; e += blockDim.x) {
-    sB[e / T][e % T] = B[e];
-    sR[e / T][e % T] = 0.0;
-    sRi[e / T][e % T] = 0.0;
-  }
-  if (tid == 0) sfail = 0;
-  __syncthreads();
+  const int tid = threadIdx.x, nth = blockDim.x;
   double m = 0.0;
-  for (int e = tid; e < T * T; e += blockDim.x) {
+  for (int e = tid; e < T * T; e += nth) {
     const int i = e / T, j = e % T;
-    if (j >= i) m = fmax(m, fabs(sB[i][j]));
+    const double b = B[e];
+    sA[i][j] = b;
+    sR[i][j] = 0.0;
+    sY[i][j] = (i == j) ? 1.0 : 0.0;
+    if (j >= i) m = fmax(m, fabs(b));
   }
+  if (g != nullptr && tid < T) sg[tid] = g[tid];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
   if ((tid & 31) == 0) sred[tid >> 5] = m;
+  if (tid == 0) sfail = 0;
   __syncthreads();
-  if (tid == 0) {
-    double bm = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) bm = fmax(bm, sred[w]);
-    sred[0] = bm;
-  }
-  __syncthreads();
-  const double thr = __dmul_rn((double)T * 0x1p-52, sred[0]);
+  double bm = 0.0;
+  for (int w = 0; w < (nth >> 5); ++w) bm = fmax(bm, sred[w]);
+  const double thr = __dmul_rn((double)T * 0x1p-52, bm);
   for (int k = 0; k < T; ++k) {
     if (tid == 0) {
-      double d = sB[k][k];
-      for (int i = 0; i < k; ++i) d = __dsub_rn(d, __dmul_rn(sR[i][k], sR[i][k]));
+      const double d = sA[k][k];
       if (!(d > thr)) sfail = 1;
       sR[k][k] = __dsqrt_rn(d);
     }
     __syncthreads();
     const double rkk = sR[k][k];
-    for (int j = k + 1 + tid; j < T; j += blockDim.x) {
-      double v = sB[k][j];
-      for (int i = 0; i < k; ++i) v = __dsub_rn(v, __dmul_rn(sR[i][k], sR[i][j]));
-      sR[k][j] = __ddiv_rn(v, rkk);
+    for (int j = k + 1 + tid; j < T; j += nth) sR[k][j] = __ddiv_rn(sA[k][j], rkk);
+    __syncthreads();
+    const int m1 = T - k - 1;  // trailing upper triangle (i <= j, both > k)
+    for (int e = tid; e < m1 * m1; e += nth) {
+      const int i = k + 1 + e / m1, j = k + 1 + e % m1;
+      if (j >= i) sA[i][j] = __dsub_rn(sA[i][j], __dmul_rn(sR[k][i], sR[k][j]));
     }
     __syncthreads();
   }
-  // R⁻¹ column by column (upper triangular back substitution)
-  for (int j = tid; j < T; j += blockDim.x) {
-    sRi[j][j] = __ddiv_rn(1.0, sR[j][j]);
-    for (int i = j - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int l = i + 1; l <= j; ++l) s = __fma_rn(sR[i][l], sRi[l][j], s);
-      sRi[i][j] = -__ddiv_rn(s, sR[i][i]);
+  // R X = I, X upper triangular: X_k· = Y_k· / R_kk, then Y_i· -= R_ik X_k· for i < k (k descending)
+  for (int k = T - 1; k >= 0; --k) {
+    const double rkk = sR[k][k];
+    for (int j = k + tid; j < T; j += nth) sY[k][j] = __ddiv_rn(sY[k][j], rkk);
+    __syncthreads();
+    const int w = T - k;
+    for (int e = tid; e < k * w; e += nth) {
+      const int i = e / w, j = k + e % w;
+      sY[i][j] = __fma_rn(-sR[i][k], sY[k][j], sY[i][j]);
     }
+    __syncthreads();
   }
-  __syncthreads();
-  for (int e = tid; e < T * T; e += blockDim.x) {
+  for (int e = tid; e < T * T; e += nth) {
     if (Rout) Rout[e] = sR[e / T][e % T];
-    Rinv[e] = sRi[e / T][e % T];
+    Rinv[e] = sY[e / T][e % T];
   }
   if (g != nullptr && alpha != nullptr) {
-    // alpha = R⁻ᵀ g = Rinvᵀ g: alpha_j = Σ_{i<=j} Rinv[i][j] g_i, one thread per j
-    double* sg = &sB[0][0];  // B is no longer needed
-    __syncthreads();
-    for (int j = tid; j < T; j += blockDim.x) sg[j] = g[j];
-    __syncthreads();
-    for (int j = tid; j < T; j += blockDim.x) {
+    // alpha = R⁻ᵀ g: alpha_j = Σ_{i<=j} Rinv[i][j] g_i
+    for (int j = tid; j < T; j += nth) {
       double a = 0.0;
-      for (int i = 0; i <= j; ++i) a = __fma_rn(sRi[i][j], sg[i], a);
+      for (int i = 0; i <= j; ++i) a = __fma_rn(sY[i][j], sg[i], a);
       alpha[j] = a;
     }
   }
@@ -557,8 +557,7 @@ cudaError_t launch_chol(cudaStream_t st, int t, const double* B, const double* g
   EKS_DISPATCH_T(t, {
     const size_t sm = (size_t)3 * T * (T + 1) * 8;
     cudaFuncSetAttribute(k_chol<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    // one warp for t <= 32 (cheaper barriers on the serial factorization), two for t = 64
-    k_chol<T><<<1, T > 32 ? 64 : 32, sm, st>>>(B, g, R, Rinv, alpha, flag, gblock);
+    k_chol<T><<<1, 256, sm, st>>>(B, g, R, Rinv, alpha, flag, gblock);
   });
   return cudaGetLastError();
 }

@@ -250,17 +250,15 @@ __global__ void __launch_bounds__(256, 1)
 // ----------------------------------------------------------------------------
 template <int T>
 struct ApCfg {
-  static constexpr int TR = (T == 8) ? 64 : 32;
+  static constexpr int TR = 64;  // 8 warps × 8 rows: every warp owns complete rows
   static constexpr int S = T + 4;
   static constexpr int TILE = TR * S;
   static constexpr int STAGE = 2 * TILE + 3 * TR;  // Z2, AZ2 tiles + r_in, dx, x vectors
   static constexpr int NSA = (100 * 1024 / 8 - T * (T + 4)) / STAGE;
   static constexpr int NS0 = NSA >= 3 ? NSA : (200 * 1024 / 8 - T * (T + 4)) / STAGE;
   static constexpr int NS = NS0 > 8 ? 8 : (NS0 < 2 ? 2 : NS0);
-  static constexpr int UT = (TR / 8) * (T / 8);
-  static constexpr int UPW = UT / 8;
-  static constexpr int NT = T / 8;
-  static constexpr int SMEM = NS * STAGE + T * (T + 4) + T + 2 * TR * NT;
+  static constexpr int NT = T / 8;  // column tiles per row group (all in the same warp)
+  static constexpr int SMEM = NS * STAGE + T * (T + 4) + T;
 };
 
 template <int T>
@@ -279,8 +277,6 @@ __global__ void __launch_bounds__(256, 1)
   const int ntiles = (int)((hi - lo + K::TR - 1) / K::TR);
   double* sRi = sm + K::NS * K::STAGE;
   double* sA = sRi + T * SR;
-  double* su = sA + T;            // [TR][NT]: W·alpha partial per row and column tile
-  double* sq = su + K::TR * K::NT;  // [TR][NT]: AW·alpha
   const bool first = mode & 1, last = mode & 2, basis = mode & 4;
   const bool skip = basis || (flag != nullptr && *flag != INT_MAX);
   for (int e = tid; e < T * T; e += 256) sRi[(e / T) * SR + e % T] = Rinv[e];
@@ -314,53 +310,42 @@ __global__ void __launch_bounds__(256, 1)
     const double* sv = sZ + 2 * K::TILE;
     const int64_t row = lo + (int64_t)i * K::TR;
     const int rows = (int)((hi - row) < K::TR ? (hi - row) : K::TR);
+    // warp `warp` owns rows 8·warp … 8·warp+7 of the tile, all NT column tiles
+    const int rr = warp * 8 + g;
+    double pu = 0.0, pq = 0.0;  // row dot products with alpha, summed over column tiles in order
 #pragma unroll
-    for (int u = 0; u < K::UPW; ++u) {
-      const int tile = warp * K::UPW + u;
-      const int mi = tile / K::NT, ni = tile % K::NT;
+    for (int ni = 0; ni < K::NT; ++ni) {
       double w0 = 0.0, w1 = 0.0, y0 = 0.0, y1 = 0.0;
 #pragma unroll
       for (int kk = 0; kk < T; kk += 4) {
         const double b = sRi[(kk + q4) * SR + ni * 8 + g];
-        dmma(w0, w1, sZ[(mi * 8 + g) * S + kk + q4], b);
-        dmma(y0, y1, sY[(mi * 8 + g) * S + kk + q4], b);
+        dmma(w0, w1, sZ[rr * S + kk + q4], b);
+        dmma(y0, y1, sY[rr * S + kk + q4], b);
       }
-      const int rr = mi * 8 + g, c = ni * 8 + 2 * q4;
+      const int c = ni * 8 + 2 * q4;
       if (rr < rows) {
         *reinterpret_cast<double2*>(Z2W + (row + rr) * T + c) = make_double2(w0, w1);
         *reinterpret_cast<double2*>(AZ2AW + (row + rr) * T + c) = make_double2(y0, y1);
       }
-      // row dot products with alpha: sum the row group's 4 lanes, keep one value per (row, column tile)
-      double pu = fma(w0, sA[c], w1 * sA[c + 1]);
-      double pq = fma(y0, sA[c], y1 * sA[c + 1]);
-      pu += __shfl_xor_sync(0xffffffffu, pu, 1);
-      pq += __shfl_xor_sync(0xffffffffu, pq, 1);
-      pu += __shfl_xor_sync(0xffffffffu, pu, 2);
-      pq += __shfl_xor_sync(0xffffffffu, pq, 2);
-      if (q4 == 0) {
-        su[rr * K::NT + ni] = pu;
-        sq[rr * K::NT + ni] = pq;
-      }
+      double tu = fma(w0, sA[c], w1 * sA[c + 1]);
+      double tq = fma(y0, sA[c], y1 * sA[c + 1]);
+      tu += __shfl_xor_sync(0xffffffffu, tu, 1);
+      tq += __shfl_xor_sync(0xffffffffu, tq, 1);
+      tu += __shfl_xor_sync(0xffffffffu, tu, 2);
+      tq += __shfl_xor_sync(0xffffffffu, tq, 2);
+      pu += tu;
+      pq += tq;
     }
-    __syncthreads();
-    if (!skip) {
-      for (int rr = tid; rr < rows; rr += 256) {
-        double u = 0.0, qv = 0.0;
-#pragma unroll
-        for (int cn = 0; cn < K::NT; ++cn) {
-          u += su[rr * K::NT + cn];
-          qv += sq[rr * K::NT + cn];
-        }
-        const int64_t rg = row + rr;
-        const double dxi = first ? u : sv[K::TR + rr] + u;
-        const double rn = sv[rr] - qv;
-        rnew[rg] = rn;
-        if (last) {
-          x[rg] = sv[2 * K::TR + rr] + dxi;
-          rr_acc = fma(rn, rn, rr_acc);
-        } else {
-          dx[rg] = dxi;
-        }
+    if (!skip && q4 == 0 && rr < rows) {
+      const int64_t rg = row + rr;
+      const double dxi = first ? pu : sv[K::TR + rr] + pu;
+      const double rn = sv[rr] - pq;
+      rnew[rg] = rn;
+      if (last) {
+        x[rg] = sv[2 * K::TR + rr] + dxi;
+        rr_acc = fma(rn, rn, rr_acc);
+      } else {
+        dx[rg] = dxi;
       }
     }
   }
