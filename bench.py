@@ -293,6 +293,14 @@ def main():
 
     roofline = roof(dom)
     spmm_roof = roof("spmm")
+    # DRAM traffic per launch of the same kernel from the committed ncu --set full capture
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
+    if os.path.exists(tf) and args.workload == "cfg2":
+        tr = json.load(open(tf)).get("classes", {})
+        for rf in (roofline, spmm_roof):
+            if rf is not None and tr.get(rf["kernel"]):
+                rf["traffic"] = tr[rf["kernel"]]
+                rf["traffic_source"] = "profiles/ncu_traffic_r01.json (ncu dram__bytes_read+write per launch)"
     share = {c: agg["ms"][c] / max(1e-9, sum(agg["ms"].values())) for c in agg["ms"]}
 
     # ---------------- e2e: C-ABI with pinned HOST buffers, setup + solve per step, wall clock

@@ -69,6 +69,9 @@ struct eks_ctx {
   size_t part_cap = 0;  // doubles
   double *C1 = nullptr, *C2 = nullptr;
   size_t C_cap = 0;
+  double* part2 = nullptr;  // per-CTA partials of the fused next-block C1
+  size_t part2_cap = 0;
+  bool c1_ready = false;    // C1 of the next CGS pass already reduced into C1
   double *Bg = nullptr, *Rm = nullptr, *Rinv = nullptr, *alpha = nullptr, *scal = nullptr;
   int alpha_cap = 0;
   int* flag = nullptr;
@@ -200,6 +203,10 @@ void free_workspace(eks_ctx* c) {
   dfree(c->flag);
   c->flag = nullptr;
   c->part_cap = c->C_cap = 0;
+  dfree(c->part2);
+  c->part2 = nullptr;
+  c->part2_cap = 0;
+  c->c1_ready = false;
   c->alpha_cap = 0;
   c->ws_t = 0;
 }
@@ -422,8 +429,11 @@ eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const doubl
 eks_status cgs2(eks_ctx* ctx, int t, const std::vector<const double*>& Q, const std::vector<const double*>& AQ,
                 const double* Z, double* Zout) {
   const int nq = (int)Q.size();
-  ST(ensure_C(ctx, (size_t)nq * t * t));
-  ST(tn_reduce(ctx, t, nq, AQ.data(), Z, nullptr, ctx->C1));  // C1 = (AQ)ᵀ Z
+  if (!ctx->c1_ready) {
+    ST(ensure_C(ctx, (size_t)nq * t * t));
+    ST(tn_reduce(ctx, t, nq, AQ.data(), Z, nullptr, ctx->C1));  // C1 = (AQ)ᵀ Z
+  }
+  ctx->c1_ready = false;  // (else C1 came fused from the previous block's R⁻¹ kernel)
   if (eks::sweep_supported(t) && eks::sweep_fused_supported(t, nq)) {
     ST(update_coef(ctx, t, nq, Q.data(), AQ.data(), ctx->C1, Z, ctx->Z1.loc, ctx->C2));  // Z1, C2 = (AQ)ᵀ Z1
   } else {
@@ -537,13 +547,43 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
   ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg));
   ST(chol(ctx, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
           with_update ? ctx->alpha + alpha_off : nullptr, gb));
+  // SRE-CG: the next block's window is {W_prev, W_new} and its Z is AW_new, so the R⁻¹ kernel
+  // that produces AW_new also accumulates the next CGS pass-1 coefficients C1 = [AW_prev, AW_new]ᵀAW_new.
+  const int c1n = (ring && eks::apply_c1_supported(t, 2)) ? (nblocks == 0 ? 1 : 2) : 0;
+  if (c1n) {
+    ST(ensure_C(ctx, (size_t)2 * t * t));
+    if (ctx->part2_cap < (size_t)ctx->nblk * 2 * t * t) {
+      dfree(ctx->part2);
+      ctx->part2 = nullptr;
+      ST(dalloc(ctx, &ctx->part2, (size_t)ctx->nblk * 2 * t * t));
+      ctx->part2_cap = (size_t)ctx->nblk * 2 * t * t;
+    }
+  }
   {
     KScope k(ctx, EKS_K_APPLY);
-    account(ctx, EKS_K_APPLY, 8.0 * ctx->n * (4.0 * t + 4.0), 2.0 * ctx->n * t * (t + 2));
-    auto fn = eks::sweep_supported(t) ? eks::launch_apply_tc : eks::launch_apply;
-    CK(fn(ctx->stream, t, ctx->n, Wn->loc, AWn->loc, ctx->Rinv, with_update ? ctx->alpha + alpha_off : nullptr,
-          ctx->xv.loc, ctx->dx, ctx->r, ctx->rnew, ctx->part, ctx->flag, mode, ctx->nblk));
-    ctx->rho_nblk = eks::sweep_supported(t) ? eks::sweep_last_grid() : ctx->nblk;
+    account(ctx, EKS_K_APPLY, 8.0 * ctx->n * (4.0 * t + 4.0 + (c1n == 2 ? t : 0)),
+            2.0 * ctx->n * t * (t + 2 + c1n * t));
+    if (eks::sweep_supported(t)) {
+      CK(eks::launch_apply_tc(ctx->stream, t, ctx->n, Wn->loc, AWn->loc, ctx->Rinv,
+                              with_update ? ctx->alpha + alpha_off : nullptr, ctx->xv.loc, ctx->dx, ctx->r, ctx->rnew,
+                              ctx->part, ctx->flag, mode, ctx->nblk, c1n,
+                              c1n == 2 ? ctx->AWpool[(nblocks - 1) % ring].loc : nullptr, ctx->part2));
+      ctx->rho_nblk = eks::sweep_last_grid();
+    } else {
+      CK(eks::launch_apply(ctx->stream, t, ctx->n, Wn->loc, AWn->loc, ctx->Rinv,
+                           with_update ? ctx->alpha + alpha_off : nullptr, ctx->xv.loc, ctx->dx, ctx->r, ctx->rnew,
+                           ctx->part, ctx->flag, mode, ctx->nblk));
+      ctx->rho_nblk = ctx->nblk;
+    }
+  }
+  if (c1n) {
+    {
+      KScope k(ctx, EKS_K_REDUCE);
+      CK(eks::launch_reduce(ctx->stream, ctx->part2, ctx->rho_nblk, (size_t)c1n * t * t, (size_t)c1n * t * t,
+                            ctx->C1));
+    }
+    ST(allreduce(ctx, ctx->C1, (size_t)c1n * t * t));
+    ctx->c1_ready = true;
   }
   return EKS_OK;
 }
@@ -646,6 +686,7 @@ void begin_run(eks_ctx* ctx, const eks_options* opt) {
   ctx->prof = eks_profile{};
   ctx->launches = 0;
   ctx->model_bytes = ctx->model_flops = 0.0;
+  ctx->c1_ready = false;
 }
 
 }  // namespace
@@ -823,9 +864,10 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   ctx->have_matrix = false;
   std::vector<int32_t> rp32(n + 1);
   for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)rp[i];
-  CK(cudaMalloc((void**)&ctx->d_rp, sizeof(int) * (n + 1)));
-  CK(cudaMalloc((void**)&ctx->d_col, sizeof(int) * (nnz ? nnz : 1)));
-  CK(cudaMalloc((void**)&ctx->d_val, sizeof(double) * (nnz ? nnz : 1)));
+  // +16 bytes of padding: the fused SpMM copies aligned 16-byte chunks that may run past the end
+  CK(cudaMalloc((void**)&ctx->d_rp, sizeof(int) * (n + 1) + 16));
+  CK(cudaMalloc((void**)&ctx->d_col, sizeof(int) * nnz + 16));
+  CK(cudaMalloc((void**)&ctx->d_val, sizeof(double) * nnz + 16));
   CK(cudaMemcpy(ctx->d_rp, rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->d_col, ecol.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->d_val, val.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
@@ -1103,9 +1145,12 @@ eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double
   if (W != Z) CK(cudaMemcpyAsync(W, Z, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
   ST(spmm_gram(ctx, wb, AW, t, nullptr, ctx->Bg));
   ST(chol(ctx, t, ctx->Bg, nullptr, ctx->Rm, ctx->Rinv, nullptr, 0));
-  auto fn = eks::sweep_supported(t) ? eks::launch_apply_tc : eks::launch_apply;
-  CK(fn(ctx->stream, t, ctx->n, W, AW, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 4,
-        ctx->nblk));
+  if (eks::sweep_supported(t))
+    CK(eks::launch_apply_tc(ctx->stream, t, ctx->n, W, AW, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr,
+                            nullptr, nullptr, 4, ctx->nblk));
+  else
+    CK(eks::launch_apply(ctx->stream, t, ctx->n, W, AW, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr,
+                         nullptr, nullptr, 4, ctx->nblk));
   if (R) CK(cudaMemcpyAsync(R, ctx->Rm, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
   if (B) CK(cudaMemcpyAsync(B, ctx->Bg, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
   ST(sync_scalars(ctx, 1));

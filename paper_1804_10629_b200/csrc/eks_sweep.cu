@@ -42,7 +42,10 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ int64_t chunk_lo(int64_t n, int b, int nb) { return (int64_t)b * n / nb; }
+// CTA b's rows start at a multiple of 8 (16-byte alignment of every int32/fp64 row-indexed copy).
+__device__ __forceinline__ int64_t chunk_lo(int64_t n, int b, int nb) {
+  return b >= nb ? n : (((int64_t)b * n / nb) & ~(int64_t)7);
+}
 
 // Copy rows [row, row+rows) of a row-major n×T block into a padded smem tile
 // (row stride S doubles); rows rows..TR-1 are zero-filled.  All threads take part.
@@ -248,26 +251,35 @@ __global__ void __launch_bounds__(256, 1)
 // W = Z2·R⁻¹, AW = AZ2·R⁻¹ (in place) and the fused x/r update of the block
 // (see launch_apply).  Same pipeline; both products on DMMA.
 // ----------------------------------------------------------------------------
-template <int T>
+template <int T, int C1N>
 struct ApCfg {
   static constexpr int TR = 64;  // 8 warps × 8 rows: every warp owns complete rows
   static constexpr int S = T + 4;
   static constexpr int TILE = TR * S;
-  static constexpr int STAGE = 2 * TILE + 3 * TR;  // Z2, AZ2 tiles + r_in, dx, x vectors
+  // Z2, AZ2 tiles (+ AW_prev tile when C1N == 2) + r_in, dx, x vectors
+  static constexpr int STAGE = (C1N == 2 ? 3 : 2) * TILE + 3 * TR;
   static constexpr int NSA = (100 * 1024 / 8 - T * (T + 4)) / STAGE;
   static constexpr int NS0 = NSA >= 3 ? NSA : (200 * 1024 / 8 - T * (T + 4)) / STAGE;
   static constexpr int NS = NS0 > 8 ? 8 : (NS0 < 2 ? 2 : NS0);
   static constexpr int NT = T / 8;  // column tiles per row group (all in the same warp)
-  static constexpr int SMEM = NS * STAGE + T * (T + 4) + T;
+  // fused next-pass coefficients C1 = [AW_prev, AW]ᵀ AW: C1N·(T/8)² output tiles over 8 warps
+  static constexpr int MT = T / 8;
+  static constexpr int OT = C1N * MT * MT;
+  static constexpr int WS = (C1N == 0) ? 1 : (OT >= 8 ? 1 : 8 / OT);
+  static constexpr int TPW = (C1N == 0) ? 1 : (OT >= 8 ? OT / 8 : 1);
+  static constexpr int RED = (WS > 1 ? 8 * C1N * T * T : 0);
+  static constexpr int SMEM0 = NS * STAGE + T * (T + 4) + T;
+  static constexpr int SMEM = SMEM0 > RED ? SMEM0 : RED;
 };
 
-template <int T>
+template <int T, int C1N>
 __global__ void __launch_bounds__(256, 1)
     k_apply_tc(int64_t n, double* Z2W, double* AZ2AW, const double* __restrict__ Rinv,
                const double* __restrict__ alpha, double* __restrict__ x, double* __restrict__ dx,
                const double* __restrict__ r, double* __restrict__ rnew, double* __restrict__ rho_part,
-               const int* __restrict__ flag, int mode) {
-  using K = ApCfg<T>;
+               const int* __restrict__ flag, int mode, const double* __restrict__ AWprev,
+               double* __restrict__ c1part) {
+  using K = ApCfg<T, C1N>;
   constexpr int S = K::S, SR = T + 4;
   extern __shared__ __align__(128) double sm[];
   __shared__ double sred[8];
@@ -281,6 +293,7 @@ __global__ void __launch_bounds__(256, 1)
   const bool skip = basis || (flag != nullptr && *flag != INT_MAX);
   for (int e = tid; e < T * T; e += 256) sRi[(e / T) * SR + e % T] = Rinv[e];
   for (int e = tid; e < T; e += 256) sA[e] = alpha ? alpha[e] : 0.0;
+  constexpr int VOFF = (C1N == 2 ? 3 : 2) * K::TILE;  // vectors after the tiles
   auto issue = [&](int i) {
     if (i < ntiles) {
       const int s = i % K::NS;
@@ -289,8 +302,9 @@ __global__ void __launch_bounds__(256, 1)
       double* st = sm + s * K::STAGE;
       tile_async<T, S, K::TR>(st, Z2W, row, rows);
       tile_async<T, S, K::TR>(st + K::TILE, AZ2AW, row, rows);
+      if constexpr (C1N == 2) tile_async<T, S, K::TR>(st + 2 * K::TILE, AWprev, row, rows);
       if (!skip) {
-        double* sv = st + 2 * K::TILE;
+        double* sv = st + VOFF;
         vec_async<K::TR>(sv, first ? r : rnew, row, rows);
         if (!first) vec_async<K::TR>(sv + K::TR, dx, row, rows);
         if (last) vec_async<K::TR>(sv + 2 * K::TR, x, row, rows);
@@ -301,18 +315,22 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
   for (int i = 0; i < K::NS - 1; ++i) issue(i);
   double rr_acc = 0.0;
+  double acc[K::TPW][2];
+#pragma unroll
+  for (int u = 0; u < K::TPW; ++u) acc[u][0] = acc[u][1] = 0.0;
   for (int i = 0; i < ntiles; ++i) {
     cp_wait<K::NS - 2>();
     __syncthreads();
     issue(i + K::NS - 1);
-    const double* sZ = sm + (i % K::NS) * K::STAGE;
-    const double* sY = sZ + K::TILE;
-    const double* sv = sZ + 2 * K::TILE;
+    double* sZ = sm + (i % K::NS) * K::STAGE;
+    double* sY = sZ + K::TILE;
+    const double* sv = sZ + VOFF;
     const int64_t row = lo + (int64_t)i * K::TR;
     const int rows = (int)((hi - row) < K::TR ? (hi - row) : K::TR);
     // warp `warp` owns rows 8·warp … 8·warp+7 of the tile, all NT column tiles
     const int rr = warp * 8 + g;
     double pu = 0.0, pq = 0.0;  // row dot products with alpha, summed over column tiles in order
+    double yk[K::NT][2];
 #pragma unroll
     for (int ni = 0; ni < K::NT; ++ni) {
       double w0 = 0.0, w1 = 0.0, y0 = 0.0, y1 = 0.0;
@@ -327,6 +345,8 @@ __global__ void __launch_bounds__(256, 1)
         *reinterpret_cast<double2*>(Z2W + (row + rr) * T + c) = make_double2(w0, w1);
         *reinterpret_cast<double2*>(AZ2AW + (row + rr) * T + c) = make_double2(y0, y1);
       }
+      yk[ni][0] = y0;
+      yk[ni][1] = y1;
       double tu = fma(w0, sA[c], w1 * sA[c + 1]);
       double tq = fma(y0, sA[c], y1 * sA[c + 1]);
       tu += __shfl_xor_sync(0xffffffffu, tu, 1);
@@ -348,6 +368,29 @@ __global__ void __launch_bounds__(256, 1)
         dx[rg] = dxi;
       }
     }
+    if constexpr (C1N > 0) {
+      // AW tile replaces the AZ2 tile in place (each warp owns its rows), then
+      // C1 partial += [AW_prev, AW]ᵀ AW over the tile (next block's CGS pass 1)
+#pragma unroll
+      for (int ni = 0; ni < K::NT; ++ni) {
+        sY[rr * S + ni * 8 + 2 * q4] = yk[ni][0];
+        sY[rr * S + ni * 8 + 2 * q4 + 1] = yk[ni][1];
+      }
+      __syncthreads();
+      const int slice = warp % K::WS;
+#pragma unroll
+      for (int u = 0; u < K::TPW; ++u) {
+        const int tile = (warp / K::WS) * K::TPW + u;
+        const int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
+        const double* sL = (C1N == 2 && l == 0) ? sZ + 2 * K::TILE : sY;
+        double d0 = acc[u][0], d1 = acc[u][1];
+#pragma unroll
+        for (int kk = slice * 4; kk < K::TR; kk += 4 * K::WS)
+          dmma(d0, d1, sL[(kk + q4) * S + mi * 8 + g], sY[(kk + q4) * S + ni * 8 + g]);
+        acc[u][0] = d0;
+        acc[u][1] = d1;
+      }
+    }
   }
   cp_wait<0>();
   if (last && rho_part != nullptr) {
@@ -359,6 +402,36 @@ __global__ void __launch_bounds__(256, 1)
       double sacc = 0.0;
       for (int w = 0; w < 8; ++w) sacc += sred[w];
       rho_part[blockIdx.x] = sacc;
+    }
+  }
+  if constexpr (C1N > 0) {
+    double* out = c1part + (size_t)blockIdx.x * C1N * T * T;
+    __syncthreads();
+    if constexpr (K::WS == 1) {
+#pragma unroll
+      for (int u = 0; u < K::TPW; ++u) {
+        const int tile = warp * K::TPW + u;
+        const int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
+        *reinterpret_cast<double2*>(out + l * T * T + (mi * 8 + g) * T + ni * 8 + 2 * q4) =
+            make_double2(acc[u][0], acc[u][1]);
+      }
+    } else {
+      double* red = sm;
+      {
+        const int tile = warp / K::WS;
+        const int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
+        double* dst = red + (size_t)warp * C1N * T * T + l * T * T;
+        dst[(mi * 8 + g) * T + ni * 8 + 2 * q4] = acc[0][0];
+        dst[(mi * 8 + g) * T + ni * 8 + 2 * q4 + 1] = acc[0][1];
+      }
+      __syncthreads();
+      for (int e = tid; e < C1N * T * T; e += 256) {
+        const int l = e / (T * T), m = (e / T) % T, nn = e % T;
+        const int tile = l * K::MT * K::MT + (m / 8) * K::MT + nn / 8;
+        double sacc = 0.0;
+        for (int w = tile * K::WS; w < tile * K::WS + K::WS; ++w) sacc += red[(size_t)w * C1N * T * T + e];
+        out[e] = sacc;
+      }
     }
   }
 }
@@ -374,15 +447,15 @@ __global__ void __launch_bounds__(256, 1)
 // ----------------------------------------------------------------------------
 template <int T>
 struct SgCfg {
-  static constexpr int TR = (T == 8) ? 64 : 32;
+  static constexpr int TR = 64;
   static constexpr int S = T + 4;
   static constexpr int G = T / 2;         // threads per row (2 columns each)
   static constexpr int RPP = 256 / G;      // rows per pass
   static constexpr int PASSES = TR / RPP;
   static constexpr int MAXROW = 8;         // entries per row supported by the staged path
-  static constexpr int ECAP = TR * MAXROW;
-  // stage layout (doubles): X tile | r tile | val[ECAP] | col[ECAP] (ints) + rp[TR+1] (ints)
-  static constexpr int STAGE = TR * S + TR + ECAP + (ECAP + TR + 2) / 2 + 1;
+  static constexpr int ECAP = TR * MAXROW + 4;  // + alignment slack of the 16-byte copies
+  // stage layout (doubles): X tile | r tile | val[ECAP] | col[ECAP] (ints) | rp[TR+4] (ints)
+  static constexpr int STAGE = TR * S + TR + ECAP + (ECAP + TR + 4) / 2 + 2;
   static constexpr int YT = TR * S;        // Y tile (single buffer)
   static constexpr int NSA = (100 * 1024 / 8 - YT) / STAGE;
   static constexpr int NS = NSA > 6 ? 6 : (NSA < 3 ? 3 : NSA);
@@ -432,13 +505,14 @@ __global__ void __launch_bounds__(256, (T <= 16 ? 3 : 2))
       double* sval = st + K::TR * S + K::TR;
       int* scol = reinterpret_cast<int*>(sval + K::ECAP);
       int* srp = scol + K::ECAP;
-      const int ne = pe - pb;
-      for (int e = tid; e < ne; e += 256) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr(sval + e)), "l"(val + pb + e) : "memory");
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr(scol + e)), "l"(col + pb + e) : "memory");
+      // 16-byte chunks of the aligned-down ranges (the device CSR arrays are padded by 16 bytes)
+      const int pv = pb & ~1, pc = pb & ~3;
+      const int nv = (pe - pv + 1) >> 1, nc = (pe - pc + 3) >> 2, nr = (rows + 4) >> 2;
+      for (int e = tid; e < nv + nc + nr; e += 256) {
+        if (e < nv) cp16(sval + 2 * e, val + pv + 2 * e, 16);
+        else if (e < nv + nc) cp16(scol + 4 * (e - nv), col + pc + 4 * (e - nv), 16);
+        else cp16(srp + 4 * (e - nv - nc), rp + row + 4 * (e - nv - nc), 16);
       }
-      for (int e = tid; e <= rows; e += 256)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr(srp + e)), "l"(rp + row + e) : "memory");
     }
     cp_commit();
   };
@@ -471,10 +545,10 @@ __global__ void __launch_bounds__(256, (T <= 16 ? 3 : 2))
       const int* nrp = ncol + K::ECAP;
       const int64_t nrow = row0_of(i + 1);
       const int nrows = (int)((hi - nrow) < K::TR ? (hi - nrow) : K::TR);
-      const int ne = nrp[nrows] - nrp[0];
+      const int ne = nrp[nrows] - nrp[0], nco = nrp[0] & 3;
       constexpr int LPR = (T * 8 + 127) / 128;  // 128-byte lines per X row
       for (int e = tid; e < ne * LPR; e += 256) {
-        const int c = ncol[e / LPR];
+        const int c = ncol[nco + e / LPR];
         if (c < nrow || c >= nrow + nrows)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(Xext + (int64_t)c * T + (e % LPR) * 16));
       }
@@ -487,7 +561,7 @@ __global__ void __launch_bounds__(256, (T <= 16 ? 3 : 2))
     const int* srp = scol + K::ECAP;
     const int64_t row = lo + (int64_t)i * K::TR;
     const int rows = (int)((hi - row) < K::TR ? (hi - row) : K::TR);
-    const int pbase = srp[0];
+    const int pbase = srp[0], vo = pbase & 1, co = pbase & 3;  // offsets of the aligned copies
     // ---------------- Y rows of the tile
 #pragma unroll
     for (int ps = 0; ps < K::PASSES; ++ps) {
@@ -500,11 +574,8 @@ __global__ void __launch_bounds__(256, (T <= 16 ? 3 : 2))
 #pragma unroll
         for (int k = 0; k < K::MAXROW; ++k)
           if (q0 + k < q1) {
-            a[k] = sval[q0 + k];
-            const int64_t c = scol[q0 + k];
-            const int64_t lr = c - row;  // single rank: extended index == local row
-            xv[k] = (lr >= 0 && lr < rows) ? *reinterpret_cast<const double2*>(sX + lr * S + 2 * gl)
-                                           : __ldg(reinterpret_cast<const double2*>(Xext + c * T) + gl);
+            a[k] = sval[vo + q0 + k];
+            xv[k] = __ldg(reinterpret_cast<const double2*>(Xext + (int64_t)scol[co + q0 + k] * T) + gl);
           }
 #pragma unroll
         for (int k = 0; k < K::MAXROW; ++k)
@@ -699,23 +770,50 @@ cudaError_t launch_spmm_gram(cudaStream_t st, int t, int64_t n, const int* rp, c
   return cudaGetLastError();
 }
 
+template <int T, int C1N>
+static cudaError_t apply_t(cudaStream_t st, int64_t n, double* Z2W, double* AZ2AW, const double* Rinv,
+                           const double* alpha, double* x, double* dx, const double* r, double* rnew,
+                           double* rho_part, const int* flag, int mode, const double* AWprev, double* c1part,
+                           int nblk) {
+  using K = ApCfg<T, C1N>;
+  const size_t sm = (size_t)K::SMEM * 8;
+  if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(k_apply_tc<T, C1N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_tc<T, C1N>, 256, sm);
+    if (occ < 1) occ = 1;
+  }
+  nblk = grid_for(nblk, occ);
+  t_last_grid = nblk;
+  k_apply_tc<T, C1N><<<nblk, 256, sm, st>>>(n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, rho_part, flag, mode,
+                                            AWprev, c1part);
+  return cudaGetLastError();
+}
+
+bool apply_c1_supported(int t, int c1n) {
+  if (!sweep_supported(t) || c1n < 0 || c1n > 2) return false;
+  switch (t) {
+    case 8: return ApCfg<8, 2>::SMEM * 8 <= 227 * 1024;
+    case 16: return ApCfg<16, 2>::SMEM * 8 <= 227 * 1024;
+    case 32: return ApCfg<32, 2>::SMEM * 8 <= 227 * 1024;
+    default: return c1n == 0 || ApCfg<64, 2>::SMEM * 8 <= 227 * 1024;
+  }
+}
+
 cudaError_t launch_apply_tc(cudaStream_t st, int t, int64_t n, double* Z2W, double* AZ2AW, const double* Rinv,
                             const double* alpha, double* x, double* dx, const double* r, double* rnew,
-                            double* rho_part, const int* flag, int mode, int nblk) {
+                            double* rho_part, const int* flag, int mode, int nblk, int c1n, const double* AWprev,
+                            double* c1part) {
   EKS_SW_T(t, {
-    using K = ApCfg<T>;
-    const size_t sm = (size_t)K::SMEM * 8;
-    static int occ = 0;
-    if (!occ) {
-      cudaFuncSetAttribute(k_apply_tc<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_tc<T>, 256, sm);
-      if (occ < 1) occ = 1;
-    }
-    nblk = grid_for(nblk, occ);
-    t_last_grid = nblk;
-    k_apply_tc<T><<<nblk, 256, sm, st>>>(n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, rho_part, flag, mode);
+    if (c1n == 0) return apply_t<T, 0>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, rho_part, flag, mode, AWprev,
+                                       c1part, nblk);
+    if (c1n == 1) return apply_t<T, 1>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, rho_part, flag, mode, AWprev,
+                                       c1part, nblk);
+    if (c1n == 2) return apply_t<T, 2>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, rho_part, flag, mode, AWprev,
+                                       c1part, nblk);
   });
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace eks

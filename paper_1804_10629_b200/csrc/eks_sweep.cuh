@@ -36,8 +36,12 @@ cudaError_t launch_spmm_gram(cudaStream_t st, int t, int64_t n, const int* rp, c
                              int nblk);
 
 // W = Z2·Rinv, AW = AZ2·Rinv in place + fused per-block x/r update (same contract as launch_apply).
+// c1n > 0 additionally writes per-CTA partials (layout [c1n][t][t]) of the next block's CGS pass-1
+// coefficients [AW_prev, AW]ᵀ AW (c1n = 2) or AWᵀAW (c1n = 1) into c1part — the SRE-CG window.
+bool apply_c1_supported(int t, int c1n);
 cudaError_t launch_apply_tc(cudaStream_t st, int t, int64_t n, double* Z2W, double* AZ2AW, const double* Rinv,
                             const double* alpha, double* x, double* dx, const double* r, double* rnew,
-                            double* rho_part, const int* flag, int mode, int nblk);
+                            double* rho_part, const int* flag, int mode, int nblk, int c1n = 0,
+                            const double* AWprev = nullptr, double* c1part = nullptr);
 
 }  // namespace eks
