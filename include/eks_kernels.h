@@ -38,6 +38,16 @@ eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double
 /* Cholesky alone: B (t×t device, upper triangle read) = RᵀR, R upper (device). */
 eks_status eks_k_chol(eks_ctx* ctx, int t, const double* B, double* R);
 
+/* Timing of the SpMM-block kernel on the device (bench.py's SpMM roofline and the
+ * kernel micro-benchmarks): `reps` back-to-back launches of Y = A·X between two CUDA
+ * events on the context stream after one warm-up launch; *ms = average per launch.
+ * variant 0: plain SpMM (k_spmm); 1: fused SpMM + Gram [XᵀY | Xᵀv] with per-CTA partials
+ * only; 2: + the tail reduction of the partials; 3: + the A-CholQR Cholesky in the last
+ * CTA (the configuration eks_solve runs on one rank).  v may be NULL.  Variants 1-3 need
+ * t in {8,16,32,64}. */
+eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, const double* v, int variant, int reps,
+                           double* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,7 @@ def lib():
             "eks_k_cgs2": [vp, i32, i32, vp, vp, vp, vp, vp],
             "eks_k_acholqr": [vp, i32, vp, vp, vp, vp, vp],
             "eks_k_chol": [vp, i32, vp, vp],
+            "eks_k_time_spmm": [vp, i32, vp, vp, vp, i32, i32, C.POINTER(d)],
             "eks_plan_halo": [i32, i32, vp, vp, vp, vp, vp, vp],
         }
         for name, args in sigs.items():
@@ -93,7 +94,7 @@ def lib():
 
 EXPORTED = ["eks_get_unique_id", "eks_create", "eks_set_stream", "eks_setup_csr", "eks_solve", "eks_solve_ex",
             "eks_basis_sweep", "eks_get_profile", "eks_destroy", "eks_error_string", "eks_k_split", "eks_k_spmm",
-            "eks_k_cgs2", "eks_k_acholqr", "eks_k_chol", "eks_plan_halo"]
+            "eks_k_cgs2", "eks_k_acholqr", "eks_k_chol", "eks_k_time_spmm", "eks_plan_halo"]
 
 
 def eks_plan_halo(rank: int, nranks: int, ranges, row_ptr, col):
@@ -251,6 +252,14 @@ def eks_k_chol(ctx, t, B, R):
     if st not in (EKS_OK, EKS_ERR_BREAKDOWN):
         _check(ctx, st)
     return st
+
+
+def eks_k_time_spmm(ctx, t, X, Y, v=None, variant=0, reps=10) -> float:
+    """Average device time (ms) of one SpMM-block launch (see include/eks_kernels.h)."""
+    ms = C.c_double(0.0)
+    _check(ctx, lib().eks_k_time_spmm(ctx, int(t), _ptr(X, None), _ptr(Y, None), _ptr(v, None), int(variant),
+                                      int(reps), C.byref(ms)))
+    return ms.value
 
 
 # ------------------------------------------------------------------ convenience

@@ -60,6 +60,10 @@ struct eks_ctx {
   std::vector<Send> sends;
   int64_t int_lo = 0, int_hi = 0;  // interior local rows (all columns local)
   int64_t maxrow = 0;              // longest local CSR row
+  int ell_w = 0;                   // ELL copy of A (rows ≤ 8 entries): slots per row, 0 = none
+  int* d_ecol = nullptr;
+  double* d_eval = nullptr;
+  int* d_tmax = nullptr;           // per ELL tile: largest ext column (L2 prefetch of the far slab)
   // workspace, keyed by t
   int ws_t = 0;
   std::vector<Block> Wpool, AWpool;  // Wpool ext layout, AWpool local
@@ -75,6 +79,9 @@ struct eks_ctx {
   double *Bg = nullptr, *Rm = nullptr, *Rinv = nullptr, *alpha = nullptr, *scal = nullptr;
   int alpha_cap = 0;
   int* flag = nullptr;
+  unsigned* cnt = nullptr;   // arrival counters of the tail reductions (one per call site, self-resetting)
+  bool rho_fused = false;    // ‖r_k‖² already reduced into scal[1] by the last block's R⁻¹ kernel
+  bool chol_fused = false;   // R, R⁻¹, α̃ of the block already produced by the SpMM+Gram kernel
   double* h_scal = nullptr;  // pinned: [0..3] doubles, [4] flag as double
   int* h_flag = nullptr;     // pinned INT_MAX source
   std::vector<double> hist;
@@ -202,6 +209,8 @@ void free_workspace(eks_ctx* c) {
                      &c->alpha, &c->scal}) { dfree(*p); *p = nullptr; }
   dfree(c->flag);
   c->flag = nullptr;
+  dfree(c->cnt);
+  c->cnt = nullptr;
   c->part_cap = c->C_cap = 0;
   dfree(c->part2);
   c->part2 = nullptr;
@@ -226,6 +235,10 @@ eks_status ensure_workspace(eks_ctx* ctx, int t, int s) {
   ST(dalloc(ctx, &ctx->Rinv, (size_t)t * t));
   ST(dalloc(ctx, &ctx->scal, 16));
   if (!ctx->flag) CK(cudaMalloc((void**)&ctx->flag, sizeof(int) * 4));
+  if (!ctx->cnt) {
+    CK(cudaMalloc((void**)&ctx->cnt, sizeof(unsigned) * 16));
+    CK(cudaMemset(ctx->cnt, 0, sizeof(unsigned) * 16));
+  }
   if (ctx->alpha_cap < s * t) {
     dfree(ctx->alpha);
     ctx->alpha = nullptr;
@@ -260,6 +273,17 @@ eks_status ensure_C(eks_ctx* ctx, size_t doubles) {
   ST(dalloc(ctx, &ctx->C2, doubles));
   ctx->C_cap = doubles;
   return EKS_OK;
+}
+
+// Tail reduction of a producer kernel's per-CTA partials into out[0..count) (eks_device.cuh).
+eks::Tail tail(eks_ctx* ctx, int slot, double* out, size_t count, double* out2 = nullptr, int split = INT_MAX) {
+  eks::Tail tl;
+  tl.cnt = ctx->cnt + slot;
+  tl.out = out;
+  tl.out2 = out2;
+  tl.count = (int)count;
+  tl.split = split;
+  return tl;
 }
 
 // ---------------------------------------------------------------- communication
@@ -329,14 +353,9 @@ eks_status tn_reduce(eks_ctx* ctx, int t, int nl, const double* const* L, const 
       account(ctx, EKS_K_COEF, 8.0 * ctx->n * ((double)(k + 1) * t + (v ? 1 : 0)),
               2.0 * ctx->n * t * (t * k + (v ? 1 : 0)));
       {
-        KScope ks(ctx, EKS_K_COEF);
+        KScope ks(ctx, EKS_K_COEF);  // partials reduced by the sweep's last CTAs into out
         CK(eks::launch_sweep(ctx->stream, t, 0, k, v != nullptr, ctx->n, R, nullptr, P, nullptr, v, ctx->part,
-                             ctx->nblk));
-      }
-      {
-        KScope ks(ctx, EKS_K_REDUCE);
-        CK(eks::launch_reduce(ctx->stream, ctx->part, eks::sweep_last_grid(), stride, stride,
-                              out + (size_t)j0 * t * t));
+                             ctx->nblk, tail(ctx, 1, out + (size_t)j0 * t * t, stride)));
       }
       j0 += k;
     }
@@ -391,20 +410,21 @@ eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, cons
   ST(ensure_part(ctx, stride * ctx->nblk));
   account(ctx, EKS_K_UPDATE, 8.0 * ctx->n * ((double)2 * nq * t + 2.0 * t), 4.0 * ctx->n * t * t * nq);
   {
-    KScope ks(ctx, EKS_K_UPDATE);
-    CK(eks::launch_sweep(ctx->stream, t, nq, nq, false, ctx->n, Z, Z1, P, C1, nullptr, ctx->part, ctx->nblk));
-  }
-  {
-    KScope ks(ctx, EKS_K_REDUCE);
-    CK(eks::launch_reduce(ctx->stream, ctx->part, eks::sweep_last_grid(), stride, stride, C2));
+    KScope ks(ctx, EKS_K_UPDATE);  // C2 partials reduced by the sweep's last CTAs
+    CK(eks::launch_sweep(ctx->stream, t, nq, nq, false, ctx->n, Z, Z1, P, C1, nullptr, ctx->part, ctx->nblk,
+                         tail(ctx, 0, C2, stride)));
   }
   return allreduce(ctx, C2, stride);
 }
 
 // Y = A·X and out = [XᵀY | Xᵀr] (t·t + t, allreduced): the A-CholQR Gram with the α̃ projection.
-// Single-rank stencil-like matrices (rows ≤ 8 entries) use the fused SpMM+Gram kernel.
-eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const double* r, double* out) {
-  if (ctx->nranks != 1 || !eks::sweep_supported(t) || ctx->maxrow > eks::spmm_gram_max_row()) {
+// One rank: the fused SpMM+Gram kernel, whose last CTA also factors B when `ch` is given
+// (t ≤ 32; ctx->chol_fused tells the caller).  Several ranks: SpMM with halo overlap, then
+// the Gram sweep and an allreduce.
+eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const double* r, double* out,
+                     const eks::CholArgs* ch = nullptr) {
+  ctx->chol_fused = false;
+  if (ctx->nranks != 1 || !eks::sweep_supported(t)) {
     ST(spmm(ctx, X, Y, t));
     const double* L[1] = {X.loc};
     return tn_reduce(ctx, t, 1, L, Y, r, out);
@@ -413,16 +433,25 @@ eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const doubl
   ST(ensure_part(ctx, stride * ctx->nblk));
   account(ctx, EKS_K_SPMM, 12.0 * ctx->nnz + 4.0 * (ctx->n + 1) + 16.0 * ctx->n * t, 2.0 * ctx->nnz * t);
   account(ctx, EKS_K_COEF, r ? 8.0 * ctx->n : 0.0, 2.0 * ctx->n * t * (t + 1));  // epilogue: only r is extra traffic
+  eks::CholArgs c{};
+  if (ch && eks::spmm_gram_fused_chol(t)) {
+    c = *ch;
+    c.on = 1;
+  }
   {
     KScope k(ctx, EKS_K_SPMM);
-    CK(eks::launch_spmm_gram(ctx->stream, t, ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val, X.base, X.loc, Y, r,
-                             ctx->part, ctx->nblk));
+    if (ctx->ell_w)
+      CK(eks::launch_spmm_gram_ell(ctx->stream, t, ctx->n, ctx->d_ecol, ctx->d_eval, ctx->ell_w, ctx->d_tmax, n_ext(ctx),
+                                   X.base,
+                                   (int64_t)(X.loc - X.base) / t, Y, r, ctx->part, ctx->nblk, tail(ctx, 2, out, stride),
+                                   c));
+    else
+      CK(eks::launch_spmm_gram(ctx->stream, t, ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val, (int)ctx->maxrow, X.base,
+                               (int64_t)(X.loc - X.base) / t, Y, r, ctx->part, ctx->nblk, tail(ctx, 2, out, stride),
+                               c));
   }
-  {
-    KScope k(ctx, EKS_K_REDUCE);
-    CK(eks::launch_reduce(ctx->stream, ctx->part, eks::sweep_last_grid(), stride, stride, out));
-  }
-  return allreduce(ctx, out, stride);
+  ctx->chol_fused = c.on != 0;
+  return EKS_OK;
 }
 
 // CGS2 of Z against the window (Q, AQ): two passes of C = (AQ)ᵀZ, Z -= Q C (reading R3/R24).
@@ -544,31 +573,43 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
   }
   // "A-orthonormalize W": A-CholQR with one SpMM of Z2 (AW = (A Z2) R⁻¹)
   const bool with_update = !(mode & 4);
-  ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg));
-  ST(chol(ctx, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
-          with_update ? ctx->alpha + alpha_off : nullptr, gb));
+  eks::CholArgs ch{};
+  ch.R = ctx->Rm;
+  ch.Rinv = ctx->Rinv;
+  ch.alpha = with_update ? ctx->alpha + alpha_off : nullptr;
+  ch.flag = ctx->flag;
+  ch.gblock = gb;
+  ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg, &ch));
+  if (!ctx->chol_fused)
+    ST(chol(ctx, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
+            with_update ? ctx->alpha + alpha_off : nullptr, gb));
   // SRE-CG: the next block's window is {W_prev, W_new} and its Z is AW_new, so the R⁻¹ kernel
   // that produces AW_new also accumulates the next CGS pass-1 coefficients C1 = [AW_prev, AW_new]ᵀAW_new.
   const int c1n = (ring && eks::apply_c1_supported(t, 2)) ? (nblocks == 0 ? 1 : 2) : 0;
-  if (c1n) {
-    ST(ensure_C(ctx, (size_t)2 * t * t));
-    if (ctx->part2_cap < (size_t)ctx->nblk * 2 * t * t) {
-      dfree(ctx->part2);
-      ctx->part2 = nullptr;
-      ST(dalloc(ctx, &ctx->part2, (size_t)ctx->nblk * 2 * t * t));
-      ctx->part2_cap = (size_t)ctx->nblk * 2 * t * t;
-    }
+  if (c1n) ST(ensure_C(ctx, (size_t)2 * t * t));
+  if (ctx->part2_cap < (size_t)ctx->nblk * (2 * t * t + 2)) {
+    dfree(ctx->part2);
+    ctx->part2 = nullptr;
+    ST(dalloc(ctx, &ctx->part2, (size_t)ctx->nblk * (2 * t * t + 2)));
+    ctx->part2_cap = (size_t)ctx->nblk * (2 * t * t + 2);
   }
+  const bool last = (mode & 2) && with_update;
+  ctx->rho_fused = false;
   {
     KScope k(ctx, EKS_K_APPLY);
     account(ctx, EKS_K_APPLY, 8.0 * ctx->n * (4.0 * t + 4.0 + (c1n == 2 ? t : 0)),
             2.0 * ctx->n * t * (t + 2 + c1n * t));
     if (eks::sweep_supported(t)) {
+      // partials [C1 | ‖rnew‖²] reduced by the kernel's last CTAs into C1 and scal[1]
+      const size_t cnt1 = (size_t)c1n * t * t;
+      const eks::Tail tl = (cnt1 + (last ? 1 : 0)) ? tail(ctx, 3, ctx->C1, cnt1 + (last ? 1 : 0), ctx->scal + 1,
+                                                           (int)cnt1)
+                                                    : eks::Tail{};
       CK(eks::launch_apply_tc(ctx->stream, t, ctx->n, Wn->loc, AWn->loc, ctx->Rinv,
                               with_update ? ctx->alpha + alpha_off : nullptr, ctx->xv.loc, ctx->dx, ctx->r, ctx->rnew,
-                              ctx->part, ctx->flag, mode, ctx->nblk, c1n,
-                              c1n == 2 ? ctx->AWpool[(nblocks - 1) % ring].loc : nullptr, ctx->part2));
-      ctx->rho_nblk = eks::sweep_last_grid();
+                              ctx->flag, mode, ctx->nblk, c1n,
+                              c1n == 2 ? ctx->AWpool[(nblocks - 1) % ring].loc : nullptr, ctx->part2, tl));
+      ctx->rho_fused = last;
     } else {
       CK(eks::launch_apply(ctx->stream, t, ctx->n, Wn->loc, AWn->loc, ctx->Rinv,
                            with_update ? ctx->alpha + alpha_off : nullptr, ctx->xv.loc, ctx->dx, ctx->r, ctx->rnew,
@@ -577,11 +618,6 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
     }
   }
   if (c1n) {
-    {
-      KScope k(ctx, EKS_K_REDUCE);
-      CK(eks::launch_reduce(ctx->stream, ctx->part2, ctx->rho_nblk, (size_t)c1n * t * t, (size_t)c1n * t * t,
-                            ctx->C1));
-    }
     ST(allreduce(ctx, ctx->C1, (size_t)c1n * t * t));
     ctx->c1_ready = true;
   }
@@ -855,12 +891,16 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   // ---- upload (the block workspace survives when the slab geometry is unchanged)
   if (!ctx->have_matrix || ctx->n != n || old_before != ctx->halo_before || old_after != ctx->halo_after)
     free_workspace(ctx);
-  dfree(ctx->d_rp);
-  dfree(ctx->d_col);
-  dfree(ctx->d_val);
+  for (void* p : {(void*)ctx->d_rp, (void*)ctx->d_col, (void*)ctx->d_val, (void*)ctx->d_ecol, (void*)ctx->d_eval,
+                  (void*)ctx->d_tmax})
+    dfree(p);
+  ctx->d_tmax = nullptr;
   ctx->d_rp = nullptr;
   ctx->d_col = nullptr;
   ctx->d_val = nullptr;
+  ctx->d_ecol = nullptr;
+  ctx->d_eval = nullptr;
+  ctx->ell_w = 0;
   ctx->have_matrix = false;
   std::vector<int32_t> rp32(n + 1);
   for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)rp[i];
@@ -871,6 +911,34 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   CK(cudaMemcpy(ctx->d_rp, rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->d_col, ecol.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->d_val, val.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  // ELL copy for the fused SpMM+Gram when every row has ≤ 8 entries (tiles of kEllTR rows,
+  // slot-major inside a tile; padding: value 0 and the row's own column)
+  const int w = eks::ell_width((int)ctx->maxrow);
+  if (w > 0) {
+    const int64_t TR = eks::kEllTR, ntiles = (n + TR - 1) / TR;
+    std::vector<int32_t> ec((size_t)ntiles * TR * w), tmax((size_t)ntiles, 0);
+    std::vector<double> ev((size_t)ntiles * TR * w, 0.0);
+    for (int64_t tile = 0; tile < ntiles; ++tile)
+      for (int k = 0; k < w; ++k)
+        for (int64_t rr = 0; rr < TR; ++rr) {
+          const int64_t i = tile * TR + rr, e = (tile * w + k) * TR + rr;
+          const int64_t len = i < n ? rp[i + 1] - rp[i] : 0;
+          if (k < len) {
+            ec[e] = ecol[rp[i] + k];
+            ev[e] = val[rp[i] + k];
+          } else {
+            ec[e] = (int32_t)(plan.halo_before + (i < n ? i : 0));
+          }
+          tmax[tile] = std::max(tmax[tile], ec[e]);
+        }
+    CK(cudaMalloc((void**)&ctx->d_ecol, sizeof(int32_t) * ec.size()));
+    CK(cudaMalloc((void**)&ctx->d_eval, sizeof(double) * ev.size()));
+    CK(cudaMemcpy(ctx->d_ecol, ec.data(), sizeof(int32_t) * ec.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_eval, ev.data(), sizeof(double) * ev.size(), cudaMemcpyHostToDevice));
+    CK(cudaMalloc((void**)&ctx->d_tmax, sizeof(int32_t) * tmax.size()));
+    CK(cudaMemcpy(ctx->d_tmax, tmax.data(), sizeof(int32_t) * tmax.size(), cudaMemcpyHostToDevice));
+    ctx->ell_w = w;
+  }
   ctx->n_global = n_global;
   ctx->row_begin = row_begin;
   ctx->row_end = row_end;
@@ -940,7 +1008,8 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
       ++nblocks;
     }
     if (status == EKS_ERR_OOM) break;
-    ST(reduce_scalar(ctx, ctx->scal + 1));
+    if (ctx->rho_fused) ST(allreduce(ctx, ctx->scal + 1, 1));
+    else ST(reduce_scalar(ctx, ctx->scal + 1));
     ST(sync_scalars(ctx, 2));
     const int fl = ctx->h_flag[1];
     if (fl != INT_MAX) {  // A-CholQR breakdown: x stays the last completed iterate
@@ -1075,6 +1144,9 @@ eks_status eks_destroy(eks_ctx* ctx) {
   dfree(ctx->d_rp);
   dfree(ctx->d_col);
   dfree(ctx->d_val);
+  dfree(ctx->d_ecol);
+  dfree(ctx->d_eval);
+  dfree(ctx->d_tmax);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (auto& p : ctx->prof_pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
@@ -1147,7 +1219,7 @@ eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double
   ST(chol(ctx, t, ctx->Bg, nullptr, ctx->Rm, ctx->Rinv, nullptr, 0));
   if (eks::sweep_supported(t))
     CK(eks::launch_apply_tc(ctx->stream, t, ctx->n, W, AW, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr,
-                            nullptr, nullptr, 4, ctx->nblk));
+                            nullptr, 4, ctx->nblk, 0, nullptr, ctx->part2, eks::Tail{}));
   else
     CK(eks::launch_apply(ctx->stream, t, ctx->n, W, AW, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr,
                          nullptr, nullptr, 4, ctx->nblk));
@@ -1155,6 +1227,52 @@ eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double
   if (B) CK(cudaMemcpyAsync(B, ctx->Bg, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, ctx->stream));
   ST(sync_scalars(ctx, 1));
   if (ctx->h_flag[1] != INT_MAX) return fail(ctx, EKS_ERR_BREAKDOWN, "A-CholQR breakdown");
+  return EKS_OK;
+}
+
+eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, const double* v, int variant, int reps,
+                           double* ms) {
+  ST(k_ready(ctx, t));
+  if (!X || !Y || !ms || reps < 1 || variant < 0 || variant > 3)
+    return fail(ctx, EKS_ERR_INVALID_ARG, "bad eks_k_time_spmm arguments");
+  if (variant > 0 && !eks::sweep_supported(t))
+    return fail(ctx, EKS_ERR_INVALID_ARG, "fused SpMM+Gram needs t in {8,16,32,64}");
+  ST(reset_flag(ctx));
+  const size_t stride = eks::sweep_part_stride(t, 1, true);
+  ST(ensure_part(ctx, stride * ctx->nblk));
+  eks::CholArgs ch{};
+  ch.on = variant == 3 && eks::spmm_gram_fused_chol(t);
+  ch.R = ctx->Rm;
+  ch.Rinv = ctx->Rinv;
+  ch.alpha = v ? ctx->alpha : nullptr;
+  ch.flag = ctx->flag;
+  const eks::Tail tl = variant >= 2 ? tail(ctx, 2, ctx->Bg, stride) : eks::Tail{};
+  auto run = [&]() -> cudaError_t {
+    if (variant == 0)
+      return eks::launch_spmm(ctx->stream, t, 0, (int)ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val, X, Y, ctx->sms);
+    cudaError_t e = ctx->ell_w ? eks::launch_spmm_gram_ell(ctx->stream, t, ctx->n, ctx->d_ecol, ctx->d_eval,
+                                                           ctx->ell_w, ctx->d_tmax, ctx->n, X, 0, Y, v, ctx->part,
+                                                           ctx->nblk, tl, ch)
+                               : eks::launch_spmm_gram(ctx->stream, t, ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val,
+                                                       (int)ctx->maxrow, X, 0, Y, v, ctx->part, ctx->nblk, tl, ch);
+    if (e == cudaSuccess && variant == 3 && !ch.on)
+      e = eks::launch_chol(ctx->stream, t, ctx->Bg, v ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
+                           v ? ctx->alpha : nullptr, ctx->flag, 0);
+    return e;
+  };
+  CK(run());
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, ctx->stream));
+  for (int i = 0; i < reps; ++i) CK(run());
+  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventSynchronize(e1));
+  float f = 0.f;
+  cudaEventElapsedTime(&f, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms = (double)f / reps;
   return EKS_OK;
 }
 

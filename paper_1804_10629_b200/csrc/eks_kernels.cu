@@ -3,6 +3,7 @@
 // Blocks are row-major n×T, T a power of two ≤ 64.  No fp64 atomics: every
 // reduction is a fixed-order two-stage tree (per-CTA partials, then
 // launch_reduce), so results are bitwise reproducible run to run.
+#include "eks_device.cuh"
 #include "eks_kernels.cuh"
 
 #include <climits>
@@ -552,8 +553,25 @@ __global__ void __launch_bounds__(256) k_chol(const double* __restrict__ B, cons
   if (tid == 0 && sfail && flag) atomicMin(flag, gblock);
 }
 
+// t ≤ 32: one warp, the factor in registers (chol_warp, eks_device.cuh) — same operations as k_chol.
+template <int T>
+__global__ void __launch_bounds__(32) k_chol_w(const double* __restrict__ B, const double* __restrict__ g,
+                                               double* __restrict__ Rout, double* __restrict__ Rinv,
+                                               double* __restrict__ alpha, int* flag, int gblock) {
+  chol_warp<T>(B, g, Rout, Rinv, alpha, flag, gblock);
+}
+
 cudaError_t launch_chol(cudaStream_t st, int t, const double* B, const double* g, double* R, double* Rinv,
                         double* alpha, int* flag, int gblock) {
+  switch (t) {
+    case 1: k_chol_w<1><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 2: k_chol_w<2><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 4: k_chol_w<4><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 8: k_chol_w<8><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 16: k_chol_w<16><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 32: k_chol_w<32><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    default: break;
+  }
   EKS_DISPATCH_T(t, {
     const size_t sm = (size_t)3 * T * (T + 1) * 8;
     cudaFuncSetAttribute(k_chol<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

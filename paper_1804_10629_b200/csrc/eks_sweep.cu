@@ -11,11 +11,13 @@
 // fp64 tensor cores with mma.sync.m8n8k4.f64 (DMMA; tcgen05 has no fp64 kind).
 // Per-CTA partial sums go to a per-CTA slot and are reduced in a fixed order
 // afterwards (no fp64 atomics, bitwise reproducible).
+#include "eks_device.cuh"
 #include "eks_kernels.cuh"
 #include "eks_sweep.cuh"
 
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 namespace eks {
 
@@ -40,6 +42,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// Bulk prefetch of [p, p+bytes) into L2 (address and size rounded to 16 bytes).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uint32_t nb = (bytes + 15u + (uint32_t)(reinterpret_cast<uintptr_t>(p) & 15)) & ~15u;
+  if (nb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(nb) : "memory");
 }
 
 // CTA b's rows start at a multiple of 8 (16-byte alignment of every int32/fp64 row-indexed copy).
@@ -108,7 +117,7 @@ struct SwCfg {
 template <int T, int NQ, int NL, bool V>
 __global__ void __launch_bounds__(256, 1)
     k_sweep(int64_t n, const double* Zin, double* Zout, const SweepPtrs P,
-            const double* __restrict__ Cm, const double* __restrict__ v, double* __restrict__ part) {
+            const double* __restrict__ Cm, const double* __restrict__ v, double* __restrict__ part, const Tail tl) {
   using K = SwCfg<T, NQ, NL, V>;
   constexpr int S = K::S;
   extern __shared__ __align__(128) double sm[];
@@ -244,6 +253,7 @@ __global__ void __launch_bounds__(256, 1)
         out[NL * T * T + e] = s;
       }
     }
+    if (tl.cnt != nullptr) tail_reduce(part, K::PER, tl);
   }
 }
 
@@ -276,10 +286,10 @@ template <int T, int C1N>
 __global__ void __launch_bounds__(256, 1)
     k_apply_tc(int64_t n, double* Z2W, double* AZ2AW, const double* __restrict__ Rinv,
                const double* __restrict__ alpha, double* __restrict__ x, double* __restrict__ dx,
-               const double* __restrict__ r, double* __restrict__ rnew, double* __restrict__ rho_part,
-               const int* __restrict__ flag, int mode, const double* __restrict__ AWprev,
-               double* __restrict__ c1part) {
+               const double* __restrict__ r, double* __restrict__ rnew, const int* __restrict__ flag, int mode,
+               const double* __restrict__ AWprev, double* __restrict__ part, const Tail tl) {
   using K = ApCfg<T, C1N>;
+  constexpr int PS = C1N * T * T + 2;  // per-CTA partial: [C1 (C1N·T·T) | ‖rnew‖² | pad] (16-byte rows)
   constexpr int S = K::S, SR = T + 4;
   extern __shared__ __align__(128) double sm[];
   __shared__ double sred[8];
@@ -393,7 +403,8 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
   cp_wait<0>();
-  if (last && rho_part != nullptr) {
+  if (tl.cnt == nullptr) return;  // nothing to reduce (no fused C1, not the last block)
+  if (last) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rr_acc += __shfl_down_sync(0xffffffffu, rr_acc, o);
     if (lane == 0) sred[warp] = rr_acc;
@@ -401,11 +412,11 @@ __global__ void __launch_bounds__(256, 1)
     if (tid == 0) {
       double sacc = 0.0;
       for (int w = 0; w < 8; ++w) sacc += sred[w];
-      rho_part[blockIdx.x] = sacc;
+      part[(size_t)blockIdx.x * PS + C1N * T * T] = sacc;
     }
   }
   if constexpr (C1N > 0) {
-    double* out = c1part + (size_t)blockIdx.x * C1N * T * T;
+    double* out = part + (size_t)blockIdx.x * PS;
     __syncthreads();
     if constexpr (K::WS == 1) {
 #pragma unroll
@@ -434,213 +445,46 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   }
+  tail_reduce(part, PS, tl);
 }
 
 // ----------------------------------------------------------------------------
-// Fused SpMM + Gram (A-CholQR's B = Z2ᵀ(A Z2) and Z2ᵀr, P:198/P:380; Y = A·X, P:54).
-// Per TR-row tile the CTA streams, through the cp.async ring: the tile's CSR row
-// pointers, its (col, val) entries, its own X rows and r.  Only the X gathers of
-// neighbour rows remain dependent loads (mostly L2 hits for stencils).  Y is
-// written to HBM and kept in shared memory, and the Gram partial XᵀY, Xᵀr of the
-// tile is accumulated on DMMA.  Accumulation order of every Y entry: p
-// ascending, fma from 0.0 — bitwise equal to k_spmm and to the oracle (R20).
+// Epilogue of the fused SpMM+Gram kernels: the CTA's partial [XᵀY | Xᵀr] (layout
+// of k_sweep<T,0,1,true>), the tail reduction into tl.out and, for T ≤ 16 on one
+// rank, the Cholesky of the reduced Gram by the last CTA (chol_warp, registers).
 // ----------------------------------------------------------------------------
-template <int T>
-struct SgCfg {
-  static constexpr int TR = 64;
-  static constexpr int S = T + 4;
-  static constexpr int G = T / 2;         // threads per row (2 columns each)
-  static constexpr int RPP = 256 / G;      // rows per pass
-  static constexpr int PASSES = TR / RPP;
-  static constexpr int MAXROW = 8;         // entries per row supported by the staged path
-  static constexpr int ECAP = TR * MAXROW + 4;  // + alignment slack of the 16-byte copies
-  // stage layout (doubles): X tile | r tile | val[ECAP] | col[ECAP] (ints) | rp[TR+4] (ints)
-  static constexpr int STAGE = TR * S + TR + ECAP + (ECAP + TR + 4) / 2 + 2;
-  static constexpr int YT = TR * S;        // Y tile (single buffer)
-  static constexpr int NSA = (100 * 1024 / 8 - YT) / STAGE;
-  static constexpr int NS = NSA > 6 ? 6 : (NSA < 3 ? 3 : NSA);
-  static constexpr int MT = T / 8;
-  static constexpr int OT = MT * MT;
-  static constexpr int WS = OT >= 8 ? 1 : 8 / OT;
-  static constexpr int TPW = OT >= 8 ? OT / 8 : 1;
-  static constexpr int PER = T * T + T;
-  static constexpr int RED = (WS > 1 ? 8 * T * T : 0) + 8 * T;
-  static constexpr int SMEM0 = NS * STAGE + YT;
-  static constexpr int SMEM = SMEM0 > RED ? SMEM0 : RED;
-};
-
-template <int T>
-__global__ void __launch_bounds__(256, (T <= 16 ? 3 : 2))
-    k_spmm_gram(int64_t n, const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ val,
-                const double* __restrict__ Xext, const double* __restrict__ Xloc, double* __restrict__ Y,
-                const double* __restrict__ r, double* __restrict__ part) {
-  using K = SgCfg<T>;
-  constexpr int S = K::S;
-  extern __shared__ __align__(128) double sm[];
+template <int T, int MT, int WS, int TPW>
+__device__ __forceinline__ void gram_epilogue(double* part, const double (&acc)[TPW][2], const double (&accv)[2],
+                                              double* sm, const Tail& tl, const CholArgs& ch, bool has_r) {
+  constexpr int PER = T * T + T;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q4 = lane & 3;
-  const int64_t lo = chunk_lo(n, blockIdx.x, gridDim.x), hi = chunk_lo(n, blockIdx.x + 1, gridDim.x);
-  const int ntiles = (int)((hi - lo + K::TR - 1) / K::TR);
-  double* sY = sm + K::NS * K::STAGE;
-  static_assert(K::NS >= 3, "the L2 prefetch of tile i+1 needs two landed stages");
-  auto row0_of = [&](int i) { return lo + (int64_t)i * K::TR; };
-
-  // (p_begin, p_end) of tile i, prefetched one iteration ahead of its issue
-  auto bounds = [&](int i, int& pb, int& pe) {
-    if (i < ntiles) {
-      const int64_t row = lo + (int64_t)i * K::TR;
-      const int rows = (int)((hi - row) < K::TR ? (hi - row) : K::TR);
-      pb = __ldg(rp + row);
-      pe = __ldg(rp + row + rows);
-    }
-  };
-  auto issue = [&](int i, int pb, int pe) {
-    if (i < ntiles) {
-      const int s = i % K::NS;
-      const int64_t row = lo + (int64_t)i * K::TR;
-      const int rows = (int)((hi - row) < K::TR ? (hi - row) : K::TR);
-      double* st = sm + s * K::STAGE;
-      tile_async<T, S, K::TR>(st, Xloc, row, rows);
-      if (r != nullptr) vec_async<K::TR>(st + K::TR * S, r, row, rows);
-      double* sval = st + K::TR * S + K::TR;
-      int* scol = reinterpret_cast<int*>(sval + K::ECAP);
-      int* srp = scol + K::ECAP;
-      // 16-byte chunks of the aligned-down ranges (the device CSR arrays are padded by 16 bytes)
-      const int pv = pb & ~1, pc = pb & ~3;
-      const int nv = (pe - pv + 1) >> 1, nc = (pe - pc + 3) >> 2, nr = (rows + 4) >> 2;
-      for (int e = tid; e < nv + nc + nr; e += 256) {
-        if (e < nv) cp16(sval + 2 * e, val + pv + 2 * e, 16);
-        else if (e < nv + nc) cp16(scol + 4 * (e - nv), col + pc + 4 * (e - nv), 16);
-        else cp16(srp + 4 * (e - nv - nc), rp + row + 4 * (e - nv - nc), 16);
-      }
-    }
-    cp_commit();
-  };
-  int nb[K::NS][2];
-#pragma unroll
-  for (int i = 0; i < K::NS; ++i) {
-    nb[i][0] = nb[i][1] = 0;
-    bounds(i, nb[i][0], nb[i][1]);
-  }
-#pragma unroll
-  for (int i = 0; i < K::NS - 1; ++i) issue(i, nb[i][0], nb[i][1]);
-  int pend_b = nb[K::NS - 1][0], pend_e = nb[K::NS - 1][1];  // bounds of the next tile to issue
-
-  double acc[K::TPW][2];
-#pragma unroll
-  for (int j = 0; j < K::TPW; ++j) acc[j][0] = acc[j][1] = 0.0;
-  double accv[2] = {0.0, 0.0};
-  const int grp = tid / K::G, gl = tid % K::G;
-
-  for (int i = 0; i < ntiles; ++i) {
-    cp_wait<K::NS - 3>();  // tiles i and i+1 have landed
-    __syncthreads();
-    issue(i + K::NS - 1, pend_b, pend_e);
-    int nbb = 0, nbe = 0;
-    bounds(i + K::NS, nbb, nbe);  // prefetch for the next issue
-    if (i + 1 < ntiles) {
-      // warm L2 with the out-of-tile X rows tile i+1 will gather
-      const double* sn = sm + ((i + 1) % K::NS) * K::STAGE + K::TR * S + K::TR;
-      const int* ncol = reinterpret_cast<const int*>(sn + K::ECAP);
-      const int* nrp = ncol + K::ECAP;
-      const int64_t nrow = row0_of(i + 1);
-      const int nrows = (int)((hi - nrow) < K::TR ? (hi - nrow) : K::TR);
-      const int ne = nrp[nrows] - nrp[0], nco = nrp[0] & 3;
-      constexpr int LPR = (T * 8 + 127) / 128;  // 128-byte lines per X row
-      for (int e = tid; e < ne * LPR; e += 256) {
-        const int c = ncol[nco + e / LPR];
-        if (c < nrow || c >= nrow + nrows)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(Xext + (int64_t)c * T + (e % LPR) * 16));
-      }
-    }
-    const double* st = sm + (i % K::NS) * K::STAGE;
-    const double* sX = st;
-    const double* sr = st + K::TR * S;
-    const double* sval = sr + K::TR;
-    const int* scol = reinterpret_cast<const int*>(sval + K::ECAP);
-    const int* srp = scol + K::ECAP;
-    const int64_t row = lo + (int64_t)i * K::TR;
-    const int rows = (int)((hi - row) < K::TR ? (hi - row) : K::TR);
-    const int pbase = srp[0], vo = pbase & 1, co = pbase & 3;  // offsets of the aligned copies
-    // ---------------- Y rows of the tile
-#pragma unroll
-    for (int ps = 0; ps < K::PASSES; ++ps) {
-      const int rr = ps * K::RPP + grp;
-      double ax = 0.0, ay = 0.0;
-      if (rr < rows) {
-        const int q0 = srp[rr] - pbase, q1 = srp[rr + 1] - pbase;
-        double a[K::MAXROW];
-        double2 xv[K::MAXROW];
-#pragma unroll
-        for (int k = 0; k < K::MAXROW; ++k)
-          if (q0 + k < q1) {
-            a[k] = sval[vo + q0 + k];
-            xv[k] = __ldg(reinterpret_cast<const double2*>(Xext + (int64_t)scol[co + q0 + k] * T) + gl);
-          }
-#pragma unroll
-        for (int k = 0; k < K::MAXROW; ++k)
-          if (q0 + k < q1) {
-            ax = __fma_rn(a[k], xv[k].x, ax);
-            ay = __fma_rn(a[k], xv[k].y, ay);
-          }
-        *reinterpret_cast<double2*>(Y + (row + rr) * T + 2 * gl) = make_double2(ax, ay);
-      }
-      sY[rr * S + 2 * gl] = ax;  // rows beyond the tile end stay 0 in the Gram
-      sY[rr * S + 2 * gl + 1] = ay;
-    }
-    __syncthreads();
-    // ---------------- Gram partial Xᵀ Y and Xᵀ r of the tile (X rows beyond `rows` are zero-filled)
-    {
-      const int slice = warp % K::WS;
-#pragma unroll
-      for (int u = 0; u < K::TPW; ++u) {
-        const int tile = (warp / K::WS) * K::TPW + u;
-        const int mi = tile / K::MT, ni = tile % K::MT;
-        double d0 = acc[u][0], d1 = acc[u][1];
-#pragma unroll
-        for (int kk = slice * 4; kk < K::TR; kk += 4 * K::WS)
-          dmma(d0, d1, sX[(kk + q4) * S + mi * 8 + g], sY[(kk + q4) * S + ni * 8 + g]);
-        acc[u][0] = d0;
-        acc[u][1] = d1;
-      }
-      for (int rr = warp; r != nullptr && rr < rows; rr += 8) {
-        const double vr = sr[rr];
-        if (lane < T) accv[0] = fma(sX[rr * S + lane], vr, accv[0]);
-        if (lane + 32 < T) accv[1] = fma(sX[rr * S + lane + 32], vr, accv[1]);
-      }
-    }
-    pend_b = nbb;
-    pend_e = nbe;
-  }
-  cp_wait<0>();
-  // ---------------- per-CTA partial (same layout as k_sweep<T,0,1,true>)
-  double* out = part + (size_t)blockIdx.x * K::PER;
+  double* out = part + (size_t)blockIdx.x * PER;
   double* red = sm;
-  __syncthreads();
-  if constexpr (K::WS == 1) {
+  if constexpr (WS == 1) {
 #pragma unroll
-    for (int u = 0; u < K::TPW; ++u) {
-      const int tile = warp * K::TPW + u;
-      const int mi = tile / K::MT, ni = tile % K::MT;
-      *reinterpret_cast<double2*>(out + (mi * 8 + g) * T + ni * 8 + 2 * q4) = make_double2(acc[u][0], acc[u][1]);
+    for (int uu = 0; uu < TPW; ++uu) {
+      const int ot = warp * TPW + uu;
+      const int mi = ot / MT, ni = ot % MT;
+      *reinterpret_cast<double2*>(out + (mi * 8 + g) * T + ni * 8 + 2 * q4) = make_double2(acc[uu][0], acc[uu][1]);
     }
   } else {
     {
-      const int tile = warp / K::WS;
-      const int mi = tile / K::MT, ni = tile % K::MT;
+      const int ot = warp / WS;
+      const int mi = ot / MT, ni = ot % MT;
       red[(size_t)warp * T * T + (mi * 8 + g) * T + ni * 8 + 2 * q4] = acc[0][0];
       red[(size_t)warp * T * T + (mi * 8 + g) * T + ni * 8 + 2 * q4 + 1] = acc[0][1];
     }
     __syncthreads();
     for (int e = tid; e < T * T; e += 256) {
       const int m = e / T, nn = e % T;
-      const int tile = (m / 8) * K::MT + nn / 8;
+      const int ot = (m / 8) * MT + nn / 8;
       double s = 0.0;
-      for (int w = tile * K::WS; w < tile * K::WS + K::WS; ++w) s += red[(size_t)w * T * T + e];
+      for (int w = ot * WS; w < ot * WS + WS; ++w) s += red[(size_t)w * T * T + e];
       out[e] = s;
     }
   }
-  double* rv = red + (K::WS > 1 ? 8 * T * T : 0);
+  double* rv = red + (WS > 1 ? 8 * T * T : 0);
   if (lane < T) rv[warp * T + lane] = accv[0];
   if (lane + 32 < T) rv[warp * T + lane + 32] = accv[1];
   __syncthreads();
@@ -649,6 +493,325 @@ __global__ void __launch_bounds__(256, (T <= 16 ? 3 : 2))
     for (int w = 0; w < 8; ++w) s += rv[w * T + e];
     out[T * T + e] = s;
   }
+  if (tl.cnt != nullptr) {
+    const bool last = tail_reduce(part, PER, tl);
+    if constexpr (T <= 16) {
+      if (last && ch.on && warp == 0)
+        chol_warp<T>(tl.out, has_r ? tl.out + T * T : nullptr, ch.R, ch.Rinv, ch.alpha, ch.flag, ch.gblock);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Fused SpMM + Gram (A-CholQR's B = Z2ᵀ(A Z2) and Z2ᵀr, P:198/P:380; Y = A·X, P:54).
+// Tiles of TR rows are dealt round-robin to the CTAs (tile = blockIdx + k·grid), so
+// at any moment the whole grid works on one contiguous window of rows and the
+// stencil neighbours of X (rows ±1, ±N, ±N²) are re-read from L2 rather than HBM.
+// G = T/2 threads per row, each owning 2 columns (16-byte gathers of the row-major
+// X rows).  A tile is processed in PASSES units of RPP rows; a unit's (col, val)
+// entries are loaded cooperatively, one entry per lane (SL slots per lane), and
+// handed out by shuffles.  Software pipeline over units: while unit u's X gathers
+// are in flight, the entries of unit u+1 and the row pointers of unit u+2 are
+// loaded, so the gathers are the only exposed latency.  The diagonal entry's
+// gather is the row's own X row (every row has a diagonal, checked at setup): the
+// Gram needs no extra read of X.  The tile's X and Y rows are kept in shared memory
+// and XᵀY, Xᵀr accumulate on DMMA.  Accumulation order of every Y entry: p
+// ascending, fma from 0.0 — bitwise equal to k_spmm and to the oracle (R20).  Rows
+// longer than NZ take a plain loop.  The per-CTA partials are reduced by the grid's
+// last CTAs (Tail) and, on one rank, the very last CTA factors B = RᵀR (T ≤ 16).
+// ----------------------------------------------------------------------------
+template <int T, int NZ>
+struct SgCfg {
+  static constexpr int TR = 64;
+  static constexpr int S = T + 4;
+  static constexpr int G = T / 2;       // threads per row (2 columns each)
+  static constexpr int RPP = 256 / G;    // rows per unit
+  static constexpr int PASSES = TR / RPP;
+  static constexpr int SL = (NZ + G - 1) / G;  // (col, val) slots per lane
+  static constexpr int MT = T / 8;
+  static constexpr int OT = MT * MT;
+  static constexpr int WS = OT >= 8 ? 1 : 8 / OT;
+  static constexpr int TPW = OT >= 8 ? OT / 8 : 1;
+  static constexpr int PER = T * T + T;
+  static constexpr int RED = (WS > 1 ? 8 * T * T : 0) + 8 * T;
+  static constexpr int SMEM0 = 2 * TR * S + TR;
+  static constexpr int SMEM = SMEM0 > RED ? SMEM0 : RED;
+};
+
+template <int T, int NZ>
+__global__ void __launch_bounds__(256, (T >= 64 ? 2 : 3))
+    k_spmm_gram(int64_t n, const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ val,
+                const double* __restrict__ Xext, int64_t xoff, double* __restrict__ Y, const double* __restrict__ r,
+                double* __restrict__ part, const Tail tl, const CholArgs ch) {
+  using K = SgCfg<T, NZ>;
+  constexpr int S = K::S, G = K::G, SL = K::SL, P = K::PASSES, RPP = K::RPP;
+  extern __shared__ __align__(128) double sm[];
+  double* sX = sm;
+  double* sY = sm + K::TR * S;
+  double* sr = sm + 2 * K::TR * S;
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q4 = lane & 3;
+  const int grp = tid / G, gl = tid % G;
+  const int64_t ntiles = (n + K::TR - 1) / K::TR;
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t nunits = my_tiles * P;
+  // global row of this thread in unit u (may be >= n)
+  auto row_of = [&](int64_t u) { return (blockIdx.x + (u / P) * gridDim.x) * K::TR + (u % P) * RPP + grp; };
+  auto load_rp = [&](int64_t u, int& p0, int& len) {
+    p0 = 0;
+    len = 0;
+    const int64_t i = row_of(u);
+    if (u < nunits && i < n) {
+      p0 = __ldg(rp + i);
+      len = __ldg(rp + i + 1) - p0;
+    }
+  };
+  auto load_cv = [&](int p0, int len, int (&c)[SL], double (&v)[SL]) {
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+      const int k = s * G + gl;
+      c[s] = 0;
+      v[s] = 0.0;
+      if (k < len && k < NZ) {
+        c[s] = __ldg(col + p0 + k);
+        v[s] = __ldg(val + p0 + k);
+      }
+    }
+  };
+
+  double acc[K::TPW][2];
+#pragma unroll
+  for (int j = 0; j < K::TPW; ++j) acc[j][0] = acc[j][1] = 0.0;
+  double accv[2] = {0.0, 0.0};
+
+  // pipeline state: unit u (entries ready), unit u+1 (row pointers ready)
+  int p0c, lenc, p0n, lenn, cc[SL];
+  double cv[SL];
+  load_rp(0, p0c, lenc);
+  load_rp(1, p0n, lenn);
+  load_cv(p0c, lenc, cc, cv);
+  for (int64_t u = 0; u < nunits; ++u) {
+    const int ps = (int)(u % P);
+    const int64_t tile = blockIdx.x + (u / P) * gridDim.x;
+    const int64_t row0 = tile * K::TR;
+    const int rr = ps * RPP + grp;
+    const int64_t i = row0 + rr;
+    int p0nn, lennn, cn[SL];
+    double vn[SL];
+    load_rp(u + 2, p0nn, lennn);
+    double2 y = make_double2(0.0, 0.0), xd = make_double2(0.0, 0.0);
+    if (__all_sync(FULL, lenc <= NZ)) {
+      const int dcol = (int)(xoff + i);
+      double2 xv[NZ];
+      unsigned dm = 0;  // bit k: entry k is the diagonal
+#pragma unroll
+      for (int k = 0; k < NZ; ++k) {
+        const int c = __shfl_sync(FULL, cc[k / G], k % G, G);
+        dm |= (c == dcol ? 1u : 0u) << k;
+        if (k < lenc) xv[k] = __ldg(reinterpret_cast<const double2*>(Xext + (int64_t)c * T) + gl);
+      }
+      load_cv(p0n, lenn, cn, vn);  // next unit's entries, behind this unit's gathers
+#pragma unroll
+      for (int k = 0; k < NZ; ++k) {
+        const double a = __shfl_sync(FULL, cv[k / G], k % G, G);
+        if (k < lenc) {
+          y.x = __fma_rn(a, xv[k].x, y.x);
+          y.y = __fma_rn(a, xv[k].y, y.y);
+          if ((dm >> k) & 1u) xd = xv[k];
+        }
+      }
+    } else {
+      load_cv(p0n, lenn, cn, vn);
+      const int dcol = (int)(xoff + i);
+      for (int p = p0c; p < p0c + lenc; ++p) {  // long rows: plain loop, same order
+        const int c = __ldg(col + p);
+        const double2 xv = __ldg(reinterpret_cast<const double2*>(Xext + (int64_t)c * T) + gl);
+        const double a = __ldg(val + p);
+        y.x = __fma_rn(a, xv.x, y.x);
+        y.y = __fma_rn(a, xv.y, y.y);
+        if (c == dcol) xd = xv;
+      }
+    }
+    if (i < n) *reinterpret_cast<double2*>(Y + i * T + 2 * gl) = y;
+    *reinterpret_cast<double2*>(sY + rr * S + 2 * gl) = y;  // rows beyond the end stay 0 in the Gram
+    *reinterpret_cast<double2*>(sX + rr * S + 2 * gl) = xd;
+    p0c = p0n;
+    lenc = lenn;
+    p0n = p0nn;
+    lenn = lennn;
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+      cc[s] = cn[s];
+      cv[s] = vn[s];
+    }
+    if (ps == P - 1) {
+      // ---------------- Gram partial Xᵀ Y and Xᵀ r of the tile
+      const int rows = (int)((n - row0) < K::TR ? (n - row0) : K::TR);
+      if (r != nullptr)
+        for (int e = tid; e < K::TR; e += 256) sr[e] = e < rows ? __ldg(r + row0 + e) : 0.0;
+      __syncthreads();
+      const int slice = warp % K::WS;
+#pragma unroll
+      for (int uu = 0; uu < K::TPW; ++uu) {
+        const int ot = (warp / K::WS) * K::TPW + uu;
+        const int mi = ot / K::MT, ni = ot % K::MT;
+        double d0 = acc[uu][0], d1 = acc[uu][1];
+#pragma unroll
+        for (int kk = slice * 4; kk < K::TR; kk += 4 * K::WS)
+          dmma(d0, d1, sX[(kk + q4) * S + mi * 8 + g], sY[(kk + q4) * S + ni * 8 + g]);
+        acc[uu][0] = d0;
+        acc[uu][1] = d1;
+      }
+      if (r != nullptr)
+        for (int q = warp; q < rows; q += 8) {
+          const double vr = sr[q];
+          if (lane < T) accv[0] = fma(sX[q * S + lane], vr, accv[0]);
+          if (lane + 32 < T) accv[1] = fma(sX[q * S + lane + 32], vr, accv[1]);
+        }
+      __syncthreads();
+    }
+  }
+  gram_epilogue<T, K::MT, K::WS, K::TPW>(part, acc, accv, sm, tl, ch, r != nullptr);
+}
+
+// ----------------------------------------------------------------------------
+// The same fused SpMM + Gram on the ELL copy of A that eks_setup_csr builds when
+// every row has ≤ 8 entries (all stencil operators): tiles of kEllTR = 64 rows,
+// slot k of row tile·64 + rr at index (tile·W + k)·64 + rr, padded slots holding
+// value 0 and a valid column.  Every address is computed, not loaded; no
+// predication, no shuffles.  Tiles are dealt round-robin to the CTAs so the grid
+// sweeps one window of rows (far neighbours ±N² are L2 hits, A and X leave HBM
+// once).  The tile's own X rows are streamed into shared memory with cp.async one
+// tile ahead (double buffer); entries whose column falls inside the tile (the
+// diagonal and the ±1 neighbours of a stencil) read that copy, only the others are
+// 16-byte global gathers — and that copy is also the X of the Gram.  The columns of
+// the next unit are loaded while this unit's gathers are in flight.  Padded slots
+// add fma(0, x, y) = y exactly (y is never −0 from a +0 start), so Y stays bitwise
+// equal to the ascending-p CSR accumulation (R20).
+// ----------------------------------------------------------------------------
+template <int T, int W>
+struct SeCfg {
+  static constexpr int TR = kEllTR;
+  static constexpr int S = T + 4;
+  static constexpr int G = T / 2;       // threads per row (2 columns each)
+  static constexpr int RPP = 256 / G;    // rows per unit
+  static constexpr int PASSES = TR / RPP;
+  static constexpr int MT = T / 8;
+  static constexpr int OT = MT * MT;
+  static constexpr int WS = OT >= 8 ? 1 : 8 / OT;
+  static constexpr int TPW = OT >= 8 ? OT / 8 : 1;
+  static constexpr int RED = (WS > 1 ? 8 * T * T : 0) + 8 * T;
+  static constexpr int SMEM0 = 3 * TR * S + TR;  // 2 X tiles, Y tile, r
+  static constexpr int SMEM = SMEM0 > RED ? SMEM0 : RED;
+};
+
+template <int T, int W>
+__global__ void __launch_bounds__(256, (T >= 64 ? 2 : 3))
+    k_spmm_gram_ell(int64_t n, const int* __restrict__ ecol, const double* __restrict__ eval,
+                    const double* __restrict__ Xext, int64_t xoff, double* __restrict__ Y,
+                    const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch) {
+  using K = SeCfg<T, W>;
+  constexpr int S = K::S, G = K::G, P = K::PASSES, RPP = K::RPP, TR = K::TR, H = T / 2;
+  extern __shared__ __align__(128) double sm[];
+  double* sY = sm + 2 * TR * S;
+  double* sr = sm + 3 * TR * S;
+  const double2* __restrict__ X2 = reinterpret_cast<const double2*>(Xext);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q4 = lane & 3;
+  const int grp = tid / G, gl = tid % G;
+  const int64_t ntiles = (n + TR - 1) / TR;
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto load_xtile = [&](int64_t tile, double* dst) {  // own X rows of a tile, zero-filled past n
+    const int64_t row0 = tile * TR;
+    const int rows = (int)((n - row0) < TR ? (n - row0) : TR);
+    for (int e = tid; e < TR * H; e += 256) {
+      const int q = e / H, c = (e % H) * 2;
+      const bool ok = q < rows;
+      cp16(dst + q * S + c, ok ? (const void*)(Xext + (xoff + row0 + q) * T + c) : (const void*)Xext, ok ? 16 : 0);
+    }
+    cp_commit();
+  };
+
+  double acc[K::TPW][2];
+#pragma unroll
+  for (int j = 0; j < K::TPW; ++j) acc[j][0] = acc[j][1] = 0.0;
+  double accv[2] = {0.0, 0.0};
+
+  int cc[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) cc[k] = 0;
+  if (my_tiles > 0) {
+    const int64_t e = (int64_t)blockIdx.x * (TR * W) + grp;
+#pragma unroll
+    for (int k = 0; k < W; ++k) cc[k] = __ldg(ecol + e + k * TR);
+    load_xtile(blockIdx.x, sm);
+  }
+  for (int64_t j = 0; j < my_tiles; ++j) {
+    const int64_t tile = blockIdx.x + j * gridDim.x;
+    const int64_t row0 = tile * TR, xrow0 = xoff + row0;
+    const int rows = (int)((n - row0) < TR ? (n - row0) : TR);
+    const bool more = j + 1 < my_tiles;
+    double* sX = sm + (j & 1) * TR * S;
+    if (more) load_xtile(tile + gridDim.x, sm + ((j + 1) & 1) * TR * S);
+    else cp_commit();
+    cp_wait<1>();     // this tile's X rows have landed
+    __syncthreads();  // … and are visible to every thread
+#pragma unroll
+    for (int ps = 0; ps < P; ++ps) {
+      const int rr = ps * RPP + grp;
+      const int64_t i = row0 + rr;
+      const int64_t e = tile * (TR * W) + rr;
+      double2 xv[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        const int64_t lc = (int64_t)cc[k] - xrow0;
+        if ((uint64_t)lc < (uint64_t)TR) xv[k] = *reinterpret_cast<const double2*>(sX + lc * S + 2 * gl);
+        else xv[k] = __ldg(X2 + (int64_t)cc[k] * H + gl);
+      }
+      double a[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) a[k] = __ldg(eval + e + k * TR);
+      if (ps + 1 < P || more) {  // next unit's columns, behind this unit's gathers
+        const int64_t e1 = ps + 1 < P ? e + RPP : (tile + gridDim.x) * (TR * W) + grp;
+#pragma unroll
+        for (int k = 0; k < W; ++k) cc[k] = __ldg(ecol + e1 + k * TR);
+      }
+      double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        y.x = __fma_rn(a[k], xv[k].x, y.x);
+        y.y = __fma_rn(a[k], xv[k].y, y.y);
+      }
+      if (i < n) reinterpret_cast<double2*>(Y)[i * H + gl] = y;
+      *reinterpret_cast<double2*>(sY + rr * S + 2 * gl) = y;  // padded rows are 0 in the Gram
+    }
+    // ---------------- Gram partial Xᵀ Y and Xᵀ r of the tile
+    if (r != nullptr)
+      for (int q = tid; q < TR; q += 256) sr[q] = q < rows ? __ldg(r + row0 + q) : 0.0;
+    __syncthreads();
+    const int slice = warp % K::WS;
+#pragma unroll
+    for (int uu = 0; uu < K::TPW; ++uu) {
+      const int ot = (warp / K::WS) * K::TPW + uu;
+      const int mi = ot / K::MT, ni = ot % K::MT;
+      double d0 = acc[uu][0], d1 = acc[uu][1];
+#pragma unroll
+      for (int kk = slice * 4; kk < TR; kk += 4 * K::WS)
+        dmma(d0, d1, sX[(kk + q4) * S + mi * 8 + g], sY[(kk + q4) * S + ni * 8 + g]);
+      acc[uu][0] = d0;
+      acc[uu][1] = d1;
+    }
+    if (r != nullptr)
+      for (int q = warp; q < rows; q += 8) {
+        const double vr = sr[q];
+        if (lane < T) accv[0] = fma(sX[q * S + lane], vr, accv[0]);
+        if (lane + 32 < T) accv[1] = fma(sX[q * S + lane + 32], vr, accv[1]);
+      }
+    __syncthreads();  // sX / sY / sr are rewritten by the next tile
+  }
+  cp_wait<0>();
+  gram_epilogue<T, K::MT, K::WS, K::TPW>(part, acc, accv, sm, tl, ch, r != nullptr);
 }
 
 // ----------------------------------------------------------------------------
@@ -670,7 +833,7 @@ static int grid_for(int nblk_max, int occ) {
 }
 template <int T, int NQ, int NL, bool V>
 static cudaError_t launch_sweep_t(cudaStream_t st, int64_t n, const double* Zin, double* Zout, const SweepPtrs& P,
-                                  const double* C, const double* v, double* part, int nblk) {
+                                  const double* C, const double* v, double* part, int nblk, const Tail& tl) {
   using K = SwCfg<T, NQ, NL, V>;
   const size_t sm = (size_t)K::SMEM * 8;
   if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
@@ -682,7 +845,7 @@ static cudaError_t launch_sweep_t(cudaStream_t st, int64_t n, const double* Zin,
   }
   nblk = grid_for(nblk, occ);
   t_last_grid = nblk;
-  k_sweep<T, NQ, NL, V><<<nblk, 256, sm, st>>>(n, Zin, Zout, P, C, v, part);
+  k_sweep<T, NQ, NL, V><<<nblk, 256, sm, st>>>(n, Zin, Zout, P, C, v, part, NL > 0 ? tl : Tail{});
   return cudaGetLastError();
 }
 
@@ -714,67 +877,111 @@ size_t sweep_part_stride(int t, int nl, bool v) { return (size_t)nl * t * t + (v
 
 template <int T, int K>
 static cudaError_t sweep_k(cudaStream_t st, bool upd, int64_t n, const double* Zin, double* Zout, const SweepPtrs& P,
-                           const double* C, const double* vec, double* part, int nblk) {
+                           const double* C, const double* vec, double* part, int nblk, const Tail& tl) {
   if constexpr (K <= 8 && (T <= 16 || (T == 32 && K <= 4) || (T == 64 && K <= 2))) {
-    if (upd) return launch_sweep_t<T, K, 0, false>(st, n, Zin, Zout, P, C, vec, part, nblk);
+    if (upd) return launch_sweep_t<T, K, 0, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
     // partial products need NL·(T/8)² to be a multiple or divisor of the 8 warps
-    if constexpr ((K & (K - 1)) == 0) return launch_sweep_t<T, 0, K, false>(st, n, Zin, Zout, P, C, vec, part, nblk);
+    if constexpr ((K & (K - 1)) == 0)
+      return launch_sweep_t<T, 0, K, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
   }
   return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_sweep(cudaStream_t st, int t, int nq, int nl, bool v, int64_t n, const double* Zin, double* Zout,
-                         const SweepPtrs& P, const double* C, const double* vec, double* part, int nblk) {
+                         const SweepPtrs& P, const double* C, const double* vec, double* part, int nblk,
+                         const Tail& tl) {
   if (nq > sweep_max_blocks(t) || nl > sweep_max_blocks(t)) return cudaErrorInvalidValue;
   EKS_SW_T(t, {
-    if (nq == 0 && nl == 1 && v) return launch_sweep_t<T, 0, 1, true>(st, n, Zin, Zout, P, C, vec, part, nblk);
+    if (nq == 0 && nl == 1 && v) return launch_sweep_t<T, 0, 1, true>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
     if (v) return cudaErrorInvalidValue;
-    if (nq == 1 && nl == 1) return launch_sweep_t<T, 1, 1, false>(st, n, Zin, Zout, P, C, vec, part, nblk);
-    if (nq == 2 && nl == 2) return launch_sweep_t<T, 2, 2, false>(st, n, Zin, Zout, P, C, vec, part, nblk);
+    if (nq == 1 && nl == 1) return launch_sweep_t<T, 1, 1, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
+    if (nq == 2 && nl == 2) return launch_sweep_t<T, 2, 2, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
     if (nq > 0 && nl > 0) return cudaErrorInvalidValue;
     const bool upd = nq > 0;
     switch (upd ? nq : nl) {
-      case 1: return sweep_k<T, 1>(st, upd, n, Zin, Zout, P, C, vec, part, nblk);
-      case 2: return sweep_k<T, 2>(st, upd, n, Zin, Zout, P, C, vec, part, nblk);
-      case 3: return sweep_k<T, 3>(st, upd, n, Zin, Zout, P, C, vec, part, nblk);
-      case 4: return sweep_k<T, 4>(st, upd, n, Zin, Zout, P, C, vec, part, nblk);
-      case 5: return sweep_k<T, 5>(st, upd, n, Zin, Zout, P, C, vec, part, nblk);
-      case 6: return sweep_k<T, 6>(st, upd, n, Zin, Zout, P, C, vec, part, nblk);
-      case 7: return sweep_k<T, 7>(st, upd, n, Zin, Zout, P, C, vec, part, nblk);
-      case 8: return sweep_k<T, 8>(st, upd, n, Zin, Zout, P, C, vec, part, nblk);
+      case 1: return sweep_k<T, 1>(st, upd, n, Zin, Zout, P, C, vec, part, nblk, tl);
+      case 2: return sweep_k<T, 2>(st, upd, n, Zin, Zout, P, C, vec, part, nblk, tl);
+      case 3: return sweep_k<T, 3>(st, upd, n, Zin, Zout, P, C, vec, part, nblk, tl);
+      case 4: return sweep_k<T, 4>(st, upd, n, Zin, Zout, P, C, vec, part, nblk, tl);
+      case 5: return sweep_k<T, 5>(st, upd, n, Zin, Zout, P, C, vec, part, nblk, tl);
+      case 6: return sweep_k<T, 6>(st, upd, n, Zin, Zout, P, C, vec, part, nblk, tl);
+      case 7: return sweep_k<T, 7>(st, upd, n, Zin, Zout, P, C, vec, part, nblk, tl);
+      case 8: return sweep_k<T, 8>(st, upd, n, Zin, Zout, P, C, vec, part, nblk, tl);
       default: return cudaErrorInvalidValue;
     }
   });
   return cudaErrorInvalidValue;
 }
 
-int spmm_gram_max_row() { return 8; }
+bool spmm_gram_fused_chol(int t) { return t == 8 || t == 16; }
+
+template <int T, int NZ>
+static cudaError_t spmm_gram_t(cudaStream_t st, int64_t n, const int* rp, const int* col, const double* val,
+                               const double* Xext, int64_t xoff, double* Y, const double* r, double* part, int nblk,
+                               const Tail& tl, const CholArgs& ch) {
+  using K = SgCfg<T, NZ>;
+  const size_t sm = (size_t)K::SMEM * 8;
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(k_spmm_gram<T, NZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmm_gram<T, NZ>, 256, sm);
+    if (occ < 1) occ = 1;
+  }
+  nblk = grid_for(nblk, occ);
+  t_last_grid = nblk;
+  k_spmm_gram<T, NZ><<<nblk, 256, sm, st>>>(n, rp, col, val, Xext, xoff, Y, r, part, tl, ch);
+  return cudaGetLastError();
+}
+
+template <int T, int W>
+static cudaError_t spmm_gram_ell_t(cudaStream_t st, int64_t n, const int* ecol, const double* eval, const int* tmax,
+                                   int64_t n_ext, const double* Xext, int64_t xoff, double* Y, const double* r,
+                                   double* part, int nblk, const Tail& tl, const CholArgs& ch) {
+  using K = SeCfg<T, W>;
+  const size_t sm = (size_t)K::SMEM * 8;
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(k_spmm_gram_ell<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmm_gram_ell<T, W>, 256, sm);
+    if (occ < 1) occ = 1;
+  }
+  nblk = grid_for(nblk, occ);
+  t_last_grid = nblk;
+  (void)tmax;
+  (void)n_ext;
+  k_spmm_gram_ell<T, W><<<nblk, 256, sm, st>>>(n, ecol, eval, Xext, xoff, Y, r, part, tl, ch);
+  return cudaGetLastError();
+}
+
+int ell_width(int maxrow) { return maxrow <= 5 ? 5 : (maxrow <= 7 ? 7 : (maxrow <= 8 ? 8 : 0)); }
+
+cudaError_t launch_spmm_gram_ell(cudaStream_t st, int t, int64_t n, const int* ecol, const double* eval, int w,
+                                 const int* tmax, int64_t n_ext, const double* Xext, int64_t xoff, double* Y,
+                                 const double* r, double* part, int nblk, const Tail& tl, const CholArgs& ch) {
+  if (ch.on && !spmm_gram_fused_chol(t)) return cudaErrorInvalidValue;
+  EKS_SW_T(t, {
+    if (w == 5) return spmm_gram_ell_t<T, 5>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+    if (w == 7) return spmm_gram_ell_t<T, 7>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+    if (w == 8) return spmm_gram_ell_t<T, 8>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+  });
+  return cudaErrorInvalidValue;
+}
 
 cudaError_t launch_spmm_gram(cudaStream_t st, int t, int64_t n, const int* rp, const int* col, const double* val,
-                             const double* Xext, const double* Xloc, double* Y, const double* r, double* part,
-                             int nblk) {
+                             int maxrow, const double* Xext, int64_t xoff, double* Y, const double* r, double* part,
+                             int nblk, const Tail& tl, const CholArgs& ch) {
+  if (ch.on && !spmm_gram_fused_chol(t)) return cudaErrorInvalidValue;
   EKS_SW_T(t, {
-    using K = SgCfg<T>;
-    static_assert(K::MAXROW == 8, "spmm_gram_max_row");
-    const size_t sm = (size_t)K::SMEM * 8;
-    static int occ = 0;
-    if (!occ) {
-      cudaFuncSetAttribute(k_spmm_gram<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmm_gram<T>, 256, sm);
-      if (occ < 1) occ = 1;
-    }
-    nblk = grid_for(nblk, occ);
-    t_last_grid = nblk;
-    k_spmm_gram<T><<<nblk, 256, sm, st>>>(n, rp, col, val, Xext, Xloc, Y, r, part);
+    (void)maxrow;  // rows of any length (the ELL kernel covers rows of ≤ 8 entries)
+    return spmm_gram_t<T, 8>(st, n, rp, col, val, Xext, xoff, Y, r, part, nblk, tl, ch);
   });
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 template <int T, int C1N>
 static cudaError_t apply_t(cudaStream_t st, int64_t n, double* Z2W, double* AZ2AW, const double* Rinv,
-                           const double* alpha, double* x, double* dx, const double* r, double* rnew,
-                           double* rho_part, const int* flag, int mode, const double* AWprev, double* c1part,
-                           int nblk) {
+                           const double* alpha, double* x, double* dx, const double* r, double* rnew, const int* flag,
+                           int mode, const double* AWprev, double* part, int nblk, const Tail& tl) {
   using K = ApCfg<T, C1N>;
   const size_t sm = (size_t)K::SMEM * 8;
   if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
@@ -786,8 +993,8 @@ static cudaError_t apply_t(cudaStream_t st, int64_t n, double* Z2W, double* AZ2A
   }
   nblk = grid_for(nblk, occ);
   t_last_grid = nblk;
-  k_apply_tc<T, C1N><<<nblk, 256, sm, st>>>(n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, rho_part, flag, mode,
-                                            AWprev, c1part);
+  k_apply_tc<T, C1N><<<nblk, 256, sm, st>>>(n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part,
+                                            tl);
   return cudaGetLastError();
 }
 
@@ -802,16 +1009,15 @@ bool apply_c1_supported(int t, int c1n) {
 }
 
 cudaError_t launch_apply_tc(cudaStream_t st, int t, int64_t n, double* Z2W, double* AZ2AW, const double* Rinv,
-                            const double* alpha, double* x, double* dx, const double* r, double* rnew,
-                            double* rho_part, const int* flag, int mode, int nblk, int c1n, const double* AWprev,
-                            double* c1part) {
+                            const double* alpha, double* x, double* dx, const double* r, double* rnew, const int* flag,
+                            int mode, int nblk, int c1n, const double* AWprev, double* part, const Tail& tl) {
   EKS_SW_T(t, {
-    if (c1n == 0) return apply_t<T, 0>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, rho_part, flag, mode, AWprev,
-                                       c1part, nblk);
-    if (c1n == 1) return apply_t<T, 1>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, rho_part, flag, mode, AWprev,
-                                       c1part, nblk);
-    if (c1n == 2) return apply_t<T, 2>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, rho_part, flag, mode, AWprev,
-                                       c1part, nblk);
+    if (c1n == 0)
+      return apply_t<T, 0>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part, nblk, tl);
+    if (c1n == 1)
+      return apply_t<T, 1>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part, nblk, tl);
+    if (c1n == 2)
+      return apply_t<T, 2>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part, nblk, tl);
   });
   return cudaErrorInvalidValue;
 }

@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "eks_device.cuh"
+
 namespace eks {
 
 constexpr int kSweepMaxBlocks = 8;
@@ -25,23 +27,36 @@ int sweep_last_grid();
 //   part[b] = Σ_{rows of CTA b} [L_0 … L_{nl-1}]ᵀ R  (+ L_0ᵀ vec when v)        (nl > 0)
 // Supported (nq, nl): (k,0) for k ≤ sweep_max_blocks(t); (0,k) for k a power of two
 // ≤ sweep_max_blocks(t); (0,1)+v; (1,1); (2,2).
+// With tl.cnt set (nl > 0) the grid's last CTAs also reduce the partials into tl.out (see Tail).
 cudaError_t launch_sweep(cudaStream_t st, int t, int nq, int nl, bool v, int64_t n, const double* Zin, double* Zout,
-                         const SweepPtrs& P, const double* C, const double* vec, double* part, int nblk);
+                         const SweepPtrs& P, const double* C, const double* vec, double* part, int nblk,
+                         const Tail& tl = Tail{});
 
-// Fused Y = A·X (rows [0,n), CSR with ext-indexed columns, every row ≤ spmm_gram_max_row() entries)
-// and per-CTA partials of [XᵀY | Xᵀr] (layout of sweep_part_stride(t,1,true); r may be NULL).
-int spmm_gram_max_row();
+// Fused Y = A·X (rows [0,n), CSR with columns into Xext; row i's diagonal is column xoff+i)
+// and per-CTA partials of [XᵀY | Xᵀr] (layout of sweep_part_stride(t,1,true); r may be NULL),
+// reduced into tl.out (t·t + t) when tl.cnt is set; with ch.on (t ∈ {8,16}) the last CTA then
+// factors B = RᵀR and writes R, R⁻¹, α̃ = R⁻ᵀ(Xᵀr) like launch_chol.
+bool spmm_gram_fused_chol(int t);
+// ELL copy of A for rows of ≤ 8 entries (eks_setup_csr): tiles of kEllTR rows, slot k of
+// row tile·kEllTR + rr at (tile·w + k)·kEllTR + rr; padding: value 0, a valid column.
+constexpr int kEllTR = 64;
+int ell_width(int maxrow);  // 5, 7 or 8; 0: rows too long for the ELL path
+// tmax[tile] = the largest X row (ext index) a tile gathers (drives the L2 prefetch); n_ext = rows of Xext.
+cudaError_t launch_spmm_gram_ell(cudaStream_t st, int t, int64_t n, const int* ecol, const double* eval, int w,
+                                 const int* tmax, int64_t n_ext, const double* Xext, int64_t xoff, double* Y,
+                                 const double* r, double* part, int nblk, const Tail& tl, const CholArgs& ch);
+// maxrow = longest CSR row (selects the register-resident fast path; longer rows still work).
 cudaError_t launch_spmm_gram(cudaStream_t st, int t, int64_t n, const int* rp, const int* col, const double* val,
-                             const double* Xext, const double* Xloc, double* Y, const double* r, double* part,
-                             int nblk);
+                             int maxrow, const double* Xext, int64_t xoff, double* Y, const double* r, double* part,
+                             int nblk, const Tail& tl, const CholArgs& ch);
 
 // W = Z2·Rinv, AW = AZ2·Rinv in place + fused per-block x/r update (same contract as launch_apply).
-// c1n > 0 additionally writes per-CTA partials (layout [c1n][t][t]) of the next block's CGS pass-1
-// coefficients [AW_prev, AW]ᵀ AW (c1n = 2) or AWᵀAW (c1n = 1) into c1part — the SRE-CG window.
+// Per-CTA partials in `part` (stride c1n·t·t + 2): the next block's CGS pass-1 coefficients
+// [AW_prev, AW]ᵀ AW (c1n = 2) or AWᵀAW (c1n = 1) — the SRE-CG window — then ‖rnew‖² (last block).
+// They are reduced by the grid's tail into tl (tl.count = c1n·t·t [+1]); tl.cnt == NULL: none.
 bool apply_c1_supported(int t, int c1n);
 cudaError_t launch_apply_tc(cudaStream_t st, int t, int64_t n, double* Z2W, double* AZ2AW, const double* Rinv,
-                            const double* alpha, double* x, double* dx, const double* r, double* rnew,
-                            double* rho_part, const int* flag, int mode, int nblk, int c1n = 0,
-                            const double* AWprev = nullptr, double* c1part = nullptr);
+                            const double* alpha, double* x, double* dx, const double* r, double* rnew, const int* flag,
+                            int mode, int nblk, int c1n, const double* AWprev, double* part, const Tail& tl);
 
 }  // namespace eks
