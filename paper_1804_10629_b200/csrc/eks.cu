@@ -64,6 +64,16 @@ struct eks_ctx {
   int* d_ecol = nullptr;
   double* d_eval = nullptr;
   int* d_tmax = nullptr;           // per ELL tile: largest ext column (L2 prefetch of the far slab)
+  // segment plan of the TMA-staged SpMM (eks_sweep.cuh SegPlan); device arrays owned here
+  bool seg_ok = false;
+  eks::SegPlan seg{};
+  int* d_seg = nullptr;
+  int* d_segrows = nullptr;
+  int* d_segown = nullptr;
+  unsigned short* d_lidx = nullptr;
+  double* d_sval = nullptr;
+  int spmm_path = 0;               // 0 auto, 1 ell, 2 csr, 3 seg (EKS_SPMM_PATH, for A/B measurements)
+  int chol_mode = 0;               // 0 separate one-warp Cholesky launch, 1 in the SpMM+Gram tail (EKS_CHOL)
   // workspace, keyed by t
   int ws_t = 0;
   std::vector<Block> Wpool, AWpool;  // Wpool ext layout, AWpool local
@@ -440,7 +450,14 @@ eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const doubl
   }
   {
     KScope k(ctx, EKS_K_SPMM);
-    if (ctx->ell_w)
+    // measured (tools/spmm_micro.py): the ELL gather kernel is fastest for t ≤ 32, the TMA-staged
+    // segment kernel for t = 64; EKS_SPMM_PATH=seg|ell|csr forces one for A/B measurements
+    const bool use_seg = ctx->seg_ok && eks::spmm_seg_fits(t, ctx->ell_w, ctx->seg.cap) &&
+                         (ctx->spmm_path == 3 || (ctx->spmm_path == 0 && t == 64));
+    if (use_seg)
+      CK(eks::launch_spmm_seg(ctx->stream, t, ctx->n, ctx->seg, ctx->ell_w, X.base, Y, r, ctx->part, ctx->nblk,
+                              tail(ctx, 2, out, stride), c));
+    else if (ctx->ell_w && ctx->spmm_path <= 1)
       CK(eks::launch_spmm_gram_ell(ctx->stream, t, ctx->n, ctx->d_ecol, ctx->d_eval, ctx->ell_w, ctx->d_tmax, n_ext(ctx),
                                    X.base,
                                    (int64_t)(X.loc - X.base) / t, Y, r, ctx->part, ctx->nblk, tail(ctx, 2, out, stride),
@@ -579,10 +596,15 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
   ch.alpha = with_update ? ctx->alpha + alpha_off : nullptr;
   ch.flag = ctx->flag;
   ch.gblock = gb;
-  ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg, &ch));
-  if (!ctx->chol_fused)
-    ST(chol(ctx, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
-            with_update ? ctx->alpha + alpha_off : nullptr, gb));
+  // t ≤ 32: the R⁻¹ kernel factors the Gram itself (every CTA, identical inputs on every rank);
+  // otherwise the last CTA of the SpMM+Gram kernel or a separate Cholesky launch does it.
+  ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg,
+               ctx->chol_mode == 1 ? &ch : nullptr));
+  if (!ctx->chol_fused) {  // default: one-warp Cholesky launch (rsqrt pivots for t ≤ 32)
+    KScope k(ctx, EKS_K_CHOL);
+    CK(eks::launch_chol_fast(ctx->stream, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
+                             with_update ? ctx->alpha + alpha_off : nullptr, ctx->flag, gb));
+  }
   // SRE-CG: the next block's window is {W_prev, W_new} and its Z is AW_new, so the R⁻¹ kernel
   // that produces AW_new also accumulates the next CGS pass-1 coefficients C1 = [AW_prev, AW_new]ᵀAW_new.
   const int c1n = (ring && eks::apply_c1_supported(t, 2)) ? (nblocks == 0 ? 1 : 2) : 0;
@@ -717,6 +739,87 @@ void plan_halo(int rank, int nranks, const int64_t* ranges, int64_t n, const int
   P.int_hi = best_lo + best_len;
 }
 
+// Segment plan for the TMA-staged SpMM (eks_sweep.cuh SegPlan): per plan tile of kSegPT rows,
+// the sorted distinct X rows its entries use, merged into runs (gaps of ≤ 2 rows are copied
+// too); every entry's column becomes a row of the concatenated runs.  Not built (the ELL
+// gather kernel runs instead) when a tile needs more than kSegMax runs.
+eks_status build_seg_plan(eks_ctx* ctx, int64_t n, const std::vector<int64_t>& rp, const std::vector<int32_t>& ecol,
+                          const std::vector<double>& val, int64_t halo_before, int w) {
+  constexpr int PT = eks::kSegPT, SM = eks::kSegMax, GAP = 2;
+  const int64_t ntp = (n + PT - 1) / PT;
+  std::vector<int32_t> seg((size_t)ntp * SM * 2, 0), rows((size_t)ntp, 0), own((size_t)ntp, 0);
+  const int VS = (w + 1) & ~1;  // value slots per row (eks::seg_vs)
+  std::vector<uint16_t> lidx((size_t)ntp * PT * 8, 0);
+  std::vector<double> sv((size_t)ntp * PT * VS, 0.0);
+  std::vector<int32_t> cols;
+  int cap = 0;
+  for (int64_t p = 0; p < ntp; ++p) {
+    cols.clear();
+    const int64_t i0 = p * PT, i1 = std::min(n, i0 + PT);
+    for (int64_t i = i0; i < i1; ++i) {
+      cols.push_back((int32_t)(halo_before + i));
+      for (int64_t q = rp[i]; q < rp[i + 1]; ++q) cols.push_back(ecol[q]);
+    }
+    std::sort(cols.begin(), cols.end());
+    cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+    int32_t rs[SM], rl[SM], ro[SM];
+    int nr = 0, tot = 0;
+    for (int32_t c : cols) {
+      if (nr > 0 && c <= rs[nr - 1] + rl[nr - 1] + GAP) {
+        rl[nr - 1] = c - rs[nr - 1] + 1;
+        continue;
+      }
+      if (nr == SM) return EKS_OK;  // too irregular: keep the gather kernels
+      rs[nr] = c;
+      rl[nr] = 1;
+      ++nr;
+    }
+    for (int q = 0; q < nr; ++q) {
+      ro[q] = tot;
+      tot += rl[q];
+      seg[((size_t)p * SM + q) * 2] = rs[q];
+      seg[((size_t)p * SM + q) * 2 + 1] = rl[q];
+    }
+    if (tot > 65535) return EKS_OK;
+    cap = std::max(cap, tot);
+    rows[p] = tot;
+    auto bufrow = [&](int32_t c) {
+      int q = 0;
+      while (q + 1 < nr && c >= rs[q + 1]) ++q;
+      return ro[q] + (c - rs[q]);
+    };
+    own[p] = bufrow((int32_t)(halo_before + i0));
+    for (int rr = 0; rr < PT; ++rr)
+      for (int k = 0; k < 8; ++k) {  // row-major: 8 local indices (16 bytes) and VS values per row
+        const int64_t i = i0 + rr, e = ((size_t)p * PT + rr) * 8 + k, ev = ((size_t)p * PT + rr) * VS + k;
+        if (i < n && k < rp[i + 1] - rp[i]) {
+          lidx[e] = (uint16_t)bufrow(ecol[rp[i] + k]);
+          sv[ev] = val[rp[i] + k];
+        } else {
+          lidx[e] = (uint16_t)(i < n ? bufrow((int32_t)(halo_before + i)) : 0);
+        }
+      }
+  }
+  auto up = [&](void** d, const void* h, size_t bytes) -> eks_status {
+    CK(cudaMalloc(d, bytes + 16));
+    CK(cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice));
+    return EKS_OK;
+  };
+  ST(up((void**)&ctx->d_seg, seg.data(), sizeof(int32_t) * seg.size()));
+  ST(up((void**)&ctx->d_segrows, rows.data(), sizeof(int32_t) * rows.size()));
+  ST(up((void**)&ctx->d_segown, own.data(), sizeof(int32_t) * own.size()));
+  ST(up((void**)&ctx->d_lidx, lidx.data(), sizeof(uint16_t) * lidx.size()));
+  ST(up((void**)&ctx->d_sval, sv.data(), sizeof(double) * sv.size()));
+  ctx->seg.seg = ctx->d_seg;
+  ctx->seg.rows = ctx->d_segrows;
+  ctx->seg.own = ctx->d_segown;
+  ctx->seg.lidx = ctx->d_lidx;
+  ctx->seg.val = ctx->d_sval;
+  ctx->seg.cap = cap;
+  ctx->seg_ok = true;
+  return EKS_OK;
+}
+
 void begin_run(eks_ctx* ctx, const eks_options* opt) {
   ctx->prof_on = opt && opt->profile;
   ctx->prof = eks_profile{};
@@ -777,6 +880,9 @@ eks_status eks_create(eks_ctx** out, const eks_dist* dist) {
     if (cudaMallocHost((void**)&ctx->h_scal, 16 * sizeof(double)) != cudaSuccess) { st = EKS_ERR_CUDA; break; }
     if (cudaMallocHost((void**)&ctx->h_flag, 4 * sizeof(int)) != cudaSuccess) { st = EKS_ERR_CUDA; break; }
     ctx->h_flag[0] = INT_MAX;
+    if (const char* e = getenv("EKS_CHOL")) ctx->chol_mode = atoi(e);
+    if (const char* e = getenv("EKS_SPMM_PATH"))
+      ctx->spmm_path = !strcmp(e, "ell") ? 1 : (!strcmp(e, "csr") ? 2 : (!strcmp(e, "seg") ? 3 : 0));
     if (ctx->nranks > 1) {
       ncclUniqueId u;
       memcpy(&u, dist->nccl_id, 128);
@@ -892,9 +998,13 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   if (!ctx->have_matrix || ctx->n != n || old_before != ctx->halo_before || old_after != ctx->halo_after)
     free_workspace(ctx);
   for (void* p : {(void*)ctx->d_rp, (void*)ctx->d_col, (void*)ctx->d_val, (void*)ctx->d_ecol, (void*)ctx->d_eval,
-                  (void*)ctx->d_tmax})
+                  (void*)ctx->d_tmax, (void*)ctx->d_seg, (void*)ctx->d_segrows, (void*)ctx->d_segown,
+                  (void*)ctx->d_lidx, (void*)ctx->d_sval})
     dfree(p);
-  ctx->d_tmax = nullptr;
+  ctx->d_tmax = ctx->d_seg = ctx->d_segrows = ctx->d_segown = nullptr;
+  ctx->d_lidx = nullptr;
+  ctx->d_sval = nullptr;
+  ctx->seg_ok = false;
   ctx->d_rp = nullptr;
   ctx->d_col = nullptr;
   ctx->d_val = nullptr;
@@ -937,6 +1047,7 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
     CK(cudaMemcpy(ctx->d_eval, ev.data(), sizeof(double) * ev.size(), cudaMemcpyHostToDevice));
     CK(cudaMalloc((void**)&ctx->d_tmax, sizeof(int32_t) * tmax.size()));
     CK(cudaMemcpy(ctx->d_tmax, tmax.data(), sizeof(int32_t) * tmax.size(), cudaMemcpyHostToDevice));
+    ST(build_seg_plan(ctx, n, rp, ecol, val, plan.halo_before, w));
     ctx->ell_w = w;
   }
   ctx->n_global = n_global;
@@ -1147,6 +1258,11 @@ eks_status eks_destroy(eks_ctx* ctx) {
   dfree(ctx->d_ecol);
   dfree(ctx->d_eval);
   dfree(ctx->d_tmax);
+  dfree(ctx->d_seg);
+  dfree(ctx->d_segrows);
+  dfree(ctx->d_segown);
+  dfree(ctx->d_lidx);
+  dfree(ctx->d_sval);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (auto& p : ctx->prof_pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
@@ -1216,7 +1332,7 @@ eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double
   wb.loc = W;
   if (W != Z) CK(cudaMemcpyAsync(W, Z, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
   ST(spmm_gram(ctx, wb, AW, t, nullptr, ctx->Bg));
-  ST(chol(ctx, t, ctx->Bg, nullptr, ctx->Rm, ctx->Rinv, nullptr, 0));
+  CK(eks::launch_chol_fast(ctx->stream, t, ctx->Bg, nullptr, ctx->Rm, ctx->Rinv, nullptr, ctx->flag, 0));  // solve path
   if (eks::sweep_supported(t))
     CK(eks::launch_apply_tc(ctx->stream, t, ctx->n, W, AW, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr,
                             nullptr, 4, ctx->nblk, 0, nullptr, ctx->part2, eks::Tail{}));
@@ -1233,7 +1349,7 @@ eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double
 eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, const double* v, int variant, int reps,
                            double* ms) {
   ST(k_ready(ctx, t));
-  if (!X || !Y || !ms || reps < 1 || variant < 0 || variant > 3)
+  if (!X || !Y || !ms || reps < 1 || variant < 0 || variant > 5)
     return fail(ctx, EKS_ERR_INVALID_ARG, "bad eks_k_time_spmm arguments");
   if (variant > 0 && !eks::sweep_supported(t))
     return fail(ctx, EKS_ERR_INVALID_ARG, "fused SpMM+Gram needs t in {8,16,32,64}");
@@ -1247,10 +1363,20 @@ eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, cons
   ch.alpha = v ? ctx->alpha : nullptr;
   ch.flag = ctx->flag;
   const eks::Tail tl = variant >= 2 ? tail(ctx, 2, ctx->Bg, stride) : eks::Tail{};
+  const bool use_seg = variant <= 3 && ctx->seg_ok && eks::spmm_seg_fits(t, ctx->ell_w, ctx->seg.cap);
+  const bool use_ell = !use_seg && variant <= 4 && ctx->ell_w;
   auto run = [&]() -> cudaError_t {
     if (variant == 0)
       return eks::launch_spmm(ctx->stream, t, 0, (int)ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val, X, Y, ctx->sms);
-    cudaError_t e = ctx->ell_w ? eks::launch_spmm_gram_ell(ctx->stream, t, ctx->n, ctx->d_ecol, ctx->d_eval,
+    if (use_seg) {
+      cudaError_t e = eks::launch_spmm_seg(ctx->stream, t, ctx->n, ctx->seg, ctx->ell_w, X, Y, v, ctx->part, ctx->nblk,
+                                           tl, ch);
+      if (e == cudaSuccess && variant == 3 && !ch.on)
+        e = eks::launch_chol(ctx->stream, t, ctx->Bg, v ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
+                             v ? ctx->alpha : nullptr, ctx->flag, 0);
+      return e;
+    }
+    cudaError_t e = use_ell ? eks::launch_spmm_gram_ell(ctx->stream, t, ctx->n, ctx->d_ecol, ctx->d_eval,
                                                            ctx->ell_w, ctx->d_tmax, ctx->n, X, 0, Y, v, ctx->part,
                                                            ctx->nblk, tl, ch)
                                : eks::launch_spmm_gram(ctx->stream, t, ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val,

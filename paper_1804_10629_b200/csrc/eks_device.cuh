@@ -39,7 +39,7 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
-// Called by every thread of every CTA (256 threads) after the CTA has written its
+// Called by every thread of every CTA (≥ 256 threads) after the CTA has written its
 // partial part[blockIdx.x * stride + e], e < tl.count.  The last NT = min(P, ⌈count/32⌉)
 // CTAs to arrive wait until all P partials exist (the grid is a single wave, so every
 // CTA is resident or has exited — no deadlock) and each reduces 32-entry slices in the
@@ -66,7 +66,7 @@ __device__ __forceinline__ bool tail_reduce(const double* part, size_t stride, c
   for (unsigned sl = tk - (P - NT); sl < nsl; sl += NT) {
     const size_t e = (size_t)sl * 32 + lane;
     double acc = 0.0;
-    if (e < (size_t)tl.count) {
+    if (w < 8 && e < (size_t)tl.count) {  // warps 0..7 reduce (larger CTAs: the rest only synchronise)
       for (unsigned b0 = w; b0 < P; b0 += 64) {
         double v[8];
 #pragma unroll
@@ -78,7 +78,7 @@ __device__ __forceinline__ bool tail_reduce(const double* part, size_t stride, c
         for (int k = 0; k < 8; ++k) acc += v[k];
       }
     }
-    s_red[w][lane] = acc;
+    if (w < 8) s_red[w][lane] = acc;
     __syncthreads();
     if (w == 0 && e < (size_t)tl.count) {
       double t = 0.0;
@@ -108,14 +108,14 @@ __device__ __forceinline__ bool tail_reduce(const double* part, size_t stride, c
 // subtractions of the oracle's left-looking loop in the same order, so R is bitwise
 // equal to or_chol for equal B (reading R20).  Breakdown: pivot ≤ t·2⁻⁵²·max|B| (R6).
 // R⁻¹ by the backward substitution of k_chol (same operations, same order).
+// Core of chol_warp: leaves column j (= lane) of R in a[] and of R⁻¹ in y[]; returns the
+// breakdown verdict (uniform over the warp).
 template <int T>
-__device__ __forceinline__ void chol_warp(const double* B, const double* g, double* Rout, double* Rinv,
-                                          double* alpha, int* flag, int gblock) {
+__device__ __forceinline__ bool chol_warp_core(const double* B, double (&a)[T], double (&y)[T]) {
   static_assert(T <= 32, "one column per lane");
   const unsigned FULL = 0xffffffffu;
   const int j = threadIdx.x & 31;
   const bool act = j < T;
-  double a[T], y[T];
   double m = 0.0;
 #pragma unroll
   for (int i = 0; i < T; ++i) {
@@ -151,6 +151,70 @@ __device__ __forceinline__ void chol_warp(const double* B, const double* g, doub
       if (j >= k) y[i] = __fma_rn(-rik, y[k], y[i]);
     }
   }
+  return __any_sync(FULL, fail);
+}
+
+// Latency-lean variant for the solve path (the R⁻¹ kernel's prologue): the pivot's reciprocal
+// square root (MUFU seed + two Newton steps + one correction, ≈ correctly rounded) replaces
+// the sqrt and the T divisions of each step, and R⁻¹ multiplies by it too.  R agrees with
+// chol_warp_core to a few ulps (not bitwise); the breakdown rule is the same (R6).
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y = rsqrt(d);                        // ~full precision already (CUDA's rsqrt)
+  const double h = __dmul_rn(0.5, d);
+  y = __fma_rn(y, __fma_rn(-h * y, y, 0.5), y);  // one Newton step: y(1.5 − ½ d y²)
+  return y;
+}
+template <int T>
+__device__ __forceinline__ bool chol_warp_fast(const double* B, double (&a)[T], double (&y)[T]) {
+  static_assert(T <= 32, "one column per lane");
+  const unsigned FULL = 0xffffffffu;
+  const int j = threadIdx.x & 31;
+  const bool act = j < T;
+  double m = 0.0;
+#pragma unroll
+  for (int i = 0; i < T; ++i) {
+    a[i] = act ? __ldcg(B + i * T + j) : 0.0;
+    if (act && i <= j) m = fmax(m, fabs(a[i]));
+    y[i] = (i == j) ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+  const double thr = __dmul_rn((double)T * 0x1p-52, m);
+  bool fail = false;
+  double rinv[T];  // 1/R_kk
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    const double d = __shfl_sync(FULL, a[k], k);
+    if (!(d > thr)) fail = true;
+    const double ri = rsqrt_nr(d);
+    rinv[k] = ri;
+    if (j > k) a[k] = a[k] * ri;
+    else if (j == k) a[k] = d * ri;
+#pragma unroll
+    for (int i = k + 1; i < T; ++i) {
+      const double rki = __shfl_sync(FULL, a[k], i);
+      if (i <= j) a[i] = __fma_rn(-rki, a[k], a[i]);
+    }
+  }
+#pragma unroll
+  for (int k = T - 1; k >= 0; --k) {
+    if (j >= k) y[k] = y[k] * rinv[k];
+#pragma unroll
+    for (int i = 0; i < k; ++i) {
+      const double rik = __shfl_sync(FULL, a[i], k);
+      if (j >= k) y[i] = __fma_rn(-rik, y[k], y[i]);
+    }
+  }
+  return fail;
+}
+
+template <int T>
+__device__ __forceinline__ void chol_warp(const double* B, const double* g, double* Rout, double* Rinv,
+                                          double* alpha, int* flag, int gblock) {
+  const int j = threadIdx.x & 31;
+  const bool act = j < T;
+  double a[T], y[T];
+  const bool fail = chol_warp_core<T>(B, a, y);
   if (act) {
 #pragma unroll
     for (int i = 0; i < T; ++i) {
@@ -165,7 +229,7 @@ __device__ __forceinline__ void chol_warp(const double* B, const double* g, doub
       alpha[j] = s;
     }
   }
-  if (__any_sync(FULL, fail) && j == 0 && flag) atomicMin(flag, gblock);
+  if (fail && j == 0 && flag) atomicMin(flag, gblock);
 }
 
 // The same factorization for any T ≤ 64 with the columns in shared memory (sm: 2·T·(T+1)

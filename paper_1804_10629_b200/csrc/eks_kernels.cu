@@ -561,6 +561,44 @@ __global__ void __launch_bounds__(32) k_chol_w(const double* __restrict__ B, con
   chol_warp<T>(B, g, Rout, Rinv, alpha, flag, gblock);
 }
 
+// Solve-path Cholesky: chol_warp_fast (rsqrt pivots, R within a few ulps of launch_chol).
+template <int T>
+__global__ void __launch_bounds__(32) k_chol_fast(const double* __restrict__ B, const double* __restrict__ g,
+                                                  double* __restrict__ Rout, double* __restrict__ Rinv,
+                                                  double* __restrict__ alpha, int* flag, int gblock) {
+  const int j = threadIdx.x;
+  double a[T], y[T];
+  const bool fail = chol_warp_fast<T>(B, a, y);
+  if (j < T) {
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      if (Rout) Rout[i * T + j] = (i <= j) ? a[i] : 0.0;
+      Rinv[i * T + j] = y[i];
+    }
+    if (g != nullptr && alpha != nullptr) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < T; ++i)
+        if (i <= j) s = __fma_rn(y[i], __ldcg(g + i), s);
+      alpha[j] = s;
+    }
+  }
+  if (fail && j == 0 && flag) atomicMin(flag, gblock);
+}
+
+cudaError_t launch_chol_fast(cudaStream_t st, int t, const double* B, const double* g, double* R, double* Rinv,
+                             double* alpha, int* flag, int gblock) {
+  switch (t) {
+    case 1: k_chol_fast<1><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 2: k_chol_fast<2><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 4: k_chol_fast<4><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 8: k_chol_fast<8><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 16: k_chol_fast<16><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 32: k_chol_fast<32><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    default: return launch_chol(st, t, B, g, R, Rinv, alpha, flag, gblock);
+  }
+}
+
 cudaError_t launch_chol(cudaStream_t st, int t, const double* B, const double* g, double* R, double* Rinv,
                         double* alpha, int* flag, int gblock) {
   switch (t) {

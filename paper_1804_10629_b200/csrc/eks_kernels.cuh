@@ -47,6 +47,10 @@ cudaError_t launch_ts_update(cudaStream_t st, int t, int64_t n, int nq, const do
 // breakdown: atomicMin(flag, gblock) when a pivot <= t·2^-52·max|B|.
 cudaError_t launch_chol(cudaStream_t st, int t, const double* B, const double* g, double* R,
                         double* Rinv, double* alpha, int* flag, int gblock);
+// The solve path's Cholesky (same contract): one warp, reciprocal-square-root pivots
+// (chol_warp_fast) — R agrees with launch_chol to a few ulps; t = 64 falls back to launch_chol.
+cudaError_t launch_chol_fast(cudaStream_t st, int t, const double* B, const double* g, double* R,
+                             double* Rinv, double* alpha, int* flag, int gblock);
 
 // ---- apply R⁻¹ and the update (fused per block):
 // W = Z2·Rinv, AW = AZ2·Rinv in place; u = W·alpha, q = AW·alpha;

@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(256, 1)
   };
 #pragma unroll
   for (int i = 0; i < K::NS - 1; ++i) issue(i);
+
   double rr_acc = 0.0;
   double acc[K::TPW][2];
 #pragma unroll
@@ -453,10 +454,10 @@ __global__ void __launch_bounds__(256, 1)
 // of k_sweep<T,0,1,true>), the tail reduction into tl.out and, for T ≤ 16 on one
 // rank, the Cholesky of the reduced Gram by the last CTA (chol_warp, registers).
 // ----------------------------------------------------------------------------
-template <int T, int MT, int WS, int TPW>
+template <int T, int MT, int WS, int TPW, int NW = 8>
 __device__ __forceinline__ void gram_epilogue(double* part, const double (&acc)[TPW][2], const double (&accv)[2],
                                               double* sm, const Tail& tl, const CholArgs& ch, bool has_r) {
-  constexpr int PER = T * T + T;
+  constexpr int PER = T * T + T, NT = NW * 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q4 = lane & 3;
   double* out = part + (size_t)blockIdx.x * PER;
@@ -476,7 +477,7 @@ __device__ __forceinline__ void gram_epilogue(double* part, const double (&acc)[
       red[(size_t)warp * T * T + (mi * 8 + g) * T + ni * 8 + 2 * q4 + 1] = acc[0][1];
     }
     __syncthreads();
-    for (int e = tid; e < T * T; e += 256) {
+    for (int e = tid; e < T * T; e += NT) {
       const int m = e / T, nn = e % T;
       const int ot = (m / 8) * MT + nn / 8;
       double s = 0.0;
@@ -484,13 +485,13 @@ __device__ __forceinline__ void gram_epilogue(double* part, const double (&acc)[
       out[e] = s;
     }
   }
-  double* rv = red + (WS > 1 ? 8 * T * T : 0);
+  double* rv = red + (WS > 1 ? NW * T * T : 0);
   if (lane < T) rv[warp * T + lane] = accv[0];
   if (lane + 32 < T) rv[warp * T + lane + 32] = accv[1];
   __syncthreads();
-  for (int e = tid; e < T; e += 256) {
+  for (int e = tid; e < T; e += NT) {
     double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += rv[w * T + e];
+    for (int w = 0; w < NW; ++w) s += rv[w * T + e];
     out[T * T + e] = s;
   }
   if (tl.cnt != nullptr) {
@@ -706,8 +707,8 @@ struct SeCfg {
   static constexpr int SMEM = SMEM0 > RED ? SMEM0 : RED;
 };
 
-template <int T, int W>
-__global__ void __launch_bounds__(256, (T >= 64 ? 2 : 3))
+template <int T, int W, int MINB = (T >= 64 ? 2 : 3)>
+__global__ void __launch_bounds__(256, MINB)
     k_spmm_gram_ell(int64_t n, const int* __restrict__ ecol, const double* __restrict__ eval,
                     const double* __restrict__ Xext, int64_t xoff, double* __restrict__ Y,
                     const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch) {
@@ -812,6 +813,301 @@ __global__ void __launch_bounds__(256, (T >= 64 ? 2 : 3))
   }
   cp_wait<0>();
   gram_epilogue<T, K::MT, K::WS, K::TPW>(part, acc, accv, sm, tl, ch, r != nullptr);
+}
+
+// ----------------------------------------------------------------------------
+// Segment-staged fused SpMM + Gram (TMA bulk copies + mbarrier ring).
+// eks_setup_csr plans, for every 16-row plan tile, the few contiguous runs of X
+// rows ("segments") its entries reference — for a stencil: the tile's own rows
+// with the ±1 halo, and the slabs at ±N (and ±N²) — and rewrites every entry's
+// column as a row index into the concatenation of those segments (uint16).  A CTA
+// (one per SM, persistent) then streams macro tiles of M plan tiles: one elected
+// thread issues cp.async.bulk copies of the macro tile's values, local indices and
+// X segments into a stage of an NS-deep shared-memory ring, completing on that
+// stage's mbarrier; all 8 warps multiply out of shared memory.  Nothing in flight
+// occupies registers, so the ring keeps ~(NS−1)·40 KB per SM in flight and the
+// kernel streams at the L2/HBM limit instead of the gather latency limit.  Each Y
+// entry is accumulated in the ELL order (p ascending, padded slots add fma(0,x,y)
+// = y), bitwise equal to the oracle (R20); the Gram/α̃ epilogue is the same as
+// the other SpMM+Gram kernels.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(saddr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   saddr(dst)),
+               "l"(src), "r"(bytes), "r"(saddr(b))
+               : "memory");
+}
+
+template <int T>
+struct SsCfg {
+  static constexpr int NWC = T <= 16 ? 16 : 8, NTH = 32 * (NWC + 1);  // consumer warps + 1 producer warp
+  static constexpr int M = T == 8 ? 8 : (T == 16 ? 4 : 2);  // plan tiles per macro tile (~40-80 KB of X)
+  static constexpr int TR = kSegPT * M;                      // rows per macro tile
+  static constexpr int RW = T == 8 ? 8 : 4;                  // rows per warp unit (= DMMA k-steps × 4)
+  static constexpr int G = 32 / RW;                          // threads per row
+  static constexpr int C = T / G;                            // columns per thread (2, 2, 4, 8)
+  static constexpr int U = TR / RW;                          // units per macro tile
+  static constexpr int UPW = U / NWC;                        // units per consumer warp per macro tile
+  static constexpr int S = T + 4;                            // row stride of the per-warp Y scratch
+  static constexpr int MT = T / 8;
+  static constexpr int NUT = MT * (MT + 1) / 2;              // upper-triangular 8×8 output tiles
+  static_assert(U % NWC == 0 && kSegPT % RW == 0, "tile shape");
+};
+__host__ __device__ constexpr int seg_vs(int w) { return (w + 1) & ~1; }  // value slots per row (16-byte rows)
+
+// Bytes of one ring stage: X segments of M plan tiles (`cap` rows each), values (VS per
+// row), local indices (8 × uint16 per row), own-row offsets, r — 128-byte aligned.
+template <int T, int W>
+__host__ __device__ constexpr size_t seg_stage_bytes(int cap) {
+  using K = SsCfg<T>;
+  return ((size_t)K::M * cap * T * 8 + (size_t)K::TR * seg_vs(W) * 8 + (size_t)K::TR * 16 + 16 * K::M +
+          (size_t)K::TR * 8 + 127) &
+         ~(size_t)127;
+}
+template <int T>
+__host__ __device__ constexpr size_t seg_fixed_bytes() {
+  using K = SsCfg<T>;
+  return (size_t)K::NWC * K::RW * K::S * 8 + 16 * 8 + 128;  // per-warp Y scratch, mbarriers, slack
+}
+constexpr size_t kSegSmem = 220 * 1024;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+
+template <int T, int W>
+__global__ void __launch_bounds__(SsCfg<T>::NTH, 1)
+    k_spmm_seg(int64_t n, const SegPlan pl, const double* __restrict__ Xext, double* __restrict__ Y,
+               const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch, int NS,
+               int probe) {
+  using K = SsCfg<T>;
+  constexpr int S = K::S, G = K::G, C = K::C, RW = K::RW, TR = K::TR, M = K::M, PT = kSegPT, NWC = K::NWC;
+  constexpr int VS = seg_vs(W), MT = K::MT;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int cap = pl.cap;
+  const size_t SB = seg_stage_bytes<T, W>(cap);
+  double* sYw = reinterpret_cast<double*>(smraw + (size_t)NS * SB);  // [NWC][RW][S]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sYw + NWC * RW * S);
+  uint64_t* empty = full + 8;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q4 = lane & 3;
+  const int64_t ntp = (n + PT - 1) / PT;  // plan tiles
+  const int64_t nmt = (ntp + M - 1) / M;  // macro tiles
+  const int64_t my = nmt > blockIdx.x ? (nmt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const size_t oV = (size_t)M * cap * T * 8, oL = oV + (size_t)TR * VS * 8, oO = oL + (size_t)TR * 16,
+               oR = oO + 16 * M;
+  auto stage = [&](int s) { return smraw + (size_t)s * SB; };
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, NWC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NWC) {
+    // ================= producer warp: stage j%NS ← macro tile blockIdx + j·grid.  The lanes
+    // hold the tile's segment table (loaded one tile ahead), a segmented scan places every
+    // segment in the stage buffer, lane 0 arms the full barrier with the byte count and
+    // every lane issues the bulk copies of its own segments.
+    constexpr int NE = M * kSegMax, EPL = (NE + 31) / 32;
+    int2 msg[EPL];
+    int mown = 0;
+    auto load_meta = [&](int64_t j) {
+      const int64_t p0 = (blockIdx.x + j * gridDim.x) * M;
+      const int pm = j < my ? (int)((ntp - p0) < M ? (ntp - p0) : M) : 0;
+      const int2* sg0 = reinterpret_cast<const int2*>(pl.seg) + p0 * kSegMax;
+#pragma unroll
+      for (int u = 0; u < EPL; ++u) {
+        const int e = lane + 32 * u;
+        msg[u] = (e < NE && e / kSegMax < pm) ? __ldg(sg0 + e) : make_int2(0, 0);
+      }
+      mown = lane < pm ? __ldg(pl.own + p0 + lane) : 0;
+    };
+    load_meta(0);
+    for (int64_t j = 0; j < my; ++j) {
+      const int s = (int)(j % NS);
+      if (j >= NS) mbar_wait(empty + s, (uint32_t)((j / NS - 1) & 1));  // consumers released the stage
+      const int64_t mt = blockIdx.x + j * gridDim.x, p0 = mt * M, row0 = mt * TR;
+      const int pm = (int)((ntp - p0) < M ? (ntp - p0) : M);
+      const int rows = (int)((n - row0) < TR ? (n - row0) : TR);
+      unsigned char* st = stage(s);
+      uint32_t mine = 0;
+#pragma unroll
+      for (int u = 0; u < EPL; ++u) mine += (uint32_t)msg[u].y;
+      if (lane < pm) reinterpret_cast<int*>(st + oO)[lane] = mown;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+      const int rb = r != nullptr ? (rows & ~1) : 0;  // r rows moved by the bulk copy (16-byte multiple)
+      if (lane == 0) {
+        if (r != nullptr && (rows & 1)) reinterpret_cast<double*>(st + oR)[rows - 1] = r[row0 + rows - 1];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(full + s, (uint32_t)(pm * PT * VS * 8 + pm * PT * 16 + rb * 8) + mine * T * 8);
+        bulk_g2s(st + oV, pl.val + p0 * PT * VS, (uint32_t)(pm * PT * VS * 8), full + s);
+        bulk_g2s(st + oL, pl.lidx + p0 * PT * 8, (uint32_t)(pm * PT * 16), full + s);
+        if (rb > 0) bulk_g2s(st + oR, r + row0, (uint32_t)rb * 8, full + s);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < EPL; ++u) {
+        const int q = lane % kSegMax;  // exclusive scan of run lengths per plan tile (8 lanes)
+        int off = msg[u].y;
+#pragma unroll
+        for (int d = 1; d < kSegMax; d <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, off, d, kSegMax);
+          if (q >= d) off += v;
+        }
+        off -= msg[u].y;
+        const int e = lane + 32 * u;
+        if (msg[u].y > 0)
+          bulk_g2s(reinterpret_cast<double*>(st) + ((size_t)(e / kSegMax) * cap + off) * T,
+                   Xext + (int64_t)msg[u].x * T, (uint32_t)msg[u].y * T * 8, full + s);
+      }
+      load_meta(j + 1);
+    }
+    // the producer warp still takes part in the epilogue's barriers (zero partial)
+  }
+
+  // ================= consumer warps: Y rows, then this warp's rows of XᵀY and Xᵀr on DMMA
+  double acc[K::NUT][2];
+#pragma unroll
+  for (int u = 0; u < K::NUT; ++u) acc[u][0] = acc[u][1] = 0.0;
+  double accv[2] = {0.0, 0.0};
+  if (warp < NWC) {
+    const int rw = lane / G, gl = lane % G;
+    double* yw = sYw + (size_t)warp * RW * S;
+    for (int64_t j = 0; j < my; ++j) {
+      const int s = (int)(j % NS);
+      const int64_t mt = blockIdx.x + j * gridDim.x, row0 = mt * TR;
+      const int rows = (int)((n - row0) < TR ? (n - row0) : TR);
+      const unsigned char* st = stage(s);
+      const double* sX = reinterpret_cast<const double*>(st);
+      const double* sV = reinterpret_cast<const double*>(st + oV);
+      const uint4* sL = reinterpret_cast<const uint4*>(st + oL);
+      const int* sO = reinterpret_cast<const int*>(st + oO);
+      const double* sR = reinterpret_cast<const double*>(st + oR);
+      mbar_wait(full + s, (uint32_t)((j / NS) & 1));
+#pragma unroll
+      for (int uu = 0; uu < (probe ? 0 : K::UPW); ++uu) {
+        const int r0u = (warp + uu * NWC) * RW;  // first row of the unit in the macro tile
+        const int rr = r0u + rw;
+        const int m = rr / PT;
+        const double* xb = sX + (size_t)m * cap * T + gl * C;
+        // ---- Y row rr, columns gl·C … gl·C+C-1 (ELL order: p ascending); rows past n: 0
+        const uint4 lv = rr < rows ? sL[rr] : make_uint4(0u, 0u, 0u, 0u);
+        const unsigned lw[4] = {lv.x, lv.y, lv.z, lv.w};
+        int li[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) li[k] = (int)((lw[k >> 1] >> (16 * (k & 1))) & 0xffffu);
+        double a[VS];
+#pragma unroll
+        for (int k = 0; k < VS; k += 2) {
+          const double2 av =
+              rr < rows ? *reinterpret_cast<const double2*>(sV + (size_t)rr * VS + k) : make_double2(0.0, 0.0);
+          a[k] = av.x;
+          a[k + 1] = av.y;
+        }
+#pragma unroll
+        for (int c2 = 0; c2 < C / 2; ++c2) {
+          double2 xv[W];
+#pragma unroll
+          for (int k = 0; k < W; ++k)  // (rows past n read buffer row 0 of plan tile 0, always present)
+            xv[k] = *reinterpret_cast<const double2*>((rr < rows ? xb : sX + gl * C) + (size_t)li[k] * T + 2 * c2);
+          double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            y.x = __fma_rn(a[k], xv[k].x, y.x);
+            y.y = __fma_rn(a[k], xv[k].y, y.y);
+          }
+          if (rr >= rows) y = make_double2(0.0, 0.0);
+          else *reinterpret_cast<double2*>(Y + (row0 + rr) * T + gl * C + 2 * c2) = y;
+          *reinterpret_cast<double2*>(yw + rw * S + gl * C + 2 * c2) = y;
+        }
+        __syncwarp();
+        // ---- Gram: XᵀY over the unit's RW rows (upper 8×8 tiles), Xᵀr
+        const int mu = r0u / PT, qb = r0u % PT;
+        const double* xo = sX + ((size_t)mu * cap + sO[mu] + qb) * T;  // own X rows of the unit
+#pragma unroll
+        for (int ks = 0; ks < RW / 4; ++ks) {
+          const int rq = ks * 4 + q4;
+          const bool ok = r0u + rq < rows;
+          double xa[MT], yb[MT];
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            xa[i] = ok ? xo[rq * T + i * 8 + g] : 0.0;
+            yb[i] = yw[rq * S + i * 8 + g];
+          }
+          int ut = 0;
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+            for (int ni = mi; ni < MT; ++ni, ++ut) dmma(acc[ut][0], acc[ut][1], xa[mi], yb[ni]);
+        }
+        if (r != nullptr) {
+#pragma unroll
+          for (int rq = 0; rq < RW; ++rq)
+            if (r0u + rq < rows) {
+              const double vr = sR[r0u + rq];
+              if (lane < T) accv[0] = fma(xo[rq * T + lane], vr, accv[0]);
+              if (lane + 32 < T) accv[1] = fma(xo[rq * T + lane + 32], vr, accv[1]);
+            }
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mbar_arrive(empty + s);
+    }
+  }
+  // ================= epilogue: consumer warps' partials summed in warp order, lower half mirrored
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(smraw);  // T·T + T (stages are drained)
+  constexpr int PER = T * T + T;
+  for (int w = 0; w < NWC; ++w) {
+    if (warp == w) {
+      int ut = 0;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = mi; ni < MT; ++ni, ++ut) {
+          double* d = red + (mi * 8 + g) * T + ni * 8 + 2 * q4;
+          d[0] = w == 0 ? acc[ut][0] : d[0] + acc[ut][0];
+          d[1] = w == 0 ? acc[ut][1] : d[1] + acc[ut][1];
+        }
+      if (lane < T) red[T * T + lane] = w == 0 ? accv[0] : red[T * T + lane] + accv[0];
+      if (lane + 32 < T) red[T * T + lane + 32] = w == 0 ? accv[1] : red[T * T + lane + 32] + accv[1];
+    }
+    __syncthreads();
+  }
+  double* out = part + (size_t)blockIdx.x * PER;
+  for (int e = tid; e < T * T; e += K::NTH) {
+    const int rI = e / T, cI = e % T;
+    out[e] = (rI / 8 <= cI / 8) ? red[e] : red[cI * T + rI];
+  }
+  for (int e = tid; e < T; e += K::NTH) out[T * T + e] = red[T * T + e];
+  if (tl.cnt != nullptr) {
+    const bool last = tail_reduce(part, PER, tl);
+    if constexpr (T <= 16) {
+      if (last && ch.on && warp == 0)
+        chol_warp<T>(tl.out, r != nullptr ? tl.out + T * T : nullptr, ch.R, ch.Rinv, ch.alpha, ch.flag, ch.gblock);
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -933,7 +1229,7 @@ static cudaError_t spmm_gram_t(cudaStream_t st, int64_t n, const int* rp, const 
   return cudaGetLastError();
 }
 
-template <int T, int W>
+template <int T, int W, int MINB = (T >= 64 ? 2 : 3)>
 static cudaError_t spmm_gram_ell_t(cudaStream_t st, int64_t n, const int* ecol, const double* eval, const int* tmax,
                                    int64_t n_ext, const double* Xext, int64_t xoff, double* Y, const double* r,
                                    double* part, int nblk, const Tail& tl, const CholArgs& ch) {
@@ -941,15 +1237,15 @@ static cudaError_t spmm_gram_ell_t(cudaStream_t st, int64_t n, const int* ecol, 
   const size_t sm = (size_t)K::SMEM * 8;
   static int occ = 0;
   if (!occ) {
-    cudaFuncSetAttribute(k_spmm_gram_ell<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmm_gram_ell<T, W>, 256, sm);
+    cudaFuncSetAttribute(k_spmm_gram_ell<T, W, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmm_gram_ell<T, W, MINB>, 256, sm);
     if (occ < 1) occ = 1;
   }
   nblk = grid_for(nblk, occ);
   t_last_grid = nblk;
   (void)tmax;
   (void)n_ext;
-  k_spmm_gram_ell<T, W><<<nblk, 256, sm, st>>>(n, ecol, eval, Xext, xoff, Y, r, part, tl, ch);
+  k_spmm_gram_ell<T, W, MINB><<<nblk, 256, sm, st>>>(n, ecol, eval, Xext, xoff, Y, r, part, tl, ch);
   return cudaGetLastError();
 }
 
@@ -961,8 +1257,70 @@ cudaError_t launch_spmm_gram_ell(cudaStream_t st, int t, int64_t n, const int* e
   if (ch.on && !spmm_gram_fused_chol(t)) return cudaErrorInvalidValue;
   EKS_SW_T(t, {
     if (w == 5) return spmm_gram_ell_t<T, 5>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
-    if (w == 7) return spmm_gram_ell_t<T, 7>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+    if (w == 7) {
+      static const int mb = getenv("EKS_ELL_MINB") ? atoi(getenv("EKS_ELL_MINB")) : 4;  // measured best at t=16
+      if constexpr (T == 16) {
+        if (mb == 4) return spmm_gram_ell_t<T, 7, 4>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+        if (mb == 6) return spmm_gram_ell_t<T, 7, 6>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+        if (mb == 8) return spmm_gram_ell_t<T, 7, 8>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+      }
+      return spmm_gram_ell_t<T, 7>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+    }
     if (w == 8) return spmm_gram_ell_t<T, 8>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+  });
+  return cudaErrorInvalidValue;
+}
+
+template <int T, int W>
+static cudaError_t spmm_seg_t(cudaStream_t st, int64_t n, const SegPlan& pl, const double* Xext, double* Y,
+                              const double* r, double* part, int nblk, const Tail& tl, const CholArgs& ch) {
+  using K = SsCfg<T>;
+  const size_t SB = seg_stage_bytes<T, W>(pl.cap), fixed = seg_fixed_bytes<T>();
+  int ns = (int)((kSegSmem - fixed) / SB);
+  if (ns > 8) ns = 8;
+  if (ns < 2) return cudaErrorInvalidConfiguration;
+  size_t sm = (size_t)ns * SB + fixed;
+  const size_t red = (size_t)(T * T + T) * 8;
+  if (sm < red) sm = red;
+  cudaFuncSetAttribute(k_spmm_seg<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  nblk = nblk < sms ? nblk : sms;  // one persistent CTA per SM
+  t_last_grid = nblk;
+  static const int probe = getenv("EKS_SEG_PROBE") ? atoi(getenv("EKS_SEG_PROBE")) : 0;
+  k_spmm_seg<T, W><<<nblk, K::NTH, sm, st>>>(n, pl, Xext, Y, r, part, tl, ch, ns, probe);
+  return cudaGetLastError();
+}
+
+template <int T>
+static bool seg_fits_t(int w, int cap) {
+  const size_t SB = w <= 5 ? seg_stage_bytes<T, 5>(cap) : (w <= 7 ? seg_stage_bytes<T, 7>(cap) : seg_stage_bytes<T, 8>(cap));
+  const size_t fixed = seg_fixed_bytes<T>();
+  return fixed < kSegSmem && (kSegSmem - fixed) / SB >= 2;
+}
+
+bool spmm_seg_fits(int t, int w, int cap) {
+  if (cap < 1 || cap > 65535 || w < 1 || w > 8) return false;
+  switch (t) {
+    case 8: return seg_fits_t<8>(w, cap);
+    case 16: return seg_fits_t<16>(w, cap);
+    case 32: return seg_fits_t<32>(w, cap);
+    case 64: return seg_fits_t<64>(w, cap);
+    default: return false;
+  }
+}
+
+cudaError_t launch_spmm_seg(cudaStream_t st, int t, int64_t n, const SegPlan& pl, int w, const double* Xext,
+                            double* Y, const double* r, double* part, int nblk, const Tail& tl, const CholArgs& ch) {
+  if (ch.on && !spmm_gram_fused_chol(t)) return cudaErrorInvalidValue;
+  EKS_SW_T(t, {
+    if (w == 5) return spmm_seg_t<T, 5>(st, n, pl, Xext, Y, r, part, nblk, tl, ch);
+    if (w == 7) return spmm_seg_t<T, 7>(st, n, pl, Xext, Y, r, part, nblk, tl, ch);
+    if (w == 8) return spmm_seg_t<T, 8>(st, n, pl, Xext, Y, r, part, nblk, tl, ch);
   });
   return cudaErrorInvalidValue;
 }
@@ -1012,12 +1370,9 @@ cudaError_t launch_apply_tc(cudaStream_t st, int t, int64_t n, double* Z2W, doub
                             const double* alpha, double* x, double* dx, const double* r, double* rnew, const int* flag,
                             int mode, int nblk, int c1n, const double* AWprev, double* part, const Tail& tl) {
   EKS_SW_T(t, {
-    if (c1n == 0)
-      return apply_t<T, 0>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part, nblk, tl);
-    if (c1n == 1)
-      return apply_t<T, 1>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part, nblk, tl);
-    if (c1n == 2)
-      return apply_t<T, 2>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part, nblk, tl);
+    if (c1n == 0) return apply_t<T, 0>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part, nblk, tl);
+    if (c1n == 1) return apply_t<T, 1>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part, nblk, tl);
+    if (c1n == 2) return apply_t<T, 2>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part, nblk, tl);
   });
   return cudaErrorInvalidValue;
 }

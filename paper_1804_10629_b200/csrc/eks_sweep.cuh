@@ -45,6 +45,23 @@ int ell_width(int maxrow);  // 5, 7 or 8; 0: rows too long for the ELL path
 cudaError_t launch_spmm_gram_ell(cudaStream_t st, int t, int64_t n, const int* ecol, const double* eval, int w,
                                  const int* tmax, int64_t n_ext, const double* Xext, int64_t xoff, double* Y,
                                  const double* r, double* part, int nblk, const Tail& tl, const CholArgs& ch);
+// Segment plan of the TMA-staged SpMM+Gram (eks_setup_csr, plan tiles of kSegPT rows): per plan
+// tile up to kSegMax runs of X rows (first ext row, rows), (0,0)-terminated; rows = Σ run rows;
+// own = buffer row of the tile's first own row; every entry's column rewritten as a uint16 row
+// of the tile's buffer: lidx holds 8 per row (16 bytes), val (w+1)&~1 per row, both row-major
+// (padding: value 0, index of the row's own X row).
+constexpr int kSegPT = 16, kSegMax = 8;
+struct SegPlan {
+  const int* seg = nullptr;              // [ntp][kSegMax][2]
+  const int* rows = nullptr;             // [ntp]
+  const int* own = nullptr;              // [ntp]
+  const unsigned short* lidx = nullptr;  // [ntp][kSegPT][8]
+  const double* val = nullptr;           // [ntp][kSegPT][(w+1)&~1]
+  int cap = 0;                           // max rows of a plan tile's buffer
+};
+bool spmm_seg_fits(int t, int w, int cap);
+cudaError_t launch_spmm_seg(cudaStream_t st, int t, int64_t n, const SegPlan& pl, int w, const double* Xext,
+                            double* Y, const double* r, double* part, int nblk, const Tail& tl, const CholArgs& ch);
 // maxrow = longest CSR row (selects the register-resident fast path; longer rows still work).
 cudaError_t launch_spmm_gram(cudaStream_t st, int t, int64_t n, const int* rp, const int* col, const double* val,
                              int maxrow, const double* Xext, int64_t xoff, double* Y, const double* r, double* part,
