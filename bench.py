@@ -48,6 +48,101 @@ def workload(name: str):
     raise SystemExit(f"unknown workload {name}")
 
 
+def spmm_block(eks, torch, peak_gbs, N=384, ts=(8, 16, 32), reps=10):
+    """The SpMM-block kernel of the solve (fused Y = A·X + Gram [XᵀY | Xᵀr], tail reduction)
+    timed on the cfg5 operator (384³ 7-point Laplacian, BASELINE configs[4]) with CUDA events
+    over `reps` back-to-back launches; GB/s of B_spmm = 12·nnz + 4(n+1) + 16·n·t."""
+    A = ei.cfg5_operator(N)
+    s = eks.Solver(A)
+    out = {"workload": f"cfg5 operator {N}^3 7-point Laplacian, n={A.n}, nnz={A.nnz}; fused SpMM+Gram launch "
+                       f"as in eks_solve; X uniform, L2 not flushed between the {reps} launches (inputs > L2)",
+           "bytes_formula": "12*nnz + 4*(n+1) + 16*n*t", "peak_gbs": peak_gbs, "t": {}}
+    for t in ts:
+        X = torch.rand(A.n, t, dtype=torch.float64, device="cuda") - 0.5
+        Y = torch.empty_like(X)
+        v = torch.rand(A.n, dtype=torch.float64, device="cuda")
+        ms = eks.eks_k_time_spmm(s.ctx, t, X, Y, v, 2, reps)
+        B = 12.0 * A.nnz + 4.0 * (A.n + 1) + 16.0 * A.n * t
+        gbs = B / (ms * 1e-3) / 1e9
+        out["t"][str(t)] = {"us_per_launch": ms * 1e3, "gbs": gbs, "frac": gbs / peak_gbs}
+        del X, Y, v
+        torch.cuda.empty_cache()
+    s.close()
+    return out
+
+
+def run_cfg5(args, eks, torch, dist, world, rank, local):
+    """BASELINE configs[4]: basis-generation sweep only, 20 outer iterations of s blocks on the
+    384³ Laplacian from a seeded unit-norm random block (reading R27); value = outer it/s,
+    plus the GB/s of the sweep's algorithmic bytes."""
+    N, t, s_ = args.cfg5_n, args.t or 16, args.s or 4
+    A = ei.cfg5_operator(N)
+    n = A.n
+    lo = (rank * (t // world)) * n // t
+    hi = ((rank + 1) * (t // world)) * n // t
+    slab = A.rows(lo, hi)
+    uid = None
+    if world > 1:
+        obj = [eks.eks_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    solver = eks.Solver(None, rank=rank, nranks=world, device=local, nccl_id=uid)
+    solver.setup(n, lo, hi, slab.row_ptr, slab.col, slab.val)
+    del A, slab
+    X0 = ei.cfg5_start_block_torch(n, t, "cuda")[lo:hi].contiguous()
+    W = torch.empty_like(X0)
+    nblocks = 20 * s_
+    stream = torch.cuda.current_stream()
+    eks.eks_set_stream(solver.ctx, stream.cuda_stream)
+    for _ in range(args.warmup):
+        eks.eks_basis_sweep(solver.ctx, t, nblocks, X0, W)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, reps = 0.0, []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        reps.append(eks.eks_basis_sweep(solver.ctx, t, nblocks, X0, W))
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms += a.elapsed_time(b)
+    clk = clocks.stop()
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    prof = eks.eks_basis_sweep(solver.ctx, t, nblocks, X0, W, profile=True)
+    pr = eks.eks_get_profile(solver.ctx)
+    peaks = load_peaks()
+    outer = 20 * args.steps
+    model_bytes = reps[0]["model_bytes"] * world
+    if rank == 0:
+        spmm_ms = pr["ms"]["spmm"] / max(1, pr["launches"]["spmm"])
+        spmm_b = pr["bytes"]["spmm"] / max(1, pr["launches"]["spmm"])
+        line = {
+            "metric": METRIC, "value": outer / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg5: 3D 7-point Laplacian {N}^3 (n={n}), basis-generation sweep only "
+                                   f"(reading R27): 20 outer iterations x s={s_} blocks, t={t}, seeded unit-norm "
+                                   f"U[-1,1) start block", "n": n, "t": t, "s": s_,
+                       "parallelism": f"row-slabs x{world}", "l2": "inputs > L2 (3.6-14.5 GB blocks)"},
+            "sweep_gbs": model_bytes / (ms * 1e-3 / args.steps) / 1e9,
+            "sweep_frac": model_bytes / (ms * 1e-3 / args.steps) / 1e9 / peaks["hbm_gbs"],
+            "spmm_roofline": {"kernel": "spmm", "bound": "hbm", "achieved": spmm_b / (spmm_ms * 1e-3) / 1e9,
+                              "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                              "frac": spmm_b / (spmm_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                              "avg_launch_us": spmm_ms * 1e3, "bytes_per_launch": spmm_b},
+            "gpu_launches": sum(r["gpu_launches"] for r in reps), "clocks": clk,
+            "time_share": {c: pr["ms"][c] / max(1e-9, sum(pr["ms"].values())) for c in pr["ms"]},
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+
+
 def load_peaks():
     peaks = {"hbm_gbs": 6558.7, "source": "fallback"}
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -171,6 +266,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--max-outer", type=int, default=0, help="cap outer iterations per solve (profiling only)")
+    ap.add_argument("--no-spmm-block", action="store_true", help="skip the large-operator SpMM-block measurement")
+    ap.add_argument("--t", type=int, default=0, help="cfg5: block width t")
+    ap.add_argument("--s", type=int, default=0, help="cfg5: blocks per outer iteration s")
+    ap.add_argument("--cfg5-n", type=int, default=384, help="cfg5 grid size (384 = BASELINE configs[4])")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -188,6 +287,11 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.workload == "cfg5":
+        run_cfg5(args, eks, torch, dist, world, rank, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     p = workload(args.workload)
     n, t = p.A.n, p.t
@@ -342,6 +446,10 @@ def main():
                "sample": f"first {k} outer iterations of {p.name} {p.method} (definition mode, single thread, "
                          f"{os.cpu_count()} host cores present), {dt:.1f} s"}
 
+    sblock = None
+    if rank == 0 and world == 1 and not args.no_spmm_block:
+        sblock = spmm_block(eks, torch, load_peaks()["hbm_gbs"])
+
     if rank == 0:
         r0 = reps[0]
         line = {
@@ -349,7 +457,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_of(args, p, world),
-            "roofline": roofline, "spmm_roofline": spmm_roof,
+            "roofline": roofline, "spmm_roofline": spmm_roof, "spmm_block": sblock,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "solve": {"outer_iters": r0["outer_iters"], "converged": r0["converged"],
                       "true_relres": r0["true_relres"], "rho_ratio": r0["rho"] / r0["rho0"],

@@ -68,6 +68,31 @@ def uniform_pm1(seed: int, count: int, start: int = 0) -> np.ndarray:
     return 2.0 * uniform01(seed, count, start) - 1.0
 
 
+def uniform_pm1_torch(seed: int, count: int, device, start: int = 0, chunk: int = 1 << 26):
+    """The same SplitMix64 U[-1,1) draws as :func:`uniform_pm1`, generated on a torch device in
+    int64 arithmetic (wrapping multiply, logical shifts by masking) — bitwise equal values; used
+    where a host-side block would be tens of GB (cfg5)."""
+    import torch
+
+    def s64(v):  # uint64 constant → the int64 with the same bits
+        v &= MASK64
+        return v - (1 << 64) if v >= (1 << 63) else v
+
+    def lsr(z, k):
+        return (z >> k) & ((1 << (64 - k)) - 1)
+
+    out = torch.empty(count, dtype=torch.float64, device=device)
+    for lo in range(0, count, chunk):
+        hi = min(count, lo + chunk)
+        i = torch.arange(start + lo + 1, start + hi + 1, dtype=torch.int64, device=device)
+        z = i * s64(GOLDEN) + s64(seed)
+        z = (z ^ lsr(z, 30)) * s64(0xBF58476D1CE4E5B9)
+        z = (z ^ lsr(z, 27)) * s64(0x94D049BB133111EB)
+        z = z ^ lsr(z, 31)
+        out[lo:hi] = lsr(z, 11).to(torch.float64) * (2.0 ** -53) * 2.0 - 1.0
+    return out
+
+
 # ----------------------------------------------------------------------------
 # CSR container
 # ----------------------------------------------------------------------------
@@ -279,6 +304,14 @@ def cfg5_start_block(n: int, t: int, seed: int = SEED_CFG5_BLOCK) -> np.ndarray:
     """cfg5 random start: U[-1,1) drawn in row-major n×t order, columns scaled to unit 2-norm (R27)."""
     X = uniform_pm1(seed, n * t).reshape(n, t)
     X /= np.sqrt((X * X).sum(axis=0))
+    return X
+
+
+def cfg5_start_block_torch(n: int, t: int, device, seed: int = SEED_CFG5_BLOCK):
+    """cfg5 start block generated on the device (same draws as :func:`cfg5_start_block`; the
+    column norms are summed by torch, so the scaling may differ from the numpy block by rounding)."""
+    X = uniform_pm1_torch(seed, n * t, device).view(n, t)
+    X /= X.pow(2).sum(dim=0).sqrt()
     return X
 
 

@@ -41,10 +41,10 @@ eks_status eks_k_chol(eks_ctx* ctx, int t, const double* B, double* R);
 /* Timing of the SpMM-block kernel on the device (bench.py's SpMM roofline and the
  * kernel micro-benchmarks): `reps` back-to-back launches of Y = A·X between two CUDA
  * events on the context stream after one warm-up launch; *ms = average per launch.
- * variant 0: plain SpMM (k_spmm); 1: fused SpMM + Gram [XᵀY | Xᵀv] with per-CTA partials
- * only; 2: + the tail reduction of the partials; 3: + the A-CholQR Cholesky in the last
- * CTA (the configuration eks_solve runs on one rank).  v may be NULL.  Variants 1-3 need
- * t in {8,16,32,64}. */
+ * variant 0: plain CSR SpMM (k_spmm); 1: the fused SpMM + Gram [XᵀY | Xᵀv] kernel eks_solve
+ * selects for this t, per-CTA partials only; 2: + the tail reduction of the partials (what
+ * eks_solve launches); 3: + the block's Cholesky; 4: the ELL gather kernel forced; 5: the CSR
+ * gather kernel forced (4, 5 with the tail).  v may be NULL.  Variants 1-5 need t in {8,16,32,64}. */
 eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, const double* v, int variant, int reps,
                            double* ms);
 

@@ -427,6 +427,16 @@ eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, cons
   return allreduce(ctx, C2, stride);
 }
 
+// Which fused SpMM+Gram kernel runs for this t: 0 TMA-staged segments, 1 ELL gathers, 2 CSR.
+// Measured (tools/spmm_micro.py): ELL is fastest for t ≤ 32, the segment kernel for t = 64;
+// EKS_SPMM_PATH=seg|ell|csr forces one for A/B measurements.
+int spmm_path_for(const eks_ctx* ctx, int t) {
+  const bool seg = ctx->seg_ok && eks::spmm_seg_fits(t, ctx->ell_w, ctx->seg.cap);
+  if (seg && (ctx->spmm_path == 3 || (ctx->spmm_path == 0 && t == 64))) return 0;
+  if (ctx->ell_w && ctx->spmm_path <= 1) return 1;
+  return 2;
+}
+
 // Y = A·X and out = [XᵀY | Xᵀr] (t·t + t, allreduced): the A-CholQR Gram with the α̃ projection.
 // One rank: the fused SpMM+Gram kernel, whose last CTA also factors B when `ch` is given
 // (t ≤ 32; ctx->chol_fused tells the caller).  Several ranks: SpMM with halo overlap, then
@@ -450,14 +460,11 @@ eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const doubl
   }
   {
     KScope k(ctx, EKS_K_SPMM);
-    // measured (tools/spmm_micro.py): the ELL gather kernel is fastest for t ≤ 32, the TMA-staged
-    // segment kernel for t = 64; EKS_SPMM_PATH=seg|ell|csr forces one for A/B measurements
-    const bool use_seg = ctx->seg_ok && eks::spmm_seg_fits(t, ctx->ell_w, ctx->seg.cap) &&
-                         (ctx->spmm_path == 3 || (ctx->spmm_path == 0 && t == 64));
-    if (use_seg)
+    const int path = spmm_path_for(ctx, t);
+    if (path == 0)
       CK(eks::launch_spmm_seg(ctx->stream, t, ctx->n, ctx->seg, ctx->ell_w, X.base, Y, r, ctx->part, ctx->nblk,
                               tail(ctx, 2, out, stride), c));
-    else if (ctx->ell_w && ctx->spmm_path <= 1)
+    else if (path == 1)
       CK(eks::launch_spmm_gram_ell(ctx->stream, t, ctx->n, ctx->d_ecol, ctx->d_eval, ctx->ell_w, ctx->d_tmax, n_ext(ctx),
                                    X.base,
                                    (int64_t)(X.loc - X.base) / t, Y, r, ctx->part, ctx->nblk, tail(ctx, 2, out, stride),
@@ -1363,8 +1370,8 @@ eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, cons
   ch.alpha = v ? ctx->alpha : nullptr;
   ch.flag = ctx->flag;
   const eks::Tail tl = variant >= 2 ? tail(ctx, 2, ctx->Bg, stride) : eks::Tail{};
-  const bool use_seg = variant <= 3 && ctx->seg_ok && eks::spmm_seg_fits(t, ctx->ell_w, ctx->seg.cap);
-  const bool use_ell = !use_seg && variant <= 4 && ctx->ell_w;
+  const int path = variant <= 3 ? spmm_path_for(ctx, t) : (variant == 4 && ctx->ell_w ? 1 : 2);
+  const bool use_seg = path == 0, use_ell = path == 1;
   auto run = [&]() -> cudaError_t {
     if (variant == 0)
       return eks::launch_spmm(ctx->stream, t, 0, (int)ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val, X, Y, ctx->sms);

@@ -12,6 +12,32 @@
 
 namespace eks {
 
+// ---- Programmatic dependent launch (PDL): every hot kernel is launched with programmatic
+// stream serialization; at its top it waits for the previous kernel's completion and memory
+// (griddepcontrol.wait) and immediately allows the next kernel to be launched, so launch
+// processing and CTA rasterisation overlap the tail of the running kernel.  Without the
+// launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();  // EKS_PDL=0 disables (A/B measurements)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // Where a producer kernel's per-CTA partials go when it reduces them itself.
 // cnt == nullptr: no tail reduction (the host launches launch_reduce instead).
 // Entries e < split land in out[e], entries e >= split in out2[e - split].

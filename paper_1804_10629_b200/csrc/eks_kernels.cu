@@ -8,8 +8,14 @@
 
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 namespace eks {
+
+bool pdl_enabled() {
+  static const int on = getenv("EKS_PDL") ? atoi(getenv("EKS_PDL")) : 1;
+  return on != 0;
+}
 
 // Upper bound on CTAs (= per-CTA partial slots) of the row-sweep kernels; each
 // launcher uses min(this, SMs × resident CTAs per SM), i.e. one full wave.
@@ -566,6 +572,7 @@ template <int T>
 __global__ void __launch_bounds__(32) k_chol_fast(const double* __restrict__ B, const double* __restrict__ g,
                                                   double* __restrict__ Rout, double* __restrict__ Rinv,
                                                   double* __restrict__ alpha, int* flag, int gblock) {
+  pdl_enter();
   const int j = threadIdx.x;
   double a[T], y[T];
   const bool fail = chol_warp_fast<T>(B, a, y);
@@ -589,12 +596,12 @@ __global__ void __launch_bounds__(32) k_chol_fast(const double* __restrict__ B, 
 cudaError_t launch_chol_fast(cudaStream_t st, int t, const double* B, const double* g, double* R, double* Rinv,
                              double* alpha, int* flag, int gblock) {
   switch (t) {
-    case 1: k_chol_fast<1><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
-    case 2: k_chol_fast<2><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
-    case 4: k_chol_fast<4><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
-    case 8: k_chol_fast<8><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
-    case 16: k_chol_fast<16><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
-    case 32: k_chol_fast<32><<<1, 32, 0, st>>>(B, g, R, Rinv, alpha, flag, gblock); return cudaGetLastError();
+    case 1: return launch_k(k_chol_fast<1>, 1, 32, 0, st, B, g, R, Rinv, alpha, flag, gblock);
+    case 2: return launch_k(k_chol_fast<2>, 1, 32, 0, st, B, g, R, Rinv, alpha, flag, gblock);
+    case 4: return launch_k(k_chol_fast<4>, 1, 32, 0, st, B, g, R, Rinv, alpha, flag, gblock);
+    case 8: return launch_k(k_chol_fast<8>, 1, 32, 0, st, B, g, R, Rinv, alpha, flag, gblock);
+    case 16: return launch_k(k_chol_fast<16>, 1, 32, 0, st, B, g, R, Rinv, alpha, flag, gblock);
+    case 32: return launch_k(k_chol_fast<32>, 1, 32, 0, st, B, g, R, Rinv, alpha, flag, gblock);
     default: return launch_chol(st, t, B, g, R, Rinv, alpha, flag, gblock);
   }
 }

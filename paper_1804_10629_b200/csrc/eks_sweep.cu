@@ -86,15 +86,17 @@ __device__ __forceinline__ void vec_async(double* dst, const double* src, int64_
 //   NQ: blocks in the update R = Zin − Σ_q Q_q C_q (0: R = Zin, no update)
 //   NL: left blocks of the partial Lᵀ R (0: none);  V: also L_0ᵀ v
 // ----------------------------------------------------------------------------
-template <int T, int NQ, int NL, bool V>
+// AL: the last left block is Zin itself (SRE-CG: Z = A·W_{j−1} = AQ_last), so it is streamed
+// once and R goes to a separate (unstaged) tile.
+template <int T, int NQ, int NL, bool V, bool AL = false>
 struct SwCfg {
   static constexpr int TR = (T == 8) ? 64 : 32;  // rows per tile
   static constexpr int S = T + 4;                // padded smem row stride (doubles)
   static constexpr int TILE = TR * S;            // doubles per block tile
-  static constexpr int NARR = 1 + NQ + NL;       // streamed blocks
+  static constexpr int NARR = 1 + NQ + NL - (AL ? 1 : 0);  // streamed blocks
   static constexpr int STAGE = NARR * TILE + (V ? TR : 0);  // doubles per stage
   static constexpr int SC = T + 4;               // padded stride of C
-  static constexpr int CDBL = NQ * T * SC;
+  static constexpr int CDBL = NQ * T * SC + (AL ? TILE : 0);  // C, and the R tile when AL
   // Stages: as many as fit in ~100 KB (two CTAs per SM), else ~200 KB (one CTA per SM);
   // the ring keeps NS-1 tiles of every input in flight to cover HBM latency.
   static constexpr int NSA = (100 * 1024 / 8 - CDBL) / STAGE;
@@ -114,11 +116,13 @@ struct SwCfg {
   static constexpr int SMEM = SMEM0 > RED ? SMEM0 : RED;  // doubles
 };
 
-template <int T, int NQ, int NL, bool V>
+template <int T, int NQ, int NL, bool V, bool AL = false>
 __global__ void __launch_bounds__(256, 1)
     k_sweep(int64_t n, const double* Zin, double* Zout, const SweepPtrs P,
             const double* __restrict__ Cm, const double* __restrict__ v, double* __restrict__ part, const Tail tl) {
-  using K = SwCfg<T, NQ, NL, V>;
+  using K = SwCfg<T, NQ, NL, V, AL>;
+  static_assert(!AL || (NQ > 0 && NL > 0 && !V), "alias needs an update and left blocks");
+  pdl_enter();
   constexpr int S = K::S;
   extern __shared__ __align__(128) double sm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -126,6 +130,7 @@ __global__ void __launch_bounds__(256, 1)
   const int64_t lo = chunk_lo(n, blockIdx.x, gridDim.x), hi = chunk_lo(n, blockIdx.x + 1, gridDim.x);
   const int ntiles = (int)((hi - lo + K::TR - 1) / K::TR);
   double* sC = sm + K::NS * K::STAGE;
+  double* sRb = sC + NQ * T * K::SC;  // R tile (AL only)
 
   if constexpr (NQ > 0)
     for (int e = tid; e < NQ * T * T; e += 256) sC[(e / T) * K::SC + e % T] = Cm[e];
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int j = 0; j < NQ; ++j) tile_async<T, S, K::TR>(st + (1 + j) * K::TILE, P.q[j], row, rows);
 #pragma unroll
-      for (int j = 0; j < NL; ++j) tile_async<T, S, K::TR>(st + (1 + NQ + j) * K::TILE, P.l[j], row, rows);
+      for (int j = 0; j < NL - (AL ? 1 : 0); ++j) tile_async<T, S, K::TR>(st + (1 + NQ + j) * K::TILE, P.l[j], row, rows);
       if constexpr (V) vec_async<K::TR>(st + K::NARR * K::TILE, v, row, rows);
     }
     cp_commit();
@@ -178,8 +183,9 @@ __global__ void __launch_bounds__(256, 1)
         }
         const int r = mi * 8 + g, c = ni * 8 + 2 * q4;
         const double z0 = sZ[r * S + c] - d0, z1 = sZ[r * S + c + 1] - d1;
-        sZ[r * S + c] = z0;
-        sZ[r * S + c + 1] = z1;
+        double* sOut = AL ? sRb : sZ;
+        sOut[r * S + c] = z0;
+        sOut[r * S + c + 1] = z1;
         if (r < rows) *reinterpret_cast<double2*>(Zout + (row + r) * T + c) = make_double2(z0, z1);
       }
       if constexpr (NL > 0) __syncthreads();
@@ -191,11 +197,12 @@ __global__ void __launch_bounds__(256, 1)
       for (int u = 0; u < K::TPW; ++u) {
         const int tile = (warp / K::WS) * K::TPW + u;
         const int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
-        const double* sL = st + (1 + NQ + l) * K::TILE;
+        const double* sL = (AL && l == NL - 1) ? sZ : st + (1 + NQ + l) * K::TILE;
+        const double* sR = AL ? sRb : sZ;
         double d0 = acc[u][0], d1 = acc[u][1];
 #pragma unroll
         for (int kk = slice * 4; kk < K::TR; kk += 4 * K::WS)
-          dmma(d0, d1, sL[(kk + q4) * S + mi * 8 + g], sZ[(kk + q4) * S + ni * 8 + g]);
+          dmma(d0, d1, sL[(kk + q4) * S + mi * 8 + g], sR[(kk + q4) * S + ni * 8 + g]);
         acc[u][0] = d0;
         acc[u][1] = d1;
       }
@@ -289,6 +296,7 @@ __global__ void __launch_bounds__(256, 1)
                const double* __restrict__ r, double* __restrict__ rnew, const int* __restrict__ flag, int mode,
                const double* __restrict__ AWprev, double* __restrict__ part, const Tail tl) {
   using K = ApCfg<T, C1N>;
+  pdl_enter();
   constexpr int PS = C1N * T * T + 2;  // per-CTA partial: [C1 (C1N·T·T) | ‖rnew‖² | pad] (16-byte rows)
   constexpr int S = K::S, SR = T + 4;
   extern __shared__ __align__(128) double sm[];
@@ -545,6 +553,7 @@ __global__ void __launch_bounds__(256, (T >= 64 ? 2 : 3))
                 const double* __restrict__ Xext, int64_t xoff, double* __restrict__ Y, const double* __restrict__ r,
                 double* __restrict__ part, const Tail tl, const CholArgs ch) {
   using K = SgCfg<T, NZ>;
+  pdl_enter();
   constexpr int S = K::S, G = K::G, SL = K::SL, P = K::PASSES, RPP = K::RPP;
   extern __shared__ __align__(128) double sm[];
   double* sX = sm;
@@ -713,6 +722,7 @@ __global__ void __launch_bounds__(256, MINB)
                     const double* __restrict__ Xext, int64_t xoff, double* __restrict__ Y,
                     const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch) {
   using K = SeCfg<T, W>;
+  pdl_enter();
   constexpr int S = K::S, G = K::G, P = K::PASSES, RPP = K::RPP, TR = K::TR, H = T / 2;
   extern __shared__ __align__(128) double sm[];
   double* sY = sm + 2 * TR * S;
@@ -898,6 +908,7 @@ __global__ void __launch_bounds__(SsCfg<T>::NTH, 1)
                const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch, int NS,
                int probe) {
   using K = SsCfg<T>;
+  pdl_enter();
   constexpr int S = K::S, G = K::G, C = K::C, RW = K::RW, TR = K::TR, M = K::M, PT = kSegPT, NWC = K::NWC;
   constexpr int VS = seg_vs(W), MT = K::MT;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -1127,22 +1138,21 @@ static int grid_for(int nblk_max, int occ) {
   const int g = sms * occ;
   return g < nblk_max ? g : nblk_max;
 }
-template <int T, int NQ, int NL, bool V>
+template <int T, int NQ, int NL, bool V, bool AL = false>
 static cudaError_t launch_sweep_t(cudaStream_t st, int64_t n, const double* Zin, double* Zout, const SweepPtrs& P,
                                   const double* C, const double* v, double* part, int nblk, const Tail& tl) {
-  using K = SwCfg<T, NQ, NL, V>;
+  using K = SwCfg<T, NQ, NL, V, AL>;
   const size_t sm = (size_t)K::SMEM * 8;
   if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
   static int occ = 0;
   if (!occ) {
-    cudaFuncSetAttribute(k_sweep<T, NQ, NL, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<T, NQ, NL, V>, 256, sm);
+    cudaFuncSetAttribute(k_sweep<T, NQ, NL, V, AL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<T, NQ, NL, V, AL>, 256, sm);
     if (occ < 1) occ = 1;
   }
   nblk = grid_for(nblk, occ);
   t_last_grid = nblk;
-  k_sweep<T, NQ, NL, V><<<nblk, 256, sm, st>>>(n, Zin, Zout, P, C, v, part, NL > 0 ? tl : Tail{});
-  return cudaGetLastError();
+  return launch_k(k_sweep<T, NQ, NL, V, AL>, nblk, 256, sm, st, n, Zin, Zout, P, C, v, part, NL > 0 ? tl : Tail{});
 }
 
 #define EKS_SW_T(t, ...)                                   \
@@ -1191,7 +1201,10 @@ cudaError_t launch_sweep(cudaStream_t st, int t, int nq, int nl, bool v, int64_t
     if (nq == 0 && nl == 1 && v) return launch_sweep_t<T, 0, 1, true>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
     if (v) return cudaErrorInvalidValue;
     if (nq == 1 && nl == 1) return launch_sweep_t<T, 1, 1, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
-    if (nq == 2 && nl == 2) return launch_sweep_t<T, 2, 2, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
+    if (nq == 2 && nl == 2) {
+      if (P.l[1] == Zin) return launch_sweep_t<T, 2, 2, false, true>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
+      return launch_sweep_t<T, 2, 2, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
+    }
     if (nq > 0 && nl > 0) return cudaErrorInvalidValue;
     const bool upd = nq > 0;
     switch (upd ? nq : nl) {
@@ -1225,8 +1238,7 @@ static cudaError_t spmm_gram_t(cudaStream_t st, int64_t n, const int* rp, const 
   }
   nblk = grid_for(nblk, occ);
   t_last_grid = nblk;
-  k_spmm_gram<T, NZ><<<nblk, 256, sm, st>>>(n, rp, col, val, Xext, xoff, Y, r, part, tl, ch);
-  return cudaGetLastError();
+  return launch_k(k_spmm_gram<T, NZ>, nblk, 256, sm, st, n, rp, col, val, Xext, xoff, Y, r, part, tl, ch);
 }
 
 template <int T, int W, int MINB = (T >= 64 ? 2 : 3)>
@@ -1245,8 +1257,7 @@ static cudaError_t spmm_gram_ell_t(cudaStream_t st, int64_t n, const int* ecol, 
   t_last_grid = nblk;
   (void)tmax;
   (void)n_ext;
-  k_spmm_gram_ell<T, W, MINB><<<nblk, 256, sm, st>>>(n, ecol, eval, Xext, xoff, Y, r, part, tl, ch);
-  return cudaGetLastError();
+  return launch_k(k_spmm_gram_ell<T, W, MINB>, nblk, 256, sm, st, n, ecol, eval, Xext, xoff, Y, r, part, tl, ch);
 }
 
 int ell_width(int maxrow) { return maxrow <= 5 ? 5 : (maxrow <= 7 ? 7 : (maxrow <= 8 ? 8 : 0)); }
@@ -1256,16 +1267,16 @@ cudaError_t launch_spmm_gram_ell(cudaStream_t st, int t, int64_t n, const int* e
                                  const double* r, double* part, int nblk, const Tail& tl, const CholArgs& ch) {
   if (ch.on && !spmm_gram_fused_chol(t)) return cudaErrorInvalidValue;
   EKS_SW_T(t, {
-    if (w == 5) return spmm_gram_ell_t<T, 5>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
-    if (w == 7) {
-      static const int mb = getenv("EKS_ELL_MINB") ? atoi(getenv("EKS_ELL_MINB")) : 4;  // measured best at t=16
-      if constexpr (T == 16) {
-        if (mb == 4) return spmm_gram_ell_t<T, 7, 4>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
-        if (mb == 6) return spmm_gram_ell_t<T, 7, 6>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
-        if (mb == 8) return spmm_gram_ell_t<T, 7, 8>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
-      }
-      return spmm_gram_ell_t<T, 7>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+    // 4 CTAs/SM (≤ 64 registers) hides more gather latency when X streams from HBM; when the
+    // block is L2-resident the 3-CTA build (more registers, fewer spills) is faster (measured)
+    static const int mbe = getenv("EKS_ELL_MINB") ? atoi(getenv("EKS_ELL_MINB")) : 0;
+    const int mb = mbe ? mbe : ((double)n * T * 8 > 64e6 ? 4 : 3);
+    if constexpr (T == 16) {
+      if (mb == 4 && w == 5) return spmm_gram_ell_t<T, 5, 4>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+      if (mb == 4 && w == 7) return spmm_gram_ell_t<T, 7, 4>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
     }
+    if (w == 5) return spmm_gram_ell_t<T, 5>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
+    if (w == 7) return spmm_gram_ell_t<T, 7>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
     if (w == 8) return spmm_gram_ell_t<T, 8>(st, n, ecol, eval, tmax, n_ext, Xext, xoff, Y, r, part, nblk, tl, ch);
   });
   return cudaErrorInvalidValue;
@@ -1292,8 +1303,7 @@ static cudaError_t spmm_seg_t(cudaStream_t st, int64_t n, const SegPlan& pl, con
   nblk = nblk < sms ? nblk : sms;  // one persistent CTA per SM
   t_last_grid = nblk;
   static const int probe = getenv("EKS_SEG_PROBE") ? atoi(getenv("EKS_SEG_PROBE")) : 0;
-  k_spmm_seg<T, W><<<nblk, K::NTH, sm, st>>>(n, pl, Xext, Y, r, part, tl, ch, ns, probe);
-  return cudaGetLastError();
+  return launch_k(k_spmm_seg<T, W>, nblk, K::NTH, sm, st, n, pl, Xext, Y, r, part, tl, ch, ns, probe);
 }
 
 template <int T>
@@ -1351,9 +1361,8 @@ static cudaError_t apply_t(cudaStream_t st, int64_t n, double* Z2W, double* AZ2A
   }
   nblk = grid_for(nblk, occ);
   t_last_grid = nblk;
-  k_apply_tc<T, C1N><<<nblk, 256, sm, st>>>(n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part,
-                                            tl);
-  return cudaGetLastError();
+  return launch_k(k_apply_tc<T, C1N>, nblk, 256, sm, st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode,
+                  AWprev, part, tl);
 }
 
 bool apply_c1_supported(int t, int c1n) {

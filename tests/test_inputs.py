@@ -96,3 +96,14 @@ def test_subcubes_fraction_exact():
 def test_cfg5_start_block_unit_columns():
     X = ei.cfg5_start_block(1000, 8)
     assert np.allclose(np.linalg.norm(X, axis=0), 1.0, atol=1e-14)
+
+
+def test_torch_splitmix_matches_numpy():
+    """The device-side generator (used for the cfg5 block in bench.py) draws the same bits."""
+    import torch
+    for seed, start, count in [(1855, 0, 1000), (1806, 12345, 70001), (0, 0, 17)]:
+        a = ei.uniform_pm1(seed, count, start=start)
+        b = ei.uniform_pm1_torch(seed, count, "cpu", start=start, chunk=4096).numpy()
+        assert np.array_equal(a, b)
+    X = ei.cfg5_start_block_torch(500, 8, "cpu").numpy()
+    assert np.allclose(X, ei.cfg5_start_block(500, 8), rtol=1e-14, atol=0)
