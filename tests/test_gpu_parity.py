@@ -289,3 +289,70 @@ def test_maxiter_and_determinism_and_host_pointers(eks, torch_cuda):
     assert np.array_equal(host(a["x"]), c["x"])
     assert np.array_equal(a["hist"], c["hist"])
     S.close()
+
+
+# ------------------------------------------------------------------ BASELINE full sizes
+def _full_operator(cfg):
+    return {"cfg3": lambda: ei.cfg3().A, "cfg4": lambda: ei.cfg4().A, "cfg5": lambda: ei.cfg5_operator()}[cfg]()
+
+
+def _sub_csr(A, rows):
+    """Rows `rows` of A with their columns renumbered into the set of columns they use."""
+    starts, ends = A.row_ptr[rows], A.row_ptr[rows + 1]
+    idx = np.concatenate([np.arange(s, e) for s, e in zip(starts, ends)])
+    ucols, inv = np.unique(A.col[idx], return_inverse=True)
+    rp = np.concatenate([[0], np.cumsum(ends - starts)]).astype(np.int64)
+    return ei.Csr(len(rows), rp, inv.astype(np.int32), A.val[idx].copy()), ucols
+
+
+@pytest.mark.parametrize("cfg,t", [("cfg3", 32), ("cfg4", 64), ("cfg5", 16)])
+def test_full_size_spmm_gram_sampled(eks, torch_cuda, oracle_lib, cfg, t):
+    """The SpMM-block kernel eks_solve launches, at the BASELINE operator sizes: sampled rows of
+    Y = A·X bitwise against the oracle's row products (SpMM order, R20), the Gram XᵀY and Xᵀv
+    against a cuBLAS fp64 reference within 1e-12."""
+    torch = torch_cuda
+    A = _full_operator(cfg)
+    S = eks.Solver(A)
+    X = ei.uniform_pm1_torch(77, A.n * t, "cuda").view(A.n, t)
+    v = ei.uniform_pm1_torch(78, A.n, "cuda")
+    Y = torch.empty_like(X)
+    G = torch.empty(t, t, dtype=torch.float64, device="cuda")
+    g = torch.empty(t, dtype=torch.float64, device="cuda")
+    eks.eks_k_spmm(S.ctx, t, X, Y, G, v, g)
+    rng = np.random.default_rng(11)
+    edges = [0, 1, 15, 16, 63, 64, A.n // 2, A.n - 65, A.n - 64, A.n - 2, A.n - 1]
+    rows = np.unique(np.concatenate([rng.integers(0, A.n, 3000), edges])).astype(np.int64)
+    sub, ucols = _sub_csr(A, rows)
+    Xs = host(X[torch.from_numpy(ucols).cuda()])
+    Yo = oracle_lib.spmm(sub, Xs)[: len(rows)]
+    assert np.array_equal(host(Y[torch.from_numpy(rows).cuda()]), Yo)
+    assert rel(host(G), host(X.T @ Y)) <= 1e-12
+    assert rel(host(g), host(X.T @ v)) <= 1e-12
+    S.close()
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4"])
+def test_full_size_solve_prefix_properties(eks, torch_cuda, cfg):
+    """First outer iterations of the BASELINE solves at full size (the oracle cannot run them):
+    the library's true residual matches a cuSPARSE fp64 b − A·x, the recursive residual tracks
+    it, and φ(x) = ½xᵀAx − bᵀx decreases (the A-norm error is minimised over a growing space)."""
+    torch = torch_cuda
+    p = ei.cfg3() if cfg == "cfg3" else ei.cfg4()
+    A = p.A
+    At = torch.sparse_csr_tensor(torch.from_numpy(A.row_ptr), torch.from_numpy(A.col.astype(np.int64)),
+                                 torch.from_numpy(A.val), size=(A.n, A.n)).cuda()
+    b = dev(torch, p.b)
+    S = eks.Solver(A)
+    phis = [0.0]
+    for k in (1, 2):
+        rep = S.solve(b, p.method, p.s, p.t, 0.0, max_outer=k + 1)
+        assert rep["outer_iters"] == k
+        x = rep["x"]
+        Ax = (At @ x.unsqueeze(1)).squeeze(1)
+        r = b - Ax
+        relres = float(r.norm() / b.norm())
+        assert abs(relres - rep["true_relres"]) <= 1e-10 * max(1.0, relres)
+        assert abs(float(r.norm()) - rep["rho"]) <= 1e-9 * float(b.norm())
+        phis.append(float(0.5 * x.dot(Ax) - b.dot(x)))
+    assert phis[2] < phis[1] < phis[0]
+    S.close()
