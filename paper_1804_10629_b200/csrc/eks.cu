@@ -418,7 +418,10 @@ eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, cons
   }
   const size_t stride = eks::sweep_part_stride(t, nq, false);
   ST(ensure_part(ctx, stride * ctx->nblk));
-  account(ctx, EKS_K_UPDATE, 8.0 * ctx->n * ((double)2 * nq * t + 2.0 * t), 4.0 * ctx->n * t * t * nq);
+  // algorithmic bytes: read Z, Q_j, AQ_j (once each — for SRE-CG Z is AQ_last itself), write Z1
+  const bool alias = nq > 0 && AQ[nq - 1] == Z;
+  account(ctx, EKS_K_UPDATE, 8.0 * ctx->n * ((double)2 * nq * t + 2.0 * t - (alias ? t : 0)),
+          4.0 * ctx->n * t * t * nq);
   {
     KScope ks(ctx, EKS_K_UPDATE);  // C2 partials reduced by the sweep's last CTAs
     CK(eks::launch_sweep(ctx->stream, t, nq, nq, false, ctx->n, Z, Z1, P, C1, nullptr, ctx->part, ctx->nblk,
