@@ -44,7 +44,8 @@ eks_status eks_k_chol(eks_ctx* ctx, int t, const double* B, double* R);
  * variant 0: plain CSR SpMM (k_spmm); 1: the fused SpMM + Gram [XᵀY | Xᵀv] kernel eks_solve
  * selects for this t, per-CTA partials only; 2: + the tail reduction of the partials (what
  * eks_solve launches); 3: + the block's Cholesky; 4: the ELL gather kernel forced; 5: the CSR
- * gather kernel forced (4, 5 with the tail).  v may be NULL.  Variants 1-5 need t in {8,16,32,64}. */
+ * gather kernel forced, 6: the plane-marching stencil kernel forced (4-6 with the tail; 6 needs a
+ * stencil-structured matrix).  v may be NULL.  Variants 1-6 need t in {8,16,32,64}. */
 eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, const double* v, int variant, int reps,
                            double* ms);
 

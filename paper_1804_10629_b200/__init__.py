@@ -112,6 +112,14 @@ def eks_plan_halo(rank: int, nranks: int, ranges, row_ptr, col):
                                               interior_lo=int(geom[2]), interior_hi=int(geom[3]))
 
 
+def _order_after_torch():
+    """The library runs on its own (non-blocking) stream or the one set by eks_set_stream: before
+    it reads torch tensors, the work torch queued on its current stream must be complete (the C
+    ABI's contract: the producing stream is synchronized before the call)."""
+    import torch
+    torch.cuda.current_stream().synchronize()
+
+
 def _where(*arrays):
     dev = [hasattr(a, "data_ptr") for a in arrays if a is not None]
     if dev and all(dev):
@@ -125,6 +133,8 @@ def _ptr(a, dtype):
     if a is None:
         return None
     if hasattr(a, "data_ptr"):
+        if a.is_cuda:
+            _order_after_torch()
         if not a.is_contiguous():
             raise ValueError("device tensor must be contiguous")
         return C.c_void_p(a.data_ptr())

@@ -10,8 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libeks.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("eks.cu", "eks_kernels.cu", "eks_sweep.cu")]
-HEADERS = [os.path.join(CSRC, "eks_kernels.cuh"), os.path.join(CSRC, "eks_sweep.cuh"), os.path.join(ROOT, "include", "eks.h"),
+SOURCES = [os.path.join(CSRC, f) for f in ("eks.cu", "eks_kernels.cu", "eks_sweep.cu", "eks_grid.cu")]
+HEADERS = [os.path.join(CSRC, "eks_kernels.cuh"), os.path.join(CSRC, "eks_sweep.cuh"), os.path.join(CSRC, "eks_device.cuh"), os.path.join(ROOT, "include", "eks.h"),
            os.path.join(ROOT, "include", "eks_kernels.h")]
 
 

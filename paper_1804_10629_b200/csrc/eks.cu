@@ -72,7 +72,11 @@ struct eks_ctx {
   int* d_segown = nullptr;
   unsigned short* d_lidx = nullptr;
   double* d_sval = nullptr;
-  int spmm_path = 0;               // 0 auto, 1 ell, 2 csr, 3 seg (EKS_SPMM_PATH, for A/B measurements)
+  int spmm_path = 0;               // 0 auto, 1 ell, 2 csr, 3 seg, 4 grid (EKS_SPMM_PATH, for A/B measurements)
+  // stencil structure (eks_grid.cu GridPlan): plane-marching SpMM
+  bool grid_ok = false;
+  eks::GridPlan gplan{};
+  double* d_sv = nullptr;
   int chol_mode = 0;               // 0 separate one-warp Cholesky launch, 1 in the SpMM+Gram tail (EKS_CHOL)
   // workspace, keyed by t
   int ws_t = 0;
@@ -430,10 +434,13 @@ eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, cons
   return allreduce(ctx, C2, stride);
 }
 
-// Which fused SpMM+Gram kernel runs for this t: 0 TMA-staged segments, 1 ELL gathers, 2 CSR.
-// Measured (tools/spmm_micro.py): ELL is fastest for t ≤ 32, the segment kernel for t = 64;
-// EKS_SPMM_PATH=seg|ell|csr forces one for A/B measurements.
+// Which fused SpMM+Gram kernel runs for this t: 4 plane-marching (stencil-structured A), 0 TMA-
+// staged segments, 1 ELL gathers, 2 CSR.  Measured (tools/spmm_micro.py): plane-marching is
+// fastest for t ≤ 32, then ELL; the segment kernel for t = 64.  EKS_SPMM_PATH=grid|seg|ell|csr
+// forces one for A/B measurements.
 int spmm_path_for(const eks_ctx* ctx, int t) {
+  const bool grid = ctx->grid_ok && ctx->nranks == 1 && eks::spmm_grid_fits(t, ctx->gplan);
+  if (grid && (ctx->spmm_path == 4 || (ctx->spmm_path == 0 && t <= 32))) return 4;
   const bool seg = ctx->seg_ok && eks::spmm_seg_fits(t, ctx->ell_w, ctx->seg.cap);
   if (seg && (ctx->spmm_path == 3 || (ctx->spmm_path == 0 && t == 64))) return 0;
   if (ctx->ell_w && ctx->spmm_path <= 1) return 1;
@@ -464,7 +471,10 @@ eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const doubl
   {
     KScope k(ctx, EKS_K_SPMM);
     const int path = spmm_path_for(ctx, t);
-    if (path == 0)
+    if (path == 4)
+      CK(eks::launch_spmm_grid(ctx->stream, t, ctx->gplan, X.base, Y, r, ctx->part, ctx->nblk,
+                               tail(ctx, 2, out, stride), c));
+    else if (path == 0)
       CK(eks::launch_spmm_seg(ctx->stream, t, ctx->n, ctx->seg, ctx->ell_w, X.base, Y, r, ctx->part, ctx->nblk,
                               tail(ctx, 2, out, stride), c));
     else if (path == 1)
@@ -830,6 +840,68 @@ eks_status build_seg_plan(eks_ctx* ctx, int64_t n, const std::vector<int64_t>& r
   return EKS_OK;
 }
 
+// Stencil structure for the plane-marching SpMM (eks_grid.cu): the distinct positive column
+// offsets must be {1, b} (2D: nx = b, planes are x-lines) or {1, b, c} with b | c (3D: nx = b,
+// ny = c/b), mirrored by the negative ones, with n a multiple of the plane size, and no ±1
+// (±nx) entry may cross an x-line (y-plane) boundary.  Values are stored per row in ascending
+// offset order, 0 in absent slots.  Otherwise nothing is built (the ELL kernel runs).
+eks_status build_grid_plan(eks_ctx* ctx, int64_t n, const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
+                           const std::vector<double>& val) {
+  int64_t pos[3] = {0, 0, 0};
+  int np = 0;
+  bool neg_ok = true;
+  for (int64_t i = 0; i < n && np <= 3; ++i)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t o = (int64_t)col[p] - i;
+      if (o <= 0) continue;
+      int k = 0;
+      while (k < np && pos[k] != o) ++k;
+      if (k == np) {
+        if (np == 3) return EKS_OK;
+        pos[np++] = o;
+      }
+    }
+  std::sort(pos, pos + np);
+  if (np < 2 || pos[0] != 1) return EKS_OK;
+  const int64_t b = pos[1], c = np == 3 ? pos[2] : 0;
+  int64_t nx = b, ny = 1, plane = b;
+  if (np == 3) {
+    if (c % b) return EKS_OK;
+    ny = c / b;
+    plane = c;
+  }
+  if (n % plane) return EKS_OK;
+  const int64_t nz = n / plane;
+  if (nx >= INT32_MAX || ny >= INT32_MAX || nz >= INT32_MAX) return EKS_OK;
+  const int w = np == 3 ? 7 : 5, VS = (w + 1) & ~1;
+  const int64_t offs[7] = {-c, -b, -1, 0, 1, b, c};
+  const int64_t offs2[5] = {-b, -1, 0, 1, b};
+  std::vector<double> sv((size_t)n * VS, 0.0);
+  for (int64_t i = 0; i < n && neg_ok; ++i) {
+    const int64_t x = i % nx, y = (i / nx) % ny;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t o = (int64_t)col[p] - i;
+      int k = -1;
+      for (int q = 0; q < w; ++q)
+        if ((w == 7 ? offs[q] : offs2[q]) == o) k = q;
+      if (k < 0) { neg_ok = false; break; }
+      if ((o == 1 && x + 1 >= nx) || (o == -1 && x == 0)) { neg_ok = false; break; }
+      if (w == 7 && ((o == b && y + 1 >= ny) || (o == -b && y == 0))) { neg_ok = false; break; }
+      sv[(size_t)i * VS + k] = val[p];
+    }
+  }
+  if (!neg_ok) return EKS_OK;
+  CK(cudaMalloc((void**)&ctx->d_sv, sizeof(double) * sv.size()));
+  CK(cudaMemcpy(ctx->d_sv, sv.data(), sizeof(double) * sv.size(), cudaMemcpyHostToDevice));
+  ctx->gplan.nx = (int)nx;
+  ctx->gplan.ny = (int)ny;
+  ctx->gplan.nz = (int)nz;
+  ctx->gplan.w = w;
+  ctx->gplan.sv = ctx->d_sv;
+  ctx->grid_ok = true;
+  return EKS_OK;
+}
+
 void begin_run(eks_ctx* ctx, const eks_options* opt) {
   ctx->prof_on = opt && opt->profile;
   ctx->prof = eks_profile{};
@@ -892,7 +964,7 @@ eks_status eks_create(eks_ctx** out, const eks_dist* dist) {
     ctx->h_flag[0] = INT_MAX;
     if (const char* e = getenv("EKS_CHOL")) ctx->chol_mode = atoi(e);
     if (const char* e = getenv("EKS_SPMM_PATH"))
-      ctx->spmm_path = !strcmp(e, "ell") ? 1 : (!strcmp(e, "csr") ? 2 : (!strcmp(e, "seg") ? 3 : 0));
+      ctx->spmm_path = !strcmp(e, "ell") ? 1 : (!strcmp(e, "csr") ? 2 : (!strcmp(e, "seg") ? 3 : (!strcmp(e, "grid") ? 4 : 0)));
     if (ctx->nranks > 1) {
       ncclUniqueId u;
       memcpy(&u, dist->nccl_id, 128);
@@ -1011,6 +1083,9 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
                   (void*)ctx->d_tmax, (void*)ctx->d_seg, (void*)ctx->d_segrows, (void*)ctx->d_segown,
                   (void*)ctx->d_lidx, (void*)ctx->d_sval})
     dfree(p);
+  dfree(ctx->d_sv);
+  ctx->d_sv = nullptr;
+  ctx->grid_ok = false;
   ctx->d_tmax = ctx->d_seg = ctx->d_segrows = ctx->d_segown = nullptr;
   ctx->d_lidx = nullptr;
   ctx->d_sval = nullptr;
@@ -1058,6 +1133,7 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
     CK(cudaMalloc((void**)&ctx->d_tmax, sizeof(int32_t) * tmax.size()));
     CK(cudaMemcpy(ctx->d_tmax, tmax.data(), sizeof(int32_t) * tmax.size(), cudaMemcpyHostToDevice));
     ST(build_seg_plan(ctx, n, rp, ecol, val, plan.halo_before, w));
+    if (ctx->nranks == 1) ST(build_grid_plan(ctx, n, rp, col, val));
     ctx->ell_w = w;
   }
   ctx->n_global = n_global;
@@ -1273,6 +1349,7 @@ eks_status eks_destroy(eks_ctx* ctx) {
   dfree(ctx->d_segown);
   dfree(ctx->d_lidx);
   dfree(ctx->d_sval);
+  dfree(ctx->d_sv);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (auto& p : ctx->prof_pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
@@ -1359,7 +1436,7 @@ eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double
 eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, const double* v, int variant, int reps,
                            double* ms) {
   ST(k_ready(ctx, t));
-  if (!X || !Y || !ms || reps < 1 || variant < 0 || variant > 5)
+  if (!X || !Y || !ms || reps < 1 || variant < 0 || variant > 6)
     return fail(ctx, EKS_ERR_INVALID_ARG, "bad eks_k_time_spmm arguments");
   if (variant > 0 && !eks::sweep_supported(t))
     return fail(ctx, EKS_ERR_INVALID_ARG, "fused SpMM+Gram needs t in {8,16,32,64}");
@@ -1373,11 +1450,23 @@ eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, cons
   ch.alpha = v ? ctx->alpha : nullptr;
   ch.flag = ctx->flag;
   const eks::Tail tl = variant >= 2 ? tail(ctx, 2, ctx->Bg, stride) : eks::Tail{};
-  const int path = variant <= 3 ? spmm_path_for(ctx, t) : (variant == 4 && ctx->ell_w ? 1 : 2);
+  int path = variant <= 3 ? spmm_path_for(ctx, t) : (variant == 4 && ctx->ell_w ? 1 : 2);
+  if (variant == 6) {
+    if (!(ctx->grid_ok && eks::spmm_grid_fits(t, ctx->gplan)))
+      return fail(ctx, EKS_ERR_INVALID_ARG, "matrix is not stencil-structured (no grid plan)");
+    path = 4;
+  }
   const bool use_seg = path == 0, use_ell = path == 1;
   auto run = [&]() -> cudaError_t {
     if (variant == 0)
       return eks::launch_spmm(ctx->stream, t, 0, (int)ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val, X, Y, ctx->sms);
+    if (path == 4) {
+      cudaError_t e = eks::launch_spmm_grid(ctx->stream, t, ctx->gplan, X, Y, v, ctx->part, ctx->nblk, tl, ch);
+      if (e == cudaSuccess && variant == 3 && !ch.on)
+        e = eks::launch_chol(ctx->stream, t, ctx->Bg, v ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
+                             v ? ctx->alpha : nullptr, ctx->flag, 0);
+      return e;
+    }
     if (use_seg) {
       cudaError_t e = eks::launch_spmm_seg(ctx->stream, t, ctx->n, ctx->seg, ctx->ell_w, X, Y, v, ctx->part, ctx->nblk,
                                            tl, ch);

@@ -1,0 +1,381 @@
+// eks_grid.cu — plane-marching fused SpMM + Gram for stencil-structured matrices.
+//
+// When eks_setup_csr finds that A is a 5-point (2D) or 7-point (3D) stencil on an
+// nx × ny × nz lexicographic grid (every entry at an offset 0, ±1, ±nx, ±nx·ny that
+// stays inside the grid), A·X is computed by 2.5D blocking: a CTA owns an (x, y)
+// block of bx × by grid points and marches along z.  For every plane the producer
+// warp streams the block's X rows with a one-point halo (by+2 contiguous runs) and
+// the rows' 7 (5) stencil values into a stage of a shared-memory ring with
+// cp.async.bulk (TMA) on full/empty mbarriers; the 8 consumer warps form each Y row
+// from the three resident planes z−1, z, z+1 at fixed shared-memory offsets.  Every
+// X row therefore crosses L2 → SM about (1 + 2/by + 2/bx)(1 + 2/zc) times instead of
+// once per stencil entry, and the ±N² plane reuse never depends on L2 retention —
+// the limit of the gather kernels.
+//
+// Accumulation order per Y entry: the stencil slots in ascending column order with
+// value 0 in absent (boundary) slots — fma(0, x, y) = y exactly for finite x — i.e.
+// the oracle's p-ascending CSR order (reading R20): Y is bitwise equal to k_spmm.
+// The Gram / α̃ epilogue is the one of k_spmm_seg (per-warp DMMA over the warp's own
+// rows, fixed warp order, tail reduction, optional Cholesky).
+#include "eks_device.cuh"
+#include "eks_sweep.cuh"
+
+#include <cstdint>
+#include <cstdlib>
+
+namespace eks {
+
+namespace {
+
+template <int T>
+struct GrCfg {
+  static constexpr int NWC = 8, NTH = 32 * (NWC + 1);  // 8 consumer warps + 1 producer warp
+  static constexpr int R = 2048 / T;                   // output rows per plane-block (bx·by)
+  static constexpr int RW = T == 8 ? 8 : 4;            // rows per warp unit (DMMA k = 4 rows)
+  static constexpr int G = 32 / RW;                    // threads per row
+  static constexpr int C = T / G;                      // columns per thread
+  static constexpr int U = R / RW;                     // units per plane-block
+  static constexpr int UPW = U / NWC;                  // units per consumer warp per plane
+  static constexpr int S = T + 4;                      // Y scratch row stride
+  static constexpr int MT = T / 8;
+  static constexpr int NUT = MT * (MT + 1) / 2;        // upper 8×8 output tiles
+  static_assert(U % NWC == 0, "units");
+};
+
+}  // namespace
+
+// Stage bytes: X plane-block (bx+2)·(by+2·hy) rows, then R rows of VS stencil values, then R
+// entries of r.
+template <int T>
+__host__ __device__ inline size_t grid_stage_bytes(int bx, int by, int hy, int vs) {
+  using K = GrCfg<T>;
+  return (((size_t)(bx + 2) * (by + 2 * hy) * T * 8 + (size_t)K::R * vs * 8 + (size_t)K::R * 8) + 127) & ~(size_t)127;
+}
+
+template <int T, int W>
+__global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
+    k_spmm_grid(const GridPlan gp, int bx, int by, int zc, const double* __restrict__ X, double* __restrict__ Y,
+                const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch, int NS) {
+  using K = GrCfg<T>;
+  pdl_enter();
+  constexpr int S = K::S, G = K::G, C = K::C, RW = K::RW, NWC = K::NWC, MT = K::MT, H = T / 2;
+  constexpr int VS = (W + 1) & ~1;
+  static_assert(W == 5 || W == 7, "2D 5-point or 3D 7-point stencil");
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nx = gp.nx, ny = gp.ny, nz = gp.nz;
+  const int hy = ny > 1 ? 1 : 0;               // y halo (3D only)
+  const int PW = bx + 2, PH = by + 2 * hy;     // plane-block extent
+  const int64_t plane = (int64_t)nx * ny;
+  const size_t SB = grid_stage_bytes<T>(bx, by, hy, VS);
+  double* sYw = reinterpret_cast<double*>(smraw + (size_t)NS * SB);  // [NWC][RW][S]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sYw + NWC * RW * S);
+  uint64_t* empty = full + 8;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q4 = lane & 3;
+  const int nbx = (nx + bx - 1) / bx, nby = (ny + by - 1) / by, nzc = (nz + zc - 1) / zc;
+  const bool rbulk = (nx % 2) == 0;  // r lines start 16-byte aligned (x0, bx even)
+  const int64_t nunits = (int64_t)nbx * nby * nzc;
+  // unit → block origin and z range
+  auto unit_geom = [&](int64_t u, int& x0, int& y0, int& z0, int& z1) {
+    const int zi = (int)(u % nzc);
+    const int64_t b = u / nzc;
+    x0 = (int)(b % nbx) * bx;
+    y0 = (int)(b / nbx) * by;
+    z0 = zi * zc;
+    z1 = z0 + zc < nz ? z0 + zc : nz;
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, NWC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // zero the X ring once: halo cells outside the grid are never written and must be finite
+  for (size_t e = tid; e < (size_t)NS * SB / 16; e += K::NTH) reinterpret_cast<double2*>(smraw)[e] = make_double2(0, 0);
+  __syncthreads();
+
+  if (warp == NWC) {
+    // ================= producer: one load step = one X plane-block (+ the values of the plane below it)
+    int cur = 0;             // ring stage of this load step
+    uint32_t eph = 0;        // empty-barrier phase parity of the stage's previous use
+    int64_t gstep = 0;
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+      int x0, y0, z0, z1;
+      unit_geom(u, x0, y0, z0, z1);
+      const int xa = x0 - 1 > 0 ? x0 - 1 : 0, xb = x0 + bx + 1 < nx ? x0 + bx + 1 : nx;  // X run [xa, xb)
+      const int ob = x0 + bx < nx ? x0 + bx : nx;                                        // output x range [x0, ob)
+      for (int p = z0 - 1; p <= z1; ++p, ++gstep) {
+        const int s = cur;
+        if (gstep >= NS) mbar_wait(empty + s, eph);
+        if (++cur == NS) {
+          cur = 0;
+          if (gstep >= NS) eph ^= 1u;  // lap L ≥ 1 waits for release phase (L − 1) & 1
+        }
+        unsigned char* st = smraw + (size_t)s * SB;
+        // lane l < PH: X line y0 − hy + l of plane p;  lane PH + l < PH + by: values of output line y0 + l, plane p − 1
+        uint32_t bytes = 0;
+        const int yy = y0 - hy + lane;
+        const bool xline = lane < PH && p >= 0 && p < nz && yy >= 0 && yy < ny;
+        const int vl = lane - PH, vy = y0 + vl;
+        const bool vline = vl >= 0 && vl < by && p - 1 >= z0 && p - 1 < z1 && vy < ny;
+        const int rl = lane - PH - by, ry = y0 + rl;  // lanes for the lines of r (16-byte rows: nx even)
+        const bool rline = r != nullptr && rbulk && rl >= 0 && rl < by && p - 1 >= z0 && p - 1 < z1 && ry < ny;
+        if (xline) bytes += (uint32_t)(xb - xa) * T * 8;
+        if (vline) bytes += (uint32_t)(ob - x0) * VS * 8;
+        if (rline) bytes += (uint32_t)(ob - x0) * 8;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(full + s, bytes);  // 0 bytes (plane outside the grid): the phase completes at once
+        }
+        __syncwarp();
+        if (xline) {
+          const int64_t row = (int64_t)p * plane + (int64_t)yy * nx + xa;
+          double* dst = reinterpret_cast<double*>(st) + ((size_t)lane * PW + (xa - x0 + 1)) * T;
+          bulk_g2s(dst, X + row * T, (uint32_t)(xb - xa) * T * 8, full + s);
+        }
+        if (vline) {
+          const int64_t row = (int64_t)(p - 1) * plane + (int64_t)vy * nx + x0;
+          double* dst = reinterpret_cast<double*>(st + (size_t)PW * PH * T * 8) + (size_t)vl * bx * VS;
+          bulk_g2s(dst, gp.sv + row * VS, (uint32_t)(ob - x0) * VS * 8, full + s);
+        }
+        if (rline) {
+          const int64_t row = (int64_t)(p - 1) * plane + (int64_t)ry * nx + x0;
+          double* dst = reinterpret_cast<double*>(st + (size_t)PW * PH * T * 8 + (size_t)K::R * VS * 8) + (size_t)rl * bx;
+          bulk_g2s(dst, r + row, (uint32_t)(ob - x0) * 8, full + s);
+        }
+      }
+    }
+  }
+
+  double acc[K::NUT][2], accr[MT][2];  // XᵀY (upper tiles) and Xᵀr (column 0 of an r-tile)
+#pragma unroll
+  for (int uu = 0; uu < K::NUT; ++uu) acc[uu][0] = acc[uu][1] = 0.0;
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi) accr[mi][0] = accr[mi][1] = 0.0;
+  if (warp < NWC) {
+    // ================= consumers
+    const int rw = lane / G, gl = lane % G;
+    const int bxs = 31 - __clz(bx);  // bx is a power of two
+    double* yw = sYw + (size_t)warp * RW * S;
+    int cur = 0;        // stage of the current load step
+    uint32_t ph = 0;    // its full-barrier phase parity
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+      int x0, y0, z0, z1;
+      unit_geom(u, x0, y0, z0, z1);
+      for (int p = z0 - 1; p <= z1; ++p) {
+        mbar_wait(full + cur, ph);
+        const int sm1 = cur == 0 ? NS - 1 : cur - 1, sm2 = sm1 == 0 ? NS - 1 : sm1 - 1;
+        const int q = p - 1;  // output plane of this step
+        if (q >= z0) {
+          const double* Pm = reinterpret_cast<const double*>(smraw + (size_t)sm2 * SB);
+          const double* P0 = reinterpret_cast<const double*>(smraw + (size_t)sm1 * SB);
+          const double* Pp = reinterpret_cast<const double*>(smraw + (size_t)cur * SB);
+          const double* Vs = reinterpret_cast<const double*>(smraw + (size_t)cur * SB + (size_t)PW * PH * T * 8);
+          const double* Rs = Vs + K::R * VS;
+          const int64_t qrow = (int64_t)q * plane + (int64_t)y0 * nx + x0;  // global row of block point (0,0)
+#pragma unroll
+          for (int uu = 0; uu < K::UPW; ++uu) {
+            const int r0u = (warp + uu * NWC) * RW;  // first row of the unit in the plane-block
+            const int ir = r0u + rw;
+            const int ix = ir & (bx - 1), iy = ir >> bxs;
+            const bool ok = x0 + ix < nx && y0 + iy < ny;
+            const int64_t grow = qrow + (int64_t)iy * nx + ix;
+            const int cen = (iy + hy) * PW + ix + 1;
+            double vr = 0.0;
+            if (r != nullptr && ok) vr = rbulk ? Rs[ir] : __ldg(r + grow);
+            double a[VS];
+#pragma unroll
+            for (int k = 0; k < VS; k += 2) {
+              const double2 av = ok ? *reinterpret_cast<const double2*>(Vs + ir * VS + k) : make_double2(0, 0);
+              a[k] = av.x;
+              a[k + 1] = av.y;
+            }
+            // stencil slots in ascending column order
+            const double* src[W];
+            if constexpr (W == 7) {
+              src[0] = Pm + cen * T;
+              src[1] = P0 + (cen - PW) * T;
+              src[2] = P0 + (cen - 1) * T;
+              src[3] = P0 + cen * T;
+              src[4] = P0 + (cen + 1) * T;
+              src[5] = P0 + (cen + PW) * T;
+              src[6] = Pp + cen * T;
+            } else {
+              src[0] = Pm + cen * T;
+              src[1] = P0 + (cen - 1) * T;
+              src[2] = P0 + cen * T;
+              src[3] = P0 + (cen + 1) * T;
+              src[4] = Pp + cen * T;
+            }
+#pragma unroll
+            for (int c2 = 0; c2 < C / 2; ++c2) {
+              double2 xv[W];
+#pragma unroll
+              for (int k = 0; k < W; ++k) xv[k] = *reinterpret_cast<const double2*>(src[k] + gl * C + 2 * c2);
+              double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+              for (int k = 0; k < W; ++k) {
+                y.x = __fma_rn(a[k], xv[k].x, y.x);
+                y.y = __fma_rn(a[k], xv[k].y, y.y);
+              }
+              if (!ok) y = make_double2(0.0, 0.0);
+              else reinterpret_cast<double2*>(Y)[grow * H + (gl * C) / 2 + c2] = y;
+              *reinterpret_cast<double2*>(yw + rw * S + gl * C + 2 * c2) = y;
+            }
+            __syncwarp();
+            // ---- Gram over the unit's RW rows on DMMA: A = own X rows (plane q), B = [Y rows | r]
+#pragma unroll
+            for (int ks = 0; ks < RW / 4; ++ks) {
+              const int rq = ks * 4 + q4, irq = r0u + rq, ixq = irq & (bx - 1), iyq = irq >> bxs;
+              const bool okq = x0 + ixq < nx && y0 + iyq < ny;
+              const double* xo = P0 + ((iyq + hy) * PW + ixq + 1) * T;
+              double xa[MT], yb[MT];
+#pragma unroll
+              for (int i = 0; i < MT; ++i) {
+                xa[i] = okq ? xo[i * 8 + g] : 0.0;
+                yb[i] = yw[rq * S + i * 8 + g];
+              }
+              int ut = 0;
+#pragma unroll
+              for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+                for (int ni = mi; ni < MT; ++ni, ++ut) dmma(acc[ut][0], acc[ut][1], xa[mi], yb[ni]);
+              if (r != nullptr) {
+                const double rv = __shfl_sync(0xffffffffu, vr, rq * G);  // lane rq·G holds row rq's r
+                const double br = g == 0 ? rv : 0.0;                     // r as column 0 of a tile
+#pragma unroll
+                for (int mi = 0; mi < MT; ++mi) dmma(accr[mi][0], accr[mi][1], xa[mi], br);
+              }
+            }
+            __syncwarp();
+          }
+          if (lane == 0) mbar_arrive(empty + sm2);  // plane q−1 is no longer needed
+        }
+        if (p == z1 && lane == 0) {  // end of the unit: release the last two planes
+          mbar_arrive(empty + sm1);
+          mbar_arrive(empty + cur);
+        }
+        if (++cur == NS) {
+          cur = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  }
+  // ================= epilogue (as k_spmm_seg): consumer warps' partials in warp order, lower half mirrored
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(smraw);
+  constexpr int PER = T * T + T;
+  for (int w = 0; w < NWC; ++w) {
+    if (warp == w) {
+      int ut = 0;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = mi; ni < MT; ++ni, ++ut) {
+          double* d = red + (mi * 8 + g) * T + ni * 8 + 2 * q4;
+          d[0] = w == 0 ? acc[ut][0] : d[0] + acc[ut][0];
+          d[1] = w == 0 ? acc[ut][1] : d[1] + acc[ut][1];
+        }
+      if (q4 == 0)
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) {
+          double* d = red + T * T + mi * 8 + g;
+          *d = w == 0 ? accr[mi][0] : *d + accr[mi][0];
+        }
+    }
+    __syncthreads();
+  }
+  double* out = part + (size_t)blockIdx.x * PER;
+  for (int e = tid; e < T * T; e += K::NTH) {
+    const int rI = e / T, cI = e % T;
+    out[e] = (rI / 8 <= cI / 8) ? red[e] : red[cI * T + rI];
+  }
+  for (int e = tid; e < T; e += K::NTH) out[T * T + e] = red[T * T + e];
+  if (tl.cnt != nullptr) {
+    const bool last = tail_reduce(part, PER, tl);
+    if constexpr (T <= 16) {
+      if (last && ch.on && warp == 0)
+        chol_warp<T>(tl.out, r != nullptr ? tl.out + T * T : nullptr, ch.R, ch.Rinv, ch.alpha, ch.flag, ch.gblock);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+template <int T>
+static void grid_shape(const GridPlan& gp, int& bx, int& by, int& zc, int sms) {
+  using K = GrCfg<T>;
+  by = gp.ny > 1 ? 4 : 1;
+  bx = K::R / by;
+  const int64_t blocks = (int64_t)((gp.nx + bx - 1) / bx) * ((gp.ny + by - 1) / by);
+  // z chunks so that every SM gets ≥ ~4 units (each chunk re-reads 2 halo planes)
+  int64_t want = 4 * (int64_t)sms;
+  int64_t nzc = (want + blocks - 1) / blocks;
+  if (nzc < 1) nzc = 1;
+  zc = (int)((gp.nz + nzc - 1) / nzc);
+  if (zc < 8) zc = gp.nz < 8 ? gp.nz : 8;
+}
+
+template <int T, int W>
+static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, double* Y, const double* r,
+                          double* part, int nblk, const Tail& tl, const CholArgs& ch) {
+  using K = GrCfg<T>;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int bx, by, zc;
+  grid_shape<T>(gp, bx, by, zc, sms);
+  const int hy = gp.ny > 1 ? 1 : 0, vs = (W + 1) & ~1;
+  const size_t SB = grid_stage_bytes<T>(bx, by, hy, vs);
+  const size_t fixed = (size_t)K::NWC * K::RW * K::S * 8 + 16 * 8 + 128;
+  int ns = (int)((220 * 1024 - fixed) / SB);
+  if (ns > 8) ns = 8;
+  if (ns < 4) return cudaErrorInvalidConfiguration;
+  size_t sm = (size_t)ns * SB + fixed;
+  if (sm < (size_t)(T * T + T) * 8) sm = (size_t)(T * T + T) * 8;
+  cudaFuncSetAttribute(k_spmm_grid<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  nblk = nblk < sms ? nblk : sms;  // one persistent CTA per SM
+  return launch_k(k_spmm_grid<T, W>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns);
+}
+
+bool spmm_grid_fits(int t, const GridPlan& gp) {
+  if (gp.sv == nullptr || (gp.w != 5 && gp.w != 7)) return false;
+  int bx = 0, by = 0, zc = 0;
+  switch (t) {
+    case 8: grid_shape<8>(gp, bx, by, zc, 148); break;
+    case 16: grid_shape<16>(gp, bx, by, zc, 148); break;
+    case 32: grid_shape<32>(gp, bx, by, zc, 148); break;
+    case 64: grid_shape<64>(gp, bx, by, zc, 148); break;
+    default: return false;
+  }
+  const int hy = gp.ny > 1 ? 1 : 0;
+  const size_t SB = (size_t)(bx + 2) * (by + 2 * hy) * t * 8 + (size_t)(2048 / t) * ((gp.w + 1) & ~1) * 8 + 128;
+  return 4 * SB + 16 * 1024 < 220 * 1024;
+}
+
+cudaError_t launch_spmm_grid(cudaStream_t st, int t, const GridPlan& gp, const double* X, double* Y, const double* r,
+                             double* part, int nblk, const Tail& tl, const CholArgs& ch) {
+  if (ch.on && !(t == 8 || t == 16)) return cudaErrorInvalidValue;
+#define EKS_GRID_W(TT)                                                                  \
+  return gp.w == 7 ? grid_t<TT, 7>(st, gp, X, Y, r, part, nblk, tl, ch)                 \
+                   : grid_t<TT, 5>(st, gp, X, Y, r, part, nblk, tl, ch);
+  switch (t) {
+    case 8: EKS_GRID_W(8)
+    case 16: EKS_GRID_W(16)
+    case 32: EKS_GRID_W(32)
+    case 64: EKS_GRID_W(64)
+    default: return cudaErrorInvalidValue;
+  }
+#undef EKS_GRID_W
+}
+
+}  // namespace eks

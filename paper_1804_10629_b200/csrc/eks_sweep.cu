@@ -23,8 +23,6 @@ namespace eks {
 
 namespace {
 
-__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
 // 16-byte async copy global → shared; src_bytes = 0 zero-fills the destination.
 __device__ __forceinline__ void cp16(void* dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr(dst)), "l"(src), "r"(src_bytes)
@@ -34,14 +32,6 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// D(8×8) += A(8×4, row) · B(4×8, col): lane (g = lane>>2, q = lane&3) holds
-// a = A[g][q], b = B[q][g], d = {D[g][2q], D[g][2q+1]}.
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
 }
 
 // Bulk prefetch of [p, p+bytes) into L2 (address and size rounded to 16 bytes).
@@ -841,30 +831,6 @@ __global__ void __launch_bounds__(256, MINB)
 // = y), bitwise equal to the oracle (R20); the Gram/α̃ epilogue is the same as
 // the other SpMM+Gram kernels.
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      " .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n"
-      "}\n" ::"r"(saddr(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   saddr(dst)),
-               "l"(src), "r"(bytes), "r"(saddr(b))
-               : "memory");
-}
-
 template <int T>
 struct SsCfg {
   static constexpr int NWC = T <= 16 ? 16 : 8, NTH = 32 * (NWC + 1);  // consumer warps + 1 producer warp
@@ -897,10 +863,6 @@ __host__ __device__ constexpr size_t seg_fixed_bytes() {
   return (size_t)K::NWC * K::RW * K::S * 8 + 16 * 8 + 128;  // per-warp Y scratch, mbarriers, slack
 }
 constexpr size_t kSegSmem = 220 * 1024;
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
-}
 
 template <int T, int W>
 __global__ void __launch_bounds__(SsCfg<T>::NTH, 1)

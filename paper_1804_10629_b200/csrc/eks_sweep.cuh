@@ -62,6 +62,17 @@ struct SegPlan {
 bool spmm_seg_fits(int t, int w, int cap);
 cudaError_t launch_spmm_seg(cudaStream_t st, int t, int64_t n, const SegPlan& pl, int w, const double* Xext,
                             double* Y, const double* r, double* part, int nblk, const Tail& tl, const CholArgs& ch);
+// Stencil-structured A (eks_grid.cu): nx × ny × nz lexicographic grid (2D: ny = 1, "planes" are
+// x-lines), every entry at offset 0, ±1, ±nx (3D), ±nx·ny inside the grid; sv holds per row the
+// w = 7 (3D) or 5 (2D) stencil values in ascending column order, 0 in absent slots, padded to
+// (w+1)&~1 doubles per row.  Single rank only.
+struct GridPlan {
+  int nx = 0, ny = 0, nz = 0, w = 0;
+  const double* sv = nullptr;
+};
+bool spmm_grid_fits(int t, const GridPlan& gp);
+cudaError_t launch_spmm_grid(cudaStream_t st, int t, const GridPlan& gp, const double* X, double* Y, const double* r,
+                             double* part, int nblk, const Tail& tl, const CholArgs& ch);
 // maxrow = longest CSR row (selects the register-resident fast path; longer rows still work).
 cudaError_t launch_spmm_gram(cudaStream_t st, int t, int64_t n, const int* rp, const int* col, const double* val,
                              int maxrow, const double* Xext, int64_t xoff, double* Y, const double* r, double* part,
