@@ -33,7 +33,9 @@ struct GrCfg {
   static constexpr int R = 2048 / T;                   // output rows per plane-block (bx·by)
   static constexpr int RW = T == 8 ? 8 : 4;            // rows per warp unit (DMMA k = 4 rows)
   static constexpr int G = 32 / RW;                    // threads per row
-  static constexpr int C = T / G;                      // columns per thread
+  static constexpr int C = T / G;                      // columns per thread: pairs 2(gl + G·c2), c2 < C/2
+                                                       // (the G lanes of a row read 16·G contiguous bytes
+                                                       // per instruction: conflict-free shared loads)
   static constexpr int U = R / RW;                     // units per plane-block
   static constexpr int UPW = U / NWC;                  // units per consumer warp per plane
   static constexpr int S = T + 4;                      // Y scratch row stride
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
             for (int c2 = 0; c2 < C / 2; ++c2) {
               double2 xv[W];
 #pragma unroll
-              for (int k = 0; k < W; ++k) xv[k] = *reinterpret_cast<const double2*>(src[k] + gl * C + 2 * c2);
+              for (int k = 0; k < W; ++k) xv[k] = *reinterpret_cast<const double2*>(src[k] + 2 * (gl + G * c2));
               double2 y = make_double2(0.0, 0.0);
 #pragma unroll
               for (int k = 0; k < W; ++k) {
@@ -223,8 +225,8 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
                 y.y = __fma_rn(a[k], xv[k].y, y.y);
               }
               if (!ok) y = make_double2(0.0, 0.0);
-              else reinterpret_cast<double2*>(Y)[grow * H + (gl * C) / 2 + c2] = y;
-              *reinterpret_cast<double2*>(yw + rw * S + gl * C + 2 * c2) = y;
+              else reinterpret_cast<double2*>(Y)[grow * H + gl + G * c2] = y;
+              *reinterpret_cast<double2*>(yw + rw * S + 2 * (gl + G * c2)) = y;
             }
             __syncwarp();
             // ---- Gram over the unit's RW rows on DMMA: A = own X rows (plane q), B = [Y rows | r]
