@@ -77,7 +77,7 @@ struct eks_ctx {
   bool grid_ok = false;
   eks::GridPlan gplan{};
   double* d_sv = nullptr;
-  int chol_mode = 0;               // 0 separate one-warp Cholesky launch, 1 in the SpMM+Gram tail (EKS_CHOL)
+  int chol_mode = 0;               // 0 one-warp Cholesky launch (default), 1 in the SpMM kernel's tail (EKS_CHOL)
   // workspace, keyed by t
   int ws_t = 0;
   std::vector<Block> Wpool, AWpool;  // Wpool ext layout, AWpool local
@@ -464,13 +464,16 @@ eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const doubl
   account(ctx, EKS_K_SPMM, 12.0 * ctx->nnz + 4.0 * (ctx->n + 1) + 16.0 * ctx->n * t, 2.0 * ctx->nnz * t);
   account(ctx, EKS_K_COEF, r ? 8.0 * ctx->n : 0.0, 2.0 * ctx->n * t * (t + 1));  // epilogue: only r is extra traffic
   eks::CholArgs c{};
-  if (ch && eks::spmm_gram_fused_chol(t)) {
+  const int path = spmm_path_for(ctx, t);
+  // EKS_CHOL=1: the SpMM kernel's last CTA factors B (measured slower than the separate one-warp
+  // launch the solve uses by default: 1894 vs 2085 outer it/s on cfg2)
+  if (ch && ctx->chol_mode == 1 &&
+      ((path == 4 && eks::spmm_grid_fused_chol(t)) || (path != 4 && eks::spmm_gram_fused_chol(t)))) {
     c = *ch;
     c.on = 1;
   }
   {
     KScope k(ctx, EKS_K_SPMM);
-    const int path = spmm_path_for(ctx, t);
     if (path == 4)
       CK(eks::launch_spmm_grid(ctx->stream, t, ctx->gplan, X.base, Y, r, ctx->part, ctx->nblk,
                                tail(ctx, 2, out, stride), c));
@@ -618,8 +621,7 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
   ch.gblock = gb;
   // t ≤ 32: the R⁻¹ kernel factors the Gram itself (every CTA, identical inputs on every rank);
   // otherwise the last CTA of the SpMM+Gram kernel or a separate Cholesky launch does it.
-  ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg,
-               ctx->chol_mode == 1 ? &ch : nullptr));
+  ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg, &ch));
   if (!ctx->chol_fused) {  // default: one-warp Cholesky launch (rsqrt pivots for t ≤ 32)
     KScope k(ctx, EKS_K_CHOL);
     CK(eks::launch_chol_fast(ctx->stream, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,

@@ -274,6 +274,30 @@ __device__ __forceinline__ bool chol_warp_fast(const double* B, double (&a)[T], 
   return fail;
 }
 
+// chol_warp_fast with the outputs of launch_chol_fast (R, R⁻¹, α̃ = R⁻ᵀg, breakdown flag).
+template <int T>
+__device__ __forceinline__ void chol_warp_fast_out(const double* B, const double* g, double* Rout, double* Rinv,
+                                                   double* alpha, int* flag, int gblock) {
+  const int j = threadIdx.x & 31;
+  double a[T], y[T];
+  const bool fail = chol_warp_fast<T>(B, a, y);
+  if (j < T) {
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      if (Rout) Rout[i * T + j] = (i <= j) ? a[i] : 0.0;
+      Rinv[i * T + j] = y[i];
+    }
+    if (g != nullptr && alpha != nullptr) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < T; ++i)
+        if (i <= j) s = __fma_rn(y[i], __ldcg(g + i), s);
+      alpha[j] = s;
+    }
+  }
+  if (fail && j == 0 && flag) atomicMin(flag, gblock);
+}
+
 template <int T>
 __device__ __forceinline__ void chol_warp(const double* B, const double* g, double* Rout, double* Rinv,
                                           double* alpha, int* flag, int gblock) {

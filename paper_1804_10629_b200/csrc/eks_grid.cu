@@ -300,9 +300,10 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
   for (int e = tid; e < T; e += K::NTH) out[T * T + e] = red[T * T + e];
   if (tl.cnt != nullptr) {
     const bool last = tail_reduce(part, PER, tl);
-    if constexpr (T <= 16) {
+    if constexpr (T <= 32) {  // the block's Cholesky by the last CTA (solve path: rsqrt pivots)
       if (last && ch.on && warp == 0)
-        chol_warp<T>(tl.out, r != nullptr ? tl.out + T * T : nullptr, ch.R, ch.Rinv, ch.alpha, ch.flag, ch.gblock);
+        chol_warp_fast_out<T>(tl.out, r != nullptr ? tl.out + T * T : nullptr, ch.R, ch.Rinv, ch.alpha, ch.flag,
+                              ch.gblock);
     }
   }
 }
@@ -349,6 +350,8 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
   return launch_k(k_spmm_grid<T, W>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns);
 }
 
+bool spmm_grid_fused_chol(int t) { return t == 8 || t == 16 || t == 32; }
+
 bool spmm_grid_fits(int t, const GridPlan& gp) {
   if (gp.sv == nullptr || (gp.w != 5 && gp.w != 7)) return false;
   int bx = 0, by = 0, zc = 0;
@@ -366,7 +369,7 @@ bool spmm_grid_fits(int t, const GridPlan& gp) {
 
 cudaError_t launch_spmm_grid(cudaStream_t st, int t, const GridPlan& gp, const double* X, double* Y, const double* r,
                              double* part, int nblk, const Tail& tl, const CholArgs& ch) {
-  if (ch.on && !(t == 8 || t == 16)) return cudaErrorInvalidValue;
+  if (ch.on && !spmm_grid_fused_chol(t)) return cudaErrorInvalidValue;
 #define EKS_GRID_W(TT)                                                                  \
   return gp.w == 7 ? grid_t<TT, 7>(st, gp, X, Y, r, part, nblk, tl, ch)                 \
                    : grid_t<TT, 5>(st, gp, X, Y, r, part, nblk, tl, ch);

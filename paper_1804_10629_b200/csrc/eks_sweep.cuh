@@ -71,6 +71,7 @@ struct GridPlan {
   const double* sv = nullptr;
 };
 bool spmm_grid_fits(int t, const GridPlan& gp);
+bool spmm_grid_fused_chol(int t);  // ch.on allowed: the last CTA runs the solve-path Cholesky
 cudaError_t launch_spmm_grid(cudaStream_t st, int t, const GridPlan& gp, const double* X, double* Y, const double* r,
                              double* part, int nblk, const Tail& tl, const CholArgs& ch);
 // maxrow = longest CSR row (selects the register-resident fast path; longer rows still work).
