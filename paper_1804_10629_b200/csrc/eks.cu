@@ -440,7 +440,7 @@ eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, cons
 // forces one for A/B measurements.
 int spmm_path_for(const eks_ctx* ctx, int t) {
   const bool grid = ctx->grid_ok && ctx->nranks == 1 && eks::spmm_grid_fits(t, ctx->gplan);
-  if (grid && (ctx->spmm_path == 4 || (ctx->spmm_path == 0 && t <= 32))) return 4;
+  if (grid && (ctx->spmm_path == 4 || ctx->spmm_path == 0)) return 4;
   const bool seg = ctx->seg_ok && eks::spmm_seg_fits(t, ctx->ell_w, ctx->seg.cap);
   if (seg && (ctx->spmm_path == 3 || (ctx->spmm_path == 0 && t == 64))) return 0;
   if (ctx->ell_w && ctx->spmm_path <= 1) return 1;

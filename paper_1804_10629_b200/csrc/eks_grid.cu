@@ -41,7 +41,13 @@ struct GrCfg {
   static constexpr int S = T + 4;                      // Y scratch row stride
   static constexpr int MT = T / 8;
   static constexpr int NUT = MT * (MT + 1) / 2;        // upper 8×8 output tiles
+  // t = 64: the 36 upper tiles (+ 8 Xᵀr tiles) are dealt to the warps and accumulated over the
+  // whole plane-block from a CTA-level Y tile (double-buffered, one consumer barrier per plane)
+  static constexpr bool CG = T >= 64;
+  static constexpr int JOBS = NUT + MT;                // Gram tiles + r tiles
+  static constexpr int JPW = CG ? (JOBS + NWC - 1) / NWC : 1;
   static_assert(U % NWC == 0, "units");
+  static_assert(!CG || UPW == 1, "CTA-level Gram: one unit per warp, the warps' scratches form the Y tile");
 };
 
 }  // namespace
@@ -69,8 +75,8 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
   const int PW = bx + 2, PH = by + 2 * hy;     // plane-block extent
   const int64_t plane = (int64_t)nx * ny;
   const size_t SB = grid_stage_bytes<T>(bx, by, hy, VS);
-  double* sYw = reinterpret_cast<double*>(smraw + (size_t)NS * SB);  // [NWC][RW][S]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sYw + NWC * RW * S);
+  double* sYw = reinterpret_cast<double*>(smraw + (size_t)NS * SB);  // [2 (CG)][NWC][RW][S]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sYw + (K::CG ? 2 : 1) * NWC * RW * S);
   uint64_t* empty = full + 8;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q4 = lane & 3;
@@ -153,16 +159,37 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
     }
   }
 
-  double acc[K::NUT][2], accr[MT][2];  // XᵀY (upper tiles) and Xᵀr (column 0 of an r-tile)
+  constexpr int NACC = K::CG ? 1 : K::NUT, NACR = K::CG ? 1 : MT;
+  double acc[NACC][2], accr[NACR][2];  // XᵀY (upper tiles) and Xᵀr (column 0 of an r-tile)
+  double accj[K::JPW][2];               // CG: this warp's Gram / r tiles over the whole block
 #pragma unroll
-  for (int uu = 0; uu < K::NUT; ++uu) acc[uu][0] = acc[uu][1] = 0.0;
+  for (int uu = 0; uu < NACC; ++uu) acc[uu][0] = acc[uu][1] = 0.0;
 #pragma unroll
-  for (int mi = 0; mi < MT; ++mi) accr[mi][0] = accr[mi][1] = 0.0;
+  for (int mi = 0; mi < NACR; ++mi) accr[mi][0] = accr[mi][1] = 0.0;
+#pragma unroll
+  for (int jj = 0; jj < K::JPW; ++jj) accj[jj][0] = accj[jj][1] = 0.0;
+  int ybuf = 0;  // CG: Y tile buffer of this plane
+  // CG: this warp's jobs, decoded once — job < NUT: upper tile (mi, ni); else the r tile of row block mi
+  int jmi[K::JPW], jni[K::JPW];
+#pragma unroll
+  for (int jj = 0; jj < K::JPW; ++jj) {
+    const int job = warp + jj * NWC;
+    jmi[jj] = -1;
+    jni[jj] = -1;
+    if (job < K::NUT) {
+      int mi = 0, rem = job;
+      while (rem >= MT - mi) { rem -= MT - mi; ++mi; }
+      jmi[jj] = mi;
+      jni[jj] = mi + rem;
+    } else if (job < K::JOBS) {
+      jmi[jj] = job - K::NUT;
+    }
+  }
   if (warp < NWC) {
     // ================= consumers
     const int rw = lane / G, gl = lane % G;
     const int bxs = 31 - __clz(bx);  // bx is a power of two
-    double* yw = sYw + (size_t)warp * RW * S;
+    double* yw0 = sYw + (size_t)warp * RW * S;
     int cur = 0;        // stage of the current load step
     uint32_t ph = 0;    // its full-barrier phase parity
     for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -179,6 +206,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
           const double* Vs = reinterpret_cast<const double*>(smraw + (size_t)cur * SB + (size_t)PW * PH * T * 8);
           const double* Rs = Vs + K::R * VS;
           const int64_t qrow = (int64_t)q * plane + (int64_t)y0 * nx + x0;  // global row of block point (0,0)
+          double* yw = yw0 + (K::CG ? ybuf * NWC * RW * S : 0);
 #pragma unroll
           for (int uu = 0; uu < K::UPW; ++uu) {
             const int r0u = (warp + uu * NWC) * RW;  // first row of the unit in the plane-block
@@ -230,8 +258,9 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
             }
             __syncwarp();
             // ---- Gram over the unit's RW rows on DMMA: A = own X rows (plane q), B = [Y rows | r]
+            // (t = 64: over the whole block below instead)
 #pragma unroll
-            for (int ks = 0; ks < RW / 4; ++ks) {
+            for (int ks = 0; ks < (K::CG ? 0 : RW / 4); ++ks) {
               const int rq = ks * 4 + q4, irq = r0u + rq, ixq = irq & (bx - 1), iyq = irq >> bxs;
               const bool okq = x0 + ixq < nx && y0 + iyq < ny;
               const double* xo = P0 + ((iyq + hy) * PW + ixq + 1) * T;
@@ -241,19 +270,43 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
                 xa[i] = okq ? xo[i * 8 + g] : 0.0;
                 yb[i] = yw[rq * S + i * 8 + g];
               }
-              int ut = 0;
+              if constexpr (!K::CG) {
+                int ut = 0;
 #pragma unroll
-              for (int mi = 0; mi < MT; ++mi)
+                for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-                for (int ni = mi; ni < MT; ++ni, ++ut) dmma(acc[ut][0], acc[ut][1], xa[mi], yb[ni]);
-              if (r != nullptr) {
-                const double rv = __shfl_sync(0xffffffffu, vr, rq * G);  // lane rq·G holds row rq's r
-                const double br = g == 0 ? rv : 0.0;                     // r as column 0 of a tile
+                  for (int ni = mi; ni < MT; ++ni, ++ut) dmma(acc[ut][0], acc[ut][1], xa[mi], yb[ni]);
+                if (r != nullptr) {
+                  const double rv = __shfl_sync(0xffffffffu, vr, rq * G);  // lane rq·G holds row rq's r
+                  const double br = g == 0 ? rv : 0.0;                     // r as column 0 of a tile
 #pragma unroll
-                for (int mi = 0; mi < MT; ++mi) dmma(accr[mi][0], accr[mi][1], xa[mi], br);
+                  for (int mi = 0; mi < MT; ++mi) dmma(accr[mi][0], accr[mi][1], xa[mi], br);
+                }
               }
             }
             __syncwarp();
+          }
+          if constexpr (K::CG) {
+            // ---- CTA-level Gram: all consumer warps' Y rows are in the Y tile; each warp
+            // accumulates its tiles over the block's R rows (k-steps of 4 rows)
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * NWC) : "memory");
+            const double* Yt = sYw + ybuf * NWC * RW * S;
+#pragma unroll 2
+            for (int kk = 0; kk < K::R; kk += 4) {  // the warp's jobs interleaved: independent DMMA chains
+              const int irq = kk + q4, ixq = irq & (bx - 1), iyq = irq >> bxs;
+              const bool okq = x0 + ixq < nx && y0 + iyq < ny;
+              const double* xo = P0 + ((iyq + hy) * PW + ixq + 1) * T;
+              const double rr = (g == 0 && okq && r != nullptr)
+                                    ? (rbulk ? Rs[irq] : __ldg(r + qrow + (int64_t)iyq * nx + ixq)) : 0.0;
+#pragma unroll
+              for (int jj = 0; jj < K::JPW; ++jj)
+                if (jmi[jj] >= 0) {
+                  const double xa = okq ? xo[jmi[jj] * 8 + g] : 0.0;
+                  const double bb = jni[jj] >= 0 ? Yt[irq * S + jni[jj] * 8 + g] : rr;
+                  dmma(accj[jj][0], accj[jj][1], xa, bb);
+                }
+            }
+            ybuf ^= 1;
           }
           if (lane == 0) mbar_arrive(empty + sm2);  // plane q−1 is no longer needed
         }
@@ -272,7 +325,28 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
   __syncthreads();
   double* red = reinterpret_cast<double*>(smraw);
   constexpr int PER = T * T + T;
-  for (int w = 0; w < NWC; ++w) {
+  if constexpr (K::CG) {
+    if (warp < NWC) {
+#pragma unroll
+      for (int jj = 0; jj < K::JPW; ++jj) {
+        const int job = warp + jj * NWC;
+        if (job < K::JOBS) {
+          if (job < K::NUT) {
+            int mi = 0, rem = job;
+            while (rem >= MT - mi) { rem -= MT - mi; ++mi; }
+            const int ni = mi + rem;
+            double* d = red + (mi * 8 + g) * T + ni * 8 + 2 * q4;
+            d[0] = accj[jj][0];
+            d[1] = accj[jj][1];
+          } else if (q4 == 0) {
+            red[T * T + (job - K::NUT) * 8 + g] = accj[jj][0];
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int w = 0; w < (K::CG ? 0 : NWC); ++w) {
     if (warp == w) {
       int ut = 0;
 #pragma unroll
@@ -300,7 +374,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
   for (int e = tid; e < T; e += K::NTH) out[T * T + e] = red[T * T + e];
   if (tl.cnt != nullptr) {
     const bool last = tail_reduce(part, PER, tl);
-    if constexpr (T <= 32) {  // the block's Cholesky by the last CTA (solve path: rsqrt pivots)
+    if constexpr (T <= 16) {  // the block's Cholesky by the last CTA (solve path: rsqrt pivots)
       if (last && ch.on && warp == 0)
         chol_warp_fast_out<T>(tl.out, r != nullptr ? tl.out + T * T : nullptr, ch.R, ch.Rinv, ch.alpha, ch.flag,
                               ch.gblock);
@@ -339,7 +413,7 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
   grid_shape<T>(gp, bx, by, zc, sms);
   const int hy = gp.ny > 1 ? 1 : 0, vs = (W + 1) & ~1;
   const size_t SB = grid_stage_bytes<T>(bx, by, hy, vs);
-  const size_t fixed = (size_t)K::NWC * K::RW * K::S * 8 + 16 * 8 + 128;
+  const size_t fixed = (size_t)(K::CG ? 2 : 1) * K::NWC * K::RW * K::S * 8 + 16 * 8 + 128;
   int ns = (int)((220 * 1024 - fixed) / SB);
   if (ns > 8) ns = 8;
   if (ns < 4) return cudaErrorInvalidConfiguration;
@@ -350,7 +424,7 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
   return launch_k(k_spmm_grid<T, W>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns);
 }
 
-bool spmm_grid_fused_chol(int t) { return t == 8 || t == 16 || t == 32; }
+bool spmm_grid_fused_chol(int t) { return t == 8 || t == 16; }
 
 bool spmm_grid_fits(int t, const GridPlan& gp) {
   if (gp.sv == nullptr || (gp.w != 5 && gp.w != 7)) return false;
