@@ -356,3 +356,46 @@ def test_full_size_solve_prefix_properties(eks, torch_cuda, cfg):
         phis.append(float(0.5 * x.dot(Ax) - b.dot(x)))
     assert phis[2] < phis[1] < phis[0]
     S.close()
+
+
+# ------------------------------------------------------------------ paper Table 2-4 protocol on the GPU
+@pytest.mark.parametrize("key,method", [("sre_cg_t2", "sre-cg"), ("sre_cg2_t2", "sre-cg2"),
+                                        ("msdo_cg_t2", "msdo-cg"), ("sre_cg_t4", "sre-cg")])
+def test_paper_poisson2d_rows_gpu(eks, torch_cuda, oracle_lib, key, method):
+    """Poisson2D (gallery('poisson',100)), b = A·x_rand, tol 1e-6: the GPU's outer-iteration
+    counts equal the oracle's and lie within the paper's printed cells (Tables 2-4, ±15 %: the
+    partition is contiguous, not Metis)."""
+    import json
+    import os
+    paper = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_poisson2d.json")))
+    A = ei.poisson2d(100)
+    b = ei.paper_poisson_rhs(A)
+    t = 4 if key.endswith("t4") else 2
+    S = eks.Solver(A)
+    for s_, want in zip(paper[key]["s"], paper[key]["k"]):
+        rep = S.solve(dev(torch_cuda, b), method, s_, t, paper["tol"])
+        ref = oracle_lib.solve(A, b, method, s=s_, t=t, tol=paper["tol"])
+        assert rep["converged"] and ref["converged"]
+        assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"])), (s_,)
+        assert abs(rep["outer_iters"] - want) <= paper["tolerance_enlarged"] * want, (key, s_, rep["outer_iters"], want)
+    S.close()
+
+
+@pytest.mark.parametrize("method,t", [("sre-cg", 8), ("sre-cg", 16), ("sre-cg", 32), ("sre-cg2", 8),
+                                      ("msdo-cg", 8)])
+def test_paper_poisson2d_large_t_gpu(eks, torch_cuda, oracle_lib, method, t):
+    """The Table 2-4 protocol at the partition counts the DMMA/TMA kernels serve (t ≥ 8), s = 3:
+    GPU and oracle counts agree and x agrees to 1e-6; for SRE-CG k(s=3) = ⌈k(s=1)/3⌉.
+    (Larger t and full-basis t ≥ 16 are left out: the single-thread oracle's cost grows with k·s·t.)"""
+    A = ei.poisson2d(100)
+    b = ei.paper_poisson_rhs(A)
+    S = eks.Solver(A)
+    rep = S.solve(dev(torch_cuda, b), method, 3, t, 1e-6)
+    ref = oracle_lib.solve(A, b, method, s=3, t=t, tol=1e-6)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+    if method == "sre-cg":
+        r1 = S.solve(dev(torch_cuda, b), method, 1, t, 1e-6)
+        assert rep["outer_iters"] == math.ceil(r1["outer_iters"] / 3)
+    S.close()
