@@ -69,6 +69,9 @@ def lib():
         _lib.or_solve.restype = i32
         _lib.or_basis_sweep.argtypes = [C.POINTER(_Csr), i32, vp, i32, vp]
         _lib.or_basis_sweep.restype = i32
+        _lib.or_solve_ca.argtypes = [C.POINTER(_Csr), vp, vp, i32, i32, i32, i32, d, i32,
+                                     C.POINTER(_Report), ITER_CB, vp]
+        _lib.or_solve_ca.restype = i32
     return _lib
 
 
@@ -168,6 +171,31 @@ def solve(A, b, method="sre-cg", s=1, t=1, tol=1e-8, kmax=5000, x0=None, mode=MO
         cb = ITER_CB(_cb)
     m = METHODS[method] if isinstance(method, str) else int(method)
     st = lib().or_solve(C.byref(ref.s), _p(b), _p(x), m, s, t, tol, kmax, mode, C.byref(rep), cb, None)
+    k = rep.outer_iters
+    return dict(x=x, outer_iters=k, converged=bool(rep.converged), status=st, rho0=rep.rho0,
+                rho=rep.rho, true_relres=rep.true_relres, hist=hist[: k + 1].copy(),
+                breakdown_block=rep.breakdown_block)
+
+
+def solve_ca(A, b, method="sre-cg", arnoldi=7, s=1, t=1, tol=1e-8, kmax=5000, x0=None, callback=None):
+    """Run or_solve_ca (CA SRE-CG / CA SRE-CG2 / CA MSDO-CG with Alg 5 or Alg 7); same dict as solve()."""
+    b = _f64(b)
+    x = np.zeros(A.n) if x0 is None else _f64(x0).copy()
+    hist = np.zeros(kmax + 1)
+    rep = _Report(0, 0, 0, -1, 0.0, 0.0, 0.0, hist.ctypes.data)
+    ref = _CsrRef(A)
+    if callback is None:
+        cb = ITER_CB()
+    else:
+        def _cb(user, k, n, st, V, alpha, xx, rr, rho):
+            callback(k,
+                     np.ctypeslib.as_array(V, shape=(n, st)).copy(),
+                     np.ctypeslib.as_array(alpha, shape=(st,)).copy(),
+                     np.ctypeslib.as_array(xx, shape=(n,)).copy(),
+                     np.ctypeslib.as_array(rr, shape=(n,)).copy(), rho)
+        cb = ITER_CB(_cb)
+    m = METHODS[method] if isinstance(method, str) else int(method)
+    st = lib().or_solve_ca(C.byref(ref.s), _p(b), _p(x), m, int(arnoldi), s, t, tol, kmax, C.byref(rep), cb, None)
     k = rep.outer_iters
     return dict(x=x, outer_iters=k, converged=bool(rep.converged), status=st, rho0=rep.rho0,
                 rho=rep.rho, true_relres=rep.true_relres, hist=hist[: k + 1].copy(),

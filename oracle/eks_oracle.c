@@ -410,3 +410,136 @@ int or_basis_sweep(const or_csr* A, int t, const double* X0, int nblocks, double
   free(R);
   return status;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Communication-avoiding variants                      */
+/* ------------------------------------------------------------------------ */
+/* CGS2 of the wide block V (n × zc) against nq blocks Q_j (n × t) — "A-orthonormalize V
+ * against Q" of Alg 5 line 8 / Alg 7 line 9: twice
+ * { AV = A·V ; C_j = Q_jᵀ AV (t × zc) ; V = V − Σ_j Q_j C_j }, the arithmetic of or_cgs2
+ * column by column (for zc = t it is or_cgs2 itself). */
+static void cgs2_wide(const or_csr* A, int t, int zc, int nq, const double* const* Q, double* V) {
+  int64_t n = A->n;
+  double* AV = dalloc((size_t)n * zc);
+  double* C = dalloc((size_t)nq * t * zc);
+  for (int pass = 0; pass < 2; ++pass) {
+    or_spmm(A, zc, V, AV);
+    for (int j = 0; j < nq; ++j) or_xty(n, t, Q[j], zc, AV, C + (size_t)j * t * zc);
+    for (int64_t row = 0; row < n; ++row)
+      for (int c = 0; c < zc; ++c) {
+        double acc = 0.0;
+        for (int j = 0; j < nq; ++j)
+          for (int a = 0; a < t; ++a) acc += Q[j][row * t + a] * C[((size_t)j * t + a) * zc + c];
+        V[row * zc + c] -= acc;
+      }
+  }
+  free(AV);
+  free(C);
+}
+
+/* Alg 5 / Alg 7 basis of one outer iteration into V (n × st), then the update of
+ * Alg 3/4/6 lines "α̃ = Vᵀr_{k-1}; x_k = x_{k-1} + Vα̃; r_k = r_{k-1} − AVα̃".
+ *   Alg 5: W_j = T(r_{k-1}) or A·W_{j-1};  V = [W_j, A W_j, …, A^{s-1} W_j];
+ *                      A-orthonormalize V against Q (k > 1), then V itself.
+ *   Alg 7: as Alg 5 but W_j is first A-orthonormalized against Q and itself.
+ * Window Q: CA SRE-CG the last (s+1)t vectors (Alg 5 input m = (s+1)t); CA SRE-CG2 and
+ * CA MSDO-CG all previous vectors (m = kst).  CA MSDO-CG seeds every iteration with
+ * T(r_{k-1}) ("W_j = W_{j-1}"). */
+int or_solve_ca(const or_csr* A, const double* b, double* x, int method, int arnoldi, int s, int t,
+                double eps, int kmax, or_report* rep, or_iter_cb cb, void* user) {
+  int64_t n = A->n;
+  if (s < 1 || t < 1 || (int64_t)s * t > n || !(eps >= 0.0) || method < 0 || method > 2 ||
+      (arnoldi != 5 && arnoldi != 7))
+    return OR_BADARG;
+  const int st = s * t;
+  const size_t blk = (size_t)n * t, big = (size_t)n * st;
+  double* r = dalloc((size_t)n);
+  double* tmp = dalloc((size_t)n);
+  double* u = dalloc((size_t)n);
+  or_spmm(A, 1, x, tmp);
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - tmp[i];
+  double rho0 = norm2(n, r), rho = rho0;
+  if (rep) {
+    rep->rho0 = rho0;
+    rep->breakdown_block = -1;
+    if (rep->rho_history) rep->rho_history[0] = rho0;
+  }
+  blist Q = {0, 0, NULL, NULL};
+  double* W = dalloc(blk);
+  double* W1 = dalloc(blk);
+  double* V = dalloc(big);
+  double* Vo = dalloc(big);
+  double* Rt = dalloc((size_t)t * t);
+  double* Rs = dalloc((size_t)st * st);
+  double* alpha = dalloc((size_t)st);
+  double* pw = dalloc(blk);
+  double* nw = dalloc(blk);
+  int status = OR_OK, k = 1;
+  while (rho > eps * rho0 && k < kmax) {
+    /* window: the last (s+1) blocks (CA SRE-CG) or all blocks */
+    int w0 = (method == OR_SRE_CG && Q.count > s + 1) ? Q.count - (s + 1) : 0, nq = Q.count - w0;
+    if (method == OR_MSDO_CG || k == 1) or_split(n, t, r, W);
+    else or_spmm(A, t, Q.W[Q.count - 1], W);
+    if (arnoldi == 7) {  /* Alg 7 lines 1-4 */
+      if (nq > 0) or_cgs2(A, t, nq, (const double* const*)(Q.W + w0), W, NULL, NULL);
+      if (or_acholqr(A, t, W, W1, Rt, NULL) != OR_OK) { status = OR_BREAKDOWN; break; }
+      memcpy(W, W1, sizeof(double) * blk);
+    }
+    /* V = [W, A W, …, A^{s-1} W] (Alg 5 lines 1-7 / Alg 7 lines 5-8) */
+    memcpy(pw, W, sizeof(double) * blk);
+    for (int i = 0; i < s; ++i) {
+      if (i > 0) {
+        or_spmm(A, t, pw, nw);
+        memcpy(pw, nw, sizeof(double) * blk);
+      }
+      for (int64_t row = 0; row < n; ++row)
+        for (int c = 0; c < t; ++c) V[row * st + i * t + c] = pw[row * t + c];
+    }
+    if (nq > 0) cgs2_wide(A, t, st, nq, (const double* const*)(Q.W + w0), V);
+    if (or_acholqr(A, st, V, Vo, Rs, NULL) != OR_OK) { status = OR_BREAKDOWN; break; }
+    /* α̃ = Vᵀ r_{k-1}; u = V α̃; x += u; r −= A u  (reading R9) */
+    or_xty(n, st, Vo, 1, r, alpha);
+    for (int64_t row = 0; row < n; ++row) {
+      double acc = 0.0;
+      for (int c = 0; c < st; ++c) acc += Vo[row * st + c] * alpha[c];
+      u[row] = acc;
+    }
+    or_spmm(A, 1, u, tmp);
+    for (int64_t row = 0; row < n; ++row) { x[row] += u[row]; r[row] -= tmp[row]; }
+    rho = norm2(n, r);
+    for (int i = 0; i < s; ++i) {  /* the s new blocks join Q */
+      double* Wb = dalloc(blk);
+      for (int64_t row = 0; row < n; ++row)
+        for (int c = 0; c < t; ++c) Wb[row * t + c] = Vo[row * st + i * t + c];
+      bl_push(&Q, Wb, dalloc(1));
+    }
+    if (method == OR_SRE_CG)
+      while (Q.count > s + 1) {
+        free(Q.W[0]);
+        free(Q.AW[0]);
+        memmove(Q.W, Q.W + 1, sizeof(double*) * (size_t)(Q.count - 1));
+        memmove(Q.AW, Q.AW + 1, sizeof(double*) * (size_t)(Q.count - 1));
+        Q.count--;
+      }
+    if (cb) cb(user, k, n, st, Vo, alpha, x, r, rho);
+    if (rep && rep->rho_history) rep->rho_history[k] = rho;
+    k = k + 1;
+  }
+  if (rep) {
+    if (status == OR_BREAKDOWN) rep->breakdown_block = (k - 1) * s;
+    rep->outer_iters = k - 1;
+    rep->rho = rho;
+    rep->converged = rho <= eps * rho0;
+    or_spmm(A, 1, x, tmp);
+    for (int64_t i = 0; i < n; ++i) tmp[i] = b[i] - tmp[i];
+    double nb = norm2(n, b);
+    rep->true_relres = nb > 0 ? norm2(n, tmp) / nb : 0.0;
+  }
+  if (status == OR_OK && !(rho <= eps * rho0)) status = OR_MAXITER;
+  if (rep) rep->status = status;
+  bl_free(&Q);
+  free(W); free(W1); free(V); free(Vo); free(Rt); free(Rs); free(alpha); free(pw); free(nw);
+  free(r); free(tmp); free(u);
+  return status;
+}
+

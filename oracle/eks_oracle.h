@@ -76,6 +76,14 @@ int or_acholqr(const or_csr* A, int t, const double* Z, double* W, double* R, do
 int or_solve(const or_csr* A, const double* b, double* x, int method, int s, int t,
              double eps, int kmax, int mode, or_report* rep, or_iter_cb cb, void* user);
 
+/* Communication-avoiding s-step enlarged CG: CA SRE-CG, CA SRE-CG2
+ * (method 0 / 1) and CA MSDO-CG (method 2) with the CA-Arnoldi
+ * A-orthonormalization (arnoldi = 5, Alg 5) or its modified, stabilised form
+ * (arnoldi = 7, Alg 7).  The st vectors of an outer iteration are formed as a
+ * monomial block [W, AW, …, A^{s-1}W] and A-orthonormalized together (one st×st CholQR). */
+int or_solve_ca(const or_csr* A, const double* b, double* x, int method, int arnoldi, int s, int t,
+                double eps, int kmax, or_report* rep, or_iter_cb cb, void* user);
+
 /* s-step SRE-CG basis sweep only (cfg5, reading R27): starting block X0 (n×t)
  * is A-orthonormalized, then nblocks-1 further blocks W=A-orth(A·W_prev) against
  * the last min(2,#) blocks.  Writes the last block to W_last.  Returns status. */
