@@ -33,7 +33,14 @@ extern "C" {
 typedef struct eks_ctx eks_ctx;
 
 /* The three s-step methods: Alg 4, Alg 3, Alg 6. */
-typedef enum { EKS_SRE_CG = 0, EKS_SRE_CG2 = 1, EKS_MSDO_CG = 2 } eks_method;
+/* 0-2: s-step methods (Alg 4 / Alg 3 / Alg 6).  3-5: their communication-avoiding versions
+ * (CA SRE-CG, CA SRE-CG2 P:245-281; CA MSDO-CG P:351): each outer iteration forms the monomial
+ * block [W, AW, …, A^{s-1}W], A-orthonormalizes it against the window with CGS2 and then with ONE
+ * A-CholQR of its s·t columns (s·t ≤ 96); the CA-Arnoldi variant is eks_options.arnoldi. */
+typedef enum {
+  EKS_SRE_CG = 0, EKS_SRE_CG2 = 1, EKS_MSDO_CG = 2,
+  EKS_CA_SRE_CG = 3, EKS_CA_SRE_CG2 = 4, EKS_CA_MSDO_CG = 5
+} eks_method;
 
 typedef enum { EKS_MEM_HOST = 0, EKS_MEM_DEVICE = 1 } eks_mem;
 
@@ -79,7 +86,9 @@ typedef struct {
   int max_outer;          /* <=0: 5000 (reading R7) */
   int use_graph;          /* 1: capture one outer iteration as a CUDA graph and replay it */
   int profile;            /* 1: record per-kernel-class CUDA events (see eks_profile) */
-  int reserved[8];
+  int arnoldi;            /* CA methods: 7 = modified CA-Arnoldi (Alg 7, default when 0),
+                             5 = CA-Arnoldi (Alg 5) */
+  int reserved[7];
 } eks_options;
 
 /* Per-kernel-class device time accumulated while options.profile == 1. */

@@ -19,7 +19,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libeks.so")
 
 EKS_SRE_CG, EKS_SRE_CG2, EKS_MSDO_CG = 0, 1, 2
-METHODS = {"sre-cg": EKS_SRE_CG, "sre-cg2": EKS_SRE_CG2, "msdo-cg": EKS_MSDO_CG}
+METHODS = {"sre-cg": EKS_SRE_CG, "sre-cg2": EKS_SRE_CG2, "msdo-cg": EKS_MSDO_CG,
+           "ca-sre-cg": 3, "ca-sre-cg2": 4, "ca-msdo-cg": 5}
 EKS_MEM_HOST, EKS_MEM_DEVICE = 0, 1
 STATUS = {0: "EKS_OK", 1: "EKS_ERR_INVALID_ARG", 2: "EKS_ERR_STATE", 3: "EKS_ERR_BAD_MATRIX", 4: "EKS_ERR_OOM",
           5: "EKS_ERR_CUDA", 6: "EKS_ERR_NCCL", 7: "EKS_ERR_BREAKDOWN", 8: "EKS_ERR_MAXITER"}
@@ -45,7 +46,8 @@ class _Report(C.Structure):
 
 
 class _Options(C.Structure):
-    _fields_ = [("max_outer", C.c_int), ("use_graph", C.c_int), ("profile", C.c_int), ("reserved", C.c_int * 8)]
+    _fields_ = [("max_outer", C.c_int), ("use_graph", C.c_int), ("profile", C.c_int), ("arnoldi", C.c_int),
+                ("reserved", C.c_int * 7)]
 
 
 class _Profile(C.Structure):
@@ -186,11 +188,12 @@ def _report(rep: _Report):
                 gpu_launches=rep.gpu_launches, hist=hist)
 
 
-def eks_solve_ex(ctx, method, s, t, tol, b, x, max_outer=0, profile=False, raise_on=(5, 6, 1, 2, 3)):
-    """Returns (status, report dict).  x holds x0 on entry and the solution on exit."""
+def eks_solve_ex(ctx, method, s, t, tol, b, x, max_outer=0, profile=False, raise_on=(5, 6, 1, 2, 3), arnoldi=0):
+    """Returns (status, report dict).  x holds x0 on entry and the solution on exit.
+    arnoldi (CA methods only): 7 = modified CA-Arnoldi (default), 5 = CA-Arnoldi."""
     m = METHODS[method] if isinstance(method, str) else int(method)
     where = _where(b, x)
-    opt = _Options(int(max_outer), 0, int(bool(profile)))
+    opt = _Options(int(max_outer), 0, int(bool(profile)), int(arnoldi))
     rep = _Report()
     st = lib().eks_solve_ex(ctx, m, int(s), int(t), float(tol), _ptr(b, np.float64), _ptr(x, np.float64), where,
                             C.byref(opt), C.byref(rep))
@@ -291,13 +294,14 @@ class Solver:
         vl = np.ascontiguousarray(val, np.float64) if isinstance(val, np.ndarray) else val
         eks_setup_csr(self.ctx, n_global, row_begin, row_end, rp, cl, vl)
 
-    def solve(self, b, method="sre-cg", s=1, t=1, tol=1e-8, x0=None, max_outer=0, profile=False):
+    def solve(self, b, method="sre-cg", s=1, t=1, tol=1e-8, x0=None, max_outer=0, profile=False, arnoldi=0):
         if isinstance(b, np.ndarray):
             b = np.ascontiguousarray(b, np.float64)
             x = np.zeros_like(b) if x0 is None else np.ascontiguousarray(x0, np.float64).copy()
         else:
             x = b.new_zeros(b.shape) if x0 is None else x0.clone()
-        st, rep = eks_solve_ex(self.ctx, method, s, t, tol, b, x, max_outer=max_outer, profile=profile)
+        st, rep = eks_solve_ex(self.ctx, method, s, t, tol, b, x, max_outer=max_outer, profile=profile,
+                               arnoldi=arnoldi)
         rep["status"] = st
         rep["x"] = x
         return rep

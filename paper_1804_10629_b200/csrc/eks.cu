@@ -77,6 +77,11 @@ struct eks_ctx {
   bool grid_ok = false;
   eks::GridPlan gplan{};
   double* d_sv = nullptr;
+  // communication-avoiding outer iteration: the s monomial blocks, their A-products, the st×st
+  // Gram / factor / inverse, g = Vᵀr and α̃
+  std::vector<Block> Vca, AVca;
+  double *Bca = nullptr, *gca = nullptr, *Rca = nullptr, *Rinvca = nullptr, *alphaca = nullptr, *Btmp = nullptr;
+  int ca_cap = 0;  // st the buffers were sized for
   int chol_mode = 0;               // 0 one-warp Cholesky launch (default), 1 in the SpMM kernel's tail (EKS_CHOL)
   // workspace, keyed by t
   int ws_t = 0;
@@ -214,6 +219,12 @@ eks_status alloc_block(eks_ctx* ctx, Block* B, int t, bool ext) {
 }
 
 void free_workspace(eks_ctx* c) {
+  for (auto& b : c->Vca) dfree(b.base);
+  for (auto& b : c->AVca) dfree(b.base);
+  c->Vca.clear();
+  c->AVca.clear();
+  for (double** p : {&c->Bca, &c->gca, &c->Rca, &c->Rinvca, &c->alphaca, &c->Btmp}) { dfree(*p); *p = nullptr; }
+  c->ca_cap = 0;
   for (auto& b : c->Wpool) dfree(b.base);
   for (auto& b : c->AWpool) dfree(b.base);
   c->Wpool.clear();
@@ -665,6 +676,132 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
     ST(allreduce(ctx, ctx->C1, (size_t)c1n * t * t));
     ctx->c1_ready = true;
   }
+  return EKS_OK;
+}
+
+// A-CholQR of one block in place (the Alg 7 seed): B = Zᵀ(AZ), R, W = Z R⁻¹, AW = (AZ) R⁻¹.
+eks_status acholqr_block(eks_ctx* ctx, int t, Block& Z, double* AZ, int gb) {
+  ST(spmm_gram(ctx, Z, AZ, t, nullptr, ctx->Bg));
+  {
+    KScope k(ctx, EKS_K_CHOL);
+    CK(eks::launch_chol_fast(ctx->stream, t, ctx->Bg, nullptr, ctx->Rm, ctx->Rinv, nullptr, ctx->flag, gb));
+  }
+  KScope k(ctx, EKS_K_APPLY);
+  if (eks::sweep_supported(t))
+    CK(eks::launch_apply_tc(ctx->stream, t, ctx->n, Z.loc, AZ, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr,
+                            nullptr, 4, ctx->nblk, 0, nullptr, ctx->part2, eks::Tail{}));
+  else
+    CK(eks::launch_apply(ctx->stream, t, ctx->n, Z.loc, AZ, ctx->Rinv, nullptr, nullptr, nullptr, nullptr, nullptr,
+                         nullptr, nullptr, 4, ctx->nblk));
+  return EKS_OK;
+}
+
+// One outer iteration of CA SRE-CG / CA SRE-CG2 / CA MSDO-CG (base = the s-step method):
+//   W = T(r_{k−1}) (k = 1, or every k for MSDO) or A·W_last;  Alg 7: A-orthonormalize W
+//   against the window and itself;  V = [W, AW, …, A^{s−1}W];  CGS2 of every V_i
+//   against the window (column-wise identical to CGS2 of the n×st block);  ONE A-CholQR of the
+//   st columns: AV_i = A·V_i, B_ij = V_iᵀ AV_j (i ≤ j) and g = Vᵀr_{k−1}, R = chol(B), W = V R⁻¹,
+//   AW = AV R⁻¹, α̃ = R⁻ᵀ g;  x += W α̃, r_k = r_{k−1} − AW α̃  (reading R28).
+// Window: the last (s+1) blocks (CA SRE-CG, Alg 5 input m = (s+1)t) or all blocks.
+eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, int& nblocks, int ring) {
+  const int st = s * t;
+  ctx->rho_fused = false;  // ‖r_k‖² comes from k_ca_update's per-CTA partials
+  ctx->c1_ready = false;
+  if (ctx->ca_cap != st || (int)ctx->Vca.size() != s) {
+    for (auto& b : ctx->Vca) dfree(b.base);
+    for (auto& b : ctx->AVca) dfree(b.base);
+    for (double** p : {&ctx->Bca, &ctx->gca, &ctx->Rca, &ctx->Rinvca, &ctx->alphaca, &ctx->Btmp}) {
+      dfree(*p);
+      *p = nullptr;
+    }
+    ctx->Vca.assign(s, Block{});
+    ctx->AVca.assign(s, Block{});
+    for (int i = 0; i < s; ++i) {
+      ST(alloc_block(ctx, &ctx->Vca[i], t, true));
+      ST(alloc_block(ctx, &ctx->AVca[i], t, false));
+    }
+    ST(dalloc(ctx, &ctx->Bca, (size_t)st * st));
+    ST(dalloc(ctx, &ctx->gca, (size_t)st));
+    ST(dalloc(ctx, &ctx->Rca, (size_t)st * st));
+    ST(dalloc(ctx, &ctx->Rinvca, (size_t)st * st));
+    ST(dalloc(ctx, &ctx->alphaca, (size_t)st));
+    ST(dalloc(ctx, &ctx->Btmp, (size_t)s * t * t + t));
+    ctx->ca_cap = st;
+  }
+  std::vector<const double*> Q, AQ;
+  const int first = base == EKS_SRE_CG ? std::max(0, nblocks - (s + 1)) : 0;
+  for (int j = first; j < nblocks; ++j) {
+    const int idx = ring ? j % ring : j;
+    Q.push_back(ctx->Wpool[idx].loc);
+    AQ.push_back(ctx->AWpool[idx].loc);
+  }
+  std::vector<Block>& V = ctx->Vca;
+  std::vector<Block>& AV = ctx->AVca;
+  // seed
+  if (base == EKS_MSDO_CG || k == 1) {
+    KScope kk(ctx, EKS_K_SPLIT);
+    CK(eks::launch_split(ctx->stream, t, ctx->n, ctx->row_begin, ctx->n_global, ctx->r, V[0].loc));
+  } else {
+    const int idx = ring ? (nblocks - 1) % ring : nblocks - 1;
+    ST(spmm(ctx, ctx->Wpool[idx], V[0].loc, t));
+  }
+  if (arnoldi == 7) {  // Alg 7 lines 1-4
+    if (!Q.empty()) ST(cgs2(ctx, t, Q, AQ, V[0].loc, V[0].loc));
+    ST(acholqr_block(ctx, t, V[0], AV[0].loc, nblocks));
+  }
+  for (int i = 1; i < s; ++i) ST(spmm(ctx, V[i - 1], V[i].loc, t));  // monomial powers
+  if (!Q.empty())
+    for (int i = 0; i < s; ++i) ST(cgs2(ctx, t, Q, AQ, V[i].loc, V[i].loc));
+  for (int i = 0; i < s; ++i) ST(spmm(ctx, V[i], AV[i].loc, t));
+  // Gram B (st×st, upper blocks) and g = Vᵀ r_{k−1}
+  std::vector<const double*> L(s);
+  for (int i = 0; i < s; ++i) L[i] = V[i].loc;
+  auto place = [&](int i, int j) -> eks_status {
+    CK(cudaMemcpy2DAsync(ctx->Bca + (size_t)i * t * st + (size_t)j * t, sizeof(double) * st,
+                         ctx->Btmp + (size_t)i * t * t, sizeof(double) * t, sizeof(double) * t, t,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+    return EKS_OK;
+  };
+  for (int j = 0; j < s; ++j) {
+    if (j > 0) {
+      ST(tn_reduce(ctx, t, j, L.data(), AV[j].loc, nullptr, ctx->Btmp));
+      for (int i = 0; i < j; ++i) ST(place(i, j));
+    }
+    const double* Lj[1] = {V[j].loc};
+    ST(tn_reduce(ctx, t, 1, Lj, AV[j].loc, ctx->r, ctx->Btmp));
+    CK(cudaMemcpy2DAsync(ctx->Bca + (size_t)j * t * st + (size_t)j * t, sizeof(double) * st, ctx->Btmp,
+                         sizeof(double) * t, sizeof(double) * t, t, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->gca + (size_t)j * t, ctx->Btmp + (size_t)t * t, sizeof(double) * t,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  {
+    KScope kk(ctx, EKS_K_CHOL);
+    CK(eks::launch_chol_dyn(ctx->stream, st, ctx->Bca, ctx->gca, ctx->Rca, ctx->Rinvca, ctx->alphaca, ctx->flag,
+                            nblocks));
+  }
+  // W = V R⁻¹, AW = AV R⁻¹ into the new slots
+  eks::CaPtrs Pw{}, Pa{}, Pu{};
+  for (int j = 0; j < s; ++j) {
+    Block *Wn = nullptr, *AWn = nullptr;
+    ST(slot(ctx, t, ring ? (nblocks + j) % ring : nblocks + j, &Wn, &AWn));
+    Pw.in[j] = V[j].loc;
+    Pw.out[j] = Wn->loc;
+    Pa.in[j] = AV[j].loc;
+    Pa.out[j] = AWn->loc;
+    Pu.in[j] = Wn->loc;
+    Pu.out[j] = AWn->loc;
+  }
+  Pw.flag = Pa.flag = Pu.flag = ctx->flag;
+  {
+    KScope kk(ctx, EKS_K_APPLY);
+    CK(eks::launch_ca_combine(ctx->stream, ctx->n, t, s, Pw, ctx->Rinvca, ctx->sms, false));
+    CK(eks::launch_ca_combine(ctx->stream, ctx->n, t, s, Pa, ctx->Rinvca, ctx->sms, false));
+    CK(eks::launch_ca_update(ctx->stream, ctx->n, t, s, Pu, ctx->alphaca, ctx->xv.loc, ctx->r, ctx->rnew, ctx->part,
+                             ctx->nblk));
+    ctx->rho_nblk = ctx->nblk;
+  }
+  account(ctx, EKS_K_APPLY, 8.0 * ctx->n * (4.0 * st + 3.0), 2.0 * ctx->n * st * (st + 2));
+  nblocks += s;
   return EKS_OK;
 }
 
@@ -1157,7 +1294,13 @@ eks_status eks_solve(eks_ctx* ctx, eks_method method, int s, int t, double tol, 
 eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double tol, const double* b, double* x,
                         eks_mem where, const eks_options* opt, eks_report* rep) {
   ST(check_ready(ctx));
-  if (method < EKS_SRE_CG || method > EKS_MSDO_CG) return fail(ctx, EKS_ERR_INVALID_ARG, "unknown method");
+  if (method < EKS_SRE_CG || method > EKS_CA_MSDO_CG) return fail(ctx, EKS_ERR_INVALID_ARG, "unknown method");
+  const bool ca = method >= EKS_CA_SRE_CG;
+  const int base = ca ? method - EKS_CA_SRE_CG : method;
+  const int arnoldi = (opt && opt->arnoldi) ? opt->arnoldi : 7;
+  if (ca && (arnoldi != 5 && arnoldi != 7)) return fail(ctx, EKS_ERR_INVALID_ARG, "arnoldi must be 5 or 7");
+  if (ca && (s * t > eks::kCaMax || s > eks::kCaMaxBlocks))
+    return fail(ctx, EKS_ERR_INVALID_ARG, "CA methods need s*t <= %d and s <= %d", eks::kCaMax, eks::kCaMaxBlocks);
   if (s < 1 || !valid_t(t) || t > ctx->n_global) return fail(ctx, EKS_ERR_INVALID_ARG, "bad s=%d or t=%d", s, t);
   if (!(tol >= 0.0)) return fail(ctx, EKS_ERR_INVALID_ARG, "tol must be >= 0");
   if (!b || !x) return fail(ctx, EKS_ERR_INVALID_ARG, "NULL b or x");
@@ -1172,7 +1315,7 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   begin_run(ctx, opt);
   auto wall0 = std::chrono::steady_clock::now();
   ST(ensure_workspace(ctx, t, s));
-  const int ring = (method == EKS_SRE_CG) ? 3 : 0;
+  const int ring = (method == EKS_SRE_CG) ? 3 : (method == EKS_CA_SRE_CG ? 2 * s + 1 : 0);
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -1190,7 +1333,17 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   // while (ρ > ε ρ0 and k < k_max)   (reading R7)
   while (rho > tol * rho0 && k < kmax) {
     ST(reset_flag(ctx));
-    for (int i = 0; i < s; ++i) {
+    if (ca) {
+      const int nb0 = nblocks;
+      eks_status cs = ca_outer(ctx, t, s, base, arnoldi, k, nblocks, ring);
+      if (cs == EKS_ERR_OOM) {
+        max_fit = nb0 / s;
+        status = EKS_ERR_OOM;
+        break;
+      }
+      ST(cs);
+    }
+    for (int i = 0; i < (ca ? 0 : s); ++i) {
       Block *Wn = nullptr, *AWn = nullptr;
       const int idx = ring ? nblocks % ring : nblocks;
       eks_status as = slot(ctx, t, idx, &Wn, &AWn);
@@ -1244,7 +1397,7 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
     rep->outer_iters = k - 1;
     rep->converged = converged;
     rep->breakdown_block = breakdown_block;
-    rep->max_outer_fit = (method == EKS_SRE_CG) ? -1 : max_fit;
+    rep->max_outer_fit = (base == EKS_SRE_CG) ? -1 : max_fit;
     rep->rho0 = rho0;
     rep->rho = rho;
     const double nb = std::sqrt(ctx->h_scal[3]);

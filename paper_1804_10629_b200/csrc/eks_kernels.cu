@@ -724,6 +724,175 @@ cudaError_t launch_apply(cudaStream_t st, int t, int64_t n, double* Z2W, double*
   return cudaGetLastError();
 }
 
+
+// ============================================================================
+// Communication-avoiding variants (CA SRE-CG / CA SRE-CG2 / CA MSDO-CG):
+// the s·t columns of an outer iteration are A-orthonormalized by ONE CholQR.
+// ============================================================================
+// Cholesky of the m×m Gram (m = s·t ≤ kCaMax), R⁻¹ and α̃ = R⁻ᵀ g: k_chol's right-looking
+// elimination (R bitwise equal to the oracle's or_chol for equal B, reading R20) at run-time size.
+template <bool G>
+__global__ void __launch_bounds__(256) k_chol_dyn(int m, const double* __restrict__ B, const double* __restrict__ g,
+                                                  double* __restrict__ Rout, double* __restrict__ Rinv,
+                                                  double* __restrict__ alpha, int* flag, int gblock) {
+  pdl_enter();
+  extern __shared__ double csm[];
+  const int M1 = m + 1;
+  double* sA = csm;            // m × (m+1)
+  double* sY = csm + m * M1;   // m × (m+1)
+  __shared__ double sred[8];
+  __shared__ int sfail;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  double mx = 0.0;
+  for (int e = tid; e < m * m; e += nth) {
+    const int i = e / m, j = e % m;
+    const double b = B[e];
+    sA[i * M1 + j] = b;
+    sY[i * M1 + j] = (i == j) ? 1.0 : 0.0;
+    if (j >= i) mx = fmax(mx, fabs(b));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  if ((tid & 31) == 0) sred[tid >> 5] = mx;
+  if (tid == 0) sfail = 0;
+  __syncthreads();
+  double bm = 0.0;
+  for (int w = 0; w < (nth >> 5); ++w) bm = fmax(bm, sred[w]);
+  const double thr = __dmul_rn((double)m * 0x1p-52, bm);
+  __shared__ double srkk;
+  for (int k = 0; k < m; ++k) {
+    if (tid == 0) {
+      const double d = sA[k * M1 + k];
+      if (!(d > thr)) sfail = 1;
+      srkk = __dsqrt_rn(d);
+      sA[k * M1 + k] = srkk;
+    }
+    __syncthreads();
+    const double rkk = srkk;
+    for (int j = k + 1 + tid; j < m; j += nth) sA[k * M1 + j] = __ddiv_rn(sA[k * M1 + j], rkk);
+    __syncthreads();
+    const int m1 = m - k - 1;
+    for (int e = tid; e < m1 * m1; e += nth) {
+      const int i = k + 1 + e / m1, j = k + 1 + e % m1;
+      if (j >= i) sA[i * M1 + j] = __dsub_rn(sA[i * M1 + j], __dmul_rn(sA[k * M1 + i], sA[k * M1 + j]));
+    }
+    __syncthreads();
+  }
+  for (int k = m - 1; k >= 0; --k) {
+    const double rkk = sA[k * M1 + k];
+    for (int j = k + tid; j < m; j += nth) sY[k * M1 + j] = __ddiv_rn(sY[k * M1 + j], rkk);
+    __syncthreads();
+    const int w = m - k;
+    for (int e = tid; e < k * w; e += nth) {
+      const int i = e / w, j = k + e % w;
+      sY[i * M1 + j] = __fma_rn(-sA[i * M1 + k], sY[k * M1 + j], sY[i * M1 + j]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < m * m; e += nth) {
+    const int i = e / m, j = e % m;
+    if (Rout) Rout[e] = j >= i ? sA[i * M1 + j] : 0.0;
+    Rinv[e] = sY[i * M1 + j];
+  }
+  if (G && alpha != nullptr)
+    for (int j = tid; j < m; j += nth) {
+      double a = 0.0;
+      for (int i = 0; i <= j; ++i) a = __fma_rn(sY[i * M1 + j], g[i], a);
+      alpha[j] = a;
+    }
+  if (tid == 0 && sfail && flag) atomicMin(flag, gblock);
+}
+
+cudaError_t launch_chol_dyn(cudaStream_t st, int m, const double* B, const double* g, double* R, double* Rinv,
+                            double* alpha, int* flag, int gblock) {
+  if (m < 1 || m > kCaMax) return cudaErrorInvalidValue;
+  const size_t sm = (size_t)2 * m * (m + 1) * 8;
+  if (g) {
+    cudaFuncSetAttribute(k_chol_dyn<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    return launch_k(k_chol_dyn<true>, 1, 256, sm, st, m, B, g, R, Rinv, alpha, flag, gblock);
+  }
+  cudaFuncSetAttribute(k_chol_dyn<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  return launch_k(k_chol_dyn<false>, 1, 256, sm, st, m, B, g, R, Rinv, alpha, flag, gblock);
+}
+
+// out_j = Σ_{i ≤ j} in_i · Rinv[i·t.., j·t..] for the s blocks (W = V R⁻¹ and AW = AV R⁻¹ of the
+// st-column CholQR, R upper so only i ≤ j contributes).  R⁻¹ in shared memory; a thread owns one
+// (row, column) and all s output blocks.
+__global__ void __launch_bounds__(256) k_ca_combine(int64_t n, int t, int s, CaPtrs P, const double* __restrict__ Rinv,
+                                                    int skip) {
+  pdl_enter();
+  extern __shared__ double sR[];
+  const int m = s * t;
+  if (skip != 0 && *reinterpret_cast<const volatile int*>(P.flag) != INT_MAX) return;  // breakdown
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) sR[e] = Rinv[e];
+  __syncthreads();
+  const int rows_per = blockDim.x / t;
+  const int c = threadIdx.x % t, rl = threadIdx.x / t;
+  if (rl >= rows_per) return;
+  for (int64_t row = (int64_t)blockIdx.x * rows_per + rl; row < n; row += (int64_t)gridDim.x * rows_per) {
+    for (int j = 0; j < s; ++j) {
+      double acc = 0.0;
+      for (int i = 0; i <= j; ++i) {
+        const double* v = P.in[i] + row * t;
+        const double* rr = sR + (size_t)(i * t) * m + j * t + c;
+        for (int a = 0; a < t; ++a) acc = __fma_rn(__ldg(v + a), rr[(size_t)a * m], acc);
+      }
+      P.out[j][row * t + c] = acc;
+    }
+  }
+}
+
+cudaError_t launch_ca_combine(cudaStream_t st, int64_t n, int t, int s, const CaPtrs& P, const double* Rinv,
+                              int sms, bool skip_on_breakdown) {
+  const int m = s * t;
+  if (m > kCaMax || s > kCaMaxBlocks) return cudaErrorInvalidValue;
+  const size_t sm = (size_t)m * m * 8;
+  cudaFuncSetAttribute(k_ca_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int rows_per = 256 / t;
+  int64_t blocks = (n + rows_per - 1) / rows_per;
+  if (blocks > (int64_t)sms * 4) blocks = (int64_t)sms * 4;
+  return launch_k(k_ca_combine, (int)blocks, 256, sm, st, n, t, s, P, Rinv, skip_on_breakdown ? 1 : 0);
+}
+
+// x += Σ_j W_j α_j, r −= Σ_j AW_j α_j (α = α̃ = R⁻ᵀ Vᵀr of the outer iteration), partial ‖r‖² per CTA;
+// nothing when the breakdown flag is set (x stays the last completed iterate).
+__global__ void __launch_bounds__(256) k_ca_update(int64_t n, int t, int s, CaPtrs P, const double* __restrict__ alpha,
+                                                   double* __restrict__ x, const double* __restrict__ r,
+                                                   double* __restrict__ rnew, double* __restrict__ part) {
+  pdl_enter();
+  __shared__ double sa[kCaMax];
+  __shared__ double sred[32];
+  const int m = s * t;
+  const bool skip = *reinterpret_cast<const volatile int*>(P.flag) != INT_MAX;
+  for (int e = threadIdx.x; e < m; e += blockDim.x) sa[e] = alpha[e];
+  __syncthreads();
+  const int64_t lo = (int64_t)blockIdx.x * n / gridDim.x, hi = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    double dx = 0.0, dr = 0.0;
+    for (int j = 0; j < s; ++j)
+      for (int c = 0; c < t; ++c) {
+        dx = __fma_rn(P.in[j][i * t + c], sa[j * t + c], dx);
+        dr = __fma_rn(P.out[j][i * t + c], sa[j * t + c], dr);
+      }
+    double ri = r[i];
+    if (!skip) {
+      x[i] += dx;
+      ri -= dr;
+    }
+    rnew[i] = ri;
+    acc = __fma_rn(ri, ri, acc);
+  }
+  const double tot = block_sum(acc, sred);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+cudaError_t launch_ca_update(cudaStream_t st, int64_t n, int t, int s, const CaPtrs& P, const double* alpha,
+                             double* x, const double* r, double* rnew, double* part, int nblk) {
+  if (s * t > kCaMax || s > kCaMaxBlocks) return cudaErrorInvalidValue;
+  return launch_k(k_ca_update, nblk, 256, 0, st, n, t, s, P, alpha, x, r, rnew, part);
+}
+
 // ============================================================================
 // Vector kernels
 // ============================================================================

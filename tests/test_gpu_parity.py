@@ -399,3 +399,50 @@ def test_paper_poisson2d_large_t_gpu(eks, torch_cuda, oracle_lib, method, t):
         r1 = S.solve(dev(torch_cuda, b), method, 1, t, 1e-6)
         assert rep["outer_iters"] == math.ceil(r1["outer_iters"] / 3)
     S.close()
+
+
+# ------------------------------------------------------------------ §8(f) row 1: communication-avoiding variants
+@pytest.mark.parametrize("method,arnoldi,s_,t", [("ca-sre-cg", 7, 3, 4), ("ca-sre-cg", 5, 2, 4), ("ca-sre-cg2", 7, 2, 8),
+                                                 ("ca-msdo-cg", 7, 3, 4), ("ca-msdo-cg", 5, 2, 8),
+                                                 ("ca-sre-cg", 7, 3, 16), ("ca-sre-cg", 7, 2, 32)])
+def test_ca_end_to_end(eks, torch_cuda, oracle_lib, method, arnoldi, s_, t):
+    """CA SRE-CG / CA SRE-CG2 / CA MSDO-CG (Alg 5 or 7, one st-column A-CholQR per outer iteration)
+    on the well-conditioned Poisson2D 48² (the paper's CA regime): GPU and oracle
+    reach 1e-8 with counts within max(5 %, 1) and x within 1e-6."""
+    A = ei.poisson2d(48)
+    b = ei.uniform_pm1(1805, A.n)
+    base = method[3:]
+    S = eks.Solver(A)
+    rep = S.solve(dev(torch_cuda, b), method, s_, t, 1e-8, arnoldi=arnoldi)
+    S.close()
+    ref = oracle_lib.solve_ca(A, b, base, arnoldi=arnoldi, s=s_, t=t, tol=1e-8)
+    assert rep["converged"] and ref["converged"], (rep["status"], ref["status"])
+    assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+    assert rep["true_relres"] <= 2e-8
+
+
+def test_ca_ill_conditioned_agrees_with_oracle(eks, torch_cuda, oracle_lib):
+    """On the κ = 1e3 band problem (cfg2 recipe at 64²) CA SRE-CG converges for s = 2 and its
+    monomial basis breaks down for s = 3 — on both sides (the paper's instability)."""
+    p = ei.cfg2(N=64)
+    S = eks.Solver(p.A)
+    ok = S.solve(dev(torch_cuda, p.b), "ca-sre-cg", 2, 4, 1e-8, arnoldi=5)
+    bad = S.solve(dev(torch_cuda, p.b), "ca-sre-cg", 3, 4, 1e-8)
+    S.close()
+    ref_ok = oracle_lib.solve_ca(p.A, p.b, "sre-cg", arnoldi=5, s=2, t=4, tol=1e-8)
+    ref_bad = oracle_lib.solve_ca(p.A, p.b, "sre-cg", arnoldi=7, s=3, t=4, tol=1e-8)
+    assert ok["converged"] and ref_ok["converged"]
+    assert abs(ok["outer_iters"] - ref_ok["outer_iters"]) <= max(1, round(0.05 * ref_ok["outer_iters"]))
+    assert bad["status"] == eks.EKS_ERR_BREAKDOWN and ref_bad["status"] == oracle_lib.BREAKDOWN
+    assert bad["outer_iters"] == ref_bad["outer_iters"]
+
+
+def test_ca_breakdown_reported(eks, torch_cuda, oracle_lib):
+    A = ei.poisson2d(64)
+    b = ei.paper_poisson_rhs(A)
+    S = eks.Solver(A)
+    rep = S.solve(dev(torch_cuda, b), "ca-sre-cg", 10, 2, 1e-6)
+    S.close()
+    assert rep["status"] == eks.EKS_ERR_BREAKDOWN and rep["outer_iters"] == 0
+    assert float(rep["x"].abs().max()) == 0.0
