@@ -14,6 +14,7 @@ the same workload instead: each step = a bounded sample of outer iterations.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -214,16 +215,30 @@ def oracle_sample(p, iters: int):
     import oracle
     oracle.build()
     t0 = time.perf_counter()
-    r = oracle.solve(p.A, p.b, p.method, p.s, p.t, 0.0, kmax=iters + 1)
+    if p.method.startswith("ca-"):
+        r = oracle.solve_ca(p.A, p.b, p.method[3:], arnoldi=p.arnoldi, s=p.s, t=p.t, tol=0.0, kmax=iters + 1)
+    else:
+        r = oracle.solve(p.A, p.b, p.method, p.s, p.t, 0.0, kmax=iters + 1)
     dt = time.perf_counter() - t0
     return r["outer_iters"], dt
+
+
+def problem_of(args):
+    """The workload, with --method/--s/--arnoldi overrides (CA variants: §8(f) item 1)."""
+    p = workload(args.workload)
+    if args.method:
+        p = dataclasses.replace(p, method=args.method)
+    if args.s:
+        p = dataclasses.replace(p, s=args.s)
+    p.arnoldi = args.arnoldi if p.method.startswith("ca-") else 0
+    return p
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    p = workload(args.workload)
+    p = problem_of(args)
     per_step = args.ref_iters
     for _ in range(args.warmup):
         oracle_sample(p, per_step)
@@ -247,7 +262,8 @@ def run_reference(args):
 
 
 def config_of(args, p, N):
-    return {"workload": f"{p.name}: {p.note}; s-step {p.method}, s={p.s}, t={p.t}, tol={p.tol:g}",
+    kind = f"CA (Alg {p.arnoldi})" if p.method.startswith("ca-") else "s-step"
+    return {"workload": f"{p.name}: {p.note}; {kind} {p.method}, s={p.s}, t={p.t}, tol={p.tol:g}",
             "n": p.A.n, "nnz": p.A.nnz, "method": p.method, "s": p.s, "t": p.t, "tol": p.tol,
             "parallelism": f"row-slabs x{N} (t/N domains per GPU)",
             "l2": "flushed: 256 MiB buffer written between timed steps (outside the step events)"}
@@ -268,7 +284,9 @@ def main():
     ap.add_argument("--max-outer", type=int, default=0, help="cap outer iterations per solve (profiling only)")
     ap.add_argument("--no-spmm-block", action="store_true", help="skip the large-operator SpMM-block measurement")
     ap.add_argument("--t", type=int, default=0, help="cfg5: block width t")
-    ap.add_argument("--s", type=int, default=0, help="cfg5: blocks per outer iteration s")
+    ap.add_argument("--s", type=int, default=0, help="blocks per outer iteration s (cfg5, or override)")
+    ap.add_argument("--method", default="", help="override the workload's method (e.g. ca-sre-cg)")
+    ap.add_argument("--arnoldi", type=int, default=7, help="CA variants: Alg 5 or Alg 7")
     ap.add_argument("--cfg5-n", type=int, default=384, help="cfg5 grid size (384 = BASELINE configs[4])")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -293,7 +311,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    p = workload(args.workload)
+    p = problem_of(args)
     n, t = p.A.n, p.t
     if t % world:
         raise SystemExit("t must be divisible by the number of GPUs")
@@ -323,7 +341,7 @@ def main():
         with torch.cuda.stream(stream):
             x.zero_()
         st, rep = eks.eks_solve_ex(solver.ctx, p.method, p.s, p.t, p.tol, b, x, profile=profile,
-                                   max_outer=args.max_outer)
+                                   max_outer=args.max_outer, arnoldi=p.arnoldi)
         if st not in ((0, 8) if args.max_outer else (0,)):
             raise SystemExit(f"solve failed: {eks.STATUS.get(st)} {eks.eks_error_string(solver.ctx)}")
         return rep
@@ -424,7 +442,7 @@ def main():
         for k in range(args.steps):
             e2e_solver.setup(n, lo, hi, hrp, hcol, hval)
             hx[:] = 0.0
-            st, rep = eks.eks_solve_ex(e2e_solver.ctx, p.method, p.s, p.t, p.tol, hb, hx)
+            st, rep = eks.eks_solve_ex(e2e_solver.ctx, p.method, p.s, p.t, p.tol, hb, hx, arnoldi=p.arnoldi)
             e_outer += rep["outer_iters"]
         torch.cuda.synchronize()
         barrier()

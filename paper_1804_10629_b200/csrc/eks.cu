@@ -360,10 +360,10 @@ eks_status spmm(eks_ctx* ctx, const Block& X, double* Y, int t) {
   return EKS_OK;
 }
 
-// out (nl·t·t [+t]) = Σ over all rows of Lᵀ R [and L_0ᵀ v], allreduced.
-// out (nl·t·t [+t]) = Σ over all rows of Lᵀ R [and L_0ᵀ v], allreduced over ranks.
+// out (nl·t·t [+t]) = Σ over all rows of Lᵀ R [and L_0ᵀ v], allreduced over ranks unless `ar` is
+// false (the caller then stacks several outputs into one allreduce).
 eks_status tn_reduce(eks_ctx* ctx, int t, int nl, const double* const* L, const double* R, const double* v,
-                     double* out) {
+                     double* out, bool ar = true) {
   if (v && nl != 1) return fail(ctx, EKS_ERR_INVALID_ARG, "internal: v needs one left block");
   const size_t total = (size_t)nl * t * t + (v ? t : 0);
   if (eks::sweep_supported(t)) {
@@ -384,7 +384,7 @@ eks_status tn_reduce(eks_ctx* ctx, int t, int nl, const double* const* L, const 
       }
       j0 += k;
     }
-    return allreduce(ctx, out, total);
+    return ar ? allreduce(ctx, out, total) : EKS_OK;
   }
   const size_t stride = eks::tn_partials_stride(t, nl, v != nullptr);
   ST(ensure_part(ctx, stride * ctx->nblk));
@@ -397,7 +397,7 @@ eks_status tn_reduce(eks_ctx* ctx, int t, int nl, const double* const* L, const 
     KScope k(ctx, EKS_K_REDUCE);
     CK(eks::launch_reduce(ctx->stream, ctx->part, ctx->nblk, stride, stride, out));
   }
-  return allreduce(ctx, out, stride);
+  return ar ? allreduce(ctx, out, stride) : EKS_OK;
 }
 
 // Zout = Zin − Σ_j Q_j C_j  (CGS update)
@@ -425,7 +425,7 @@ eks_status ts_update(eks_ctx* ctx, int t, int nq, const double* const* Q, const 
 
 // Fused CGS pass: Z1 = Z − Q C1 and C2 = (AQ)ᵀ Z1 in one sweep (nq ≤ 2 window of SRE-CG).
 eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, const double* const* AQ,
-                       const double* C1, const double* Z, double* Z1, double* C2) {
+                       const double* C1, const double* Z, double* Z1, double* C2, bool ar = true) {
   eks::SweepPtrs P{};
   for (int j = 0; j < nq; ++j) {
     P.q[j] = Q[j];
@@ -442,7 +442,7 @@ eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, cons
     CK(eks::launch_sweep(ctx->stream, t, nq, nq, false, ctx->n, Z, Z1, P, C1, nullptr, ctx->part, ctx->nblk,
                          tail(ctx, 0, C2, stride)));
   }
-  return allreduce(ctx, C2, stride);
+  return ar ? allreduce(ctx, C2, stride) : EKS_OK;
 }
 
 // Which fused SpMM+Gram kernel runs for this t: 4 plane-marching (stencil-structured A), 0 TMA-
@@ -463,12 +463,12 @@ int spmm_path_for(const eks_ctx* ctx, int t) {
 // (t ≤ 32; ctx->chol_fused tells the caller).  Several ranks: SpMM with halo overlap, then
 // the Gram sweep and an allreduce.
 eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const double* r, double* out,
-                     const eks::CholArgs* ch = nullptr) {
+                     const eks::CholArgs* ch = nullptr, bool ar = true) {
   ctx->chol_fused = false;
   if (ctx->nranks != 1 || !eks::sweep_supported(t)) {
     ST(spmm(ctx, X, Y, t));
     const double* L[1] = {X.loc};
-    return tn_reduce(ctx, t, 1, L, Y, r, out);
+    return tn_reduce(ctx, t, 1, L, Y, r, out, ar);
   }
   const size_t stride = eks::sweep_part_stride(t, 1, true);
   ST(ensure_part(ctx, stride * ctx->nblk));
@@ -521,6 +521,29 @@ eks_status cgs2(eks_ctx* ctx, int t, const std::vector<const double*>& Q, const 
     ST(tn_reduce(ctx, t, nq, AQ.data(), ctx->Z1.loc, nullptr, ctx->C2));
   }
   ST(ts_update(ctx, t, nq, Q.data(), ctx->C2, ctx->Z1.loc, Zout));  // Z2 = Z1 − Q C2
+  return EKS_OK;
+}
+
+// CGS2 of the s blocks V_i against the window with the reductions stacked: C1 of every block in
+// one allreduce, C2 of every block in a second one (same kernels and arithmetic order as cgs2()).
+eks_status cgs2_stacked(eks_ctx* ctx, int t, const std::vector<const double*>& Q,
+                        const std::vector<const double*>& AQ, std::vector<Block>& V, std::vector<Block>& V1) {
+  const int nq = (int)Q.size(), s = (int)V.size();
+  const size_t cb = (size_t)nq * t * t;
+  ST(ensure_C(ctx, cb * s));
+  for (int i = 0; i < s; ++i) ST(tn_reduce(ctx, t, nq, AQ.data(), V[i].loc, nullptr, ctx->C1 + cb * i, false));
+  ST(allreduce(ctx, ctx->C1, cb * s));
+  const bool fused = eks::sweep_supported(t) && eks::sweep_fused_supported(t, nq);
+  for (int i = 0; i < s; ++i) {
+    if (fused) {
+      ST(update_coef(ctx, t, nq, Q.data(), AQ.data(), ctx->C1 + cb * i, V[i].loc, V1[i].loc, ctx->C2 + cb * i, false));
+    } else {
+      ST(ts_update(ctx, t, nq, Q.data(), ctx->C1 + cb * i, V[i].loc, V1[i].loc));
+      ST(tn_reduce(ctx, t, nq, AQ.data(), V1[i].loc, nullptr, ctx->C2 + cb * i, false));
+    }
+  }
+  ST(allreduce(ctx, ctx->C2, cb * s));
+  for (int i = 0; i < s; ++i) ST(ts_update(ctx, t, nq, Q.data(), ctx->C2 + cb * i, V1[i].loc, V[i].loc));
   return EKS_OK;
 }
 
@@ -725,7 +748,7 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
     ST(dalloc(ctx, &ctx->Rca, (size_t)st * st));
     ST(dalloc(ctx, &ctx->Rinvca, (size_t)st * st));
     ST(dalloc(ctx, &ctx->alphaca, (size_t)st));
-    ST(dalloc(ctx, &ctx->Btmp, (size_t)s * t * t + t));
+    ST(dalloc(ctx, &ctx->Btmp, (size_t)s * (s + 1) / 2 * t * t + (size_t)s * t));
     ctx->ca_cap = st;
   }
   std::vector<const double*> Q, AQ;
@@ -750,28 +773,24 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
     ST(acholqr_block(ctx, t, V[0], AV[0].loc, nblocks));
   }
   for (int i = 1; i < s; ++i) ST(spmm(ctx, V[i - 1], V[i].loc, t));  // monomial powers
-  if (!Q.empty())
-    for (int i = 0; i < s; ++i) ST(cgs2(ctx, t, Q, AQ, V[i].loc, V[i].loc));
-  for (int i = 0; i < s; ++i) ST(spmm(ctx, V[i], AV[i].loc, t));
-  // Gram B (st×st, upper blocks) and g = Vᵀ r_{k−1}
+  if (!Q.empty()) ST(cgs2_stacked(ctx, t, Q, AQ, V, AV));  // AV serves as the pass-1 scratch
+  // Gram B (st×st, upper blocks) and g = Vᵀ r_{k−1}: block column j = [V_0..V_{j−1}]ᵀAV_j, then
+  // [V_jᵀAV_j | V_jᵀr] from the fused SpMM+Gram kernel that forms AV_j, into Btmp (column j at
+  // offset (j(j+1)/2)·t·t + j·t); ONE allreduce for all of them.
   std::vector<const double*> L(s);
   for (int i = 0; i < s; ++i) L[i] = V[i].loc;
-  auto place = [&](int i, int j) -> eks_status {
-    CK(cudaMemcpy2DAsync(ctx->Bca + (size_t)i * t * st + (size_t)j * t, sizeof(double) * st,
-                         ctx->Btmp + (size_t)i * t * t, sizeof(double) * t, sizeof(double) * t, t,
-                         cudaMemcpyDeviceToDevice, ctx->stream));
-    return EKS_OK;
-  };
+  auto off = [&](int j) { return (size_t)j * (j + 1) / 2 * t * t + (size_t)j * t; };
   for (int j = 0; j < s; ++j) {
-    if (j > 0) {
-      ST(tn_reduce(ctx, t, j, L.data(), AV[j].loc, nullptr, ctx->Btmp));
-      for (int i = 0; i < j; ++i) ST(place(i, j));
-    }
-    const double* Lj[1] = {V[j].loc};
-    ST(tn_reduce(ctx, t, 1, Lj, AV[j].loc, ctx->r, ctx->Btmp));
-    CK(cudaMemcpy2DAsync(ctx->Bca + (size_t)j * t * st + (size_t)j * t, sizeof(double) * st, ctx->Btmp,
-                         sizeof(double) * t, sizeof(double) * t, t, cudaMemcpyDeviceToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->gca + (size_t)j * t, ctx->Btmp + (size_t)t * t, sizeof(double) * t,
+    ST(spmm_gram(ctx, V[j], AV[j].loc, t, ctx->r, ctx->Btmp + off(j) + (size_t)j * t * t, nullptr, false));
+    if (j > 0) ST(tn_reduce(ctx, t, j, L.data(), AV[j].loc, nullptr, ctx->Btmp + off(j), false));
+  }
+  ST(allreduce(ctx, ctx->Btmp, off(s)));
+  for (int j = 0; j < s; ++j) {
+    for (int i = 0; i <= j; ++i)
+      CK(cudaMemcpy2DAsync(ctx->Bca + (size_t)i * t * st + (size_t)j * t, sizeof(double) * st,
+                           ctx->Btmp + off(j) + (size_t)i * t * t, sizeof(double) * t, sizeof(double) * t, t,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->gca + (size_t)j * t, ctx->Btmp + off(j) + (size_t)(j + 1) * t * t, sizeof(double) * t,
                        cudaMemcpyDeviceToDevice, ctx->stream));
   }
   {
@@ -794,8 +813,25 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
   Pw.flag = Pa.flag = Pu.flag = ctx->flag;
   {
     KScope kk(ctx, EKS_K_APPLY);
-    CK(eks::launch_ca_combine(ctx->stream, ctx->n, t, s, Pw, ctx->Rinvca, ctx->sms, false));
-    CK(eks::launch_ca_combine(ctx->stream, ctx->n, t, s, Pa, ctx->Rinvca, ctx->sms, false));
+    if (eks::sweep_supported(t) && s <= eks::sweep_max_blocks(t)) {
+      // W_j = 0 − Σ_{i≤j} V_i·(−R⁻¹_ij) on the DMMA update sweep (−R⁻¹ column blocks packed)
+      CK(eks::launch_ca_pack(ctx->stream, t, s, ctx->Rinvca, ctx->Btmp));
+      for (int j = 0; j < s; ++j) {
+        const double* C = ctx->Btmp + (size_t)j * (j + 1) / 2 * t * t;
+        eks::SweepPtrs Sw{}, Sa{};
+        for (int i = 0; i <= j; ++i) {
+          Sw.q[i] = Pw.in[i];
+          Sa.q[i] = Pa.in[i];
+        }
+        CK(eks::launch_sweep(ctx->stream, t, j + 1, 0, false, ctx->n, nullptr, Pw.out[j], Sw, C, nullptr, nullptr,
+                             ctx->nblk));
+        CK(eks::launch_sweep(ctx->stream, t, j + 1, 0, false, ctx->n, nullptr, Pa.out[j], Sa, C, nullptr, nullptr,
+                             ctx->nblk));
+      }
+    } else {
+      CK(eks::launch_ca_combine(ctx->stream, ctx->n, t, s, Pw, ctx->Rinvca, ctx->sms, false));
+      CK(eks::launch_ca_combine(ctx->stream, ctx->n, t, s, Pa, ctx->Rinvca, ctx->sms, false));
+    }
     CK(eks::launch_ca_update(ctx->stream, ctx->n, t, s, Pu, ctx->alphaca, ctx->xv.loc, ctx->r, ctx->rnew, ctx->part,
                              ctx->nblk));
     ctx->rho_nblk = ctx->nblk;

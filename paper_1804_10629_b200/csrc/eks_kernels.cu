@@ -854,8 +854,33 @@ cudaError_t launch_ca_combine(cudaStream_t st, int64_t n, int t, int s, const Ca
   return launch_k(k_ca_combine, (int)blocks, 256, sm, st, n, t, s, P, Rinv, skip_on_breakdown ? 1 : 0);
 }
 
+// Column block j of −R⁻¹ packed for the update sweeps (W_j = 0 − Σ_{i≤j} V_i·(−R⁻¹_ij)):
+// pack + (j(j+1)/2)·t·t holds the t×t blocks −R⁻¹_ij, i = 0..j, each row-major (row = column of V_i).
+__global__ void __launch_bounds__(256) k_ca_pack(int t, int s, const double* __restrict__ Rinv,
+                                                 double* __restrict__ pack) {
+  pdl_enter();
+  const int m = s * t, tt = t * t;
+  const int total = s * (s + 1) / 2 * tt;
+  for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < total; e += blockDim.x * gridDim.x) {
+    const int blk = e / tt, a = (e / t) % t, c = e % t;
+    int j = 0;
+    while ((j + 1) * (j + 2) / 2 <= blk) ++j;
+    const int i = blk - j * (j + 1) / 2;
+    pack[e] = -Rinv[(size_t)(i * t + a) * m + j * t + c];
+  }
+}
+
+cudaError_t launch_ca_pack(cudaStream_t st, int t, int s, const double* Rinv, double* pack) {
+  if (s * t > kCaMax || s > kCaMaxBlocks) return cudaErrorInvalidValue;
+  const int total = s * (s + 1) / 2 * t * t;
+  return launch_k(k_ca_pack, (total + 255) / 256, 256, 0, st, t, s, Rinv, pack);
+}
+
 // x += Σ_j W_j α_j, r −= Σ_j AW_j α_j (α = α̃ = R⁻ᵀ Vᵀr of the outer iteration), partial ‖r‖² per CTA;
 // nothing when the breakdown flag is set (x stays the last completed iterate).
+// A warp owns 32/L consecutive rows per step (L = the largest power of two ≤ min(t, 32) lanes per
+// row, ⌈t/L⌉ columns per lane):
+// coalesced block reads, then a butterfly over the L lanes of a row.
 __global__ void __launch_bounds__(256) k_ca_update(int64_t n, int t, int s, CaPtrs P, const double* __restrict__ alpha,
                                                    double* __restrict__ x, const double* __restrict__ r,
                                                    double* __restrict__ rnew, double* __restrict__ part) {
@@ -866,22 +891,38 @@ __global__ void __launch_bounds__(256) k_ca_update(int64_t n, int t, int s, CaPt
   const bool skip = *reinterpret_cast<const volatile int*>(P.flag) != INT_MAX;
   for (int e = threadIdx.x; e < m; e += blockDim.x) sa[e] = alpha[e];
   __syncthreads();
+  int L = 1;
+  while (2 * L <= t && 2 * L <= 32) L *= 2;
+  const int RPW = 32 / L, CPL = (t + L - 1) / L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int sub = lane / L, lc = lane % L;
   const int64_t lo = (int64_t)blockIdx.x * n / gridDim.x, hi = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
   double acc = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+  for (int64_t r0 = lo + (int64_t)warp * RPW; r0 < hi; r0 += (int64_t)nw * RPW) {
+    const int64_t i = r0 + sub;
+    const bool ok = i < hi;
     double dx = 0.0, dr = 0.0;
-    for (int j = 0; j < s; ++j)
-      for (int c = 0; c < t; ++c) {
-        dx = __fma_rn(P.in[j][i * t + c], sa[j * t + c], dx);
-        dr = __fma_rn(P.out[j][i * t + c], sa[j * t + c], dr);
-      }
-    double ri = r[i];
-    if (!skip) {
-      x[i] += dx;
-      ri -= dr;
+    if (ok)
+      for (int j = 0; j < s; ++j)
+        for (int q = 0; q < CPL; ++q) {
+          const int c = lc + q * L;
+          if (c >= t) break;
+          dx = __fma_rn(P.in[j][i * t + c], sa[j * t + c], dx);
+          dr = __fma_rn(P.out[j][i * t + c], sa[j * t + c], dr);
+        }
+    for (int o = L >> 1; o > 0; o >>= 1) {
+      dx += __shfl_xor_sync(0xffffffffu, dx, o);
+      dr += __shfl_xor_sync(0xffffffffu, dr, o);
     }
-    rnew[i] = ri;
-    acc = __fma_rn(ri, ri, acc);
+    if (ok && lc == 0) {
+      double ri = r[i];
+      if (!skip) {
+        x[i] += dx;
+        ri -= dr;
+      }
+      rnew[i] = ri;
+      acc = __fma_rn(ri, ri, acc);
+    }
   }
   const double tot = block_sum(acc, sred);
   if (threadIdx.x == 0) part[blockIdx.x] = tot;

@@ -77,6 +77,7 @@ cudaError_t launch_chol_dyn(cudaStream_t st, int m, const double* B, const doubl
 cudaError_t launch_ca_combine(cudaStream_t st, int64_t n, int t, int s, const CaPtrs& P, const double* Rinv,
                               int sms, bool skip_on_breakdown);
 // x += Σ_j in_j α_j, rnew = r − Σ_j out_j α_j (in = W, out = AW), partial ‖rnew‖² per CTA into part[nblk].
+cudaError_t launch_ca_pack(cudaStream_t st, int t, int s, const double* Rinv, double* pack);
 cudaError_t launch_ca_update(cudaStream_t st, int64_t n, int t, int s, const CaPtrs& P, const double* alpha,
                              double* x, const double* r, double* rnew, double* part, int nblk);
 

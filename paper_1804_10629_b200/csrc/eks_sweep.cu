@@ -73,7 +73,7 @@ __device__ __forceinline__ void vec_async(double* dst, const double* src, int64_
 
 // ----------------------------------------------------------------------------
 // Compile-time configuration of one sweep kernel.
-//   NQ: blocks in the update R = Zin − Σ_q Q_q C_q (0: R = Zin, no update)
+//   NQ: blocks in the update R = Zin − Σ_q Q_q C_q (0: R = Zin, no update; Zin == nullptr: 0)
 //   NL: left blocks of the partial Lᵀ R (0: none);  V: also L_0ᵀ v
 // ----------------------------------------------------------------------------
 // AL: the last left block is Zin itself (SRE-CG: Z = A·W_{j−1} = AQ_last), so it is streamed
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256, 1)
       const int64_t row = lo + (int64_t)i * K::TR;
       const int rows = (int)((hi - row) < K::TR ? (hi - row) : K::TR);
       double* st = sm + s * K::STAGE;
-      tile_async<T, S, K::TR>(st, Zin, row, rows);
+      if (Zin != nullptr) tile_async<T, S, K::TR>(st, Zin, row, rows);  // nullptr: R starts from 0
 #pragma unroll
       for (int j = 0; j < NQ; ++j) tile_async<T, S, K::TR>(st + (1 + j) * K::TILE, P.q[j], row, rows);
 #pragma unroll
@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(256, 1)
             dmma(d0, d1, sQ[(mi * 8 + g) * S + kk + q4], Cj[(kk + q4) * K::SC + ni * 8 + g]);
         }
         const int r = mi * 8 + g, c = ni * 8 + 2 * q4;
-        const double z0 = sZ[r * S + c] - d0, z1 = sZ[r * S + c + 1] - d1;
+        const double z0 = (Zin != nullptr ? sZ[r * S + c] : 0.0) - d0;
+        const double z1 = (Zin != nullptr ? sZ[r * S + c + 1] : 0.0) - d1;
         double* sOut = AL ? sRb : sZ;
         sOut[r * S + c] = z0;
         sOut[r * S + c + 1] = z1;
