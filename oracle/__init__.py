@@ -72,6 +72,11 @@ def lib():
         _lib.or_solve_ca.argtypes = [C.POINTER(_Csr), vp, vp, i32, i32, i32, i32, d, i32,
                                      C.POINTER(_Report), ITER_CB, vp]
         _lib.or_solve_ca.restype = i32
+        _lib.or_precholqr.argtypes = [C.POINTER(_Csr), i32, vp, vp, vp]
+        _lib.or_precholqr.restype = i32
+        _lib.or_solve_ex.argtypes = [C.POINTER(_Csr), vp, vp, i32, i32, i32, d, i32, i32, i32, i32,
+                                     C.POINTER(_Report), ITER_CB, vp]
+        _lib.or_solve_ex.restype = i32
     return _lib
 
 
@@ -151,9 +156,24 @@ def acholqr(A, Z: np.ndarray):
     return st, W, R, B
 
 
+def precholqr(A, Z: np.ndarray):
+    """Pre-CholQR (reading R30).  Returns (status, W, R) with Z = W·R."""
+    Z = _f64(Z)
+    t = Z.shape[1]
+    W = np.empty_like(Z)
+    R = np.empty((t, t))
+    ref = _CsrRef(A)
+    st = lib().or_precholqr(C.byref(ref.s), t, _p(Z), _p(W), _p(R))
+    return st, W, R
+
+
+ORTHO = {"acholqr": 0, "pre-cholqr": 1}
+
+
 def solve(A, b, method="sre-cg", s=1, t=1, tol=1e-8, kmax=5000, x0=None, mode=MODE_DEFINITION,
-          callback=None):
-    """Run or_solve; returns dict(x, outer_iters, converged, status, rho0, rho, true_relres, hist)."""
+          callback=None, ortho="acholqr", restructured=False):
+    """Run or_solve_ex; returns dict(x, outer_iters, converged, status, rho0, rho, true_relres, hist).
+    ortho: "acholqr" (default) or "pre-cholqr"; restructured: Alg 1/2 (SRE-CG2 / SRE-CG only)."""
     b = _f64(b)
     x = np.zeros(A.n) if x0 is None else _f64(x0).copy()
     hist = np.zeros(kmax + 1)
@@ -170,7 +190,8 @@ def solve(A, b, method="sre-cg", s=1, t=1, tol=1e-8, kmax=5000, x0=None, mode=MO
                      np.ctypeslib.as_array(rr, shape=(n,)).copy(), rho)
         cb = ITER_CB(_cb)
     m = METHODS[method] if isinstance(method, str) else int(method)
-    st = lib().or_solve(C.byref(ref.s), _p(b), _p(x), m, s, t, tol, kmax, mode, C.byref(rep), cb, None)
+    st = lib().or_solve_ex(C.byref(ref.s), _p(b), _p(x), m, s, t, tol, kmax, mode, ORTHO[ortho],
+                           int(bool(restructured)), C.byref(rep), cb, None)
     k = rep.outer_iters
     return dict(x=x, outer_iters=k, converged=bool(rep.converged), status=st, rho0=rep.rho0,
                 rho=rep.rho, true_relres=rep.true_relres, hist=hist[: k + 1].copy(),

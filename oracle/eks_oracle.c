@@ -187,6 +187,39 @@ int or_acholqr(const or_csr* A, int t, const double* Z, double* W, double* R, do
 }
 
 /* ------------------------------------------------------------------------ */
+/* Pre-CholQR — P:198 ("A-orthonormalized using A-CholQR or Pre-CholQR"),    */
+/* P:380 ("Pre-CholQR is numerically more stable than A-CholQR"); the cited */
+/* thesis's Algorithm 23 is not in the paper, so the standard definition    */
+/* (reading R30): a Euclidean CholQR of Z (G = ZᵀZ = R1ᵀR1, */
+/* Z1 = Z R1⁻¹), then A-CholQR of Z1 (R2); Z = W·R with R = R2·R1.           */
+/* ------------------------------------------------------------------------ */
+int or_precholqr(const or_csr* A, int t, const double* Z, double* W, double* R) {
+  int64_t n = A->n;
+  double* G = dalloc((size_t)t * t);
+  double* R1 = dalloc((size_t)t * t);
+  double* R2 = dalloc((size_t)t * t);
+  double* Z1 = dalloc((size_t)n * t);
+  or_xty(n, t, Z, t, Z, G);
+  for (int i = 0; i < t; ++i)
+    for (int j = 0; j < i; ++j) G[i * t + j] = 0.0;
+  int st = or_chol(t, G, R1);
+  if (st == OR_OK) {
+    rsolve_rows(n, t, R1, Z, Z1);
+    st = or_acholqr(A, t, Z1, W, R2, NULL);
+  }
+  if (st == OR_OK && R) {
+    for (int i = 0; i < t; ++i)
+      for (int j = 0; j < t; ++j) {
+        double v = 0.0;
+        for (int k = i; k <= j; ++k) v += R2[i * t + k] * R1[k * t + j];
+        R[i * t + j] = j >= i ? v : 0.0;
+      }
+  }
+  free(G); free(R1); free(R2); free(Z1);
+  return st;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Block list (the Q of Alg 3/6 or the 2-block window of Alg 4)              */
 /* ------------------------------------------------------------------------ */
 typedef struct {
@@ -237,8 +270,17 @@ static void bl_trim(blist* L, int method) {
 /* ------------------------------------------------------------------------ */
 int or_solve(const or_csr* A, const double* b, double* x, int method, int s, int t,
              double eps, int kmax, int mode, or_report* rep, or_iter_cb cb, void* user) {
+  return or_solve_ex(A, b, x, method, s, t, eps, kmax, mode, OR_ORTHO_ACHOLQR, 0, rep, cb, user);
+}
+
+int or_solve_ex(const or_csr* A, const double* b, double* x, int method, int s, int t,
+                double eps, int kmax, int mode, int ortho, int restructured, or_report* rep,
+                or_iter_cb cb, void* user) {
   int64_t n = A->n;
   if (s < 1 || t < 1 || t > n || !(eps >= 0.0) || method < 0 || method > 2) return OR_BADARG;
+  if (ortho != OR_ORTHO_ACHOLQR && ortho != OR_ORTHO_PRE) return OR_BADARG;
+  /* restructured Alg 1/2 exist for SRE-CG2 / SRE-CG only (no restructured MSDO-CG) */
+  if (restructured && method == OR_MSDO_CG) return OR_BADARG;
   size_t blk = (size_t)n * (size_t)t;
 
   double* r = dalloc((size_t)n);
@@ -287,7 +329,7 @@ int or_solve(const or_csr* A, const double* b, double* x, int method, int s, int
       if (mode == OR_MODE_DEFINITION) {
         /* "A-orthonormalize W against Q" (CGS2), then "A-orthonormalize W" (A-CholQR). */
         if (nq > 0) or_cgs2(A, t, nq, (const double* const*)(Q.W + w0), Z, NULL, NULL);
-        int st = or_acholqr(A, t, Z, W, R, NULL);
+        int st = ortho == OR_ORTHO_PRE ? or_precholqr(A, t, Z, W, R) : or_acholqr(A, t, Z, W, R, NULL);
         if (st != OR_OK) { status = OR_BREAKDOWN; free(Z); free(W); ok = 0; break; }
         AW = dalloc(1);
       } else {
@@ -299,6 +341,15 @@ int or_solve(const or_csr* A, const double* b, double* x, int method, int s, int
           for (int pass = 0; pass < 2; ++pass)
             cgs_pass_from_AZ(n, t, nq, (const double* const*)(Q.W + w0),
                              (const double* const*)(Q.AW + w0), Z, Z, Cb);
+        }
+        if (ortho == OR_ORTHO_PRE) {
+          /* Pre-CholQR's Euclidean stage on the explicit block: Z ← Z R1⁻¹ (reading R30) */
+          or_xty(n, t, Z, t, Z, B);
+          for (int a = 0; a < t; ++a)
+            for (int c = 0; c < a; ++c) B[a * t + c] = 0.0;
+          if (or_chol(t, B, R) != OR_OK) { status = OR_BREAKDOWN; free(Z); free(W); ok = 0; break; }
+          rsolve_rows(n, t, R, Z, W);
+          memcpy(Z, W, sizeof(double) * blk);
         }
         double* AZ = dalloc(blk);
         or_spmm(A, t, Z, AZ);
@@ -324,7 +375,30 @@ int or_solve(const or_csr* A, const double* b, double* x, int method, int s, int
       /* blocks already pushed belong to Q; nothing else to release here */
       break;
     }
-    if (mode == OR_MODE_DEFINITION) {
+    if (restructured) {
+      /* Alg 1 / Alg 2 lines 14-17: for i = k..k+s-1,
+       * alpha~ = W_iᵀ r_{i-1}, x_i = x_{i-1} + W_i alpha~, r_i = r_{i-1} − A W_i alpha~
+       * (definition: A·(W_i alpha~) as one SpMV, reading R9; mirror: cached A W_i). */
+      for (int i = 0; i < s; ++i) {
+        double* a = alpha + (size_t)i * t;
+        or_xty(n, t, V[i], 1, r, a);
+        for (int64_t row = 0; row < n; ++row) {
+          double acc = 0.0;
+          for (int c = 0; c < t; ++c) acc += V[i][row * t + c] * a[c];
+          u[row] = acc;
+        }
+        if (mode == OR_MODE_DEFINITION) {
+          or_spmm(A, 1, u, tmp);
+        } else {
+          for (int64_t row = 0; row < n; ++row) {
+            double acc = 0.0;
+            for (int c = 0; c < t; ++c) acc += AV[i][row * t + c] * a[c];
+            tmp[row] = acc;
+          }
+        }
+        for (int64_t row = 0; row < n; ++row) { x[row] += u[row]; r[row] -= tmp[row]; }
+      }
+    } else if (mode == OR_MODE_DEFINITION) {
       /* alpha~ = Vᵀ r_{k-1};  x_k = x_{k-1} + V alpha~;  r_k = r_{k-1} − A V alpha~
        * (Alg 3, Alg 4, Alg 6).  Reading R9:
        * u = V alpha~ first, then r −= A·u. */

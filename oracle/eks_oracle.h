@@ -30,6 +30,7 @@ typedef struct {
 enum { OR_SRE_CG = 0, OR_SRE_CG2 = 1, OR_MSDO_CG = 2 };
 enum { OR_OK = 0, OR_BREAKDOWN = 7, OR_MAXITER = 8, OR_BADARG = 1 };
 enum { OR_MODE_DEFINITION = 0, OR_MODE_MIRROR = 1 };
+enum { OR_ORTHO_ACHOLQR = 0, OR_ORTHO_PRE = 1 };
 
 /* Per-outer-iteration hook for the invariant pins (tests only).
  * V is the n×(s·t) basis of this outer iteration, row-major; alpha = Vᵀr_{k-1};
@@ -71,10 +72,24 @@ void or_cgs2(const or_csr* A, int t, int nq, const double* const* Q, double* Z,
  * B = upper(Zᵀ(A·Z)), B = RᵀR, W = Z·R⁻¹ (row-wise forward substitution). */
 int or_acholqr(const or_csr* A, int t, const double* Z, double* W, double* R, double* B);
 
+/* Pre-CholQR "A-orthonormalize W" (reading R30): Euclidean CholQR of Z
+ * (G = upper(ZᵀZ) = R1ᵀR1, Z1 = Z·R1⁻¹), then A-CholQR of Z1 (R2); W = Z1·R2⁻¹ and
+ * R = R2·R1 (so Z = W·R).  OR_BREAKDOWN from either Cholesky. */
+int or_precholqr(const or_csr* A, int t, const double* Z, double* W, double* R);
+
 /* Solve with s-step SRE-CG (Alg 4), SRE-CG2 (Alg 3) or
  * MSDO-CG (Alg 6).  x holds x0 on entry, x_k on exit. */
 int or_solve(const or_csr* A, const double* b, double* x, int method, int s, int t,
              double eps, int kmax, int mode, or_report* rep, or_iter_cb cb, void* user);
+
+/* or_solve with the self-orthonormalization chosen (ortho = OR_ORTHO_ACHOLQR | OR_ORTHO_PRE,
+ * P:198) and, for SRE-CG / SRE-CG2, the restructured Alg 2 / Alg 1 (restructured = 1,
+ * P:58-120): the same s blocks, then s sequential updates alpha~_i = W_iᵀ r_{i-1},
+ * x_i = x_{i-1} + W_i alpha~_i, r_i = r_{i-1} − A W_i alpha~_i; convergence tested once per s.
+ * MSDO-CG has no restructured form → OR_BADARG. */
+int or_solve_ex(const or_csr* A, const double* b, double* x, int method, int s, int t,
+                double eps, int kmax, int mode, int ortho, int restructured, or_report* rep,
+                or_iter_cb cb, void* user);
 
 /* Communication-avoiding s-step enlarged CG: CA SRE-CG, CA SRE-CG2
  * (method 0 / 1) and CA MSDO-CG (method 2) with the CA-Arnoldi
