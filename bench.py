@@ -218,7 +218,8 @@ def oracle_sample(p, iters: int):
     if p.method.startswith("ca-"):
         r = oracle.solve_ca(p.A, p.b, p.method[3:], arnoldi=p.arnoldi, s=p.s, t=p.t, tol=0.0, kmax=iters + 1)
     else:
-        r = oracle.solve(p.A, p.b, p.method, p.s, p.t, 0.0, kmax=iters + 1)
+        r = oracle.solve(p.A, p.b, p.method, p.s, p.t, 0.0, kmax=iters + 1, ortho=getattr(p, "ortho", "acholqr"),
+                         restructured=getattr(p, "restructured", False))
     dt = time.perf_counter() - t0
     return r["outer_iters"], dt
 
@@ -231,6 +232,8 @@ def problem_of(args):
     if args.s:
         p = dataclasses.replace(p, s=args.s)
     p.arnoldi = args.arnoldi if p.method.startswith("ca-") else 0
+    p.ortho = args.ortho
+    p.restructured = args.restructured
     return p
 
 
@@ -262,7 +265,10 @@ def run_reference(args):
 
 
 def config_of(args, p, N):
-    kind = f"CA (Alg {p.arnoldi})" if p.method.startswith("ca-") else "s-step"
+    kind = f"CA (Alg {p.arnoldi})" if p.method.startswith("ca-") else \
+        ("restructured" if getattr(p, "restructured", False) else "s-step")
+    if getattr(p, "ortho", "acholqr") != "acholqr":
+        kind += f" + {p.ortho}"
     return {"workload": f"{p.name}: {p.note}; {kind} {p.method}, s={p.s}, t={p.t}, tol={p.tol:g}",
             "n": p.A.n, "nnz": p.A.nnz, "method": p.method, "s": p.s, "t": p.t, "tol": p.tol,
             "parallelism": f"row-slabs x{N} (t/N domains per GPU)",
@@ -287,6 +293,8 @@ def main():
     ap.add_argument("--s", type=int, default=0, help="blocks per outer iteration s (cfg5, or override)")
     ap.add_argument("--method", default="", help="override the workload's method (e.g. ca-sre-cg)")
     ap.add_argument("--arnoldi", type=int, default=7, help="CA variants: Alg 5 or Alg 7")
+    ap.add_argument("--ortho", default="acholqr", choices=["acholqr", "pre-cholqr"])
+    ap.add_argument("--restructured", action="store_true", help="restructured Alg 2 / Alg 1 (SRE-CG / SRE-CG2)")
     ap.add_argument("--cfg5-n", type=int, default=384, help="cfg5 grid size (384 = BASELINE configs[4])")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -341,7 +349,8 @@ def main():
         with torch.cuda.stream(stream):
             x.zero_()
         st, rep = eks.eks_solve_ex(solver.ctx, p.method, p.s, p.t, p.tol, b, x, profile=profile,
-                                   max_outer=args.max_outer, arnoldi=p.arnoldi)
+                                   max_outer=args.max_outer, arnoldi=p.arnoldi, ortho=p.ortho,
+                                   restructured=p.restructured)
         if st not in ((0, 8) if args.max_outer else (0,)):
             raise SystemExit(f"solve failed: {eks.STATUS.get(st)} {eks.eks_error_string(solver.ctx)}")
         return rep
@@ -442,7 +451,8 @@ def main():
         for k in range(args.steps):
             e2e_solver.setup(n, lo, hi, hrp, hcol, hval)
             hx[:] = 0.0
-            st, rep = eks.eks_solve_ex(e2e_solver.ctx, p.method, p.s, p.t, p.tol, hb, hx, arnoldi=p.arnoldi)
+            st, rep = eks.eks_solve_ex(e2e_solver.ctx, p.method, p.s, p.t, p.tol, hb, hx, arnoldi=p.arnoldi,
+                                       ortho=p.ortho, restructured=p.restructured)
             e_outer += rep["outer_iters"]
         torch.cuda.synchronize()
         barrier()

@@ -88,7 +88,13 @@ typedef struct {
   int profile;            /* 1: record per-kernel-class CUDA events (see eks_profile) */
   int arnoldi;            /* CA methods: 7 = modified CA-Arnoldi (Alg 7, default when 0),
                              5 = CA-Arnoldi (Alg 5) */
-  int reserved[7];
+  int ortho;              /* self-orthonormalization of each block: 0 = A-CholQR
+                             (default), 1 = Pre-CholQR (Euclidean CholQR, then A-CholQR; DESIGN
+                             R30).  s-step methods only (CA methods: EKS_ERR_INVALID_ARG) */
+  int restructured;       /* 1: restructured SRE-CG / SRE-CG2 (Alg 2 / Alg 1; DESIGN R31):
+                             the same s blocks, then s sequential updates with α̃_i = W_iᵀ r_{i-1};
+                             MSDO-CG and CA methods: EKS_ERR_INVALID_ARG */
+  int reserved[5];
 } eks_options;
 
 /* Per-kernel-class device time accumulated while options.profile == 1. */

@@ -81,8 +81,11 @@ struct eks_ctx {
   // Gram / factor / inverse, g = Vᵀr and α̃
   std::vector<Block> Vca, AVca;
   double *Bca = nullptr, *gca = nullptr, *Rca = nullptr, *Rinvca = nullptr, *alphaca = nullptr, *Btmp = nullptr;
+  double* cawork = nullptr;  // global workspace of the st×st Cholesky when st > kCaSmem
   int ca_cap = 0;  // st the buffers were sized for
   int chol_mode = 0;               // 0 one-warp Cholesky launch (default), 1 in the SpMM kernel's tail (EKS_CHOL)
+  int ortho = 0;                   // 0 A-CholQR, 1 Pre-CholQR (eks_options.ortho, reading R30)
+  double* pre = nullptr;           // Pre-CholQR / restructured scratch: [G | R1⁻¹ | −R1⁻¹ | g] (3t²+t)
   // workspace, keyed by t
   int ws_t = 0;
   std::vector<Block> Wpool, AWpool;  // Wpool ext layout, AWpool local
@@ -223,7 +226,10 @@ void free_workspace(eks_ctx* c) {
   for (auto& b : c->AVca) dfree(b.base);
   c->Vca.clear();
   c->AVca.clear();
-  for (double** p : {&c->Bca, &c->gca, &c->Rca, &c->Rinvca, &c->alphaca, &c->Btmp}) { dfree(*p); *p = nullptr; }
+  for (double** p : {&c->Bca, &c->gca, &c->Rca, &c->Rinvca, &c->alphaca, &c->Btmp, &c->pre, &c->cawork}) {
+    dfree(*p);
+    *p = nullptr;
+  }
   c->ca_cap = 0;
   for (auto& b : c->Wpool) dfree(b.base);
   for (auto& b : c->AWpool) dfree(b.base);
@@ -258,6 +264,7 @@ eks_status ensure_workspace(eks_ctx* ctx, int t, int s) {
   ST(dalloc(ctx, &ctx->Bg, (size_t)t * t + t));
   ST(dalloc(ctx, &ctx->Rm, (size_t)t * t));
   ST(dalloc(ctx, &ctx->Rinv, (size_t)t * t));
+  ST(dalloc(ctx, &ctx->pre, (size_t)3 * t * t + t));
   ST(dalloc(ctx, &ctx->scal, 16));
   if (!ctx->flag) CK(cudaMalloc((void**)&ctx->flag, sizeof(int) * 4));
   if (!ctx->cnt) {
@@ -627,6 +634,58 @@ Window window_for(eks_ctx* ctx, int method, int nblocks, int ring) {
   return w;
 }
 
+// Pre-CholQR's Euclidean stage on Z (in place): G = ZᵀZ = R1ᵀR1, Z ← Z R1⁻¹ (reading R30).
+// AZ is scratch (overwritten later by A·Z) for the t the update sweep does not cover.
+eks_status pre_euclid(eks_ctx* ctx, int t, const Block& Z, double* AZ, int gb) {
+  double* G = ctx->pre;
+  double* R1inv = G + (size_t)t * t;
+  double* pack = R1inv + (size_t)t * t;
+  const double* L[1] = {Z.loc};
+  ST(tn_reduce(ctx, t, 1, L, Z.loc, nullptr, G));
+  {
+    KScope k(ctx, EKS_K_CHOL);
+    CK(eks::launch_chol_fast(ctx->stream, t, G, nullptr, ctx->Rm, R1inv, nullptr, ctx->flag, gb));
+  }
+  KScope k(ctx, EKS_K_APPLY);
+  account(ctx, EKS_K_APPLY, 16.0 * ctx->n * t, 2.0 * ctx->n * t * t);
+  if (eks::sweep_supported(t)) {  // Z = 0 − Z·(−R1⁻¹) on the DMMA update sweep
+    CK(eks::launch_ca_pack(ctx->stream, t, 1, R1inv, pack));
+    eks::SweepPtrs P{};
+    P.q[0] = Z.loc;
+    CK(eks::launch_sweep(ctx->stream, t, 1, 0, false, ctx->n, nullptr, Z.loc, P, pack, nullptr, nullptr, ctx->nblk));
+  } else {
+    CK(eks::launch_apply(ctx->stream, t, ctx->n, Z.loc, AZ, R1inv, nullptr, nullptr, nullptr, nullptr, nullptr,
+                         nullptr, nullptr, 4, ctx->nblk));
+  }
+  return EKS_OK;
+}
+
+// Restructured update of one block (Alg 1/2 lines 14-17, reading R31): g = W_iᵀ r_{i−1},
+// x += W_i g, r_i = r_{i−1} − AW_i g (and the per-CTA partials of ‖r_i‖²).
+eks_status restructured_update(eks_ctx* ctx, int t, const double* W, const double* AW, const double* rin,
+                               double* rout) {
+  double* g = ctx->pre + (size_t)3 * t * t;
+  {
+    KScope k(ctx, EKS_K_COEF);
+    account(ctx, EKS_K_COEF, 8.0 * ctx->n * (t + 1), 2.0 * ctx->n * t);
+    CK(eks::launch_wtv(ctx->stream, ctx->n, t, W, rin, ctx->part, ctx->nblk));
+  }
+  {
+    KScope k(ctx, EKS_K_REDUCE);
+    CK(eks::launch_reduce(ctx->stream, ctx->part, ctx->nblk, t, t, g));
+  }
+  ST(allreduce(ctx, g, t));
+  eks::CaPtrs P{};
+  P.in[0] = W;
+  P.out[0] = const_cast<double*>(AW);
+  P.flag = ctx->flag;
+  KScope k(ctx, EKS_K_APPLY);
+  account(ctx, EKS_K_APPLY, 8.0 * ctx->n * (2.0 * t + 4.0), 4.0 * ctx->n * t);
+  CK(eks::launch_ca_update(ctx->stream, ctx->n, t, 1, P, g, ctx->xv.loc, rin, rout, ctx->part, ctx->nblk));
+  ctx->rho_nblk = ctx->nblk;
+  return EKS_OK;
+}
+
 // One A-orthonormalized block: Zsrc (or the split of r) → W_new, AW_new, R⁻¹, alpha_b.
 eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bool seed_from_r, const double* Zsrc,
                       Block* Wn, Block* AWn, int alpha_off, int gb, int mode) {
@@ -645,6 +704,7 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
   } else if (Zsrc != Wn->loc) {
     CK(cudaMemcpyAsync(Wn->loc, Zsrc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  if (ctx->ortho == 1) ST(pre_euclid(ctx, t, *Wn, AWn->loc, gb));  // Pre-CholQR (reading R30)
   // "A-orthonormalize W": A-CholQR with one SpMM of Z2 (AW = (A Z2) R⁻¹)
   const bool with_update = !(mode & 4);
   eks::CholArgs ch{};
@@ -733,7 +793,7 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
   if (ctx->ca_cap != st || (int)ctx->Vca.size() != s) {
     for (auto& b : ctx->Vca) dfree(b.base);
     for (auto& b : ctx->AVca) dfree(b.base);
-    for (double** p : {&ctx->Bca, &ctx->gca, &ctx->Rca, &ctx->Rinvca, &ctx->alphaca, &ctx->Btmp}) {
+    for (double** p : {&ctx->Bca, &ctx->gca, &ctx->Rca, &ctx->Rinvca, &ctx->alphaca, &ctx->Btmp, &ctx->cawork}) {
       dfree(*p);
       *p = nullptr;
     }
@@ -749,6 +809,7 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
     ST(dalloc(ctx, &ctx->Rinvca, (size_t)st * st));
     ST(dalloc(ctx, &ctx->alphaca, (size_t)st));
     ST(dalloc(ctx, &ctx->Btmp, (size_t)s * (s + 1) / 2 * t * t + (size_t)s * t));
+    if (eks::chol_dyn_work(st)) ST(dalloc(ctx, &ctx->cawork, eks::chol_dyn_work(st)));
     ctx->ca_cap = st;
   }
   std::vector<const double*> Q, AQ;
@@ -796,7 +857,7 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
   {
     KScope kk(ctx, EKS_K_CHOL);
     CK(eks::launch_chol_dyn(ctx->stream, st, ctx->Bca, ctx->gca, ctx->Rca, ctx->Rinvca, ctx->alphaca, ctx->flag,
-                            nblocks));
+                            nblocks, ctx->cawork));
   }
   // W = V R⁻¹, AW = AV R⁻¹ into the new slots
   eks::CaPtrs Pw{}, Pa{}, Pu{};
@@ -813,20 +874,26 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
   Pw.flag = Pa.flag = Pu.flag = ctx->flag;
   {
     KScope kk(ctx, EKS_K_APPLY);
-    if (eks::sweep_supported(t) && s <= eks::sweep_max_blocks(t)) {
-      // W_j = 0 − Σ_{i≤j} V_i·(−R⁻¹_ij) on the DMMA update sweep (−R⁻¹ column blocks packed)
+    if (eks::sweep_supported(t)) {
+      // W_j = 0 − Σ_{i≤j} V_i·(−R⁻¹_ij) on the DMMA update sweep (−R⁻¹ column blocks packed),
+      // in chunks of at most sweep_max_blocks(t) input blocks accumulated into W_j
       CK(eks::launch_ca_pack(ctx->stream, t, s, ctx->Rinvca, ctx->Btmp));
+      const int maxb = eks::sweep_max_blocks(t);
       for (int j = 0; j < s; ++j) {
         const double* C = ctx->Btmp + (size_t)j * (j + 1) / 2 * t * t;
-        eks::SweepPtrs Sw{}, Sa{};
-        for (int i = 0; i <= j; ++i) {
-          Sw.q[i] = Pw.in[i];
-          Sa.q[i] = Pa.in[i];
+        for (int c0 = 0; c0 <= j; c0 += maxb) {
+          const int kb = std::min(maxb, j + 1 - c0);
+          eks::SweepPtrs Sw{}, Sa{};
+          for (int i = 0; i < kb; ++i) {
+            Sw.q[i] = Pw.in[c0 + i];
+            Sa.q[i] = Pa.in[c0 + i];
+          }
+          const double* Ck = C + (size_t)c0 * t * t;
+          CK(eks::launch_sweep(ctx->stream, t, kb, 0, false, ctx->n, c0 ? Pw.out[j] : nullptr, Pw.out[j], Sw, Ck,
+                               nullptr, nullptr, ctx->nblk));
+          CK(eks::launch_sweep(ctx->stream, t, kb, 0, false, ctx->n, c0 ? Pa.out[j] : nullptr, Pa.out[j], Sa, Ck,
+                               nullptr, nullptr, ctx->nblk));
         }
-        CK(eks::launch_sweep(ctx->stream, t, j + 1, 0, false, ctx->n, nullptr, Pw.out[j], Sw, C, nullptr, nullptr,
-                             ctx->nblk));
-        CK(eks::launch_sweep(ctx->stream, t, j + 1, 0, false, ctx->n, nullptr, Pa.out[j], Sa, C, nullptr, nullptr,
-                             ctx->nblk));
       }
     } else {
       CK(eks::launch_ca_combine(ctx->stream, ctx->n, t, s, Pw, ctx->Rinvca, ctx->sms, false));
@@ -1335,6 +1402,12 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   const int base = ca ? method - EKS_CA_SRE_CG : method;
   const int arnoldi = (opt && opt->arnoldi) ? opt->arnoldi : 7;
   if (ca && (arnoldi != 5 && arnoldi != 7)) return fail(ctx, EKS_ERR_INVALID_ARG, "arnoldi must be 5 or 7");
+  const int ortho = opt ? opt->ortho : 0;
+  const bool restr = opt && opt->restructured;
+  if (ortho != 0 && ortho != 1) return fail(ctx, EKS_ERR_INVALID_ARG, "ortho must be 0 (A-CholQR) or 1 (Pre-CholQR)");
+  if (ca && ortho) return fail(ctx, EKS_ERR_INVALID_ARG, "Pre-CholQR is for the s-step methods");
+  if (restr && method != EKS_SRE_CG && method != EKS_SRE_CG2)
+    return fail(ctx, EKS_ERR_INVALID_ARG, "restructured exists for SRE-CG and SRE-CG2 only (P:729)");
   if (ca && (s * t > eks::kCaMax || s > eks::kCaMaxBlocks))
     return fail(ctx, EKS_ERR_INVALID_ARG, "CA methods need s*t <= %d and s <= %d", eks::kCaMax, eks::kCaMaxBlocks);
   if (s < 1 || !valid_t(t) || t > ctx->n_global) return fail(ctx, EKS_ERR_INVALID_ARG, "bad s=%d or t=%d", s, t);
@@ -1351,7 +1424,10 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   begin_run(ctx, opt);
   auto wall0 = std::chrono::steady_clock::now();
   ST(ensure_workspace(ctx, t, s));
-  const int ring = (method == EKS_SRE_CG) ? 3 : (method == EKS_CA_SRE_CG ? 2 * s + 1 : 0);
+  // ring slots: SRE-CG keeps its 2-block window + the new block (restructured: the s blocks of
+  // the outer iteration until their updates), CA SRE-CG the (s+1)-block window + s new blocks
+  const int ring = (method == EKS_SRE_CG) ? (restr ? std::max(3, s + 1) : 3) : (method == EKS_CA_SRE_CG ? 2 * s + 1 : 0);
+  ctx->ortho = ortho;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -1391,11 +1467,19 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
       ST(as);
       const bool seed = (i == 0) && (method == EKS_MSDO_CG || k == 1);
       const double* Zsrc = seed ? nullptr : ctx->AWpool[ring ? (nblocks - 1) % ring : nblocks - 1].loc;
-      const int mode = (i == 0 ? 1 : 0) | (i == s - 1 ? 2 : 0);
+      const int mode = restr ? 4 : (i == 0 ? 1 : 0) | (i == s - 1 ? 2 : 0);
       ST(make_block(ctx, t, method, ring, nblocks, seed, Zsrc, Wn, AWn, i * t, nblocks, mode));
       ++nblocks;
     }
     if (status == EKS_ERR_OOM) break;
+    if (restr) {  // Alg 1/2 lines 14-17: s sequential updates (skipped on a breakdown flag)
+      for (int i = 0; i < s; ++i) {
+        const int j = nblocks - s + i, idx = ring ? j % ring : j;
+        ST(restructured_update(ctx, t, ctx->Wpool[idx].loc, ctx->AWpool[idx].loc, i == 0 ? ctx->r : ctx->rnew,
+                               ctx->rnew));
+      }
+      ctx->rho_fused = false;
+    }
     if (ctx->rho_fused) ST(allreduce(ctx, ctx->scal + 1, 1));
     else ST(reduce_scalar(ctx, ctx->scal + 1));
     ST(sync_scalars(ctx, 2));

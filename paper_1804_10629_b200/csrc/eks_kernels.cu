@@ -732,15 +732,15 @@ cudaError_t launch_apply(cudaStream_t st, int t, int64_t n, double* Z2W, double*
 // Cholesky of the m×m Gram (m = s·t ≤ kCaMax), R⁻¹ and α̃ = R⁻ᵀ g: k_chol's right-looking
 // elimination (R bitwise equal to the oracle's or_chol for equal B, reading R20) at run-time size.
 template <bool G>
-__global__ void __launch_bounds__(256) k_chol_dyn(int m, const double* __restrict__ B, const double* __restrict__ g,
-                                                  double* __restrict__ Rout, double* __restrict__ Rinv,
-                                                  double* __restrict__ alpha, int* flag, int gblock) {
+__global__ void __launch_bounds__(1024) k_chol_dyn(int m, const double* __restrict__ B, const double* __restrict__ g,
+                                                   double* __restrict__ Rout, double* __restrict__ Rinv,
+                                                   double* __restrict__ alpha, int* flag, int gblock, double* gwork) {
   pdl_enter();
   extern __shared__ double csm[];
   const int M1 = m + 1;
-  double* sA = csm;            // m × (m+1)
-  double* sY = csm + m * M1;   // m × (m+1)
-  __shared__ double sred[8];
+  double* sA = gwork ? gwork : csm;  // m × (m+1): shared memory, or global above kCaSmem columns
+  double* sY = sA + m * M1;          // m × (m+1)
+  __shared__ double sred[32];
   __shared__ int sfail;
   const int tid = threadIdx.x, nth = blockDim.x;
   double mx = 0.0;
@@ -803,16 +803,21 @@ __global__ void __launch_bounds__(256) k_chol_dyn(int m, const double* __restric
   if (tid == 0 && sfail && flag) atomicMin(flag, gblock);
 }
 
+size_t chol_dyn_work(int m) { return m > kCaSmem ? (size_t)2 * m * (m + 1) : 0; }
+
 cudaError_t launch_chol_dyn(cudaStream_t st, int m, const double* B, const double* g, double* R, double* Rinv,
-                            double* alpha, int* flag, int gblock) {
+                            double* alpha, int* flag, int gblock, double* work) {
   if (m < 1 || m > kCaMax) return cudaErrorInvalidValue;
-  const size_t sm = (size_t)2 * m * (m + 1) * 8;
+  const bool glob = m > kCaSmem;
+  if (glob && !work) return cudaErrorInvalidValue;
+  const size_t sm = glob ? 0 : (size_t)2 * m * (m + 1) * 8;
+  const int nth = glob ? 1024 : 256;
   if (g) {
-    cudaFuncSetAttribute(k_chol_dyn<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    return launch_k(k_chol_dyn<true>, 1, 256, sm, st, m, B, g, R, Rinv, alpha, flag, gblock);
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_chol_dyn<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    return launch_k(k_chol_dyn<true>, 1, nth, sm, st, m, B, g, R, Rinv, alpha, flag, gblock, glob ? work : nullptr);
   }
-  cudaFuncSetAttribute(k_chol_dyn<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  return launch_k(k_chol_dyn<false>, 1, 256, sm, st, m, B, g, R, Rinv, alpha, flag, gblock);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_chol_dyn<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  return launch_k(k_chol_dyn<false>, 1, nth, sm, st, m, B, g, R, Rinv, alpha, flag, gblock, glob ? work : nullptr);
 }
 
 // out_j = Σ_{i ≤ j} in_i · Rinv[i·t.., j·t..] for the s blocks (W = V R⁻¹ and AW = AV R⁻¹ of the
@@ -852,6 +857,46 @@ cudaError_t launch_ca_combine(cudaStream_t st, int64_t n, int t, int s, const Ca
   int64_t blocks = (n + rows_per - 1) / rows_per;
   if (blocks > (int64_t)sms * 4) blocks = (int64_t)sms * 4;
   return launch_k(k_ca_combine, (int)blocks, 256, sm, st, n, t, s, P, Rinv, skip_on_breakdown ? 1 : 0);
+}
+
+// Per-CTA partials of Wᵀv (t values per CTA, part[b·t + c]) over the CTA's contiguous rows; a
+// warp owns 32/L consecutive rows per step (coalesced), fixed-order lane/warp reductions.
+__global__ void __launch_bounds__(256) k_wtv(int64_t n, int t, const double* __restrict__ W,
+                                             const double* __restrict__ v, double* __restrict__ part) {
+  pdl_enter();
+  __shared__ double sacc[8][64];
+  int L = 1;
+  while (2 * L <= t && 2 * L <= 32) L *= 2;
+  const int RPW = 32 / L, CPL = (t + L - 1) / L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / L, lc = lane % L;
+  const int64_t lo = (int64_t)blockIdx.x * n / gridDim.x, hi = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t r0 = lo + (int64_t)warp * RPW; r0 < hi; r0 += 8 * RPW) {
+    const int64_t i = r0 + sub;
+    if (i < hi) {
+      const double vi = v[i];
+      for (int q = 0; q < CPL; ++q) {
+        const int c = lc + q * L;
+        if (c < t) acc[q] = __fma_rn(W[i * t + c], vi, acc[q]);
+      }
+    }
+  }
+  for (int q = 0; q < CPL; ++q) {
+    for (int o = 16; o >= L; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    if (sub == 0 && lc + q * L < t) sacc[warp][lc + q * L] = acc[q];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < t; c += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += sacc[w][c];
+    part[(size_t)blockIdx.x * t + c] = s;
+  }
+}
+
+cudaError_t launch_wtv(cudaStream_t st, int64_t n, int t, const double* W, const double* v, double* part, int nblk) {
+  if (t < 1 || t > 64) return cudaErrorInvalidValue;
+  return launch_k(k_wtv, nblk, 256, 0, st, n, t, W, v, part);
 }
 
 // Column block j of −R⁻¹ packed for the update sweeps (W_j = 0 − Σ_{i≤j} V_i·(−R⁻¹_ij)):

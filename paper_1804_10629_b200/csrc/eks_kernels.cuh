@@ -64,19 +64,25 @@ cudaError_t launch_apply(cudaStream_t st, int t, int64_t n, double* Z2W, double*
 
 // ---- communication-avoiding variants (CA SRE-CG / CA SRE-CG2 / CA MSDO-CG): one CholQR of the
 // s·t columns of an outer iteration (s·t ≤ kCaMax, s ≤ kCaMaxBlocks).
-constexpr int kCaMax = 96, kCaMaxBlocks = 12;
+// st ≤ kCaMax columns per CA outer iteration (t = 64, s = 10); the st×st Cholesky runs in shared
+// memory up to kCaSmem columns, in global memory (one CTA) above
+constexpr int kCaMax = 640, kCaMaxBlocks = 12, kCaSmem = 118;
 struct CaPtrs {
   const double* in[kCaMaxBlocks];  // combine: V_i (or AV_i);  update: W_j
   double* out[kCaMaxBlocks];       // combine: W_j (or AW_j);  update: AW_j (read)
   const int* flag;                 // breakdown flag (INT_MAX = none)
 };
 // Cholesky of the m×m Gram B (upper read) = RᵀR, R⁻¹, α̃ = R⁻ᵀ g (g may be NULL); breakdown as launch_chol.
+// global workspace (chol_dyn_work(m) doubles) needed when m > kCaSmem
+size_t chol_dyn_work(int m);
 cudaError_t launch_chol_dyn(cudaStream_t st, int m, const double* B, const double* g, double* R, double* Rinv,
-                            double* alpha, int* flag, int gblock);
+                            double* alpha, int* flag, int gblock,
+                            double* work);
 // out_j = Σ_{i ≤ j} in_i Rinv[i·t.., j·t..] for j < s (n×t blocks, row-major); optionally skipped on breakdown.
 cudaError_t launch_ca_combine(cudaStream_t st, int64_t n, int t, int s, const CaPtrs& P, const double* Rinv,
                               int sms, bool skip_on_breakdown);
 // x += Σ_j in_j α_j, rnew = r − Σ_j out_j α_j (in = W, out = AW), partial ‖rnew‖² per CTA into part[nblk].
+cudaError_t launch_wtv(cudaStream_t st, int64_t n, int t, const double* W, const double* v, double* part, int nblk);
 cudaError_t launch_ca_pack(cudaStream_t st, int t, int s, const double* Rinv, double* pack);
 cudaError_t launch_ca_update(cudaStream_t st, int64_t n, int t, int s, const CaPtrs& P, const double* alpha,
                              double* x, const double* r, double* rnew, double* part, int nblk);

@@ -8,11 +8,14 @@ Tolerances (BASELINE.json north_star):
 * End to end: both reach relres <= 1e-8, outer iterations within max(5%, 1), x within 1e-6.
 """
 import math
+import os
 
 import numpy as np
 import pytest
 
 import eks_inputs as ei
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -188,6 +191,45 @@ def test_cfg2_analog_end_to_end(eks, torch_cuda, oracle_lib, method):
     assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
     assert rel(host(rep["x"]), ref["x"]) <= 1e-6
     assert rep["true_relres"] <= 2e-8
+
+
+# ------------------------------------------------------------------ §8(f) row 3: Pre-CholQR, restructured
+@pytest.mark.parametrize("method,s_,t,ortho,restr", [
+    ("sre-cg", 2, 4, "pre-cholqr", False), ("sre-cg2", 2, 4, "pre-cholqr", False),
+    ("msdo-cg", 2, 4, "pre-cholqr", False), ("sre-cg", 3, 16, "pre-cholqr", False),
+    ("sre-cg", 4, 2, "pre-cholqr", False), ("sre-cg", 3, 4, "acholqr", True), ("sre-cg2", 2, 8, "acholqr", True),
+    ("sre-cg", 3, 16, "acholqr", True), ("sre-cg", 2, 32, "pre-cholqr", True)])
+def test_pre_cholqr_restructured_end_to_end(eks, torch_cuda, oracle_lib, method, s_, t, ortho, restr):
+    """Pre-CholQR (reading R30) and restructured Alg 2 / Alg 1 (reading R31) on cfg1: counts within
+    5 %, x within 1e-6 of the oracle (mirror mode, the GPU's algebra), and after two outer
+    iterations (tol = 0) x agrees to 1e-10."""
+    p = ei.cfg1()
+    S = eks.Solver(p.A)
+    rep = S.solve(dev(torch_cuda, p.b), method, s_, t, p.tol, ortho=ortho, restructured=restr)
+    pre = S.solve(dev(torch_cuda, p.b), method, s_, t, 0.0, max_outer=3, ortho=ortho, restructured=restr)
+    S.close()
+    ref = oracle_lib.solve(p.A, p.b, method, s_, t, p.tol, mode=oracle_lib.MODE_MIRROR, ortho=ortho,
+                           restructured=restr)
+    refp = oracle_lib.solve(p.A, p.b, method, s_, t, 0.0, kmax=3, mode=oracle_lib.MODE_MIRROR, ortho=ortho,
+                            restructured=restr)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+    assert rep["true_relres"] <= 1.5e-8
+    assert pre["outer_iters"] == refp["outer_iters"] == 2
+    assert rel(host(pre["x"]), refp["x"]) <= 1e-10
+
+
+def test_pre_restructured_argument_errors(eks, torch_cuda):
+    A = ei.poisson2d(16)
+    S = eks.Solver(A)
+    b = dev(torch_cuda, ei.uniform_pm1(3, A.n))
+    for kw, method in [(dict(restructured=True), "msdo-cg"), (dict(restructured=True), "ca-sre-cg"),
+                       (dict(ortho="pre-cholqr"), "ca-sre-cg")]:
+        with pytest.raises(eks.EksError) as e:
+            S.solve(b, method, 2, 4, 1e-8, **kw)
+        assert e.value.status == 1
+    S.close()
 
 
 def test_cfg2_full_size_prefix(eks, torch_cuda, oracle_lib):
@@ -404,7 +446,8 @@ def test_paper_poisson2d_large_t_gpu(eks, torch_cuda, oracle_lib, method, t):
 # ------------------------------------------------------------------ §8(f) row 1: communication-avoiding variants
 @pytest.mark.parametrize("method,arnoldi,s_,t", [("ca-sre-cg", 7, 3, 4), ("ca-sre-cg", 5, 2, 4), ("ca-sre-cg2", 7, 2, 8),
                                                  ("ca-msdo-cg", 7, 3, 4), ("ca-msdo-cg", 5, 2, 8),
-                                                 ("ca-sre-cg", 7, 3, 16), ("ca-sre-cg", 7, 2, 32)])
+                                                 ("ca-sre-cg", 7, 3, 16), ("ca-sre-cg", 7, 2, 32),
+                                                 ("ca-sre-cg", 7, 3, 64)])  # st = 192: global-memory Cholesky
 def test_ca_end_to_end(eks, torch_cuda, oracle_lib, method, arnoldi, s_, t):
     """CA SRE-CG / CA SRE-CG2 / CA MSDO-CG (Alg 5 or 7, one st-column A-CholQR per outer iteration)
     on the well-conditioned Poisson2D 48² (the paper's CA regime): GPU and oracle
@@ -420,6 +463,27 @@ def test_ca_end_to_end(eks, torch_cuda, oracle_lib, method, arnoldi, s_, t):
     assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
     assert rel(host(rep["x"]), ref["x"]) <= 1e-6
     assert rep["true_relres"] <= 2e-8
+
+
+def test_poisson2d_tables_sweep_gpu(eks, torch_cuda):
+    """§8(f) item 4: every Poisson2D cell of Tables 2-4 through libeks (tools/poisson_tables.py):
+    all converge; t = 2 (partition-comparable, reading R1) within 15 % of the printed cells; the
+    paper's Poisson2D relations hold on our counts (restructured and s-step = ceil(k/s), P:482-484;
+    CA SRE-CG/SRE-CG2 with Alg 7 = s-step for s ≤ 4, Tables 2/3)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("poisson_tables", os.path.join(ROOT, "tools", "poisson_tables.py"))
+    pt = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(pt)
+    cells, _ = pt.sweep(eks, torch_cuda)
+    assert all(c["converged"] for c in cells.values()), [k for k, c in cells.items() if not c["converged"]]
+    for k, c in cells.items():
+        key, t, s = k.split("|")
+        if t == "2":
+            want = [c["paper"]]
+            if key == "msdo-cg/ca7":  # reading R28: the literal Alg 7 seed gives the s-step count
+                want.append(cells[f"msdo-cg/s-step|{t}|{s}"]["paper"])
+            assert min(abs(c["k"] - w) - 0.15 * w for w in want) <= 0, (k, c)
+    assert pt.relations(cells) == []
 
 
 def test_ca_ill_conditioned_agrees_with_oracle(eks, torch_cuda, oracle_lib):

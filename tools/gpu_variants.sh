@@ -1,0 +1,21 @@
+#!/bin/bash
+# bench lines of the §8(f) variants on cfg2 (s=3, t=16 unless stated)
+mkdir -p gpurun_out
+run() {
+  name=$1; shift
+  timeout 400 python bench.py --steps 3 --warmup 3 --no-spmm-block --cpu-iters 1 "$@" > gpurun_out/bench_$name.json 2> gpurun_out/bench_$name.err
+  python - "$name" <<'PY'
+import json, sys
+name = sys.argv[1]
+try:
+    d = json.loads(open(f"gpurun_out/bench_{name}.json").read().strip().splitlines()[-1])
+    print(name, round(d["value"], 1), round(d["ms_per_step"], 1), d["solve"]["outer_iters"], round(d["e2e"]["value"], 1),
+          d["roofline"]["kernel"], round(d["roofline"]["frac"], 3), {k: round(v, 3) for k, v in d["time_share"].items() if v > 0.005})
+except Exception as e:
+    print(name, "FAILED", open(f"gpurun_out/bench_{name}.err").read()[-400:])
+PY
+}
+run sstep
+run pre --ortho pre-cholqr
+run restr --restructured
+run ca2 --method ca-sre-cg --s 2
