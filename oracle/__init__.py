@@ -8,6 +8,7 @@ around the plain C routines, which cite PAPER.md line by line.
 from __future__ import annotations
 
 import ctypes as C
+import types
 import os
 import subprocess
 
@@ -77,6 +78,15 @@ def lib():
         _lib.or_solve_ex.argtypes = [C.POINTER(_Csr), vp, vp, i32, i32, i32, d, i32, i32, i32, i32,
                                      C.POINTER(_Report), ITER_CB, vp]
         _lib.or_solve_ex.restype = i32
+        _lib.or_ic0_nnz.argtypes = [C.POINTER(_Csr), i32]
+        _lib.or_ic0_nnz.restype = i64
+        _lib.or_ic0.argtypes = [C.POINTER(_Csr), i32, vp, vp, vp]
+        _lib.or_ic0.restype = i32
+        _lib.or_lsolve.argtypes = [C.POINTER(_Csr), i32, vp, vp]
+        _lib.or_ltsolve.argtypes = [C.POINTER(_Csr), i32, vp, vp]
+        _lib.or_solve_pc.argtypes = [C.POINTER(_Csr), vp, vp, i32, i32, i32, d, i32, i32, i32, i32,
+                                     C.POINTER(_Csr), C.POINTER(_Report), ITER_CB, vp]
+        _lib.or_solve_pc.restype = i32
     return _lib
 
 
@@ -170,8 +180,37 @@ def precholqr(A, Z: np.ndarray):
 ORTHO = {"acholqr": 0, "pre-cholqr": 1}
 
 
+def ic0(A, nd=64):
+    """Block-Jacobi IC(0) factor L (reading R32) of nd contiguous domains; returns (status, L as Csr)."""
+    ref = _CsrRef(A)
+    nnz = int(lib().or_ic0_nnz(C.byref(ref.s), nd))
+    rp = np.zeros(A.n + 1, np.int64)
+    col = np.zeros(nnz, np.int32)
+    val = np.zeros(nnz, np.float64)
+    st = lib().or_ic0(C.byref(ref.s), nd, _p(rp), _p(col), _p(val))
+    return st, types.SimpleNamespace(n=A.n, row_ptr=rp, col=col, val=val, nnz=nnz)
+
+
+def lsolve(L, Z):
+    """L⁻¹Z (n×t or n)."""
+    Z = _f64(Z)
+    Y = np.empty_like(Z)
+    ref = _CsrRef(L)
+    lib().or_lsolve(C.byref(ref.s), 1 if Z.ndim == 1 else Z.shape[1], _p(Z), _p(Y))
+    return Y
+
+
+def ltsolve(L, Z):
+    """L⁻ᵗZ (n×t or n)."""
+    Z = _f64(Z)
+    Y = np.empty_like(Z)
+    ref = _CsrRef(L)
+    lib().or_ltsolve(C.byref(ref.s), 1 if Z.ndim == 1 else Z.shape[1], _p(Z), _p(Y))
+    return Y
+
+
 def solve(A, b, method="sre-cg", s=1, t=1, tol=1e-8, kmax=5000, x0=None, mode=MODE_DEFINITION,
-          callback=None, ortho="acholqr", restructured=False):
+          callback=None, ortho="acholqr", restructured=False, L=None):
     """Run or_solve_ex; returns dict(x, outer_iters, converged, status, rho0, rho, true_relres, hist).
     ortho: "acholqr" (default) or "pre-cholqr"; restructured: Alg 1/2 (SRE-CG2 / SRE-CG only)."""
     b = _f64(b)
@@ -190,8 +229,9 @@ def solve(A, b, method="sre-cg", s=1, t=1, tol=1e-8, kmax=5000, x0=None, mode=MO
                      np.ctypeslib.as_array(rr, shape=(n,)).copy(), rho)
         cb = ITER_CB(_cb)
     m = METHODS[method] if isinstance(method, str) else int(method)
-    st = lib().or_solve_ex(C.byref(ref.s), _p(b), _p(x), m, s, t, tol, kmax, mode, ORTHO[ortho],
-                           int(bool(restructured)), C.byref(rep), cb, None)
+    Lref = _CsrRef(L) if L is not None else None
+    st = lib().or_solve_pc(C.byref(ref.s), _p(b), _p(x), m, s, t, tol, kmax, mode, ORTHO[ortho],
+                           int(bool(restructured)), C.byref(Lref.s) if Lref else None, C.byref(rep), cb, None)
     k = rep.outer_iters
     return dict(x=x, outer_iters=k, converged=bool(rep.converged), status=st, rho0=rep.rho0,
                 rho=rep.rho, true_relres=rep.true_relres, hist=hist[: k + 1].copy(),

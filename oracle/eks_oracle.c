@@ -220,6 +220,90 @@ int or_precholqr(const or_csr* A, int t, const double* Z, double* W, double* R) 
 }
 
 /* ------------------------------------------------------------------------ */
+/* Block-Jacobi IC(0) preconditioner M = L Lᵗ — P:872-882 (§5.2): nd        */
+/* contiguous domains (Metis in the paper, reading R32), each diagonal block */
+/* A_dd factorized by incomplete Cholesky with zero fill-in (Table 5).       */
+/* ------------------------------------------------------------------------ */
+static int64_t dom_of(int64_t n, int nd, int64_t i) {
+  int64_t d = i * nd / n;  /* candidate, then fix up against floor(d n / nd) */
+  while (d > 0 && d * n / nd > i) --d;
+  while (d + 1 < nd && (d + 1) * n / nd <= i) ++d;
+  return d;
+}
+
+int64_t or_ic0_nnz(const or_csr* A, int nd) {
+  int64_t cnt = 0;
+  for (int64_t i = 0; i < A->n; ++i)
+    for (int64_t p = A->row_ptr[i]; p < A->row_ptr[i + 1]; ++p) {
+      int64_t j = A->col[p];
+      if (j <= i && dom_of(A->n, nd, j) == dom_of(A->n, nd, i)) ++cnt;
+    }
+  return cnt;
+}
+
+/* L (CSR, rows ascending columns, diagonal last) with the pattern of the lower triangle of
+ * the block diagonal of A.  Row-oriented IC(0): for k < i in the pattern of row i,
+ * L_ik = (A_ik − Σ_{j<k} L_ij L_kj) / L_kk over j in both rows' patterns;
+ * L_ii = sqrt(A_ii − Σ_{j<i} L_ij²).  OR_BREAKDOWN if a diagonal argument is ≤ 0. */
+int or_ic0(const or_csr* A, int nd, int64_t* Lrp, int32_t* Lcol, double* Lval) {
+  int64_t n = A->n, q = 0;
+  Lrp[0] = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t di = dom_of(n, nd, i);
+    for (int64_t p = A->row_ptr[i]; p < A->row_ptr[i + 1]; ++p) {
+      int64_t j = A->col[p];
+      if (j <= i && dom_of(n, nd, j) == di) { Lcol[q] = (int32_t)j; Lval[q] = A->val[p]; ++q; }
+    }
+    Lrp[i + 1] = q;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t a = Lrp[i], e = Lrp[i + 1];
+    if (e == a || Lcol[e - 1] != i) return OR_BADARG;  /* a missing diagonal */
+    for (int64_t p = a; p < e - 1; ++p) {
+      int64_t k = Lcol[p];
+      double v = Lval[p];
+      /* Σ over j < k present in row i (positions a..p-1) and in row k */
+      int64_t pk = Lrp[k], ek = Lrp[k + 1] - 1;
+      for (int64_t pi = a; pi < p; ++pi) {
+        while (pk < ek && Lcol[pk] < Lcol[pi]) ++pk;
+        if (pk < ek && Lcol[pk] == Lcol[pi]) v = v - Lval[pi] * Lval[pk];
+      }
+      Lval[p] = v / Lval[Lrp[k + 1] - 1];
+    }
+    double d = Lval[e - 1];
+    for (int64_t p = a; p < e - 1; ++p) d = d - Lval[p] * Lval[p];
+    if (!(d > 0.0)) return OR_BREAKDOWN;
+    Lval[e - 1] = sqrt(d);
+  }
+  return OR_OK;
+}
+
+/* Y = L⁻¹ Z (n×t, row-major; Y may alias Z): forward substitution per column. */
+void or_lsolve(const or_csr* L, int t, const double* Z, double* Y) {
+  for (int64_t i = 0; i < L->n; ++i) {
+    int64_t a = L->row_ptr[i], e = L->row_ptr[i + 1];
+    for (int c = 0; c < t; ++c) {
+      double v = Z[i * t + c];
+      for (int64_t p = a; p < e - 1; ++p) v = v - L->val[p] * Y[(int64_t)L->col[p] * t + c];
+      Y[i * t + c] = v / L->val[e - 1];
+    }
+  }
+}
+
+/* Y = L⁻ᵗ Z (Y may alias Z): backward substitution, column-oriented over L's rows. */
+void or_ltsolve(const or_csr* L, int t, const double* Z, double* Y) {
+  if (Y != Z) memcpy(Y, Z, sizeof(double) * (size_t)L->n * (size_t)t);
+  for (int64_t i = L->n - 1; i >= 0; --i) {
+    int64_t a = L->row_ptr[i], e = L->row_ptr[i + 1];
+    for (int c = 0; c < t; ++c) {
+      double yi = Y[i * t + c] / L->val[e - 1];
+      Y[i * t + c] = yi;
+      for (int64_t p = a; p < e - 1; ++p) Y[(int64_t)L->col[p] * t + c] -= L->val[p] * yi;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Block list (the Q of Alg 3/6 or the 2-block window of Alg 4)              */
 /* ------------------------------------------------------------------------ */
 typedef struct {
@@ -276,7 +360,14 @@ int or_solve(const or_csr* A, const double* b, double* x, int method, int s, int
 int or_solve_ex(const or_csr* A, const double* b, double* x, int method, int s, int t,
                 double eps, int kmax, int mode, int ortho, int restructured, or_report* rep,
                 or_iter_cb cb, void* user) {
+  return or_solve_pc(A, b, x, method, s, t, eps, kmax, mode, ortho, restructured, NULL, rep, cb, user);
+}
+
+int or_solve_pc(const or_csr* A, const double* b, double* x, int method, int s, int t,
+                double eps, int kmax, int mode, int ortho, int restructured, const or_csr* L,
+                or_report* rep, or_iter_cb cb, void* user) {
   int64_t n = A->n;
+  if (L && (L->n != n || restructured)) return OR_BADARG;
   if (s < 1 || t < 1 || t > n || !(eps >= 0.0) || method < 0 || method > 2) return OR_BADARG;
   if (ortho != OR_ORTHO_ACHOLQR && ortho != OR_ORTHO_PRE) return OR_BADARG;
   /* restructured Alg 1/2 exist for SRE-CG2 / SRE-CG only (no restructured MSDO-CG) */
@@ -317,11 +408,22 @@ int or_solve_ex(const or_csr* A, const double* b, double* x, int method, int s, 
        * SRE-CG/SRE-CG2 at k=1 (Alg 3, Alg 4); otherwise the next
        * power A·W_{j-1}. */
       if (i == 0 && (method == OR_MSDO_CG || k == 1)) {
-        or_split(n, t, r, Z);
+        if (L) {
+          /* Alg 8/9 line 5, Alg 10 line 3: W = L⁻ᵗ[T(L⁻¹ r_{k-1})] */
+          or_lsolve(L, 1, r, tmp);
+          or_split(n, t, tmp, Z);
+          or_ltsolve(L, t, Z, Z);
+        } else {
+          or_split(n, t, r, Z);
+        }
       } else {
         const double* Wprev = Q.W[Q.count - 1];
         if (mode == OR_MODE_MIRROR) memcpy(Z, Q.AW[Q.count - 1], sizeof(double) * blk);
         else or_spmm(A, t, Wprev, Z);
+        if (L) { /* Alg 8-10: W_{j} = M⁻¹ A W_{j-1} = L⁻ᵗ L⁻¹ (A W_{j-1}) */
+          or_lsolve(L, t, Z, Z);
+          or_ltsolve(L, t, Z, Z);
+        }
       }
       int w0 = window_start(&Q, method), nq = Q.count - w0;
       double* W = dalloc(blk);

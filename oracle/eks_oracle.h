@@ -91,6 +91,24 @@ int or_solve_ex(const or_csr* A, const double* b, double* x, int method, int s, 
                 double eps, int kmax, int mode, int ortho, int restructured, or_report* rep,
                 or_iter_cb cb, void* user);
 
+/* Block-Jacobi IC(0) preconditioner M = L·Lᵗ (Table 5; reading R32): nd contiguous
+ * domains D_d = [floor(d n/nd), floor((d+1) n/nd)), each diagonal block factorized by incomplete
+ * Cholesky with zero fill-in.  L is CSR (ascending columns, diagonal last) with the pattern of
+ * the lower triangle of the block diagonal of A; or_ic0_nnz gives its nnz. */
+int64_t or_ic0_nnz(const or_csr* A, int nd);
+int or_ic0(const or_csr* A, int nd, int64_t* Lrp, int32_t* Lcol, double* Lval);
+/* Y = L⁻¹Z and Y = L⁻ᵗZ for n×t row-major blocks (Y may alias Z). */
+void or_lsolve(const or_csr* L, int t, const double* Z, double* Y);
+void or_ltsolve(const or_csr* L, int t, const double* Z, double* Y);
+
+/* or_solve_ex with a split preconditioner M = L·Lᵗ (L NULL: none): the split-preconditioned
+ * s-step SRE-CG / SRE-CG2 / MSDO-CG of Alg 8 / 9 / 10: seed L⁻ᵗ[T(L⁻¹r)], powers
+ * M⁻¹A·W, A-orthonormalization and the x/r update unchanged.  Not with
+ * restructured (OR_BADARG). */
+int or_solve_pc(const or_csr* A, const double* b, double* x, int method, int s, int t,
+                double eps, int kmax, int mode, int ortho, int restructured, const or_csr* L,
+                or_report* rep, or_iter_cb cb, void* user);
+
 /* Communication-avoiding s-step enlarged CG: CA SRE-CG, CA SRE-CG2
  * (method 0 / 1) and CA MSDO-CG (method 2) with the CA-Arnoldi
  * A-orthonormalization (arnoldi = 5, Alg 5) or its modified, stabilised form
