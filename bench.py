@@ -218,8 +218,9 @@ def oracle_sample(p, iters: int):
     if p.method.startswith("ca-"):
         r = oracle.solve_ca(p.A, p.b, p.method[3:], arnoldi=p.arnoldi, s=p.s, t=p.t, tol=0.0, kmax=iters + 1)
     else:
+        L = oracle.ic0(p.A, p.precond)[1] if getattr(p, "precond", 0) else None
         r = oracle.solve(p.A, p.b, p.method, p.s, p.t, 0.0, kmax=iters + 1, ortho=getattr(p, "ortho", "acholqr"),
-                         restructured=getattr(p, "restructured", False))
+                         restructured=getattr(p, "restructured", False), L=L)
     dt = time.perf_counter() - t0
     return r["outer_iters"], dt
 
@@ -234,6 +235,7 @@ def problem_of(args):
     p.arnoldi = args.arnoldi if p.method.startswith("ca-") else 0
     p.ortho = args.ortho
     p.restructured = args.restructured
+    p.precond = args.precond
     return p
 
 
@@ -269,6 +271,8 @@ def config_of(args, p, N):
         ("restructured" if getattr(p, "restructured", False) else "s-step")
     if getattr(p, "ortho", "acholqr") != "acholqr":
         kind += f" + {p.ortho}"
+    if getattr(p, "precond", 0):
+        kind = f"split-preconditioned (block-Jacobi IC(0), {p.precond} domains) " + kind
     return {"workload": f"{p.name}: {p.note}; {kind} {p.method}, s={p.s}, t={p.t}, tol={p.tol:g}",
             "n": p.A.n, "nnz": p.A.nnz, "method": p.method, "s": p.s, "t": p.t, "tol": p.tol,
             "parallelism": f"row-slabs x{N} (t/N domains per GPU)",
@@ -295,6 +299,8 @@ def main():
     ap.add_argument("--arnoldi", type=int, default=7, help="CA variants: Alg 5 or Alg 7")
     ap.add_argument("--ortho", default="acholqr", choices=["acholqr", "pre-cholqr"])
     ap.add_argument("--restructured", action="store_true", help="restructured Alg 2 / Alg 1 (SRE-CG / SRE-CG2)")
+    ap.add_argument("--precond", type=int, default=0,
+                    help="split-preconditioned Alg 8-10 with block-Jacobi IC(0) of this many domains (64 in the paper)")
     ap.add_argument("--cfg5-n", type=int, default=384, help="cfg5 grid size (384 = BASELINE configs[4])")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -334,6 +340,8 @@ def main():
         uid = obj[0]
     solver = eks.Solver(None, rank=rank, nranks=world, device=local, nccl_id=uid)
     solver.setup(n, lo, hi, slab.row_ptr, slab.col, slab.val)
+    if p.precond:
+        solver.setup_precond(p.precond)
     stream = torch.cuda.Stream()
     eks.eks_set_stream(solver.ctx, stream.cuda_stream)
 
@@ -350,7 +358,7 @@ def main():
             x.zero_()
         st, rep = eks.eks_solve_ex(solver.ctx, p.method, p.s, p.t, p.tol, b, x, profile=profile,
                                    max_outer=args.max_outer, arnoldi=p.arnoldi, ortho=p.ortho,
-                                   restructured=p.restructured)
+                                   restructured=p.restructured, precond=bool(p.precond))
         if st not in ((0, 8) if args.max_outer else (0,)):
             raise SystemExit(f"solve failed: {eks.STATUS.get(st)} {eks.eks_error_string(solver.ctx)}")
         return rep
@@ -450,9 +458,11 @@ def main():
         e_outer = 0
         for k in range(args.steps):
             e2e_solver.setup(n, lo, hi, hrp, hcol, hval)
+            if p.precond:
+                e2e_solver.setup_precond(p.precond)
             hx[:] = 0.0
             st, rep = eks.eks_solve_ex(e2e_solver.ctx, p.method, p.s, p.t, p.tol, hb, hx, arnoldi=p.arnoldi,
-                                       ortho=p.ortho, restructured=p.restructured)
+                                       ortho=p.ortho, restructured=p.restructured, precond=bool(p.precond))
             e_outer += rep["outer_iters"]
         torch.cuda.synchronize()
         barrier()

@@ -94,7 +94,10 @@ typedef struct {
   int restructured;       /* 1: restructured SRE-CG / SRE-CG2 (Alg 2 / Alg 1; DESIGN R31):
                              the same s blocks, then s sequential updates with α̃_i = W_iᵀ r_{i-1};
                              MSDO-CG and CA methods: EKS_ERR_INVALID_ARG */
-  int reserved[5];
+  int precond;            /* 1: split-preconditioned s-step method (Alg 8/9/10) with the block-Jacobi
+                             IC(0) M of eks_setup_precond: seed M⁻¹[T(r)], powers M⁻¹A·W.
+                             s-step methods only (CA / restructured: EKS_ERR_INVALID_ARG) */
+  int reserved[4];
 } eks_options;
 
 /* Per-kernel-class device time accumulated while options.profile == 1. */
@@ -125,6 +128,19 @@ eks_status eks_set_stream(eks_ctx* ctx, void* stream);
 eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t row_end,
                          const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
                          eks_mem where);
+
+/* Block-Jacobi IC(0) preconditioner M = L·Lᵗ for the split-preconditioned s-step methods
+ * (Alg 8/9/10; §5.2; DESIGN reading R32): ndomains contiguous domains
+ * D_d = [floor(d n/ndomains), floor((d+1) n/ndomains)) (Metis in the paper), each diagonal block
+ * factorized by incomplete Cholesky with zero fill-in on the host at setup (a one-time cost),
+ * L and Lᵗ uploaded with per-domain level schedules.  Pass the SAME local slab (global columns)
+ * as eks_setup_csr; the slab must be a union of preconditioner domains.  Entries coupling two
+ * domains are dropped (block Jacobi).  Errors: EKS_ERR_STATE (no eks_setup_csr), EKS_ERR_INVALID_ARG
+ * (ndomains < 1, slab not a union of domains), EKS_ERR_BREAKDOWN (an IC(0) pivot ≤ 0).
+ * A solve uses it when eks_options.precond = 1; then ndomains must be a multiple of t (each of
+ * the t domains is the union of ndomains/t preconditioner domains). */
+eks_status eks_setup_precond(eks_ctx* ctx, int ndomains, const int64_t* row_ptr, const int32_t* col_idx,
+                             const double* vals, eks_mem where);
 
 /* Solve A x = b with the chosen s-step method (Alg 3/4/6), t domains
  * D_d = [floor(d n/t), floor((d+1) n/t)) (reading R1), tolerance tol on the

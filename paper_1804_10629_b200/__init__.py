@@ -47,7 +47,8 @@ class _Report(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("max_outer", C.c_int), ("use_graph", C.c_int), ("profile", C.c_int), ("arnoldi", C.c_int),
-                ("ortho", C.c_int), ("restructured", C.c_int), ("reserved", C.c_int * 5)]
+                ("ortho", C.c_int), ("restructured", C.c_int), ("precond", C.c_int),
+                ("reserved", C.c_int * 4)]
 
 
 class _Profile(C.Structure):
@@ -71,6 +72,7 @@ def lib():
             "eks_create": [C.POINTER(vp), C.POINTER(_Dist)],
             "eks_set_stream": [vp, vp],
             "eks_setup_csr": [vp, i64, i64, i64, vp, vp, vp, i32],
+            "eks_setup_precond": [vp, i32, vp, vp, vp, i32],
             "eks_solve": [vp, i32, i32, i32, d, vp, vp, i32, i32, C.POINTER(_Report)],
             "eks_solve_ex": [vp, i32, i32, i32, d, vp, vp, i32, C.POINTER(_Options), C.POINTER(_Report)],
             "eks_basis_sweep": [vp, i32, i32, vp, vp, i32, C.POINTER(_Options), C.POINTER(_Report)],
@@ -94,7 +96,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["eks_get_unique_id", "eks_create", "eks_set_stream", "eks_setup_csr", "eks_solve", "eks_solve_ex",
+EXPORTED = ["eks_get_unique_id", "eks_create", "eks_set_stream", "eks_setup_csr", "eks_setup_precond", "eks_solve", "eks_solve_ex",
             "eks_basis_sweep", "eks_get_profile", "eks_destroy", "eks_error_string", "eks_k_split", "eks_k_spmm",
             "eks_k_cgs2", "eks_k_acholqr", "eks_k_chol", "eks_k_time_spmm", "eks_plan_halo"]
 
@@ -179,6 +181,13 @@ def eks_setup_csr(ctx, n_global, row_begin, row_end, row_ptr, col, val):
                                     _ptr(col, np.int32), _ptr(val, np.float64), where))
 
 
+def eks_setup_precond(ctx, ndomains, row_ptr, col, val):
+    """Block-Jacobi IC(0) of ndomains contiguous domains (same slab as eks_setup_csr)."""
+    where = _where(row_ptr, col, val)
+    _check(ctx, lib().eks_setup_precond(ctx, int(ndomains), _ptr(row_ptr, np.int64), _ptr(col, np.int32),
+                                        _ptr(val, np.float64), where))
+
+
 def _report(rep: _Report):
     k = rep.outer_iters
     hist = np.ctypeslib.as_array(rep.rho_history, shape=(k + 1,)).copy() if rep.rho_history else None
@@ -192,13 +201,14 @@ ORTHO = {"acholqr": 0, "pre-cholqr": 1}
 
 
 def eks_solve_ex(ctx, method, s, t, tol, b, x, max_outer=0, profile=False, raise_on=(5, 6, 1, 2, 3), arnoldi=0,
-                 ortho="acholqr", restructured=False):
+                 ortho="acholqr", restructured=False, precond=False):
     """Returns (status, report dict).  x holds x0 on entry and the solution on exit.
     arnoldi (CA methods only): 7 = modified CA-Arnoldi (default), 5 = CA-Arnoldi.
     ortho: "acholqr" (default) or "pre-cholqr"; restructured: Alg 2 / Alg 1 (SRE-CG / SRE-CG2)."""
     m = METHODS[method] if isinstance(method, str) else int(method)
     where = _where(b, x)
-    opt = _Options(int(max_outer), 0, int(bool(profile)), int(arnoldi), ORTHO[ortho], int(bool(restructured)))
+    opt = _Options(int(max_outer), 0, int(bool(profile)), int(arnoldi), ORTHO[ortho], int(bool(restructured)),
+                   int(bool(precond)))
     rep = _Report()
     st = lib().eks_solve_ex(ctx, m, int(s), int(t), float(tol), _ptr(b, np.float64), _ptr(x, np.float64), where,
                             C.byref(opt), C.byref(rep))
@@ -298,16 +308,21 @@ class Solver:
         cl = np.ascontiguousarray(col, np.int32) if isinstance(col, np.ndarray) else col
         vl = np.ascontiguousarray(val, np.float64) if isinstance(val, np.ndarray) else val
         eks_setup_csr(self.ctx, n_global, row_begin, row_end, rp, cl, vl)
+        self._csr = (rp, cl, vl)
+
+    def setup_precond(self, ndomains=64):
+        """Block-Jacobi IC(0) preconditioner (reading R32) for solve(..., precond=True)."""
+        eks_setup_precond(self.ctx, ndomains, *self._csr)
 
     def solve(self, b, method="sre-cg", s=1, t=1, tol=1e-8, x0=None, max_outer=0, profile=False, arnoldi=0,
-              ortho="acholqr", restructured=False):
+              ortho="acholqr", restructured=False, precond=False):
         if isinstance(b, np.ndarray):
             b = np.ascontiguousarray(b, np.float64)
             x = np.zeros_like(b) if x0 is None else np.ascontiguousarray(x0, np.float64).copy()
         else:
             x = b.new_zeros(b.shape) if x0 is None else x0.clone()
         st, rep = eks_solve_ex(self.ctx, method, s, t, tol, b, x, max_outer=max_outer, profile=profile,
-                               arnoldi=arnoldi, ortho=ortho, restructured=restructured)
+                               arnoldi=arnoldi, ortho=ortho, restructured=restructured, precond=precond)
         rep["status"] = st
         rep["x"] = x
         return rep

@@ -85,6 +85,19 @@ struct eks_ctx {
   int ca_cap = 0;  // st the buffers were sized for
   int chol_mode = 0;               // 0 one-warp Cholesky launch (default), 1 in the SpMM kernel's tail (EKS_CHOL)
   int ortho = 0;                   // 0 A-CholQR, 1 Pre-CholQR (eks_options.ortho, reading R30)
+  // block-Jacobi IC(0) preconditioner (eks_setup_precond, reading R32): sweep [0] = forward with
+  // the strict lower L, [1] = backward with the strict upper Lᵗ; per-domain level schedules
+  int prec_nd = 0, prec_ndl = 0;   // preconditioner domains (global), of this slab
+  int* pr_rp[2] = {nullptr, nullptr};
+  int* pr_col[2] = {nullptr, nullptr};
+  double* pr_val[2] = {nullptr, nullptr};
+  double* pr_diag = nullptr;
+  int* pr_domlev[2] = {nullptr, nullptr};
+  int* pr_levptr[2] = {nullptr, nullptr};
+  int* pr_rows[2] = {nullptr, nullptr};
+  int pr_levels[2] = {0, 0};       // longest level chain of a domain (forward, backward)
+  bool use_prec = false;           // this solve applies M⁻¹ (eks_options.precond)
+  Block Zp;                        // M⁻¹·Z of the next block
   double* pre = nullptr;           // Pre-CholQR / restructured scratch: [G | R1⁻¹ | −R1⁻¹ | g] (3t²+t)
   // workspace, keyed by t
   int ws_t = 0;
@@ -235,7 +248,7 @@ void free_workspace(eks_ctx* c) {
   for (auto& b : c->AWpool) dfree(b.base);
   c->Wpool.clear();
   c->AWpool.clear();
-  for (Block* b : {&c->Zs, &c->Z1, &c->xv, &c->tmpv}) { dfree(b->base); *b = Block{}; }
+  for (Block* b : {&c->Zs, &c->Z1, &c->xv, &c->tmpv, &c->Zp}) { dfree(b->base); *b = Block{}; }
   for (double** p : {&c->b, &c->r, &c->rnew, &c->dx, &c->part, &c->C1, &c->C2, &c->Bg, &c->Rm, &c->Rinv,
                      &c->alpha, &c->scal}) { dfree(*p); *p = nullptr; }
   dfree(c->flag);
@@ -634,6 +647,16 @@ Window window_for(eks_ctx* ctx, int method, int nblocks, int ring) {
   return w;
 }
 
+// Y = M⁻¹Z = L⁻ᵗL⁻¹Z for an n×t block (Y may alias Z): the two level-scheduled sweeps.
+eks_status prec_apply(eks_ctx* ctx, int t, const double* Z, double* Y) {
+  KScope k(ctx, EKS_K_OTHER);
+  account(ctx, EKS_K_OTHER, 2.0 * (12.0 * ctx->nnz / 2 + 16.0 * ctx->n * t), 2.0 * ctx->nnz * t);
+  for (int w = 0; w < 2; ++w)
+    CK(eks::launch_trsv_lev(ctx->stream, ctx->prec_ndl, t, ctx->pr_rp[w], ctx->pr_col[w], ctx->pr_val[w],
+                            ctx->pr_diag, ctx->pr_domlev[w], ctx->pr_levptr[w], ctx->pr_rows[w], w ? Y : Z, Y));
+  return EKS_OK;
+}
+
 // Pre-CholQR's Euclidean stage on Z (in place): G = ZᵀZ = R1ᵀR1, Z ← Z R1⁻¹ (reading R30).
 // AZ is scratch (overwritten later by A·Z) for the t the update sweep does not cover.
 eks_status pre_euclid(eks_ctx* ctx, int t, const Block& Z, double* AZ, int gb) {
@@ -691,13 +714,18 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
                       Block* Wn, Block* AWn, int alpha_off, int gb, int mode) {
   Window w = window_for(ctx, method, nblocks, ring);
   if (seed_from_r) {
-    double* dst = w.Q.empty() ? Wn->loc : ctx->Zs.loc;
+    double* dst = (w.Q.empty() && !ctx->use_prec) ? Wn->loc : ctx->Zs.loc;
     {
       KScope k(ctx, EKS_K_SPLIT);
       CK(eks::launch_split(ctx->stream, t, ctx->n, ctx->row_begin, ctx->n_global, ctx->r, dst));
     }
     account(ctx, EKS_K_SPLIT, 8.0 * ctx->n * (t + 1), 0.0);
     Zsrc = dst;
+  }
+  if (ctx->use_prec) {  // Alg 8-10: seed M⁻¹[T(r)] = L⁻ᵗ[T(L⁻¹r)], powers M⁻¹A·W
+    ST(alloc_block(ctx, &ctx->Zp, t, false));
+    ST(prec_apply(ctx, t, Zsrc, ctx->Zp.loc));
+    Zsrc = ctx->Zp.loc;
   }
   if (!w.Q.empty()) {
     ST(cgs2(ctx, t, w.Q, w.AQ, Zsrc, Wn->loc));  // "A-orthonormalize W against Q"
@@ -723,7 +751,7 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
   }
   // SRE-CG: the next block's window is {W_prev, W_new} and its Z is AW_new, so the R⁻¹ kernel
   // that produces AW_new also accumulates the next CGS pass-1 coefficients C1 = [AW_prev, AW_new]ᵀAW_new.
-  const int c1n = (ring && eks::apply_c1_supported(t, 2)) ? (nblocks == 0 ? 1 : 2) : 0;
+  const int c1n = (ring && !ctx->use_prec && eks::apply_c1_supported(t, 2)) ? (nblocks == 0 ? 1 : 2) : 0;
   if (c1n) ST(ensure_C(ctx, (size_t)2 * t * t));
   if (ctx->part2_cap < (size_t)ctx->nblk * (2 * t * t + 2)) {
     dfree(ctx->part2);
@@ -1231,6 +1259,7 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
                          const int32_t* col_idx, const double* vals, eks_mem where) {
   if (!ctx) return EKS_ERR_INVALID_ARG;
   if (!row_ptr || !col_idx || !vals) return fail(ctx, EKS_ERR_INVALID_ARG, "NULL matrix pointer");
+  ctx->prec_nd = 0;  // a new matrix invalidates the preconditioner (its buffers go on the next setup/destroy)
   if (n_global <= 0 || row_begin < 0 || row_end <= row_begin || row_end > n_global)
     return fail(ctx, EKS_ERR_INVALID_ARG, "bad row range [%lld,%lld) of n=%lld", (long long)row_begin,
                 (long long)row_end, (long long)n_global);
@@ -1387,6 +1416,156 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   return EKS_OK;
 }
 
+extern "C++" {
+namespace {
+void free_precond(eks_ctx* ctx) {
+  for (int w = 0; w < 2; ++w) {
+    for (void* p : {(void*)ctx->pr_rp[w], (void*)ctx->pr_col[w], (void*)ctx->pr_val[w], (void*)ctx->pr_domlev[w],
+                    (void*)ctx->pr_levptr[w], (void*)ctx->pr_rows[w]})
+      dfree(p);
+    ctx->pr_rp[w] = ctx->pr_col[w] = ctx->pr_domlev[w] = ctx->pr_levptr[w] = ctx->pr_rows[w] = nullptr;
+    ctx->pr_val[w] = nullptr;
+  }
+  dfree(ctx->pr_diag);
+  ctx->pr_diag = nullptr;
+  ctx->prec_nd = ctx->prec_ndl = 0;
+}
+
+template <typename T>
+eks_status upload(eks_ctx* ctx, T** dst, const std::vector<T>& v) {
+  CK(cudaMalloc((void**)dst, sizeof(T) * std::max<size_t>(1, v.size())));
+  if (!v.empty()) CK(cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return EKS_OK;
+}
+}  // namespace
+}  // extern "C++"
+
+// Block-Jacobi IC(0) (reading R32), built on the host once per matrix: for each local row i, the
+// entries of its domain's lower triangle are scattered into a dense row marker; each L_ik (k < i,
+// ascending) subtracts Σ_j L_kj·L_ij over row k's strict-lower entries found in the marker.
+eks_status eks_setup_precond(eks_ctx* ctx, int nd, const int64_t* row_ptr, const int32_t* col_idx,
+                             const double* vals, eks_mem where) {
+  if (!ctx) return EKS_ERR_INVALID_ARG;
+  if (!ctx->have_matrix) return fail(ctx, EKS_ERR_STATE, "eks_setup_csr has not been called");
+  if (nd < 1 || !row_ptr || !col_idx || !vals) return fail(ctx, EKS_ERR_INVALID_ARG, "bad eks_setup_precond arguments");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  free_precond(ctx);
+  const int64_t N = ctx->n_global, n = ctx->n, r0 = ctx->row_begin;
+  auto dlo = [&](int64_t d) { return d * N / nd; };
+  int d0 = -1, d1 = -1;
+  for (int d = 0; d <= nd; ++d) {
+    if (dlo(d) == r0 && d0 < 0 && d < nd) d0 = d;
+    if (dlo(d) == ctx->row_end) d1 = d;
+  }
+  if (d0 < 0 || d1 <= d0) return fail(ctx, EKS_ERR_INVALID_ARG, "slab is not a union of the %d preconditioner domains", nd);
+  std::vector<int64_t> rp(n + 1);
+  if (where == EKS_MEM_HOST) memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1));
+  else CK(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+  const int64_t nnz = rp[n];
+  if (nnz != ctx->nnz) return fail(ctx, EKS_ERR_INVALID_ARG, "CSR differs from eks_setup_csr's");
+  std::vector<int32_t> col(nnz);
+  std::vector<double> val(nnz);
+  if (where == EKS_MEM_HOST) {
+    memcpy(col.data(), col_idx, sizeof(int32_t) * nnz);
+    memcpy(val.data(), vals, sizeof(double) * nnz);
+  } else {
+    CK(cudaMemcpy(col.data(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(val.data(), vals, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+  }
+  // strict-lower L (local columns) and its diagonal
+  std::vector<int> dom(n);
+  for (int d = d0; d < d1; ++d)
+    for (int64_t g = dlo(d); g < dlo(d + 1); ++g) dom[g - r0] = d - d0;
+  std::vector<int> Lrp(n + 1, 0), Lcol;
+  std::vector<double> Lval, diag(n, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t j = (int64_t)col[p] - r0;
+      if (j < 0 || j > i || dom[j] != dom[i]) continue;
+      if (j == i) diag[i] = val[p];
+      else {
+        Lcol.push_back((int)j);
+        Lval.push_back(val[p]);
+      }
+    }
+    Lrp[i + 1] = (int)Lcol.size();
+  }
+  std::vector<int64_t> mark(n, -1);  // mark[j] = position of L_ij in the current row i
+  for (int64_t i = 0; i < n; ++i) {
+    for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) mark[Lcol[p]] = p;
+    for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) {
+      const int k = Lcol[p];
+      double v = Lval[p];
+      for (int q = Lrp[k]; q < Lrp[k + 1]; ++q) {  // row k's columns j < k
+        const int64_t pj = mark[Lcol[q]];
+        if (pj >= 0 && pj < p) v -= Lval[q] * Lval[pj];
+      }
+      Lval[p] = v / diag[k];
+    }
+    double dd = diag[i];
+    for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) dd -= Lval[p] * Lval[p];
+    for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) mark[Lcol[p]] = -1;
+    if (!(dd > 0.0)) return fail(ctx, EKS_ERR_BREAKDOWN, "IC(0) pivot %lld <= 0", (long long)(i + r0));
+    diag[i] = std::sqrt(dd);
+  }
+  // Lᵗ strict upper (row i: L_ki, k > i, ascending k)
+  std::vector<int> Urp(n + 1, 0), Ucol(Lcol.size());
+  std::vector<double> Uval(Lcol.size());
+  for (int c : Lcol) ++Urp[c + 1];
+  for (int64_t i = 0; i < n; ++i) Urp[i + 1] += Urp[i];
+  {
+    std::vector<int> fill(Urp.begin(), Urp.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+      for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) {
+        Ucol[fill[Lcol[p]]] = (int)i;
+        Uval[fill[Lcol[p]]++] = Lval[p];
+      }
+  }
+  // level schedules per domain: forward lev(i) = 1 + max lev(k), k < i in row i of L;
+  // backward from the last row with Lᵗ
+  const int ndl = d1 - d0;
+  for (int w = 0; w < 2; ++w) {
+    const std::vector<int>& R = w ? Urp : Lrp;
+    const std::vector<int>& Cc = w ? Ucol : Lcol;
+    std::vector<int> lev(n, 0);
+    if (!w)
+      for (int64_t i = 0; i < n; ++i)
+        for (int p = R[i]; p < R[i + 1]; ++p) lev[i] = std::max(lev[i], lev[Cc[p]] + 1);
+    else
+      for (int64_t i = n - 1; i >= 0; --i)
+        for (int p = R[i]; p < R[i + 1]; ++p) lev[i] = std::max(lev[i], lev[Cc[p]] + 1);
+    std::vector<int> domlev(ndl + 1, 0), levptr, rows;
+    int maxl = 0;
+    for (int d = 0; d < ndl; ++d) {
+      const int64_t lo = dlo(d + d0) - r0, hi = dlo(d + d0 + 1) - r0;
+      int nl = 0;
+      for (int64_t i = lo; i < hi; ++i) nl = std::max(nl, lev[i] + 1);
+      maxl = std::max(maxl, nl);
+      std::vector<std::vector<int>> by(nl);
+      for (int64_t i = lo; i < hi; ++i) by[lev[i]].push_back((int)i);
+      domlev[d] = (int)levptr.size();
+      for (auto& v : by) {
+        levptr.push_back((int)rows.size());
+        rows.insert(rows.end(), v.begin(), v.end());
+      }
+    }
+    domlev[ndl] = (int)levptr.size();
+    levptr.push_back((int)rows.size());
+    ctx->pr_levels[w] = maxl;
+    ST(upload(ctx, &ctx->pr_rp[w], R));
+    ST(upload(ctx, &ctx->pr_col[w], Cc));
+    ST(upload(ctx, &ctx->pr_val[w], w ? Uval : Lval));
+    ST(upload(ctx, &ctx->pr_domlev[w], domlev));
+    ST(upload(ctx, &ctx->pr_levptr[w], levptr));
+    ST(upload(ctx, &ctx->pr_rows[w], rows));
+  }
+  ST(upload(ctx, &ctx->pr_diag, diag));
+  ctx->prec_nd = nd;
+  ctx->prec_ndl = ndl;
+  return EKS_OK;
+}
+
 eks_status eks_solve(eks_ctx* ctx, eks_method method, int s, int t, double tol, const double* b, double* x,
                      eks_mem where, int max_outer, eks_report* rep) {
   eks_options o{};
@@ -1406,6 +1585,11 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   const bool restr = opt && opt->restructured;
   if (ortho != 0 && ortho != 1) return fail(ctx, EKS_ERR_INVALID_ARG, "ortho must be 0 (A-CholQR) or 1 (Pre-CholQR)");
   if (ca && ortho) return fail(ctx, EKS_ERR_INVALID_ARG, "Pre-CholQR is for the s-step methods");
+  const bool prec = opt && opt->precond;
+  if (prec && (ca || restr)) return fail(ctx, EKS_ERR_INVALID_ARG, "precond is for the s-step methods");
+  if (prec && !ctx->prec_nd) return fail(ctx, EKS_ERR_STATE, "eks_setup_precond has not been called");
+  if (prec && ctx->prec_nd % t)
+    return fail(ctx, EKS_ERR_INVALID_ARG, "precond needs t | ndomains (%d), P:874", ctx->prec_nd);
   if (restr && method != EKS_SRE_CG && method != EKS_SRE_CG2)
     return fail(ctx, EKS_ERR_INVALID_ARG, "restructured exists for SRE-CG and SRE-CG2 only (P:729)");
   if (ca && (s * t > eks::kCaMax || s > eks::kCaMaxBlocks))
@@ -1428,6 +1612,7 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   // the outer iteration until their updates), CA SRE-CG the (s+1)-block window + s new blocks
   const int ring = (method == EKS_SRE_CG) ? (restr ? std::max(3, s + 1) : 3) : (method == EKS_CA_SRE_CG ? 2 * s + 1 : 0);
   ctx->ortho = ortho;
+  ctx->use_prec = prec;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -1541,6 +1726,8 @@ eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks_total, const double*
     return fail(ctx, EKS_ERR_INVALID_ARG, "bad basis-sweep arguments");
   begin_run(ctx, opt);
   ST(ensure_workspace(ctx, t, 1));
+  ctx->use_prec = false;
+  ctx->ortho = 0;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -1613,6 +1800,7 @@ eks_status eks_destroy(eks_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   free_workspace(ctx);
+  free_precond(ctx);
   dfree(ctx->d_rp);
   dfree(ctx->d_col);
   dfree(ctx->d_val);

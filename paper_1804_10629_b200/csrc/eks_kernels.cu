@@ -859,6 +859,36 @@ cudaError_t launch_ca_combine(cudaStream_t st, int64_t n, int t, int s, const Ca
   return launch_k(k_ca_combine, (int)blocks, 256, sm, st, n, t, s, P, Rinv, skip_on_breakdown ? 1 : 0);
 }
 
+// Block-diagonal triangular solve of an n×t block with a level schedule (block-Jacobi IC(0),
+// Alg 8-10 M⁻¹ = L⁻ᵗL⁻¹, reading R32): one CTA per preconditioner domain walks its levels in
+// order; a level's rows are independent: Y[i][c] = (Z[i][c] − Σ_p val[p]·Y[col[p]][c]) / diag[i]
+// (p ascending, fma).  Y may alias Z (row i reads only its own Z entry).  The same kernel runs the
+// forward (strict lower L) and the backward (strict upper Lᵗ, levels from the last row) sweep.
+__global__ void __launch_bounds__(256) k_trsv_lev(int t, const int* __restrict__ rp, const int* __restrict__ col,
+                                                  const double* __restrict__ val, const double* __restrict__ diag,
+                                                  const int* __restrict__ dom_lev, const int* __restrict__ lev_ptr,
+                                                  const int* __restrict__ rows, const double* Z, double* Y) {
+  pdl_enter();
+  const int d = blockIdx.x;
+  for (int lv = dom_lev[d]; lv < dom_lev[d + 1]; ++lv) {
+    const int b = lev_ptr[lv], items = (lev_ptr[lv + 1] - b) * t;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int i = rows[b + it / t], c = it % t;
+      double v = Z[(int64_t)i * t + c];
+      for (int p = rp[i]; p < rp[i + 1]; ++p) v = __fma_rn(-val[p], Y[(int64_t)col[p] * t + c], v);
+      Y[(int64_t)i * t + c] = __ddiv_rn(v, diag[i]);
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_trsv_lev(cudaStream_t st, int ndom, int t, const int* rp, const int* col, const double* val,
+                            const double* diag, const int* dom_lev, const int* lev_ptr, const int* rows,
+                            const double* Z, double* Y) {
+  if (ndom < 1 || t < 1) return cudaErrorInvalidValue;
+  return launch_k(k_trsv_lev, ndom, 256, 0, st, t, rp, col, val, diag, dom_lev, lev_ptr, rows, Z, Y);
+}
+
 // Per-CTA partials of Wᵀv (t values per CTA, part[b·t + c]) over the CTA's contiguous rows; a
 // warp owns 32/L consecutive rows per step (coalesced), fixed-order lane/warp reductions.
 __global__ void __launch_bounds__(256) k_wtv(int64_t n, int t, const double* __restrict__ W,

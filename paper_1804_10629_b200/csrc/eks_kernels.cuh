@@ -82,6 +82,10 @@ cudaError_t launch_chol_dyn(cudaStream_t st, int m, const double* B, const doubl
 cudaError_t launch_ca_combine(cudaStream_t st, int64_t n, int t, int s, const CaPtrs& P, const double* Rinv,
                               int sms, bool skip_on_breakdown);
 // x += Σ_j in_j α_j, rnew = r − Σ_j out_j α_j (in = W, out = AW), partial ‖rnew‖² per CTA into part[nblk].
+// level-scheduled block-diagonal triangular solve (one CTA per domain), Y may alias Z
+cudaError_t launch_trsv_lev(cudaStream_t st, int ndom, int t, const int* rp, const int* col, const double* val,
+                            const double* diag, const int* dom_lev, const int* lev_ptr, const int* rows,
+                            const double* Z, double* Y);
 cudaError_t launch_wtv(cudaStream_t st, int64_t n, int t, const double* W, const double* v, double* part, int nblk);
 cudaError_t launch_ca_pack(cudaStream_t st, int t, int s, const double* Rinv, double* pack);
 cudaError_t launch_ca_update(cudaStream_t st, int64_t n, int t, int s, const CaPtrs& P, const double* alpha,

@@ -232,6 +232,59 @@ def test_pre_restructured_argument_errors(eks, torch_cuda):
     S.close()
 
 
+# ------------------------------------------------------------------ §8(f) row 2: split-preconditioned (Alg 8-10)
+@pytest.mark.parametrize("method,s_,t,nd", [("sre-cg", 1, 1, 64), ("sre-cg", 3, 4, 64), ("sre-cg2", 2, 8, 64),
+                                            ("msdo-cg", 2, 4, 64), ("sre-cg", 3, 16, 64), ("sre-cg", 2, 32, 32),
+                                            ("msdo-cg", 3, 2, 16), ("sre-cg", 2, 64, 64)])
+def test_preconditioned_end_to_end(eks, torch_cuda, oracle_lib, method, s_, t, nd):
+    """Block-Jacobi IC(0) split-preconditioned s-step methods (reading R32) on cfg1: counts within
+    5 %, x within 1e-6 of the oracle (mirror mode), a 2-iteration prefix within 1e-9, and fewer
+    outer iterations than unpreconditioned."""
+    p = ei.cfg1()
+    st, L = oracle_lib.ic0(p.A, nd)
+    assert st == 0
+    S = eks.Solver(p.A)
+    S.setup_precond(nd)
+    rep = S.solve(dev(torch_cuda, p.b), method, s_, t, p.tol, precond=True)
+    pre = S.solve(dev(torch_cuda, p.b), method, s_, t, 0.0, max_outer=3, precond=True)
+    plain = S.solve(dev(torch_cuda, p.b), method, s_, t, p.tol)
+    S.close()
+    ref = oracle_lib.solve(p.A, p.b, method, s_, t, p.tol, mode=oracle_lib.MODE_MIRROR, L=L)
+    refp = oracle_lib.solve(p.A, p.b, method, s_, t, 0.0, kmax=3, mode=oracle_lib.MODE_MIRROR, L=L)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+    assert rep["true_relres"] <= 1.5e-8
+    assert pre["outer_iters"] == refp["outer_iters"] == 2
+    assert rel(host(pre["x"]), refp["x"]) <= 1e-9
+    assert rep["outer_iters"] < plain["outer_iters"]
+
+
+def test_preconditioner_errors(eks, torch_cuda):
+    A = ei.poisson2d(16)
+    S = eks.Solver(A)
+    b = dev(torch_cuda, ei.uniform_pm1(3, A.n))
+    with pytest.raises(eks.EksError) as e:
+        S.solve(b, "sre-cg", 2, 4, 1e-8, precond=True)   # no eks_setup_precond yet
+    assert e.value.status == 2
+    S.setup_precond(8)
+    for kw in (dict(t=16), dict(method="ca-sre-cg"), dict(restructured=True)):
+        args = dict(method="sre-cg", t=4)
+        args.update(kw)
+        with pytest.raises(eks.EksError) as e:
+            S.solve(b, args.pop("method"), 2, args.pop("t"), 1e-8, precond=True, **args)
+        assert e.value.status == 1
+    # an indefinite diagonal block: IC(0) breaks down at setup
+    D = np.array([[1.0, 2.0], [2.0, 1.0]])
+    B = ei.csr_from_dense(D)
+    S2 = eks.Solver(B)
+    with pytest.raises(eks.EksError) as e:
+        S2.setup_precond(1)
+    assert e.value.status == 7
+    S2.close()
+    S.close()
+
+
 def test_cfg2_full_size_prefix(eks, torch_cuda, oracle_lib):
     # full 512² operator, first 2 outer iterations (tol=0, k_max=3) — x after the same count
     p = ei.cfg2()

@@ -15,7 +15,8 @@ except Exception as e:
     print(name, "FAILED", open(f"gpurun_out/bench_{name}.err").read()[-400:])
 PY
 }
-run sstep
-run pre --ortho pre-cholqr
-run restr --restructured
-run ca2 --method ca-sre-cg --s 2
+
+
+
+
+run prec --precond 64
