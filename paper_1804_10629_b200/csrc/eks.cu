@@ -96,6 +96,16 @@ struct eks_ctx {
   int* pr_levptr[2] = {nullptr, nullptr};
   int* pr_rows[2] = {nullptr, nullptr};
   int pr_levels[2] = {0, 0};       // longest level chain of a domain (forward, backward)
+  int pr_ring[2] = {0, 0};         // shared-memory ring rows of k_trsv_ring (0: not applicable)
+  int pr_E[2] = {0, 0};            // entries per position of the flattened schedule
+  int* pr_prow[2] = {nullptr, nullptr};
+  int* pr_pout[2] = {nullptr, nullptr};
+  int pr_maxlev[2] = {0, 0};       // most levels of one domain
+  Block Zq1, Zq2;                  // the block in forward / backward schedule order
+  int* pr_pne[2] = {nullptr, nullptr};
+  double* pr_pdiag[2] = {nullptr, nullptr};
+  int* pr_pcol[2] = {nullptr, nullptr};
+  double* pr_pval[2] = {nullptr, nullptr};
   bool use_prec = false;           // this solve applies M⁻¹ (eks_options.precond)
   Block Zp;                        // M⁻¹·Z of the next block
   double* pre = nullptr;           // Pre-CholQR / restructured scratch: [G | R1⁻¹ | −R1⁻¹ | g] (3t²+t)
@@ -248,7 +258,7 @@ void free_workspace(eks_ctx* c) {
   for (auto& b : c->AWpool) dfree(b.base);
   c->Wpool.clear();
   c->AWpool.clear();
-  for (Block* b : {&c->Zs, &c->Z1, &c->xv, &c->tmpv, &c->Zp}) { dfree(b->base); *b = Block{}; }
+  for (Block* b : {&c->Zs, &c->Z1, &c->xv, &c->tmpv, &c->Zp, &c->Zq1, &c->Zq2}) { dfree(b->base); *b = Block{}; }
   for (double** p : {&c->b, &c->r, &c->rnew, &c->dx, &c->part, &c->C1, &c->C2, &c->Bg, &c->Rm, &c->Rinv,
                      &c->alpha, &c->scal}) { dfree(*p); *p = nullptr; }
   dfree(c->flag);
@@ -651,6 +661,20 @@ Window window_for(eks_ctx* ctx, int method, int nblocks, int ring) {
 eks_status prec_apply(eks_ctx* ctx, int t, const double* Z, double* Y) {
   KScope k(ctx, EKS_K_OTHER);
   account(ctx, EKS_K_OTHER, 2.0 * (12.0 * ctx->nnz / 2 + 16.0 * ctx->n * t), 2.0 * ctx->nnz * t);
+  bool ring = true;
+  for (int w = 0; w < 2; ++w)
+    ring = ring && ctx->pr_ring[w] && eks::trsv_ring_smem(ctx->pr_ring[w], t, ctx->pr_maxlev[w]) <= 220 * 1024;
+  if (ring) {  // gather into the forward order, forward → backward order, backward → natural order
+    ST(alloc_block(ctx, &ctx->Zq1, t, false));
+    ST(alloc_block(ctx, &ctx->Zq2, t, false));
+    CK(eks::launch_perm_gather(ctx->stream, ctx->n, t, ctx->pr_prow[0], Z, ctx->Zq1.loc, ctx->sms));
+    for (int w = 0; w < 2; ++w)
+      CK(eks::launch_trsv_ring(ctx->stream, ctx->prec_ndl, t, ctx->pr_ring[w], ctx->pr_maxlev[w], ctx->pr_prow[w],
+                               ctx->pr_pout[w], ctx->pr_pne[w], ctx->pr_pdiag[w], ctx->pr_pcol[w], ctx->pr_pval[w],
+                               ctx->pr_E[w], ctx->pr_domlev[w], ctx->pr_levptr[w], w ? ctx->Zq2.loc : ctx->Zq1.loc,
+                               w ? Y : ctx->Zq2.loc));
+    return EKS_OK;
+  }
   for (int w = 0; w < 2; ++w)
     CK(eks::launch_trsv_lev(ctx->stream, ctx->prec_ndl, t, ctx->pr_rp[w], ctx->pr_col[w], ctx->pr_val[w],
                             ctx->pr_diag, ctx->pr_domlev[w], ctx->pr_levptr[w], ctx->pr_rows[w], w ? Y : Z, Y));
@@ -1421,14 +1445,18 @@ namespace {
 void free_precond(eks_ctx* ctx) {
   for (int w = 0; w < 2; ++w) {
     for (void* p : {(void*)ctx->pr_rp[w], (void*)ctx->pr_col[w], (void*)ctx->pr_val[w], (void*)ctx->pr_domlev[w],
-                    (void*)ctx->pr_levptr[w], (void*)ctx->pr_rows[w]})
+                    (void*)ctx->pr_levptr[w], (void*)ctx->pr_rows[w], (void*)ctx->pr_prow[w], (void*)ctx->pr_pne[w],
+                    (void*)ctx->pr_pdiag[w], (void*)ctx->pr_pcol[w], (void*)ctx->pr_pval[w], (void*)ctx->pr_pout[w]})
       dfree(p);
+    ctx->pr_prow[w] = ctx->pr_pne[w] = ctx->pr_pcol[w] = ctx->pr_pout[w] = nullptr;
+    ctx->pr_pdiag[w] = ctx->pr_pval[w] = nullptr;
     ctx->pr_rp[w] = ctx->pr_col[w] = ctx->pr_domlev[w] = ctx->pr_levptr[w] = ctx->pr_rows[w] = nullptr;
     ctx->pr_val[w] = nullptr;
   }
   dfree(ctx->pr_diag);
   ctx->pr_diag = nullptr;
   ctx->prec_nd = ctx->prec_ndl = 0;
+  ctx->pr_ring[0] = ctx->pr_ring[1] = 0;
 }
 
 template <typename T>
@@ -1525,6 +1553,7 @@ eks_status eks_setup_precond(eks_ctx* ctx, int nd, const int64_t* row_ptr, const
   // level schedules per domain: forward lev(i) = 1 + max lev(k), k < i in row i of L;
   // backward from the last row with Lᵗ
   const int ndl = d1 - d0;
+  std::vector<int> sched[2], ringw(2, 0), maxe_w(2, 0);
   for (int w = 0; w < 2; ++w) {
     const std::vector<int>& R = w ? Urp : Lrp;
     const std::vector<int>& Cc = w ? Ucol : Lcol;
@@ -1553,12 +1582,75 @@ eks_status eks_setup_precond(eks_ctx* ctx, int nd, const int64_t* row_ptr, const
     domlev[ndl] = (int)levptr.size();
     levptr.push_back((int)rows.size());
     ctx->pr_levels[w] = maxl;
+    // ring width: the smallest power of two W such that the row that next takes a row's slot
+    // (r + W forward, r − W backward, same domain) is solved at a later level than every reader
+    // of r; rows must have ≤ kTrsvMaxE entries.  0 = use the plain kernel.
+    {
+      std::vector<int> maxrd(n, -1);
+      int maxe = 0;
+      for (int64_t i = 0; i < n; ++i) {
+        maxe = std::max(maxe, R[i + 1] - R[i]);
+        for (int p = R[i]; p < R[i + 1]; ++p) maxrd[Cc[p]] = std::max(maxrd[Cc[p]], lev[i]);
+      }
+      int best = 0;
+      if (maxe <= eks::kTrsvMaxE)
+        for (int W = 2; W <= 4096 && !best; W *= 2) {
+          bool ok = true;
+          for (int64_t r = 0; r < n && ok; ++r) {
+            if (maxrd[r] < 0) continue;
+            const int64_t j = w ? r - W : r + W;
+            if (j < 0 || j >= n || dom[j] != dom[r]) continue;
+            ok = lev[j] > maxrd[r];
+          }
+          if (ok) best = W;
+        }
+      ringw[w] = best;
+      maxe_w[w] = maxe;
+    }
+    sched[w] = rows;
+    int maxdl = 0;
+    for (int d = 0; d < ndl; ++d) maxdl = std::max(maxdl, domlev[d + 1] - domlev[d]);
+    ctx->pr_maxlev[w] = maxdl;
     ST(upload(ctx, &ctx->pr_rp[w], R));
     ST(upload(ctx, &ctx->pr_col[w], Cc));
     ST(upload(ctx, &ctx->pr_val[w], w ? Uval : Lval));
     ST(upload(ctx, &ctx->pr_domlev[w], domlev));
     ST(upload(ctx, &ctx->pr_levptr[w], levptr));
     ST(upload(ctx, &ctx->pr_rows[w], rows));
+  }
+  // flattened level-order schedules for k_trsv_ring (both sweeps must qualify): position → row,
+  // output index (forward: the row's position in the backward schedule; backward: the row)
+  if (ringw[0] && ringw[1]) {
+    std::vector<int> bpos(n);
+    for (size_t q = 0; q < sched[1].size(); ++q) bpos[sched[1][q]] = (int)q;
+    for (int w = 0; w < 2; ++w) {
+      const std::vector<int>& R = w ? Urp : Lrp;
+      const std::vector<int>& Cc = w ? Ucol : Lcol;
+      const std::vector<double>& V = w ? Uval : Lval;
+      const std::vector<int>& rows = sched[w];
+      const int E = std::max(1, maxe_w[w]);
+      std::vector<int> prow(rows.size()), pout(rows.size()), pne(rows.size()), pcol(rows.size() * E, 0);
+      std::vector<double> pdiag(rows.size()), pval(rows.size() * E, 0.0);
+      for (size_t q = 0; q < rows.size(); ++q) {
+        const int i = rows[q];
+        prow[q] = i;
+        pout[q] = w ? i : bpos[i];
+        pne[q] = R[i + 1] - R[i];
+        pdiag[q] = diag[i];
+        for (int p = R[i], e = 0; p < R[i + 1]; ++p, ++e) {
+          pcol[q * E + e] = Cc[p];
+          pval[q * E + e] = V[p];
+        }
+      }
+      ctx->pr_E[w] = E;
+      ctx->pr_ring[w] = ringw[w];
+      ST(upload(ctx, &ctx->pr_prow[w], prow));
+      ST(upload(ctx, &ctx->pr_pout[w], pout));
+      ST(upload(ctx, &ctx->pr_pne[w], pne));
+      ST(upload(ctx, &ctx->pr_pdiag[w], pdiag));
+      ST(upload(ctx, &ctx->pr_pcol[w], pcol));
+      ST(upload(ctx, &ctx->pr_pval[w], pval));
+    }
   }
   ST(upload(ctx, &ctx->pr_diag, diag));
   ctx->prec_nd = nd;

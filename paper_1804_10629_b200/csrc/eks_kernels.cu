@@ -889,6 +889,143 @@ cudaError_t launch_trsv_lev(cudaStream_t st, int ndom, int t, const int* rp, con
   return launch_k(k_trsv_lev, ndom, 256, 0, st, t, rp, col, val, diag, dom_lev, lev_ptr, rows, Z, Y);
 }
 
+// The same sweep with the solved rows kept in a shared-memory ring of W rows (slot = row mod W):
+// the setup chose W so that a row's slot is rewritten only at a later level than its last reader
+// (eks.cu, ring width).  Everything an item needs is addressed by its schedule position: the
+// level bounds (staged in shared memory), the flattened schedule (row, output index, #entries,
+// diagonal, ≤ E entries) and the input block, which arrives already permuted into schedule order
+// (k_perm_gather for the forward sweep; the forward sweep writes its result in the backward
+// schedule's order).  So no load waits on another, and every thread keeps the items of the next
+// kTrsvD levels in flight: a level costs shared-memory reads and one barrier.
+constexpr int kTrsvE = 8, kTrsvD = 4;
+struct TrsvItem {
+  int i, o, c, ne;
+  double z, dg;
+  int k[kTrsvE];
+  double v[kTrsvE];
+};
+
+struct TrsvSched {  // flattened schedule of one sweep
+  const int* pos_row;
+  const int* pos_out;     // output row index (forward: position in the backward schedule; backward: row)
+  const int* pos_ne;
+  const double* pos_diag;
+  const int* pos_col;     // pos * E + e
+  const double* pos_val;  // pos * E + e
+  int E;
+};
+
+__device__ __forceinline__ bool trsv_fetch(TrsvItem& f, int L, int l1, const int* slev, int l0, int t,
+                                           const TrsvSched& S, const double* Zp) {
+  if (L >= l1) return false;
+  const int b = slev[L - l0], items = (slev[L - l0 + 1] - b) * t;
+  if ((int)threadIdx.x >= items) return false;
+  const int pos = b + threadIdx.x / t;
+  f.c = threadIdx.x % t;
+  f.i = __ldg(S.pos_row + pos);
+  f.o = __ldg(S.pos_out + pos);
+  f.ne = __ldg(S.pos_ne + pos);
+  f.dg = __ldg(S.pos_diag + pos);
+#pragma unroll
+  for (int e = 0; e < kTrsvE; ++e)
+    if (e < S.E) {
+      f.k[e] = __ldg(S.pos_col + (size_t)pos * S.E + e);
+      f.v[e] = __ldg(S.pos_val + (size_t)pos * S.E + e);
+    }
+  f.z = Zp[(int64_t)pos * t + f.c];
+  return true;
+}
+
+__device__ __forceinline__ void trsv_solve(const TrsvItem& f, double* ring, int wmask, int t, double* Y) {
+  double v = f.z;
+#pragma unroll
+  for (int e = 0; e < kTrsvE; ++e)
+    if (e < f.ne) v = __fma_rn(-f.v[e], ring[(f.k[e] & wmask) * t + f.c], v);
+  v = __ddiv_rn(v, f.dg);
+  ring[(f.i & wmask) * t + f.c] = v;
+  Y[(int64_t)f.o * t + f.c] = v;
+}
+
+__global__ void __launch_bounds__(256) k_trsv_ring(int t, int wmask, int maxlev, const TrsvSched S,
+                                                   const int* __restrict__ dom_lev,
+                                                   const int* __restrict__ lev_ptr, const double* Zp, double* Y) {
+  pdl_enter();
+  extern __shared__ double ring[];  // (wmask + 1) × t doubles, then maxlev + 1 level bounds
+  int* slev = reinterpret_cast<int*>(ring + (size_t)(wmask + 1) * t);
+  const int d = blockIdx.x, tid = threadIdx.x;
+  const int l0 = dom_lev[d], l1 = dom_lev[d + 1];
+  for (int e = tid; e <= l1 - l0; e += blockDim.x) slev[e] = lev_ptr[l0 + e];
+  __syncthreads();
+  TrsvItem q[kTrsvD];
+  bool h[kTrsvD];
+#pragma unroll
+  for (int u = 0; u < kTrsvD; ++u) h[u] = trsv_fetch(q[u], l0 + u, l1, slev, l0, t, S, Zp);
+  for (int lv = l0; lv < l1; lv += kTrsvD) {
+#pragma unroll
+    for (int u = 0; u < kTrsvD; ++u) {
+      const int L = lv + u;
+      if (L < l1) {  // uniform across the CTA
+        if (h[u]) trsv_solve(q[u], ring, wmask, t, Y);
+        const int b = slev[L - l0], items = (slev[L - l0 + 1] - b) * t;
+        for (int it = tid + 256; it < items; it += 256) {  // wide levels: the rest without prefetch
+          TrsvItem f;
+          const int pos = b + it / t;
+          f.c = it % t;
+          f.i = __ldg(S.pos_row + pos);
+          f.o = __ldg(S.pos_out + pos);
+          f.ne = __ldg(S.pos_ne + pos);
+          f.dg = __ldg(S.pos_diag + pos);
+#pragma unroll
+          for (int e = 0; e < kTrsvE; ++e)
+            if (e < S.E) {
+              f.k[e] = __ldg(S.pos_col + (size_t)pos * S.E + e);
+              f.v[e] = __ldg(S.pos_val + (size_t)pos * S.E + e);
+            }
+          f.z = Zp[(int64_t)pos * t + f.c];
+          trsv_solve(f, ring, wmask, t, Y);
+        }
+        h[u] = trsv_fetch(q[u], L + kTrsvD, l1, slev, l0, t, S, Zp);
+        __syncthreads();
+      }
+    }
+  }
+  (void)maxlev;
+}
+
+// Zp[pos] = Z[row(pos)] for every schedule position (the forward sweep's input in its order).
+__global__ void __launch_bounds__(256) k_perm_gather(int64_t npos, int t, const int* __restrict__ pos_row,
+                                                     const double* __restrict__ Z, double* __restrict__ Zp) {
+  pdl_enter();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < npos * t; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = e / t;
+    const int c = (int)(e % t);
+    Zp[e] = Z[(int64_t)__ldg(pos_row + pos) * t + c];
+  }
+}
+
+cudaError_t launch_perm_gather(cudaStream_t st, int64_t npos, int t, const int* pos_row, const double* Z,
+                               double* Zp, int sms) {
+  const int64_t total = npos * t;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  if (blocks < 1) blocks = 1;
+  return launch_k(k_perm_gather, (int)blocks, 256, 0, st, npos, t, pos_row, Z, Zp);
+}
+
+size_t trsv_ring_smem(int wrows, int t, int maxlev) { return (size_t)wrows * t * 8 + (size_t)(maxlev + 1) * 4; }
+
+cudaError_t launch_trsv_ring(cudaStream_t st, int ndom, int t, int wrows, int maxlev, const int* pos_row,
+                             const int* pos_out, const int* pos_ne, const double* pos_diag, const int* pos_col,
+                             const double* pos_val, int E, const int* dom_lev, const int* lev_ptr, const double* Zp,
+                             double* Y) {
+  if (ndom < 1 || t < 1 || wrows < 1 || (wrows & (wrows - 1)) || E > kTrsvE) return cudaErrorInvalidValue;
+  const size_t sm = trsv_ring_smem(wrows, t, maxlev);
+  if (sm > 220 * 1024) return cudaErrorInvalidValue;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_trsv_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const TrsvSched S{pos_row, pos_out, pos_ne, pos_diag, pos_col, pos_val, E};
+  return launch_k(k_trsv_ring, ndom, 256, sm, st, t, wrows - 1, maxlev, S, dom_lev, lev_ptr, Zp, Y);
+}
+
 // Per-CTA partials of Wᵀv (t values per CTA, part[b·t + c]) over the CTA's contiguous rows; a
 // warp owns 32/L consecutive rows per step (coalesced), fixed-order lane/warp reductions.
 __global__ void __launch_bounds__(256) k_wtv(int64_t n, int t, const double* __restrict__ W,
