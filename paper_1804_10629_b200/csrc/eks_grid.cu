@@ -388,7 +388,12 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
 template <int T>
 static void grid_shape(const GridPlan& gp, int& bx, int& by, int& zc, int sms) {
   using K = GrCfg<T>;
-  by = gp.ny > 1 ? 4 : 1;
+  static const int by_env = [] {  // EKS_GRID_BY: plane-block height override for A/B measurements
+    const char* e = getenv("EKS_GRID_BY");
+    return e ? atoi(e) : 0;
+  }();
+  by = gp.ny > 1 ? (by_env > 0 ? by_env : 4) : 1;
+  if (by > K::R / 4) by = K::R / 4;
   bx = K::R / by;
   const int64_t blocks = (int64_t)((gp.nx + bx - 1) / bx) * ((gp.ny + by - 1) / by);
   // z chunks so that every SM gets ≥ ~4 units (each chunk re-reads 2 halo planes)
@@ -397,6 +402,11 @@ static void grid_shape(const GridPlan& gp, int& bx, int& by, int& zc, int sms) {
   if (nzc < 1) nzc = 1;
   zc = (int)((gp.nz + nzc - 1) / nzc);
   if (zc < 8) zc = gp.nz < 8 ? gp.nz : 8;
+  static const int zc_env = [] {  // EKS_GRID_ZC: z-chunk override for A/B measurements
+    const char* e = getenv("EKS_GRID_ZC");
+    return e ? atoi(e) : 0;
+  }();
+  if (zc_env > 0) zc = zc_env < gp.nz ? zc_env : gp.nz;
 }
 
 template <int T, int W>
