@@ -908,8 +908,12 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
   }
   {
     KScope kk(ctx, EKS_K_CHOL);
-    CK(eks::launch_chol_dyn(ctx->stream, st, ctx->Bca, ctx->gca, ctx->Rca, ctx->Rinvca, ctx->alphaca, ctx->flag,
-                            nblocks, ctx->cawork));
+    if (st <= 32 && (st & (st - 1)) == 0)  // one-warp register Cholesky (upper triangle only)
+      CK(eks::launch_chol_fast(ctx->stream, st, ctx->Bca, ctx->gca, ctx->Rca, ctx->Rinvca, ctx->alphaca, ctx->flag,
+                               nblocks));
+    else
+      CK(eks::launch_chol_dyn(ctx->stream, st, ctx->Bca, ctx->gca, ctx->Rca, ctx->Rinvca, ctx->alphaca, ctx->flag,
+                              nblocks, ctx->cawork));
   }
   // W = V R⁻¹, AW = AV R⁻¹ into the new slots
   eks::CaPtrs Pw{}, Pa{}, Pu{};

@@ -1140,10 +1140,90 @@ __global__ void __launch_bounds__(256) k_ca_update(int64_t n, int t, int s, CaPt
   if (threadIdx.x == 0) part[blockIdx.x] = tot;
 }
 
+// The same with M = s·⌈t/L⌉ ≤ 4 (block, column) pairs per lane known at compile time and U = 4 row
+// groups per warp step: all 2·M·U block loads of a step are issued before the first FMA (memory-
+// level parallelism; the generic kernel above waits on each load).
+template <int M>
+__global__ void __launch_bounds__(256) k_ca_update_m(int64_t n, int t, int s, CaPtrs P, const double* __restrict__ alpha,
+                                                     double* __restrict__ x, const double* __restrict__ r,
+                                                     double* __restrict__ rnew, double* __restrict__ part) {
+  pdl_enter();
+  constexpr int U = 4;
+  __shared__ double sa[kCaMax];
+  __shared__ double sred[32];
+  const int m = s * t;
+  const bool skip = *reinterpret_cast<const volatile int*>(P.flag) != INT_MAX;
+  for (int e = threadIdx.x; e < m; e += blockDim.x) sa[e] = alpha[e];
+  __syncthreads();
+  int L = 1;
+  while (2 * L <= t && 2 * L <= 32) L *= 2;
+  const int RPW = 32 / L, CPL = (t + L - 1) / L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int sub = lane / L, lc = lane % L;
+  const int64_t lo = (int64_t)blockIdx.x * n / gridDim.x, hi = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
+  // this lane's (block j, column c) pairs and their α
+  int jj[M], cc[M];
+  double al[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    jj[q] = q / CPL;
+    cc[q] = lc + (q % CPL) * L;
+    al[q] = (cc[q] < t) ? sa[jj[q] * t + cc[q]] : 0.0;
+  }
+  double acc = 0.0;
+  for (int64_t r0 = lo + (int64_t)warp * RPW * U; r0 < hi; r0 += (int64_t)nw * RPW * U) {
+    double wv[U][M], av[U][M];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = r0 + u * RPW + sub;
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        const bool ok = i < hi && cc[q] < t;
+        wv[u][q] = ok ? P.in[jj[q]][i * t + cc[q]] : 0.0;
+        av[u][q] = ok ? P.out[jj[q]][i * t + cc[q]] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double dx = 0.0, dr = 0.0;
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        dx = __fma_rn(wv[u][q], al[q], dx);
+        dr = __fma_rn(av[u][q], al[q], dr);
+      }
+      for (int o = L >> 1; o > 0; o >>= 1) {
+        dx += __shfl_xor_sync(0xffffffffu, dx, o);
+        dr += __shfl_xor_sync(0xffffffffu, dr, o);
+      }
+      const int64_t i = r0 + u * RPW + sub;
+      if (i < hi && lc == 0) {
+        double ri = r[i];
+        if (!skip) {
+          x[i] += dx;
+          ri -= dr;
+        }
+        rnew[i] = ri;
+        acc = __fma_rn(ri, ri, acc);
+      }
+    }
+  }
+  const double tot = block_sum(acc, sred);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
 cudaError_t launch_ca_update(cudaStream_t st, int64_t n, int t, int s, const CaPtrs& P, const double* alpha,
                              double* x, const double* r, double* rnew, double* part, int nblk) {
   if (s * t > kCaMax || s > kCaMaxBlocks) return cudaErrorInvalidValue;
-  return launch_k(k_ca_update, nblk, 256, 0, st, n, t, s, P, alpha, x, r, rnew, part);
+  int L = 1;
+  while (2 * L <= t && 2 * L <= 32) L *= 2;
+  const int M = s * ((t + L - 1) / L);
+  switch (M) {
+    case 1: return launch_k(k_ca_update_m<1>, nblk, 256, 0, st, n, t, s, P, alpha, x, r, rnew, part);
+    case 2: return launch_k(k_ca_update_m<2>, nblk, 256, 0, st, n, t, s, P, alpha, x, r, rnew, part);
+    case 3: return launch_k(k_ca_update_m<3>, nblk, 256, 0, st, n, t, s, P, alpha, x, r, rnew, part);
+    case 4: return launch_k(k_ca_update_m<4>, nblk, 256, 0, st, n, t, s, P, alpha, x, r, rnew, part);
+    default: return launch_k(k_ca_update, nblk, 256, 0, st, n, t, s, P, alpha, x, r, rnew, part);
+  }
 }
 
 // ============================================================================

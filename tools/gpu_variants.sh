@@ -15,8 +15,11 @@ except Exception as e:
     print(name, "FAILED", open(f"gpurun_out/bench_{name}.err").read()[-400:])
 PY
 }
-
-
-
-
-run prec --precond 64
+for v in $VARIANTS; do
+  case $v in
+    ca2) run ca2 --method ca-sre-cg --s 2 ;;
+    restr) run restr --restructured ;;
+    pre) run pre --ortho pre-cholqr ;;
+    prec) run prec --precond 64 ;;
+  esac
+done
