@@ -101,6 +101,7 @@ struct eks_ctx {
   int* pr_prow[2] = {nullptr, nullptr};
   int* pr_pout[2] = {nullptr, nullptr};
   int pr_maxlev[2] = {0, 0};       // most levels of one domain
+  int pr_maxrows[2] = {0, 0};      // most rows of one level
   Block Zq1, Zq2;                  // the block in forward / backward schedule order
   int* pr_pne[2] = {nullptr, nullptr};
   double* pr_pdiag[2] = {nullptr, nullptr};
@@ -669,7 +670,8 @@ eks_status prec_apply(eks_ctx* ctx, int t, const double* Z, double* Y) {
     ST(alloc_block(ctx, &ctx->Zq2, t, false));
     CK(eks::launch_perm_gather(ctx->stream, ctx->n, t, ctx->pr_prow[0], Z, ctx->Zq1.loc, ctx->sms));
     for (int w = 0; w < 2; ++w)
-      CK(eks::launch_trsv_ring(ctx->stream, ctx->prec_ndl, t, ctx->pr_ring[w], ctx->pr_maxlev[w], ctx->pr_prow[w],
+      CK(eks::launch_trsv_ring(ctx->stream, ctx->prec_ndl, t, ctx->pr_ring[w], ctx->pr_maxlev[w], ctx->pr_maxrows[w],
+                               ctx->pr_prow[w],
                                ctx->pr_pout[w], ctx->pr_pne[w], ctx->pr_pdiag[w], ctx->pr_pcol[w], ctx->pr_pval[w],
                                ctx->pr_E[w], ctx->pr_domlev[w], ctx->pr_levptr[w], w ? ctx->Zq2.loc : ctx->Zq1.loc,
                                w ? Y : ctx->Zq2.loc));
@@ -1612,9 +1614,11 @@ eks_status eks_setup_precond(eks_ctx* ctx, int nd, const int64_t* row_ptr, const
       maxe_w[w] = maxe;
     }
     sched[w] = rows;
-    int maxdl = 0;
+    int maxdl = 0, maxr = 0;
     for (int d = 0; d < ndl; ++d) maxdl = std::max(maxdl, domlev[d + 1] - domlev[d]);
+    for (size_t q = 0; q + 1 < levptr.size(); ++q) maxr = std::max(maxr, levptr[q + 1] - levptr[q]);
     ctx->pr_maxlev[w] = maxdl;
+    ctx->pr_maxrows[w] = maxr;
     ST(upload(ctx, &ctx->pr_rp[w], R));
     ST(upload(ctx, &ctx->pr_col[w], Cc));
     ST(upload(ctx, &ctx->pr_val[w], w ? Uval : Lval));
@@ -1632,7 +1636,7 @@ eks_status eks_setup_precond(eks_ctx* ctx, int nd, const int64_t* row_ptr, const
       const std::vector<int>& Cc = w ? Ucol : Lcol;
       const std::vector<double>& V = w ? Uval : Lval;
       const std::vector<int>& rows = sched[w];
-      const int E = std::max(1, maxe_w[w]);
+      const int E = maxe_w[w] <= 4 ? std::max(1, maxe_w[w]) : 8;  // the kernel's instantiations
       std::vector<int> prow(rows.size()), pout(rows.size()), pne(rows.size()), pcol(rows.size() * E, 0);
       std::vector<double> pdiag(rows.size()), pval(rows.size() * E, 0.0);
       for (size_t q = 0; q < rows.size(); ++q) {
@@ -1640,7 +1644,7 @@ eks_status eks_setup_precond(eks_ctx* ctx, int nd, const int64_t* row_ptr, const
         prow[q] = i;
         pout[q] = w ? i : bpos[i];
         pne[q] = R[i + 1] - R[i];
-        pdiag[q] = diag[i];
+        pdiag[q] = 1.0 / diag[i];
         for (int p = R[i], e = 0; p < R[i + 1]; ++p, ++e) {
           pcol[q * E + e] = Cc[p];
           pval[q * E + e] = V[p];

@@ -897,99 +897,88 @@ cudaError_t launch_trsv_lev(cudaStream_t st, int ndom, int t, const int* rp, con
 // (k_perm_gather for the forward sweep; the forward sweep writes its result in the backward
 // schedule's order).  So no load waits on another, and every thread keeps the items of the next
 // kTrsvD levels in flight: a level costs shared-memory reads and one barrier.
-constexpr int kTrsvE = 8, kTrsvD = 4;
+constexpr int kTrsvD = 4;
+template <int E>
 struct TrsvItem {
-  int i, o, c, ne;
-  double z, dg;
-  int k[kTrsvE];
-  double v[kTrsvE];
+  int i, o, ne;
+  double z, rd;
+  int k[E];
+  double v[E];
 };
 
 struct TrsvSched {  // flattened schedule of one sweep
   const int* pos_row;
   const int* pos_out;     // output row index (forward: position in the backward schedule; backward: row)
   const int* pos_ne;
-  const double* pos_diag;
+  const double* pos_rdiag;  // 1 / L_ii
   const int* pos_col;     // pos * E + e
   const double* pos_val;  // pos * E + e
-  int E;
 };
 
-__device__ __forceinline__ bool trsv_fetch(TrsvItem& f, int L, int l1, const int* slev, int l0, int t,
-                                           const TrsvSched& S, const double* Zp) {
-  if (L >= l1) return false;
-  const int b = slev[L - l0], items = (slev[L - l0 + 1] - b) * t;
-  if ((int)threadIdx.x >= items) return false;
-  const int pos = b + threadIdx.x / t;
-  f.c = threadIdx.x % t;
+template <int E>
+__device__ __forceinline__ void trsv_load(TrsvItem<E>& f, int pos, int c, int t, const TrsvSched& S, const double* Zp) {
   f.i = __ldg(S.pos_row + pos);
   f.o = __ldg(S.pos_out + pos);
   f.ne = __ldg(S.pos_ne + pos);
-  f.dg = __ldg(S.pos_diag + pos);
+  f.rd = __ldg(S.pos_rdiag + pos);
 #pragma unroll
-  for (int e = 0; e < kTrsvE; ++e)
-    if (e < S.E) {
-      f.k[e] = __ldg(S.pos_col + (size_t)pos * S.E + e);
-      f.v[e] = __ldg(S.pos_val + (size_t)pos * S.E + e);
-    }
-  f.z = Zp[(int64_t)pos * t + f.c];
-  return true;
+  for (int e = 0; e < E; ++e) {
+    f.k[e] = __ldg(S.pos_col + (size_t)pos * E + e);
+    f.v[e] = __ldg(S.pos_val + (size_t)pos * E + e);
+  }
+  f.z = Zp[(int64_t)pos * t + c];
 }
 
-__device__ __forceinline__ void trsv_solve(const TrsvItem& f, double* ring, int wmask, int t, double* Y) {
+template <int E>
+__device__ __forceinline__ void trsv_solve(const TrsvItem<E>& f, int c, double* ring, int wmask, int t, double* Y) {
   double v = f.z;
 #pragma unroll
-  for (int e = 0; e < kTrsvE; ++e)
-    if (e < f.ne) v = __fma_rn(-f.v[e], ring[(f.k[e] & wmask) * t + f.c], v);
-  v = __ddiv_rn(v, f.dg);
-  ring[(f.i & wmask) * t + f.c] = v;
-  Y[(int64_t)f.o * t + f.c] = v;
+  for (int e = 0; e < E; ++e)
+    if (e < f.ne) v = __fma_rn(-f.v[e], ring[(f.k[e] & wmask) * t + c], v);
+  v = v * f.rd;
+  ring[(f.i & wmask) * t + c] = v;
+  Y[(int64_t)f.o * t + c] = v;
 }
 
-__global__ void __launch_bounds__(256) k_trsv_ring(int t, int wmask, int maxlev, const TrsvSched S,
+template <int E>
+__global__ void __launch_bounds__(256) k_trsv_ring(int t, int wmask, const TrsvSched S,
                                                    const int* __restrict__ dom_lev,
                                                    const int* __restrict__ lev_ptr, const double* Zp, double* Y) {
   pdl_enter();
-  extern __shared__ double ring[];  // (wmask + 1) × t doubles, then maxlev + 1 level bounds
+  extern __shared__ double ring[];  // (wmask + 1) × t doubles, then the domain's level bounds
   int* slev = reinterpret_cast<int*>(ring + (size_t)(wmask + 1) * t);
-  const int d = blockIdx.x, tid = threadIdx.x;
+  const int d = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
   const int l0 = dom_lev[d], l1 = dom_lev[d + 1];
-  for (int e = tid; e <= l1 - l0; e += blockDim.x) slev[e] = lev_ptr[l0 + e];
+  for (int e = tid; e <= l1 - l0; e += nth) slev[e] = lev_ptr[l0 + e];
   __syncthreads();
-  TrsvItem q[kTrsvD];
+  const int prow = tid / t, c = tid % t;  // this thread's (row in level, column) of a level's first nth items
+  TrsvItem<E> q[kTrsvD];
   bool h[kTrsvD];
 #pragma unroll
-  for (int u = 0; u < kTrsvD; ++u) h[u] = trsv_fetch(q[u], l0 + u, l1, slev, l0, t, S, Zp);
+  for (int u = 0; u < kTrsvD; ++u) {
+    const int L = l0 + u;
+    h[u] = L < l1 && prow < slev[L - l0 + 1] - slev[L - l0];
+    if (h[u]) trsv_load(q[u], slev[L - l0] + prow, c, t, S, Zp);
+  }
   for (int lv = l0; lv < l1; lv += kTrsvD) {
 #pragma unroll
     for (int u = 0; u < kTrsvD; ++u) {
       const int L = lv + u;
       if (L < l1) {  // uniform across the CTA
-        if (h[u]) trsv_solve(q[u], ring, wmask, t, Y);
+        if (h[u]) trsv_solve(q[u], c, ring, wmask, t, Y);
         const int b = slev[L - l0], items = (slev[L - l0 + 1] - b) * t;
-        for (int it = tid + 256; it < items; it += 256) {  // wide levels: the rest without prefetch
-          TrsvItem f;
-          const int pos = b + it / t;
-          f.c = it % t;
-          f.i = __ldg(S.pos_row + pos);
-          f.o = __ldg(S.pos_out + pos);
-          f.ne = __ldg(S.pos_ne + pos);
-          f.dg = __ldg(S.pos_diag + pos);
-#pragma unroll
-          for (int e = 0; e < kTrsvE; ++e)
-            if (e < S.E) {
-              f.k[e] = __ldg(S.pos_col + (size_t)pos * S.E + e);
-              f.v[e] = __ldg(S.pos_val + (size_t)pos * S.E + e);
-            }
-          f.z = Zp[(int64_t)pos * t + f.c];
-          trsv_solve(f, ring, wmask, t, Y);
+        for (int it = tid + nth; it < items; it += nth) {  // wide levels: the rest without prefetch
+          TrsvItem<E> f;
+          trsv_load(f, b + it / t, it % t, t, S, Zp);
+          trsv_solve(f, it % t, ring, wmask, t, Y);
         }
-        h[u] = trsv_fetch(q[u], L + kTrsvD, l1, slev, l0, t, S, Zp);
+        const int Ln = L + kTrsvD;
+        h[u] = Ln < l1 && prow < slev[Ln - l0 + 1] - slev[Ln - l0];
+        if (h[u]) trsv_load(q[u], slev[Ln - l0] + prow, c, t, S, Zp);
         __syncthreads();
       }
     }
   }
-  (void)maxlev;
 }
 
 // Zp[pos] = Z[row(pos)] for every schedule position (the forward sweep's input in its order).
@@ -1014,16 +1003,31 @@ cudaError_t launch_perm_gather(cudaStream_t st, int64_t npos, int t, const int* 
 
 size_t trsv_ring_smem(int wrows, int t, int maxlev) { return (size_t)wrows * t * 8 + (size_t)(maxlev + 1) * 4; }
 
-cudaError_t launch_trsv_ring(cudaStream_t st, int ndom, int t, int wrows, int maxlev, const int* pos_row,
-                             const int* pos_out, const int* pos_ne, const double* pos_diag, const int* pos_col,
-                             const double* pos_val, int E, const int* dom_lev, const int* lev_ptr, const double* Zp,
-                             double* Y) {
-  if (ndom < 1 || t < 1 || wrows < 1 || (wrows & (wrows - 1)) || E > kTrsvE) return cudaErrorInvalidValue;
+cudaError_t launch_trsv_ring(cudaStream_t st, int ndom, int t, int wrows, int maxlev, int maxrows,
+                             const int* pos_row, const int* pos_out, const int* pos_ne, const double* pos_rdiag,
+                             const int* pos_col, const double* pos_val, int E, const int* dom_lev, const int* lev_ptr,
+                             const double* Zp, double* Y) {
+  if (ndom < 1 || t < 1 || wrows < 1 || (wrows & (wrows - 1))) return cudaErrorInvalidValue;
   const size_t sm = trsv_ring_smem(wrows, t, maxlev);
   if (sm > 220 * 1024) return cudaErrorInvalidValue;
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_trsv_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  const TrsvSched S{pos_row, pos_out, pos_ne, pos_diag, pos_col, pos_val, E};
-  return launch_k(k_trsv_ring, ndom, 256, sm, st, t, wrows - 1, maxlev, S, dom_lev, lev_ptr, Zp, Y);
+  // threads: a level's items (rows × t), rounded to warps, at most 256; wider levels loop
+  int nth = ((maxrows * t + 31) / 32) * 32;
+  if (nth > 256) nth = 256;
+  if (nth < 32) nth = 32;
+  const TrsvSched S{pos_row, pos_out, pos_ne, pos_rdiag, pos_col, pos_val};
+#define EKS_TRSV_E(EE)                                                                                            \
+  case EE:                                                                                                        \
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_trsv_ring<EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    return launch_k(k_trsv_ring<EE>, ndom, nth, sm, st, t, wrows - 1, S, dom_lev, lev_ptr, Zp, Y);
+  switch (E) {
+    EKS_TRSV_E(1)
+    EKS_TRSV_E(2)
+    EKS_TRSV_E(3)
+    EKS_TRSV_E(4)
+    EKS_TRSV_E(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef EKS_TRSV_E
 }
 
 // Per-CTA partials of Wᵀv (t values per CTA, part[b·t + c]) over the CTA's contiguous rows; a

@@ -87,14 +87,14 @@ cudaError_t launch_trsv_lev(cudaStream_t st, int ndom, int t, const int* rp, con
                             const double* diag, const int* dom_lev, const int* lev_ptr, const int* rows,
                             const double* Z, double* Y);
 // the same with a shared-memory ring of wrows (power of two) solved rows and a flattened level-order
-// schedule (position → row, output index, #entries ≤ E ≤ kTrsvMaxE, diagonal, entries at pos·E + e);
+// schedule (position → row, output index, #entries ≤ E ∈ {1,2,3,4,8}, 1/diagonal, entries at pos·E + e);
 // the input Zp is in schedule order (launch_perm_gather), the output goes to Y[out index]
 constexpr int kTrsvMaxE = 8;
 size_t trsv_ring_smem(int wrows, int t, int maxlev);
-cudaError_t launch_trsv_ring(cudaStream_t st, int ndom, int t, int wrows, int maxlev, const int* pos_row,
-                             const int* pos_out, const int* pos_ne, const double* pos_diag, const int* pos_col,
-                             const double* pos_val, int E, const int* dom_lev, const int* lev_ptr, const double* Zp,
-                             double* Y);
+cudaError_t launch_trsv_ring(cudaStream_t st, int ndom, int t, int wrows, int maxlev, int maxrows,
+                             const int* pos_row, const int* pos_out, const int* pos_ne, const double* pos_rdiag,
+                             const int* pos_col, const double* pos_val, int E, const int* dom_lev, const int* lev_ptr,
+                             const double* Zp, double* Y);
 cudaError_t launch_perm_gather(cudaStream_t st, int64_t npos, int t, const int* pos_row, const double* Z,
                                double* Zp, int sms);
 cudaError_t launch_wtv(cudaStream_t st, int64_t n, int t, const double* W, const double* v, double* part, int nblk);
