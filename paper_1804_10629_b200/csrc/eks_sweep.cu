@@ -104,6 +104,9 @@ struct SwCfg {
   static constexpr int RED = (WS > 1 ? 8 * NL * T * T : 0) + (V ? 8 * T : 0);
   static constexpr int SMEM0 = NS * STAGE + CDBL;
   static constexpr int SMEM = SMEM0 > RED ? SMEM0 : RED;  // doubles
+  // the update's B fragments (C) held in registers when they are few (else read from sC per tile)
+  static constexpr int NCF = UPW * NQ * (T / 4);
+  static constexpr bool CREG = NQ > 0 && NCF <= 16;
 };
 
 template <int T, int NQ, int NL, bool V, bool AL = false>
@@ -124,6 +127,19 @@ __global__ void __launch_bounds__(256, 1)
 
   if constexpr (NQ > 0)
     for (int e = tid; e < NQ * T * T; e += 256) sC[(e / T) * K::SC + e % T] = Cm[e];
+  double cf[K::CREG ? K::NCF : 1];
+  if constexpr (K::CREG) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < K::UPW; ++u) {
+      const int ni = (warp * K::UPW + u) % (T / 8);
+#pragma unroll
+      for (int j = 0; j < NQ; ++j)
+#pragma unroll
+        for (int kk = 0; kk < T; kk += 4)
+          cf[(u * NQ + j) * (T / 4) + kk / 4] = sC[j * T * K::SC + (kk + q4) * K::SC + ni * 8 + g];
+    }
+  }
 
   auto issue = [&](int i) {
     if (i < ntiles) {
@@ -169,7 +185,8 @@ __global__ void __launch_bounds__(256, 1)
           const double* Cj = sC + j * T * K::SC;
 #pragma unroll
           for (int kk = 0; kk < T; kk += 4)
-            dmma(d0, d1, sQ[(mi * 8 + g) * S + kk + q4], Cj[(kk + q4) * K::SC + ni * 8 + g]);
+            dmma(d0, d1, sQ[(mi * 8 + g) * S + kk + q4],
+                 K::CREG ? cf[(u * NQ + j) * (T / 4) + kk / 4] : Cj[(kk + q4) * K::SC + ni * 8 + g]);
         }
         const int r = mi * 8 + g, c = ni * 8 + 2 * q4;
         const double z0 = (Zin != nullptr ? sZ[r * S + c] : 0.0) - d0;
@@ -323,6 +340,19 @@ __global__ void __launch_bounds__(256, 1)
   };
 #pragma unroll
   for (int i = 0; i < K::NS - 1; ++i) issue(i);
+  // R⁻¹ B fragments and α pairs in registers for T ≤ 16 (8 + 4 values), else from shared memory
+  constexpr bool RREG = T <= 16;
+  double rf[RREG ? K::NT * (T / 4) : 1], af[RREG ? 2 * K::NT : 1];
+  if constexpr (RREG) {
+    __syncthreads();
+#pragma unroll
+    for (int ni = 0; ni < K::NT; ++ni) {
+#pragma unroll
+      for (int kk = 0; kk < T; kk += 4) rf[ni * (T / 4) + kk / 4] = sRi[(kk + q4) * SR + ni * 8 + g];
+      af[2 * ni] = sA[ni * 8 + 2 * q4];
+      af[2 * ni + 1] = sA[ni * 8 + 2 * q4 + 1];
+    }
+  }
 
   double rr_acc = 0.0;
   double acc[K::TPW][2];
@@ -346,7 +376,7 @@ __global__ void __launch_bounds__(256, 1)
       double w0 = 0.0, w1 = 0.0, y0 = 0.0, y1 = 0.0;
 #pragma unroll
       for (int kk = 0; kk < T; kk += 4) {
-        const double b = sRi[(kk + q4) * SR + ni * 8 + g];
+        const double b = RREG ? rf[ni * (T / 4) + kk / 4] : sRi[(kk + q4) * SR + ni * 8 + g];
         dmma(w0, w1, sZ[rr * S + kk + q4], b);
         dmma(y0, y1, sY[rr * S + kk + q4], b);
       }
@@ -357,8 +387,9 @@ __global__ void __launch_bounds__(256, 1)
       }
       yk[ni][0] = y0;
       yk[ni][1] = y1;
-      double tu = fma(w0, sA[c], w1 * sA[c + 1]);
-      double tq = fma(y0, sA[c], y1 * sA[c + 1]);
+      const double a0 = RREG ? af[2 * ni] : sA[c], a1 = RREG ? af[2 * ni + 1] : sA[c + 1];
+      double tu = fma(w0, a0, w1 * a1);
+      double tq = fma(y0, a0, y1 * a1);
       tu += __shfl_xor_sync(0xffffffffu, tu, 1);
       tq += __shfl_xor_sync(0xffffffffu, tq, 1);
       tu += __shfl_xor_sync(0xffffffffu, tu, 2);
