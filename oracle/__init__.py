@@ -87,6 +87,9 @@ def lib():
         _lib.or_solve_pc.argtypes = [C.POINTER(_Csr), vp, vp, i32, i32, i32, d, i32, i32, i32, i32,
                                      C.POINTER(_Csr), C.POINTER(_Report), ITER_CB, vp]
         _lib.or_solve_pc.restype = i32
+        _lib.or_solve_ca_pc.argtypes = [C.POINTER(_Csr), vp, vp, i32, i32, i32, i32, d, i32, C.POINTER(_Csr),
+                                        C.POINTER(_Report), ITER_CB, vp]
+        _lib.or_solve_ca_pc.restype = i32
     return _lib
 
 
@@ -238,8 +241,9 @@ def solve(A, b, method="sre-cg", s=1, t=1, tol=1e-8, kmax=5000, x0=None, mode=MO
                 breakdown_block=rep.breakdown_block)
 
 
-def solve_ca(A, b, method="sre-cg", arnoldi=7, s=1, t=1, tol=1e-8, kmax=5000, x0=None, callback=None):
-    """Run or_solve_ca (CA SRE-CG / CA SRE-CG2 / CA MSDO-CG with Alg 5 or Alg 7); same dict as solve()."""
+def solve_ca(A, b, method="sre-cg", arnoldi=7, s=1, t=1, tol=1e-8, kmax=5000, x0=None, callback=None, L=None):
+    """Run or_solve_ca_pc (CA SRE-CG / CA SRE-CG2 / CA MSDO-CG with Alg 5 or Alg 7, optionally split-
+    preconditioned by M = L·Lᵗ); same dict as solve()."""
     b = _f64(b)
     x = np.zeros(A.n) if x0 is None else _f64(x0).copy()
     hist = np.zeros(kmax + 1)
@@ -256,7 +260,9 @@ def solve_ca(A, b, method="sre-cg", arnoldi=7, s=1, t=1, tol=1e-8, kmax=5000, x0
                      np.ctypeslib.as_array(rr, shape=(n,)).copy(), rho)
         cb = ITER_CB(_cb)
     m = METHODS[method] if isinstance(method, str) else int(method)
-    st = lib().or_solve_ca(C.byref(ref.s), _p(b), _p(x), m, int(arnoldi), s, t, tol, kmax, C.byref(rep), cb, None)
+    Lref = _CsrRef(L) if L is not None else None
+    st = lib().or_solve_ca_pc(C.byref(ref.s), _p(b), _p(x), m, int(arnoldi), s, t, tol, kmax,
+                              C.byref(Lref.s) if Lref else None, C.byref(rep), cb, None)
     k = rep.outer_iters
     return dict(x=x, outer_iters=k, converged=bool(rep.converged), status=st, rho0=rep.rho0,
                 rho=rep.rho, true_relres=rep.true_relres, hist=hist[: k + 1].copy(),

@@ -623,7 +623,13 @@ static void cgs2_wide(const or_csr* A, int t, int zc, int nq, const double* cons
  * T(r_{k-1}) ("W_j = W_{j-1}"). */
 int or_solve_ca(const or_csr* A, const double* b, double* x, int method, int arnoldi, int s, int t,
                 double eps, int kmax, or_report* rep, or_iter_cb cb, void* user) {
+  return or_solve_ca_pc(A, b, x, method, arnoldi, s, t, eps, kmax, NULL, rep, cb, user);
+}
+
+int or_solve_ca_pc(const or_csr* A, const double* b, double* x, int method, int arnoldi, int s, int t,
+                   double eps, int kmax, const or_csr* L, or_report* rep, or_iter_cb cb, void* user) {
   int64_t n = A->n;
+  if (L && L->n != n) return OR_BADARG;
   if (s < 1 || t < 1 || (int64_t)s * t > n || !(eps >= 0.0) || method < 0 || method > 2 ||
       (arnoldi != 5 && arnoldi != 7))
     return OR_BADARG;
@@ -654,8 +660,18 @@ int or_solve_ca(const or_csr* A, const double* b, double* x, int method, int arn
   while (rho > eps * rho0 && k < kmax) {
     /* window: the last (s+1) blocks (CA SRE-CG) or all blocks */
     int w0 = (method == OR_SRE_CG && Q.count > s + 1) ? Q.count - (s + 1) : 0, nq = Q.count - w0;
-    if (method == OR_MSDO_CG || k == 1) or_split(n, t, r, W);
-    else or_spmm(A, t, Q.W[Q.count - 1], W);
+    if (method == OR_MSDO_CG || k == 1) {
+      if (L) {  /* W_{j-1} = L⁻ᵗ[T(L⁻¹ r_{k-1})] */
+        or_lsolve(L, 1, r, tmp);
+        or_split(n, t, tmp, W);
+        or_ltsolve(L, t, W, W);
+      } else {
+        or_split(n, t, r, W);
+      }
+    } else {
+      or_spmm(A, t, Q.W[Q.count - 1], W);
+      if (L) { or_lsolve(L, t, W, W); or_ltsolve(L, t, W, W); }  /* M⁻¹A W_{j-1} */
+    }
     if (arnoldi == 7) {  /* Alg 7 lines 1-4 */
       if (nq > 0) or_cgs2(A, t, nq, (const double* const*)(Q.W + w0), W, NULL, NULL);
       if (or_acholqr(A, t, W, W1, Rt, NULL) != OR_OK) { status = OR_BREAKDOWN; break; }
@@ -666,6 +682,7 @@ int or_solve_ca(const or_csr* A, const double* b, double* x, int method, int arn
     for (int i = 0; i < s; ++i) {
       if (i > 0) {
         or_spmm(A, t, pw, nw);
+        if (L) { or_lsolve(L, t, nw, nw); or_ltsolve(L, t, nw, nw); }  /* M⁻¹A powers */
         memcpy(pw, nw, sizeof(double) * blk);
       }
       for (int64_t row = 0; row < n; ++row)

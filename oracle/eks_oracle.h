@@ -117,6 +117,11 @@ int or_solve_pc(const or_csr* A, const double* b, double* x, int method, int s, 
 int or_solve_ca(const or_csr* A, const double* b, double* x, int method, int arnoldi, int s, int t,
                 double eps, int kmax, or_report* rep, or_iter_cb cb, void* user);
 
+/* or_solve_ca with the split preconditioner M = L·Lᵗ (L NULL: none): the seed
+ * L⁻ᵗ[T(L⁻¹r)] and the monomial powers M⁻¹A·W. */
+int or_solve_ca_pc(const or_csr* A, const double* b, double* x, int method, int arnoldi, int s, int t,
+                   double eps, int kmax, const or_csr* L, or_report* rep, or_iter_cb cb, void* user);
+
 /* s-step SRE-CG basis sweep only (cfg5, reading R27): starting block X0 (n×t)
  * is A-orthonormalized, then nblocks-1 further blocks W=A-orth(A·W_prev) against
  * the last min(2,#) blocks.  Writes the last block to W_last.  Returns status. */

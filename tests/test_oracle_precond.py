@@ -188,3 +188,30 @@ def test_ic0_breakdown_and_badarg(oracle_lib):
     st, L = oracle_lib.ic0(A, 4)
     b = ei.uniform_pm1(1, A.n)
     assert oracle_lib.solve(A, b, "sre-cg", s=2, t=2, L=L, restructured=True)["status"] == oracle_lib.BADARG
+
+
+@pytest.mark.parametrize("method,arnoldi", [("sre-cg", 7), ("sre-cg2", 5), ("msdo-cg", 7)])
+def test_preconditioned_ca(oracle_lib, method, arnoldi):
+    """CA with M⁻¹A powers and the L⁻ᵗ[T(L⁻¹r)] seed.  s = 1 (Alg 5) is the preconditioned
+    s-step method exactly; Poisson2D counts equal the preconditioned s-step counts (Table 5: the CA
+    versions with Alg 7 converge like s-step); per-iteration A-orthonormality and Galerkin hold."""
+    A = ei.poisson2d(40)
+    st, L = oracle_lib.ic0(A, 16)
+    b = ei.paper_poisson_rhs(A)
+    if arnoldi == 5:
+        c1 = oracle_lib.solve_ca(A, b, method, arnoldi=5, s=1, t=4, tol=1e-8, L=L)
+        s1 = oracle_lib.solve(A, b, method, s=1, t=4, tol=1e-8, L=L)
+        assert c1["outer_iters"] == s1["outer_iters"]
+        assert np.array_equal(c1["x"], s1["x"])
+    D = A.to_dense()
+
+    def cb(k, V, alpha, x, r, rho):
+        assert np.abs(V.T @ D @ V - np.eye(V.shape[1])).max() <= 1e-8
+        assert np.linalg.norm(V.T @ r) <= 1e-8 * max(np.linalg.norm(alpha), 1e-300)
+
+    ca = oracle_lib.solve_ca(A, b, method, arnoldi=arnoldi, s=3, t=4, tol=1e-8, L=L, callback=cb)
+    ss = oracle_lib.solve(A, b, method, s=3, t=4, tol=1e-8, L=L)
+    plain = oracle_lib.solve_ca(A, b, method, arnoldi=arnoldi, s=3, t=4, tol=1e-8)
+    assert ca["converged"] and ss["converged"]
+    assert abs(ca["outer_iters"] - ss["outer_iters"]) <= 1, (ca["outer_iters"], ss["outer_iters"])
+    assert ca["outer_iters"] < plain["outer_iters"]
