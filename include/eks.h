@@ -96,7 +96,8 @@ typedef struct {
                              MSDO-CG and CA methods: EKS_ERR_INVALID_ARG */
   int precond;            /* 1: split-preconditioned s-step method (Alg 8/9/10) with the block-Jacobi
                              IC(0) M of eks_setup_precond: seed M⁻¹[T(r)], powers M⁻¹A·W.
-                             s-step methods only (CA / restructured: EKS_ERR_INVALID_ARG) */
+                             With a CA method: seed M⁻¹[T(r)] and monomial powers M⁻¹A·W.
+                             Restructured: EKS_ERR_INVALID_ARG */
   int reserved[4];
 } eks_options;
 

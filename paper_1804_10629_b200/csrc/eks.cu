@@ -877,17 +877,24 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
   std::vector<Block>& AV = ctx->AVca;
   // seed
   if (base == EKS_MSDO_CG || k == 1) {
-    KScope kk(ctx, EKS_K_SPLIT);
-    CK(eks::launch_split(ctx->stream, t, ctx->n, ctx->row_begin, ctx->n_global, ctx->r, V[0].loc));
+    {
+      KScope kk(ctx, EKS_K_SPLIT);
+      CK(eks::launch_split(ctx->stream, t, ctx->n, ctx->row_begin, ctx->n_global, ctx->r, V[0].loc));
+    }
+    if (ctx->use_prec) ST(prec_apply(ctx, t, V[0].loc, V[0].loc));  // L⁻ᵗ[T(L⁻¹r)] = M⁻¹[T(r)]
   } else {
     const int idx = ring ? (nblocks - 1) % ring : nblocks - 1;
     ST(spmm(ctx, ctx->Wpool[idx], V[0].loc, t));
+    if (ctx->use_prec) ST(prec_apply(ctx, t, V[0].loc, V[0].loc));  // M⁻¹A W_{j−1}
   }
   if (arnoldi == 7) {  // Alg 7 lines 1-4
     if (!Q.empty()) ST(cgs2(ctx, t, Q, AQ, V[0].loc, V[0].loc));
     ST(acholqr_block(ctx, t, V[0], AV[0].loc, nblocks));
   }
-  for (int i = 1; i < s; ++i) ST(spmm(ctx, V[i - 1], V[i].loc, t));  // monomial powers
+  for (int i = 1; i < s; ++i) {  // monomial powers (M⁻¹A with the preconditioner)
+    ST(spmm(ctx, V[i - 1], V[i].loc, t));
+    if (ctx->use_prec) ST(prec_apply(ctx, t, V[i].loc, V[i].loc));
+  }
   if (!Q.empty()) ST(cgs2_stacked(ctx, t, Q, AQ, V, AV));  // AV serves as the pass-1 scratch
   // Gram B (st×st, upper blocks) and g = Vᵀ r_{k−1}: block column j = [V_0..V_{j−1}]ᵀAV_j, then
   // [V_jᵀAV_j | V_jᵀr] from the fused SpMM+Gram kernel that forms AV_j, into Btmp (column j at
@@ -1686,7 +1693,7 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   if (ortho != 0 && ortho != 1) return fail(ctx, EKS_ERR_INVALID_ARG, "ortho must be 0 (A-CholQR) or 1 (Pre-CholQR)");
   if (ca && ortho) return fail(ctx, EKS_ERR_INVALID_ARG, "Pre-CholQR is for the s-step methods");
   const bool prec = opt && opt->precond;
-  if (prec && (ca || restr)) return fail(ctx, EKS_ERR_INVALID_ARG, "precond is for the s-step methods");
+  if (prec && restr) return fail(ctx, EKS_ERR_INVALID_ARG, "precond is not defined for the restructured methods");
   if (prec && !ctx->prec_nd) return fail(ctx, EKS_ERR_STATE, "eks_setup_precond has not been called");
   if (prec && ctx->prec_nd % t)
     return fail(ctx, EKS_ERR_INVALID_ARG, "precond needs t | ndomains (%d), P:874", ctx->prec_nd);

@@ -260,6 +260,25 @@ def test_preconditioned_end_to_end(eks, torch_cuda, oracle_lib, method, s_, t, n
     assert rep["outer_iters"] < plain["outer_iters"]
 
 
+@pytest.mark.parametrize("method,arnoldi,s_,t", [("ca-sre-cg", 7, 3, 4), ("ca-sre-cg2", 5, 2, 8),
+                                                 ("ca-msdo-cg", 7, 3, 4), ("ca-sre-cg", 7, 2, 16)])
+def test_preconditioned_ca_end_to_end(eks, torch_cuda, oracle_lib, method, arnoldi, s_, t):
+    """CA variants with the block-Jacobi IC(0) split preconditioner (seed M⁻¹[T(r)], powers
+    M⁻¹A·W) on Poisson2D 48²: counts within 5 %, x within 1e-6 of the oracle."""
+    A = ei.poisson2d(48)
+    b = ei.uniform_pm1(1805, A.n)
+    st, L = oracle_lib.ic0(A, 16)
+    S = eks.Solver(A)
+    S.setup_precond(16)
+    rep = S.solve(dev(torch_cuda, b), method, s_, t, 1e-8, arnoldi=arnoldi, precond=True)
+    S.close()
+    ref = oracle_lib.solve_ca(A, b, method[3:], arnoldi=arnoldi, s=s_, t=t, tol=1e-8, L=L)
+    assert rep["converged"] and ref["converged"], (rep["status"], ref["status"])
+    assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+    assert rep["true_relres"] <= 2e-8
+
+
 def test_preconditioner_errors(eks, torch_cuda):
     A = ei.poisson2d(16)
     S = eks.Solver(A)
@@ -268,7 +287,7 @@ def test_preconditioner_errors(eks, torch_cuda):
         S.solve(b, "sre-cg", 2, 4, 1e-8, precond=True)   # no eks_setup_precond yet
     assert e.value.status == 2
     S.setup_precond(8)
-    for kw in (dict(t=16), dict(method="ca-sre-cg"), dict(restructured=True)):
+    for kw in (dict(t=16), dict(restructured=True)):
         args = dict(method="sre-cg", t=4)
         args.update(kw)
         with pytest.raises(eks.EksError) as e:
@@ -531,7 +550,7 @@ def test_poisson2d_tables_sweep_gpu(eks, torch_cuda):
     assert all(c["converged"] for c in cells.values()), [k for k, c in cells.items() if not c["converged"]]
     for k, c in cells.items():
         key, t, s = k.split("|")
-        if t == "2":
+        if t == "2" and not key.startswith("pc-"):  # Table 5: 64 Metis preconditioner domains, context only
             want = [c["paper"]]
             if key == "msdo-cg/ca7":  # reading R28: the literal Alg 7 seed gives the s-step count
                 want.append(cells[f"msdo-cg/s-step|{t}|{s}"]["paper"])
