@@ -90,6 +90,10 @@ def lib():
         _lib.or_solve_ca_pc.argtypes = [C.POINTER(_Csr), vp, vp, i32, i32, i32, i32, d, i32, C.POINTER(_Csr),
                                         C.POINTER(_Report), ITER_CB, vp]
         _lib.or_solve_ca_pc.restype = i32
+        _lib.or_cholblk_nnz.argtypes = [C.POINTER(_Csr), i32]
+        _lib.or_cholblk_nnz.restype = i64
+        _lib.or_cholblk.argtypes = [C.POINTER(_Csr), i32, vp, vp, vp]
+        _lib.or_cholblk.restype = i32
     return _lib
 
 
@@ -183,14 +187,16 @@ def precholqr(A, Z: np.ndarray):
 ORTHO = {"acholqr": 0, "pre-cholqr": 1}
 
 
-def ic0(A, nd=64):
-    """Block-Jacobi IC(0) factor L (reading R32) of nd contiguous domains; returns (status, L as Csr)."""
+def ic0(A, nd=64, kind="ic0"):
+    """Block-Jacobi factor L (reading R32) of nd contiguous domains: IC(0) (Table 5) or the complete
+    Cholesky of each diagonal block (kind="chol", Table 6); returns (status, L as Csr)."""
     ref = _CsrRef(A)
-    nnz = int(lib().or_ic0_nnz(C.byref(ref.s), nd))
+    nnzf, fac = (lib().or_ic0_nnz, lib().or_ic0) if kind == "ic0" else (lib().or_cholblk_nnz, lib().or_cholblk)
+    nnz = int(nnzf(C.byref(ref.s), nd))
     rp = np.zeros(A.n + 1, np.int64)
     col = np.zeros(nnz, np.int32)
     val = np.zeros(nnz, np.float64)
-    st = lib().or_ic0(C.byref(ref.s), nd, _p(rp), _p(col), _p(val))
+    st = fac(C.byref(ref.s), nd, _p(rp), _p(col), _p(val))
     return st, types.SimpleNamespace(n=A.n, row_ptr=rp, col=col, val=val, nnz=nnz)
 
 

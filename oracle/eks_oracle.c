@@ -278,6 +278,57 @@ int or_ic0(const or_csr* A, int nd, int64_t* Lrp, int32_t* Lcol, double* Lval) {
   return OR_OK;
 }
 
+/* Block-Jacobi with a COMPLETE Cholesky of each diagonal block (Table 6).  For the
+ * natural ordering the factor's fill stays inside the row envelope (profile): row i of L holds
+ * the columns f_i..i of its domain, f_i = the first nonzero column of row i of A_dd.  Envelope
+ * (skyline) Cholesky, row by row: L_ij = (A_ij − Σ_{k=max(f_i,f_j)}^{j-1} L_ik L_jk) / L_jj,
+ * L_ii = sqrt(A_ii − Σ_{k=f_i}^{i-1} L_ik²).  or_cholblk_nnz gives the envelope size. */
+static int64_t env_first(const or_csr* A, int nd, int64_t i) {
+  int64_t di = dom_of(A->n, nd, i), f = i;
+  for (int64_t p = A->row_ptr[i]; p < A->row_ptr[i + 1]; ++p) {
+    int64_t j = A->col[p];
+    if (j < f && dom_of(A->n, nd, j) == di) f = j;
+  }
+  return f;
+}
+
+int64_t or_cholblk_nnz(const or_csr* A, int nd) {
+  int64_t cnt = 0;
+  for (int64_t i = 0; i < A->n; ++i) cnt += i - env_first(A, nd, i) + 1;
+  return cnt;
+}
+
+int or_cholblk(const or_csr* A, int nd, int64_t* Lrp, int32_t* Lcol, double* Lval) {
+  int64_t n = A->n, q = 0;
+  Lrp[0] = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t f = env_first(A, nd, i);
+    for (int64_t j = f; j <= i; ++j) { Lcol[q] = (int32_t)j; Lval[q] = 0.0; ++q; }
+    Lrp[i + 1] = q;
+    /* A's entries of the envelope */
+    for (int64_t p = A->row_ptr[i]; p < A->row_ptr[i + 1]; ++p) {
+      int64_t j = A->col[p];
+      if (j >= f && j <= i) Lval[Lrp[i] + (j - f)] = A->val[p];
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t fi = Lcol[Lrp[i]];
+    double* Li = Lval + Lrp[i];  /* Li[j - fi] = L_ij */
+    for (int64_t j = fi; j < i; ++j) {
+      int64_t fj = Lcol[Lrp[j]];
+      const double* Lj = Lval + Lrp[j];
+      double v = Li[j - fi];
+      for (int64_t k = fi > fj ? fi : fj; k < j; ++k) v = v - Li[k - fi] * Lj[k - fj];
+      Li[j - fi] = v / Lj[j - fj];
+    }
+    double d = Li[i - fi];
+    for (int64_t k = fi; k < i; ++k) d = d - Li[k - fi] * Li[k - fi];
+    if (!(d > 0.0)) return OR_BREAKDOWN;
+    Li[i - fi] = sqrt(d);
+  }
+  return OR_OK;
+}
+
 /* Y = L⁻¹ Z (n×t, row-major; Y may alias Z): forward substitution per column. */
 void or_lsolve(const or_csr* L, int t, const double* Z, double* Y) {
   for (int64_t i = 0; i < L->n; ++i) {

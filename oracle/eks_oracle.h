@@ -97,6 +97,11 @@ int or_solve_ex(const or_csr* A, const double* b, double* x, int method, int s, 
  * the lower triangle of the block diagonal of A; or_ic0_nnz gives its nnz. */
 int64_t or_ic0_nnz(const or_csr* A, int nd);
 int or_ic0(const or_csr* A, int nd, int64_t* Lrp, int32_t* Lcol, double* Lval);
+/* The same with a complete Cholesky of each diagonal block (Table 6; reading R32): L holds
+ * the row envelope (columns f_i..i of the domain, f_i = first nonzero of row i of A_dd), where
+ * the natural-order factor's fill lives; envelope (skyline) Cholesky. */
+int64_t or_cholblk_nnz(const or_csr* A, int nd);
+int or_cholblk(const or_csr* A, int nd, int64_t* Lrp, int32_t* Lcol, double* Lval);
 /* Y = L⁻¹Z and Y = L⁻ᵗZ for n×t row-major blocks (Y may alias Z). */
 void or_lsolve(const or_csr* L, int t, const double* Z, double* Y);
 void or_ltsolve(const or_csr* L, int t, const double* Z, double* Y);
