@@ -218,7 +218,7 @@ def oracle_sample(p, iters: int):
     if p.method.startswith("ca-"):
         r = oracle.solve_ca(p.A, p.b, p.method[3:], arnoldi=p.arnoldi, s=p.s, t=p.t, tol=0.0, kmax=iters + 1)
     else:
-        L = oracle.ic0(p.A, p.precond)[1] if getattr(p, "precond", 0) else None
+        L = oracle.ic0(p.A, p.precond, kind=getattr(p, "precond_kind", "ic0"))[1] if getattr(p, "precond", 0) else None
         r = oracle.solve(p.A, p.b, p.method, p.s, p.t, 0.0, kmax=iters + 1, ortho=getattr(p, "ortho", "acholqr"),
                          restructured=getattr(p, "restructured", False), L=L)
     dt = time.perf_counter() - t0
@@ -236,6 +236,7 @@ def problem_of(args):
     p.ortho = args.ortho
     p.restructured = args.restructured
     p.precond = args.precond
+    p.precond_kind = args.precond_kind
     return p
 
 
@@ -272,7 +273,7 @@ def config_of(args, p, N):
     if getattr(p, "ortho", "acholqr") != "acholqr":
         kind += f" + {p.ortho}"
     if getattr(p, "precond", 0):
-        kind = f"split-preconditioned (block-Jacobi IC(0), {p.precond} domains) " + kind
+        kind = f"split-preconditioned (block-Jacobi {p.precond_kind}, {p.precond} domains) " + kind
     return {"workload": f"{p.name}: {p.note}; {kind} {p.method}, s={p.s}, t={p.t}, tol={p.tol:g}",
             "n": p.A.n, "nnz": p.A.nnz, "method": p.method, "s": p.s, "t": p.t, "tol": p.tol,
             "parallelism": f"row-slabs x{N} (t/N domains per GPU)",
@@ -300,7 +301,8 @@ def main():
     ap.add_argument("--ortho", default="acholqr", choices=["acholqr", "pre-cholqr"])
     ap.add_argument("--restructured", action="store_true", help="restructured Alg 2 / Alg 1 (SRE-CG / SRE-CG2)")
     ap.add_argument("--precond", type=int, default=0,
-                    help="split-preconditioned Alg 8-10 with block-Jacobi IC(0) of this many domains (64 in the paper)")
+                    help="split-preconditioned Alg 8-10 with block Jacobi of this many domains (64 in the paper)")
+    ap.add_argument("--precond-kind", default="ic0", choices=["ic0", "chol"], help="IC(0) (Table 5) or Cholesky (Table 6)")
     ap.add_argument("--cfg5-n", type=int, default=384, help="cfg5 grid size (384 = BASELINE configs[4])")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -341,7 +343,7 @@ def main():
     solver = eks.Solver(None, rank=rank, nranks=world, device=local, nccl_id=uid)
     solver.setup(n, lo, hi, slab.row_ptr, slab.col, slab.val)
     if p.precond:
-        solver.setup_precond(p.precond)
+        solver.setup_precond(p.precond, kind=p.precond_kind)
     stream = torch.cuda.Stream()
     eks.eks_set_stream(solver.ctx, stream.cuda_stream)
 
@@ -459,7 +461,7 @@ def main():
         for k in range(args.steps):
             e2e_solver.setup(n, lo, hi, hrp, hcol, hval)
             if p.precond:
-                e2e_solver.setup_precond(p.precond)
+                e2e_solver.setup_precond(p.precond, kind=p.precond_kind)
             hx[:] = 0.0
             st, rep = eks.eks_solve_ex(e2e_solver.ctx, p.method, p.s, p.t, p.tol, hb, hx, arnoldi=p.arnoldi,
                                        ortho=p.ortho, restructured=p.restructured, precond=bool(p.precond))

@@ -133,15 +133,20 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
 /* Block-Jacobi IC(0) preconditioner M = L·Lᵗ for the split-preconditioned s-step methods
  * (Alg 8/9/10; §5.2; DESIGN reading R32): ndomains contiguous domains
  * D_d = [floor(d n/ndomains), floor((d+1) n/ndomains)) (Metis in the paper), each diagonal block
- * factorized by incomplete Cholesky with zero fill-in on the host at setup (a one-time cost),
+ * factorized (kind: IC(0) or complete Cholesky) on the host at setup (a one-time cost),
  * L and Lᵗ uploaded with per-domain level schedules.  Pass the SAME local slab (global columns)
  * as eks_setup_csr; the slab must be a union of preconditioner domains.  Entries coupling two
  * domains are dropped (block Jacobi).  Errors: EKS_ERR_STATE (no eks_setup_csr), EKS_ERR_INVALID_ARG
- * (ndomains < 1, slab not a union of domains), EKS_ERR_BREAKDOWN (an IC(0) pivot ≤ 0).
+ * (ndomains < 1, slab not a union of domains, unknown kind), EKS_ERR_BREAKDOWN (a pivot ≤ 0),
+ * EKS_ERR_OOM (the Cholesky envelope exceeds 2^31 entries).
  * A solve uses it when eks_options.precond = 1; then ndomains must be a multiple of t (each of
  * the t domains is the union of ndomains/t preconditioner domains). */
-eks_status eks_setup_precond(eks_ctx* ctx, int ndomains, const int64_t* row_ptr, const int32_t* col_idx,
-                             const double* vals, eks_mem where);
+typedef enum {
+  EKS_PREC_IC0 = 0,  /* incomplete Cholesky with zero fill-in per block (Table 5) */
+  EKS_PREC_CHOL = 1  /* complete Cholesky per block (Table 6), the fill kept in each row's envelope */
+} eks_precond;
+eks_status eks_setup_precond(eks_ctx* ctx, eks_precond kind, int ndomains, const int64_t* row_ptr,
+                             const int32_t* col_idx, const double* vals, eks_mem where);
 
 /* Solve A x = b with the chosen s-step method (Alg 3/4/6), t domains
  * D_d = [floor(d n/t), floor((d+1) n/t)) (reading R1), tolerance tol on the

@@ -72,7 +72,7 @@ def lib():
             "eks_create": [C.POINTER(vp), C.POINTER(_Dist)],
             "eks_set_stream": [vp, vp],
             "eks_setup_csr": [vp, i64, i64, i64, vp, vp, vp, i32],
-            "eks_setup_precond": [vp, i32, vp, vp, vp, i32],
+            "eks_setup_precond": [vp, i32, i32, vp, vp, vp, i32],
             "eks_solve": [vp, i32, i32, i32, d, vp, vp, i32, i32, C.POINTER(_Report)],
             "eks_solve_ex": [vp, i32, i32, i32, d, vp, vp, i32, C.POINTER(_Options), C.POINTER(_Report)],
             "eks_basis_sweep": [vp, i32, i32, vp, vp, i32, C.POINTER(_Options), C.POINTER(_Report)],
@@ -181,11 +181,15 @@ def eks_setup_csr(ctx, n_global, row_begin, row_end, row_ptr, col, val):
                                     _ptr(col, np.int32), _ptr(val, np.float64), where))
 
 
-def eks_setup_precond(ctx, ndomains, row_ptr, col, val):
-    """Block-Jacobi IC(0) of ndomains contiguous domains (same slab as eks_setup_csr)."""
+PRECOND = {"ic0": 0, "chol": 1}
+
+
+def eks_setup_precond(ctx, ndomains, row_ptr, col, val, kind="ic0"):
+    """Block-Jacobi preconditioner of ndomains contiguous domains (same slab as eks_setup_csr):
+    kind "ic0" (Table 5) or "chol" (complete Cholesky per block, Table 6)."""
     where = _where(row_ptr, col, val)
-    _check(ctx, lib().eks_setup_precond(ctx, int(ndomains), _ptr(row_ptr, np.int64), _ptr(col, np.int32),
-                                        _ptr(val, np.float64), where))
+    _check(ctx, lib().eks_setup_precond(ctx, PRECOND[kind], int(ndomains), _ptr(row_ptr, np.int64),
+                                        _ptr(col, np.int32), _ptr(val, np.float64), where))
 
 
 def _report(rep: _Report):
@@ -310,9 +314,9 @@ class Solver:
         eks_setup_csr(self.ctx, n_global, row_begin, row_end, rp, cl, vl)
         self._csr = (rp, cl, vl)
 
-    def setup_precond(self, ndomains=64):
-        """Block-Jacobi IC(0) preconditioner (reading R32) for solve(..., precond=True)."""
-        eks_setup_precond(self.ctx, ndomains, *self._csr)
+    def setup_precond(self, ndomains=64, kind="ic0"):
+        """Block-Jacobi preconditioner (reading R32) for solve(..., precond=True): "ic0" or "chol"."""
+        eks_setup_precond(self.ctx, ndomains, *self._csr, kind=kind)
 
     def solve(self, b, method="sre-cg", s=1, t=1, tol=1e-8, x0=None, max_outer=0, profile=False, arnoldi=0,
               ortho="acholqr", restructured=False, precond=False):

@@ -23,7 +23,9 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <atomic>
 #include <string>
+#include <thread>
 #include <vector>
 
 using eks::kThreads;
@@ -102,6 +104,7 @@ struct eks_ctx {
   int* pr_pout[2] = {nullptr, nullptr};
   int pr_maxlev[2] = {0, 0};       // most levels of one domain
   int pr_maxrows[2] = {0, 0};      // most rows of one level
+  int pr_maxe[2] = {0, 0};         // most off-diagonal entries of one row
   Block Zq1, Zq2;                  // the block in forward / backward schedule order
   int* pr_pne[2] = {nullptr, nullptr};
   double* pr_pdiag[2] = {nullptr, nullptr};
@@ -678,8 +681,12 @@ eks_status prec_apply(eks_ctx* ctx, int t, const double* Z, double* Y) {
     return EKS_OK;
   }
   for (int w = 0; w < 2; ++w)
-    CK(eks::launch_trsv_lev(ctx->stream, ctx->prec_ndl, t, ctx->pr_rp[w], ctx->pr_col[w], ctx->pr_val[w],
-                            ctx->pr_diag, ctx->pr_domlev[w], ctx->pr_levptr[w], ctx->pr_rows[w], w ? Y : Z, Y));
+    if (ctx->pr_maxe[w] > 32)  // long rows: a warp per (row, column)
+      CK(eks::launch_trsv_lev_long(ctx->stream, ctx->prec_ndl, t, ctx->pr_rp[w], ctx->pr_col[w], ctx->pr_val[w],
+                                   ctx->pr_diag, ctx->pr_domlev[w], ctx->pr_levptr[w], ctx->pr_rows[w], w ? Y : Z, Y));
+    else
+      CK(eks::launch_trsv_lev(ctx->stream, ctx->prec_ndl, t, ctx->pr_rp[w], ctx->pr_col[w], ctx->pr_val[w],
+                              ctx->pr_diag, ctx->pr_domlev[w], ctx->pr_levptr[w], ctx->pr_rows[w], w ? Y : Z, Y));
   return EKS_OK;
 }
 
@@ -1484,9 +1491,10 @@ eks_status upload(eks_ctx* ctx, T** dst, const std::vector<T>& v) {
 // Block-Jacobi IC(0) (reading R32), built on the host once per matrix: for each local row i, the
 // entries of its domain's lower triangle are scattered into a dense row marker; each L_ik (k < i,
 // ascending) subtracts Σ_j L_kj·L_ij over row k's strict-lower entries found in the marker.
-eks_status eks_setup_precond(eks_ctx* ctx, int nd, const int64_t* row_ptr, const int32_t* col_idx,
+eks_status eks_setup_precond(eks_ctx* ctx, eks_precond kind, int nd, const int64_t* row_ptr, const int32_t* col_idx,
                              const double* vals, eks_mem where) {
   if (!ctx) return EKS_ERR_INVALID_ARG;
+  if (kind != EKS_PREC_IC0 && kind != EKS_PREC_CHOL) return fail(ctx, EKS_ERR_INVALID_ARG, "unknown preconditioner");
   if (!ctx->have_matrix) return fail(ctx, EKS_ERR_STATE, "eks_setup_csr has not been called");
   if (nd < 1 || !row_ptr || !col_idx || !vals) return fail(ctx, EKS_ERR_INVALID_ARG, "bad eks_setup_precond arguments");
   CK(cudaSetDevice(ctx->device));
@@ -1500,6 +1508,7 @@ eks_status eks_setup_precond(eks_ctx* ctx, int nd, const int64_t* row_ptr, const
     if (dlo(d) == ctx->row_end) d1 = d;
   }
   if (d0 < 0 || d1 <= d0) return fail(ctx, EKS_ERR_INVALID_ARG, "slab is not a union of the %d preconditioner domains", nd);
+  auto ndl_of = [](int a, int b) { return b - a; };
   std::vector<int64_t> rp(n + 1);
   if (where == EKS_MEM_HOST) memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1));
   else CK(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
@@ -1520,35 +1529,93 @@ eks_status eks_setup_precond(eks_ctx* ctx, int nd, const int64_t* row_ptr, const
     for (int64_t g = dlo(d); g < dlo(d + 1); ++g) dom[g - r0] = d - d0;
   std::vector<int> Lrp(n + 1, 0), Lcol;
   std::vector<double> Lval, diag(n, 0.0);
-  for (int64_t i = 0; i < n; ++i) {
-    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-      const int64_t j = (int64_t)col[p] - r0;
-      if (j < 0 || j > i || dom[j] != dom[i]) continue;
-      if (j == i) diag[i] = val[p];
-      else {
-        Lcol.push_back((int)j);
-        Lval.push_back(val[p]);
+  if (kind == EKS_PREC_IC0) {
+    for (int64_t i = 0; i < n; ++i) {
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int64_t j = (int64_t)col[p] - r0;
+        if (j < 0 || j > i || dom[j] != dom[i]) continue;
+        if (j == i) diag[i] = val[p];
+        else {
+          Lcol.push_back((int)j);
+          Lval.push_back(val[p]);
+        }
+      }
+      Lrp[i + 1] = (int)Lcol.size();
+    }
+    std::vector<int64_t> mark(n, -1);  // mark[j] = position of L_ij in the current row i
+    for (int64_t i = 0; i < n; ++i) {
+      for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) mark[Lcol[p]] = p;
+      for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) {
+        const int k = Lcol[p];
+        double v = Lval[p];
+        for (int q = Lrp[k]; q < Lrp[k + 1]; ++q) {  // row k's columns j < k
+          const int64_t pj = mark[Lcol[q]];
+          if (pj >= 0 && pj < p) v -= Lval[q] * Lval[pj];
+        }
+        Lval[p] = v / diag[k];
+      }
+      double dd = diag[i];
+      for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) dd -= Lval[p] * Lval[p];
+      for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) mark[Lcol[p]] = -1;
+      if (!(dd > 0.0)) return fail(ctx, EKS_ERR_BREAKDOWN, "IC(0) pivot %lld <= 0", (long long)(i + r0));
+      diag[i] = std::sqrt(dd);
+    }
+  } else {
+    // complete Cholesky of each diagonal block (Table 6): the fill of the natural-order factor stays in
+    // the row envelope, so row i of the strict lower L holds columns first[i]..i−1; domains are
+    // independent and factorized on all host threads
+    std::vector<int> first(n);
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t f = i;
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int64_t j = (int64_t)col[p] - r0;
+        if (j >= 0 && j < i && dom[j] == dom[i]) f = std::min(f, j);
+        if (j == i) diag[i] = val[p];
+      }
+      first[i] = (int)f;
+      if ((int64_t)Lrp[i] + (i - f) >= INT_MAX) return fail(ctx, EKS_ERR_OOM, "Cholesky envelope exceeds 2^31 entries");
+      Lrp[i + 1] = Lrp[i] + (int)(i - f);
+    }
+    Lcol.resize(Lrp[n]);
+    Lval.assign(Lrp[n], 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+      for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) Lcol[p] = first[i] + (p - Lrp[i]);
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int64_t j = (int64_t)col[p] - r0;
+        if (j >= first[i] && j < i) Lval[Lrp[i] + (j - first[i])] = val[p];
       }
     }
-    Lrp[i + 1] = (int)Lcol.size();
-  }
-  std::vector<int64_t> mark(n, -1);  // mark[j] = position of L_ij in the current row i
-  for (int64_t i = 0; i < n; ++i) {
-    for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) mark[Lcol[p]] = p;
-    for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) {
-      const int k = Lcol[p];
-      double v = Lval[p];
-      for (int q = Lrp[k]; q < Lrp[k + 1]; ++q) {  // row k's columns j < k
-        const int64_t pj = mark[Lcol[q]];
-        if (pj >= 0 && pj < p) v -= Lval[q] * Lval[pj];
+    std::atomic<int64_t> bad{-1};
+    std::atomic<int> next{0};
+    auto work = [&]() {
+      for (int d; (d = next++) < ndl_of(d0, d1);) {
+        const int64_t lo = dlo(d + d0) - r0, hi = dlo(d + d0 + 1) - r0;
+        for (int64_t i = lo; i < hi; ++i) {
+          const int fi = first[i];
+          double* Li = Lval.data() + Lrp[i];  // Li[j − fi] = L_ij
+          for (int j = fi; j < i; ++j) {
+            const int fj = first[j];
+            const double* Lj = Lval.data() + Lrp[j];
+            double v = Li[j - fi];
+            for (int k = std::max(fi, fj); k < j; ++k) v -= Li[k - fi] * Lj[k - fj];
+            Li[j - fi] = v / diag[j];
+          }
+          double dd = diag[i];
+          for (int k = fi; k < i; ++k) dd -= Li[k - fi] * Li[k - fi];
+          if (!(dd > 0.0)) {
+            bad = i + r0;
+            return;
+          }
+          diag[i] = std::sqrt(dd);
+        }
       }
-      Lval[p] = v / diag[k];
-    }
-    double dd = diag[i];
-    for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) dd -= Lval[p] * Lval[p];
-    for (int p = Lrp[i]; p < Lrp[i + 1]; ++p) mark[Lcol[p]] = -1;
-    if (!(dd > 0.0)) return fail(ctx, EKS_ERR_BREAKDOWN, "IC(0) pivot %lld <= 0", (long long)(i + r0));
-    diag[i] = std::sqrt(dd);
+    };
+    const int nthr = std::max(1, std::min<int>(ndl_of(d0, d1), (int)std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (int k = 1; k < nthr; ++k) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+    if (bad >= 0) return fail(ctx, EKS_ERR_BREAKDOWN, "Cholesky pivot %lld <= 0", (long long)bad.load());
   }
   // Lᵗ strict upper (row i: L_ki, k > i, ascending k)
   std::vector<int> Urp(n + 1, 0), Ucol(Lcol.size());
@@ -1619,6 +1686,7 @@ eks_status eks_setup_precond(eks_ctx* ctx, int nd, const int64_t* row_ptr, const
         }
       ringw[w] = best;
       maxe_w[w] = maxe;
+      ctx->pr_maxe[w] = maxe;
     }
     sched[w] = rows;
     int maxdl = 0, maxr = 0;

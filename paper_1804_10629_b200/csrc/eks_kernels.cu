@@ -882,6 +882,35 @@ __global__ void __launch_bounds__(256) k_trsv_lev(int t, const int* __restrict__
   }
 }
 
+// The same for long rows (complete-Cholesky envelopes, hundreds of entries per row): a warp per
+// (row, column) item, the lanes split the row's entries, a butterfly reduces them.
+__global__ void __launch_bounds__(512) k_trsv_lev_long(int t, const int* __restrict__ rp, const int* __restrict__ col,
+                                                       const double* __restrict__ val, const double* __restrict__ diag,
+                                                       const int* __restrict__ dom_lev, const int* __restrict__ lev_ptr,
+                                                       const int* __restrict__ rows, const double* Z, double* Y) {
+  pdl_enter();
+  const int d = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int lv = dom_lev[d]; lv < dom_lev[d + 1]; ++lv) {
+    const int b = lev_ptr[lv], items = (lev_ptr[lv + 1] - b) * t;
+    for (int it = warp; it < items; it += nw) {
+      const int i = rows[b + it / t], c = it % t;
+      double v = 0.0;
+      for (int p = rp[i] + lane; p < rp[i + 1]; p += 32) v = __fma_rn(val[p], Y[(int64_t)col[p] * t + c], v);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) Y[(int64_t)i * t + c] = __ddiv_rn(Z[(int64_t)i * t + c] - v, diag[i]);
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_trsv_lev_long(cudaStream_t st, int ndom, int t, const int* rp, const int* col, const double* val,
+                                 const double* diag, const int* dom_lev, const int* lev_ptr, const int* rows,
+                                 const double* Z, double* Y) {
+  if (ndom < 1 || t < 1) return cudaErrorInvalidValue;
+  return launch_k(k_trsv_lev_long, ndom, 512, 0, st, t, rp, col, val, diag, dom_lev, lev_ptr, rows, Z, Y);
+}
+
 cudaError_t launch_trsv_lev(cudaStream_t st, int ndom, int t, const int* rp, const int* col, const double* val,
                             const double* diag, const int* dom_lev, const int* lev_ptr, const int* rows,
                             const double* Z, double* Y) {

@@ -86,6 +86,10 @@ cudaError_t launch_ca_combine(cudaStream_t st, int64_t n, int t, int s, const Ca
 cudaError_t launch_trsv_lev(cudaStream_t st, int ndom, int t, const int* rp, const int* col, const double* val,
                             const double* diag, const int* dom_lev, const int* lev_ptr, const int* rows,
                             const double* Z, double* Y);
+// the same with a warp per (row, column) for long rows (complete-Cholesky envelopes)
+cudaError_t launch_trsv_lev_long(cudaStream_t st, int ndom, int t, const int* rp, const int* col, const double* val,
+                                 const double* diag, const int* dom_lev, const int* lev_ptr, const int* rows,
+                                 const double* Z, double* Y);
 // the same with a shared-memory ring of wrows (power of two) solved rows and a flattened level-order
 // schedule (position → row, output index, #entries ≤ E ∈ {1,2,3,4,8}, 1/diagonal, entries at pos·E + e);
 // the input Zp is in schedule order (launch_perm_gather), the output goes to Y[out index]

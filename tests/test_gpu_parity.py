@@ -279,6 +279,26 @@ def test_preconditioned_ca_end_to_end(eks, torch_cuda, oracle_lib, method, arnol
     assert rep["true_relres"] <= 2e-8
 
 
+@pytest.mark.parametrize("method,s_,t,nd", [("sre-cg", 2, 4, 8), ("msdo-cg", 2, 8, 8), ("ca-sre-cg2", 2, 4, 8)])
+def test_complete_cholesky_preconditioner(eks, torch_cuda, oracle_lib, method, s_, t, nd):
+    """Block Jacobi with the complete Cholesky of each block (Table 6; envelope factor built on the
+    host, sweeps through the general level-scheduled kernel): parity with the oracle on cfg1."""
+    p = ei.cfg1()
+    st, L = oracle_lib.ic0(p.A, nd, kind="chol")
+    S = eks.Solver(p.A)
+    S.setup_precond(nd, kind="chol")
+    kw = dict(arnoldi=7) if method.startswith("ca-") else {}
+    rep = S.solve(dev(torch_cuda, p.b), method, s_, t, p.tol, precond=True, **kw)
+    S.close()
+    if method.startswith("ca-"):
+        ref = oracle_lib.solve_ca(p.A, p.b, method[3:], arnoldi=7, s=s_, t=t, tol=p.tol, L=L)
+    else:
+        ref = oracle_lib.solve(p.A, p.b, method, s_, t, p.tol, mode=oracle_lib.MODE_MIRROR, L=L)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+    assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+
+
 def test_preconditioner_errors(eks, torch_cuda):
     A = ei.poisson2d(16)
     S = eks.Solver(A)

@@ -21,5 +21,6 @@ for v in $VARIANTS; do
     restr) run restr --restructured ;;
     pre) run pre --ortho pre-cholqr ;;
     prec) run prec --precond 64 ;;
+    chol) run chol --precond 64 --precond-kind chol --no-cpu --no-e2e --max-outer 4 --steps 2 ;;
   esac
 done
