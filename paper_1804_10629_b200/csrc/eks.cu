@@ -1423,7 +1423,12 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   CK(cudaMemcpy(ctx->d_val, val.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
   // ELL copy for the fused SpMM+Gram when every row has ≤ 8 entries (tiles of kEllTR rows,
   // slot-major inside a tile; padding: value 0 and the row's own column)
-  const int w = eks::ell_width((int)ctx->maxrow);
+  // the plane-marching plan first: when it applies (one rank, stencil structure) and no path is
+  // forced (EKS_SPMM_PATH), the ELL copy and the TMA segment plan are never used, so they are not
+  // built (host setup time is part of the end-to-end number)
+  if (ctx->nranks == 1) ST(build_grid_plan(ctx, n, rp, col, val));
+  const bool skip_alt = ctx->grid_ok && ctx->spmm_path == 0;
+  const int w = skip_alt ? 0 : eks::ell_width((int)ctx->maxrow);
   if (w > 0) {
     const int64_t TR = eks::kEllTR, ntiles = (n + TR - 1) / TR;
     std::vector<int32_t> ec((size_t)ntiles * TR * w), tmax((size_t)ntiles, 0);
@@ -1448,7 +1453,6 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
     CK(cudaMalloc((void**)&ctx->d_tmax, sizeof(int32_t) * tmax.size()));
     CK(cudaMemcpy(ctx->d_tmax, tmax.data(), sizeof(int32_t) * tmax.size(), cudaMemcpyHostToDevice));
     ST(build_seg_plan(ctx, n, rp, ecol, val, plan.halo_before, w));
-    if (ctx->nranks == 1) ST(build_grid_plan(ctx, n, rp, col, val));
     ctx->ell_w = w;
   }
   ctx->n_global = n_global;
