@@ -84,7 +84,8 @@ typedef struct {
  * oracle's defaults (A-CholQR, k_max 5000). */
 typedef struct {
   int max_outer;          /* <=0: 5000 (reading R7) */
-  int use_graph;          /* 1: capture one outer iteration as a CUDA graph and replay it */
+  int use_graph;          /* reserved (CUDA-graph replay of an outer iteration is not built): must be 0,
+                             else EKS_ERR_INVALID_ARG */
   int profile;            /* 1: record per-kernel-class CUDA events (see eks_profile) */
   int arnoldi;            /* CA methods: 7 = modified CA-Arnoldi (Alg 7, default when 0),
                              5 = CA-Arnoldi (Alg 5) */

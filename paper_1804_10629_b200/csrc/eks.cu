@@ -1760,6 +1760,7 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   const int base = ca ? method - EKS_CA_SRE_CG : method;
   const int arnoldi = (opt && opt->arnoldi) ? opt->arnoldi : 7;
   if (ca && (arnoldi != 5 && arnoldi != 7)) return fail(ctx, EKS_ERR_INVALID_ARG, "arnoldi must be 5 or 7");
+  if (opt && opt->use_graph) return fail(ctx, EKS_ERR_INVALID_ARG, "use_graph is reserved (not implemented)");
   const int ortho = opt ? opt->ortho : 0;
   const bool restr = opt && opt->restructured;
   if (ortho != 0 && ortho != 1) return fail(ctx, EKS_ERR_INVALID_ARG, "ortho must be 0 (A-CholQR) or 1 (Pre-CholQR)");
