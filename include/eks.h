@@ -84,8 +84,11 @@ typedef struct {
  * oracle's defaults (A-CholQR, k_max 5000). */
 typedef struct {
   int max_outer;          /* <=0: 5000 (reading R7) */
-  int use_graph;          /* reserved (CUDA-graph replay of an outer iteration is not built): must be 0,
-                             else EKS_ERR_INVALID_ARG */
+  int use_graph;          /* 1: s-step SRE-CG on one rank (no ortho/restructured/precond/profile):
+                             steady-state outer iterations (k ≥ 3) are captured once per phase of
+                             their slot/pointer period as CUDA graphs and replayed (launch-bound
+                             small problems); results are bitwise those of the plain path.
+                             Ignored where it does not apply. */
   int profile;            /* 1: record per-kernel-class CUDA events (see eks_profile) */
   int arnoldi;            /* CA methods: 7 = modified CA-Arnoldi (Alg 7, default when 0),
                              5 = CA-Arnoldi (Alg 5) */

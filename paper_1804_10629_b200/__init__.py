@@ -205,14 +205,14 @@ ORTHO = {"acholqr": 0, "pre-cholqr": 1}
 
 
 def eks_solve_ex(ctx, method, s, t, tol, b, x, max_outer=0, profile=False, raise_on=(5, 6, 1, 2, 3), arnoldi=0,
-                 ortho="acholqr", restructured=False, precond=False):
+                 ortho="acholqr", restructured=False, precond=False, use_graph=False):
     """Returns (status, report dict).  x holds x0 on entry and the solution on exit.
     arnoldi (CA methods only): 7 = modified CA-Arnoldi (default), 5 = CA-Arnoldi.
     ortho: "acholqr" (default) or "pre-cholqr"; restructured: Alg 2 / Alg 1 (SRE-CG / SRE-CG2)."""
     m = METHODS[method] if isinstance(method, str) else int(method)
     where = _where(b, x)
-    opt = _Options(int(max_outer), 0, int(bool(profile)), int(arnoldi), ORTHO[ortho], int(bool(restructured)),
-                   int(bool(precond)))
+    opt = _Options(int(max_outer), int(bool(use_graph)), int(bool(profile)), int(arnoldi), ORTHO[ortho],
+                   int(bool(restructured)), int(bool(precond)))
     rep = _Report()
     st = lib().eks_solve_ex(ctx, m, int(s), int(t), float(tol), _ptr(b, np.float64), _ptr(x, np.float64), where,
                             C.byref(opt), C.byref(rep))
@@ -319,14 +319,15 @@ class Solver:
         eks_setup_precond(self.ctx, ndomains, *self._csr, kind=kind)
 
     def solve(self, b, method="sre-cg", s=1, t=1, tol=1e-8, x0=None, max_outer=0, profile=False, arnoldi=0,
-              ortho="acholqr", restructured=False, precond=False):
+              ortho="acholqr", restructured=False, precond=False, use_graph=False):
         if isinstance(b, np.ndarray):
             b = np.ascontiguousarray(b, np.float64)
             x = np.zeros_like(b) if x0 is None else np.ascontiguousarray(x0, np.float64).copy()
         else:
             x = b.new_zeros(b.shape) if x0 is None else x0.clone()
         st, rep = eks_solve_ex(self.ctx, method, s, t, tol, b, x, max_outer=max_outer, profile=profile,
-                               arnoldi=arnoldi, ortho=ortho, restructured=restructured, precond=precond)
+                               arnoldi=arnoldi, ortho=ortho, restructured=restructured, precond=precond,
+                               use_graph=use_graph)
         rep["status"] = st
         rep["x"] = x
         return rep

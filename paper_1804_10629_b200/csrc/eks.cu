@@ -1760,7 +1760,6 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   const int base = ca ? method - EKS_CA_SRE_CG : method;
   const int arnoldi = (opt && opt->arnoldi) ? opt->arnoldi : 7;
   if (ca && (arnoldi != 5 && arnoldi != 7)) return fail(ctx, EKS_ERR_INVALID_ARG, "arnoldi must be 5 or 7");
-  if (opt && opt->use_graph) return fail(ctx, EKS_ERR_INVALID_ARG, "use_graph is reserved (not implemented)");
   const int ortho = opt ? opt->ortho : 0;
   const bool restr = opt && opt->restructured;
   if (ortho != 0 && ortho != 1) return fail(ctx, EKS_ERR_INVALID_ARG, "ortho must be 0 (A-CholQR) or 1 (Pre-CholQR)");
@@ -1807,8 +1806,46 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   ctx->hist.assign(1, rho0);
   int k = 1, nblocks = 0, breakdown_block = -1, max_fit = -1;
   eks_status status = EKS_OK;
+  // CUDA-graph replay (eks_options.use_graph): steady-state s-step SRE-CG outer iterations (k ≥ 3:
+  // the 2-block window is full, the fused next-C1 is running, nothing is allocated any more) are
+  // the same stream work up to the ring slots (period 3/gcd(3, s) outer iterations) and the r / r_new
+  // swap (period 2): one graph per phase of the combined period P ∈ {2, 6} is captured from a
+  // normal iteration and replayed after that.
+  struct PhaseGraph {
+    cudaGraphExec_t exec = nullptr;
+    int nb0 = 0;             // nblocks when it was captured (block indices baked into the kernels)
+    long long launches = 0;  // this library's kernels in it
+    double bytes = 0, flops = 0;
+  };
+  const bool graphs_on = opt && opt->use_graph && method == EKS_SRE_CG && !restr && !prec && !ortho &&
+                         ctx->nranks == 1 && !ctx->prof_on;
+  const int gperiod = (s % 3 == 0) ? 2 : 6;
+  PhaseGraph pg[6];
+  struct GraphGuard {
+    PhaseGraph* g;
+    ~GraphGuard() {
+      for (int i = 0; i < 6; ++i)
+        if (g[i].exec) cudaGraphExecDestroy(g[i].exec);
+    }
+  } gguard{pg};
+  int replay_phase = -1;  // phase whose graph ran this outer iteration (for the breakdown index)
   // while (ρ > ε ρ0 and k < k_max)   (reading R7)
   while (rho > tol * rho0 && k < kmax) {
+    const int phase = (graphs_on && k >= 3) ? (k - 3) % gperiod : -1;
+    replay_phase = -1;
+    if (phase >= 0 && pg[phase].exec) {
+      CK(cudaGraphLaunch(pg[phase].exec, ctx->stream));
+      ctx->launches += pg[phase].launches;
+      ctx->model_bytes += pg[phase].bytes;
+      ctx->model_flops += pg[phase].flops;
+      replay_phase = phase;
+      nblocks += s;
+    } else {
+    const bool capture = phase >= 0;
+    const long long l0 = ctx->launches;
+    const double b0 = ctx->model_bytes, f0 = ctx->model_flops;
+    const int nb0 = nblocks;
+    if (capture) CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     ST(reset_flag(ctx));
     if (ca) {
       const int nb0 = nblocks;
@@ -1836,7 +1873,14 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
       ST(make_block(ctx, t, method, ring, nblocks, seed, Zsrc, Wn, AWn, i * t, nblocks, mode));
       ++nblocks;
     }
-    if (status == EKS_ERR_OOM) break;
+    if (status == EKS_ERR_OOM) {
+      if (capture) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(ctx->stream, &g);
+        if (g) cudaGraphDestroy(g);
+      }
+      break;
+    }
     if (restr) {  // Alg 1/2 lines 14-17: s sequential updates (skipped on a breakdown flag)
       for (int i = 0; i < s; ++i) {
         const int j = nblocks - s + i, idx = ring ? j % ring : j;
@@ -1847,10 +1891,25 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
     }
     if (ctx->rho_fused) ST(allreduce(ctx, ctx->scal + 1, 1));
     else ST(reduce_scalar(ctx, ctx->scal + 1));
+    if (capture) {
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamEndCapture(ctx->stream, &g));
+      cudaError_t ie = cudaGraphInstantiate(&pg[phase].exec, g, 0);
+      cudaGraphDestroy(g);
+      CK(ie);
+      pg[phase].nb0 = nb0;
+      pg[phase].launches = ctx->launches - l0;
+      pg[phase].bytes = ctx->model_bytes - b0;
+      pg[phase].flops = ctx->model_flops - f0;
+      CK(cudaGraphLaunch(pg[phase].exec, ctx->stream));
+      replay_phase = phase;
+    }
+    }  // graph replay / normal (or capturing) outer iteration
     ST(sync_scalars(ctx, 2));
     const int fl = ctx->h_flag[1];
     if (fl != INT_MAX) {  // A-CholQR breakdown: x stays the last completed iterate
-      breakdown_block = fl;
+      // a replayed graph carries the block indices of the iteration it was captured from
+      breakdown_block = replay_phase >= 0 ? fl + (nblocks - s - pg[replay_phase].nb0) : fl;
       status = EKS_ERR_BREAKDOWN;
       break;
     }

@@ -299,6 +299,21 @@ def test_complete_cholesky_preconditioner(eks, torch_cuda, oracle_lib, method, s
     assert rel(host(rep["x"]), ref["x"]) <= 1e-6
 
 
+@pytest.mark.parametrize("s_,t,N", [(3, 16, 64), (2, 4, 64), (4, 8, 48)])
+def test_graph_replay_bitwise(eks, torch_cuda, s_, t, N):
+    """eks_options.use_graph: steady-state SRE-CG outer iterations replayed from CUDA graphs give
+    bitwise the plain path's x, counts and residual history (period 2 for 3 | s, else 6)."""
+    A = ei.poisson2d(N)
+    b = dev(torch_cuda, ei.uniform_pm1(77, A.n))
+    S = eks.Solver(A)
+    a = S.solve(b, "sre-cg", s_, t, 1e-10)
+    g = S.solve(b, "sre-cg", s_, t, 1e-10, use_graph=True)
+    S.close()
+    assert a["converged"] and g["converged"] and a["outer_iters"] == g["outer_iters"] > 8
+    assert torch_cuda.equal(a["x"], g["x"])
+    assert a["gpu_launches"] == g["gpu_launches"]
+
+
 def test_preconditioner_errors(eks, torch_cuda):
     A = ei.poisson2d(16)
     S = eks.Solver(A)
