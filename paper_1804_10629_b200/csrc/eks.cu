@@ -1175,7 +1175,8 @@ eks_status build_grid_plan(eks_ctx* ctx, int64_t n, const std::vector<int64_t>& 
         pos[np++] = o;
       }
     }
-  std::sort(pos, pos + np);
+  for (int a2 = 1; a2 < np; ++a2)  // np ≤ 3: insertion sort (std::sort trips -Warray-bounds here)
+    for (int b2 = a2; b2 > 0 && pos[b2 - 1] > pos[b2]; --b2) std::swap(pos[b2 - 1], pos[b2]);
   if (np < 2 || pos[0] != 1) return EKS_OK;
   const int64_t b = pos[1], c = np == 3 ? pos[2] : 0;
   int64_t nx = b, ny = 1, plane = b;

@@ -34,13 +34,6 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Bulk prefetch of [p, p+bytes) into L2 (address and size rounded to 16 bytes).
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
-  const uint32_t nb = (bytes + 15u + (uint32_t)(reinterpret_cast<uintptr_t>(p) & 15)) & ~15u;
-  if (nb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(nb) : "memory");
-}
-
 // CTA b's rows start at a multiple of 8 (16-byte alignment of every int32/fp64 row-indexed copy).
 __device__ __forceinline__ int64_t chunk_lo(int64_t n, int b, int nb) {
   return b >= nb ? n : (((int64_t)b * n / nb) & ~(int64_t)7);
