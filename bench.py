@@ -277,6 +277,8 @@ def config_of(args, p, N):
     return {"workload": f"{p.name}: {p.note}; {kind} {p.method}, s={p.s}, t={p.t}, tol={p.tol:g}",
             "n": p.A.n, "nnz": p.A.nnz, "method": p.method, "s": p.s, "t": p.t, "tol": p.tol,
             "parallelism": f"row-slabs x{N} (t/N domains per GPU)",
+            "cuda_graphs": ("off" if getattr(args, "no_graph", False) or getattr(args, "impl", "eks") == "reference"
+                            else "steady s-step SRE-CG outer iterations replayed as CUDA graphs (one rank)"),
             "l2": "flushed: 256 MiB buffer written between timed steps (outside the step events)"}
 
 
@@ -300,6 +302,8 @@ def main():
     ap.add_argument("--arnoldi", type=int, default=7, help="CA variants: Alg 5 or Alg 7")
     ap.add_argument("--ortho", default="acholqr", choices=["acholqr", "pre-cholqr"])
     ap.add_argument("--restructured", action="store_true", help="restructured Alg 2 / Alg 1 (SRE-CG / SRE-CG2)")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="disable the CUDA-graph replay of steady s-step SRE-CG outer iterations (use_graph)")
     ap.add_argument("--precond", type=int, default=0,
                     help="split-preconditioned Alg 8-10 with block Jacobi of this many domains (64 in the paper)")
     ap.add_argument("--precond-kind", default="ic0", choices=["ic0", "chol"], help="IC(0) (Table 5) or Cholesky (Table 6)")
@@ -360,7 +364,7 @@ def main():
             x.zero_()
         st, rep = eks.eks_solve_ex(solver.ctx, p.method, p.s, p.t, p.tol, b, x, profile=profile,
                                    max_outer=args.max_outer, arnoldi=p.arnoldi, ortho=p.ortho,
-                                   restructured=p.restructured, precond=bool(p.precond))
+                                   restructured=p.restructured, precond=bool(p.precond), use_graph=not args.no_graph)
         if st not in ((0, 8) if args.max_outer else (0,)):
             raise SystemExit(f"solve failed: {eks.STATUS.get(st)} {eks.eks_error_string(solver.ctx)}")
         return rep
@@ -464,7 +468,8 @@ def main():
                 e2e_solver.setup_precond(p.precond, kind=p.precond_kind)
             hx[:] = 0.0
             st, rep = eks.eks_solve_ex(e2e_solver.ctx, p.method, p.s, p.t, p.tol, hb, hx, arnoldi=p.arnoldi,
-                                       ortho=p.ortho, restructured=p.restructured, precond=bool(p.precond))
+                                       ortho=p.ortho, restructured=p.restructured, precond=bool(p.precond),
+                                       use_graph=not args.no_graph)
             e_outer += rep["outer_iters"]
         torch.cuda.synchronize()
         barrier()
