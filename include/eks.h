@@ -36,7 +36,7 @@ typedef struct eks_ctx eks_ctx;
 /* 0-2: s-step methods (Alg 4 / Alg 3 / Alg 6).  3-5: their communication-avoiding versions
  * (CA SRE-CG, CA SRE-CG2 P:245-281; CA MSDO-CG P:351): each outer iteration forms the monomial
  * block [W, AW, …, A^{s-1}W], A-orthonormalizes it against the window with CGS2 and then with ONE
- * A-CholQR of its s·t columns (s·t ≤ 96); the CA-Arnoldi variant is eks_options.arnoldi. */
+ * A-CholQR of its s·t columns (s·t ≤ 640, s ≤ 12); the CA-Arnoldi variant is eks_options.arnoldi. */
 typedef enum {
   EKS_SRE_CG = 0, EKS_SRE_CG2 = 1, EKS_MSDO_CG = 2,
   EKS_CA_SRE_CG = 3, EKS_CA_SRE_CG2 = 4, EKS_CA_MSDO_CG = 5
@@ -55,7 +55,9 @@ typedef enum {
   EKS_ERR_CUDA = 5,
   EKS_ERR_NCCL = 6,
   EKS_ERR_BREAKDOWN = 7,   /* A-CholQR pivot <= t*2^-52*max|B| (reading R6): x = last completed iterate */
-  EKS_ERR_MAXITER = 8      /* k_max reached with rho > tol*rho0: x = last iterate */
+  EKS_ERR_MAXITER = 8,     /* k_max reached with rho > tol*rho0: x = last iterate */
+  EKS_ERR_NONFINITE = 9    /* the recursive residual norm rho became NaN/Inf (overflow or a corrupted
+                              basis): x = the iterate of that outer iteration, the loop stops at once */
 } eks_status;
 
 /* Multi-GPU description: one process per GPU; rank r owns the contiguous row

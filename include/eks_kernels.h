@@ -49,6 +49,17 @@ eks_status eks_k_chol(eks_ctx* ctx, int t, const double* B, double* R);
 eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, const double* v, int variant, int reps,
                            double* ms);
 
+/* Read back the A-orthonormal basis of the LAST eks_solve_ex / eks_basis_sweep on this context
+ * (parity tests of whole outer iterations against the oracle's per-iteration V, Alg 3/4/6 lines
+ * 5-11): block j (global block index, 0-based, block i of outer iteration k is j = (k-1)·s + i)
+ * into W (n×t device) and, when AW != NULL, A·W into AW.  Full-basis methods keep every block;
+ * SRE-CG keeps a ring of the last 3 blocks (restructured: max(3, s+1); CA SRE-CG 2s+1):
+ * EKS_ERR_INVALID_ARG when block j is no longer resident or was never built. */
+eks_status eks_k_last_basis(eks_ctx* ctx, int j, double* W, double* AW);
+
+/* The recursive residual r_k (n, device) at the end of the last eks_solve_ex. */
+eks_status eks_k_last_residual(eks_ctx* ctx, double* r);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,8 @@ METHODS = {"sre-cg": EKS_SRE_CG, "sre-cg2": EKS_SRE_CG2, "msdo-cg": EKS_MSDO_CG,
            "ca-sre-cg": 3, "ca-sre-cg2": 4, "ca-msdo-cg": 5}
 EKS_MEM_HOST, EKS_MEM_DEVICE = 0, 1
 STATUS = {0: "EKS_OK", 1: "EKS_ERR_INVALID_ARG", 2: "EKS_ERR_STATE", 3: "EKS_ERR_BAD_MATRIX", 4: "EKS_ERR_OOM",
-          5: "EKS_ERR_CUDA", 6: "EKS_ERR_NCCL", 7: "EKS_ERR_BREAKDOWN", 8: "EKS_ERR_MAXITER"}
+          5: "EKS_ERR_CUDA", 6: "EKS_ERR_NCCL", 7: "EKS_ERR_BREAKDOWN", 8: "EKS_ERR_MAXITER",
+          9: "EKS_ERR_NONFINITE"}
 EKS_OK, EKS_ERR_BREAKDOWN, EKS_ERR_MAXITER, EKS_ERR_OOM = 0, 7, 8, 4
 KCLASSES = ["split", "spmm", "coef", "update", "reduce", "chol", "apply", "comm", "other"]
 
@@ -85,6 +86,8 @@ def lib():
             "eks_k_chol": [vp, i32, vp, vp],
             "eks_k_time_spmm": [vp, i32, vp, vp, vp, i32, i32, C.POINTER(d)],
             "eks_plan_halo": [i32, i32, vp, vp, vp, vp, vp, vp],
+            "eks_k_last_basis": [vp, i32, vp, vp],
+            "eks_k_last_residual": [vp, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -98,7 +101,8 @@ def lib():
 
 EXPORTED = ["eks_get_unique_id", "eks_create", "eks_set_stream", "eks_setup_csr", "eks_setup_precond", "eks_solve", "eks_solve_ex",
             "eks_basis_sweep", "eks_get_profile", "eks_destroy", "eks_error_string", "eks_k_split", "eks_k_spmm",
-            "eks_k_cgs2", "eks_k_acholqr", "eks_k_chol", "eks_k_time_spmm", "eks_plan_halo"]
+            "eks_k_cgs2", "eks_k_acholqr", "eks_k_chol", "eks_k_time_spmm", "eks_plan_halo", "eks_k_last_basis",
+            "eks_k_last_residual"]
 
 
 def eks_plan_halo(rank: int, nranks: int, ranges, row_ptr, col):
@@ -292,6 +296,15 @@ def eks_k_time_spmm(ctx, t, X, Y, v=None, variant=0, reps=10) -> float:
     _check(ctx, lib().eks_k_time_spmm(ctx, int(t), _ptr(X, None), _ptr(Y, None), _ptr(v, None), int(variant),
                                       int(reps), C.byref(ms)))
     return ms.value
+
+
+def eks_k_last_basis(ctx, j, W, AW=None):
+    """Block j of the last solve's basis (and A·W) into device tensors W, AW."""
+    _check(ctx, lib().eks_k_last_basis(ctx, int(j), _ptr(W, None), _ptr(AW, None)))
+
+
+def eks_k_last_residual(ctx, r):
+    _check(ctx, lib().eks_k_last_residual(ctx, _ptr(r, None)))
 
 
 # ------------------------------------------------------------------ convenience

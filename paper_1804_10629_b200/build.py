@@ -31,19 +31,37 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """nvcc -c of every translation unit in parallel (objects under build/), then one -shared link."""
     if not force and not needs_build():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     nd = nccl_dir()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
-           "-o", LIB] + SOURCES + [
-           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
+    flags = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+             "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include")]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+        flags.insert(1, "-Xptxas=-v")
+    odir = os.path.join(ROOT, "build", "eks")
+    os.makedirs(odir, exist_ok=True)
+    objs = [os.path.join(odir, os.path.basename(f)[:-3] + ".o") for f in SOURCES]
+
+    def cc(src_obj):
+        src, obj = src_obj
+        cmd = flags + ["-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        return subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(cc, zip(SOURCES, objs)))
+    for r in results:
+        sys.stderr.write(r.stderr)
+        if r.returncode != 0:
+            raise subprocess.CalledProcessError(r.returncode, r.args)
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB] + objs + [
+            "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
+    subprocess.check_call(link)
     return LIB
 
 

@@ -141,6 +141,8 @@ struct eks_ctx {
   eks_profile prof{};
   long long launches = 0;
   double model_bytes = 0.0, model_flops = 0.0;
+  // basis bookkeeping of the last solve / sweep (eks_k_last_basis)
+  int last_t = 0, last_nblocks = 0, last_ring = 0;
 };
 
 namespace {
@@ -1217,6 +1219,65 @@ eks_status build_grid_plan(eks_ctx* ctx, int64_t n, const std::vector<int64_t>& 
   return EKS_OK;
 }
 
+// Timing events of one solve, destroyed on every exit path.
+struct EventPair {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaError_t create() {
+    cudaError_t e = cudaEventCreate(&e0);
+    return e == cudaSuccess ? cudaEventCreate(&e1) : e;
+  }
+  ~EventPair() {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+  }
+};
+
+// A stream capture that is ended on every exit path: an error inside the captured region must not
+// leave the (possibly caller-owned) stream in an invalidated capture state.
+struct CaptureGuard {
+  cudaStream_t st;
+  bool open = false;
+  explicit CaptureGuard(cudaStream_t s) : st(s) {}
+  cudaError_t begin() {
+    cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    open = e == cudaSuccess;
+    return e;
+  }
+  cudaError_t end(cudaGraph_t* g) {
+    open = false;
+    return cudaStreamEndCapture(st, g);
+  }
+  ~CaptureGuard() {
+    if (!open) return;
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(st, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+  }
+};
+
+// Everything a steady-state s-step SRE-CG outer iteration allocates lazily (ring slots, C1/C2 of the
+// 2-block window, per-CTA partials of every sweep, the fused next-C1 partials), allocated up front
+// so that a CUDA-graph capture never meets a cudaMalloc/cudaFree.
+eks_status prealloc_steady(eks_ctx* ctx, int t, int ring) {
+  for (int idx = 0; idx < ring; ++idx) {
+    Block *W = nullptr, *AW = nullptr;
+    ST(slot(ctx, t, idx, &W, &AW));
+  }
+  ST(ensure_C(ctx, (size_t)2 * t * t));
+  size_t stride = std::max(eks::tn_partials_stride(t, 2, false), eks::tn_partials_stride(t, 1, true));
+  if (eks::sweep_supported(t))
+    stride = std::max({stride, eks::sweep_part_stride(t, 2, false), eks::sweep_part_stride(t, 1, true)});
+  ST(ensure_part(ctx, stride * ctx->nblk));
+  if (ctx->part2_cap < (size_t)ctx->nblk * (2 * t * t + 2)) {
+    dfree(ctx->part2);
+    ctx->part2 = nullptr;
+    ST(dalloc(ctx, &ctx->part2, (size_t)ctx->nblk * (2 * t * t + 2)));
+    ctx->part2_cap = (size_t)ctx->nblk * (2 * t * t + 2);
+  }
+  return EKS_OK;
+}
+
 void begin_run(eks_ctx* ctx, const eks_options* opt) {
   ctx->prof_on = opt && opt->profile;
   ctx->prof = eks_profile{};
@@ -1517,6 +1578,7 @@ eks_status eks_setup_precond(eks_ctx* ctx, eks_precond kind, int nd, const int64
   std::vector<int64_t> rp(n + 1);
   if (where == EKS_MEM_HOST) memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1));
   else CK(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+  if (rp[0] != 0) return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr[0] != 0");
   const int64_t nnz = rp[n];
   if (nnz != ctx->nnz) return fail(ctx, EKS_ERR_INVALID_ARG, "CSR differs from eks_setup_csr's");
   std::vector<int32_t> col(nnz);
@@ -1527,6 +1589,23 @@ eks_status eks_setup_precond(eks_ctx* ctx, eks_precond kind, int nd, const int64
   } else {
     CK(cudaMemcpy(col.data(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(val.data(), vals, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+  }
+  // the same validation as eks_setup_csr: the IC(0) elimination below relies on
+  // strictly ascending columns within a row (p < q stands in for col[p] < col[q])
+  for (int64_t i = 0; i < n; ++i) {
+    if (rp[i + 1] < rp[i]) return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr not monotone at row %lld", (long long)i);
+    bool diag = false;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t c = col[p];
+      if (c < 0 || c >= N) return fail(ctx, EKS_ERR_BAD_MATRIX, "column %lld out of range", (long long)c);
+      if (p > rp[i] && col[p - 1] >= c)
+        return fail(ctx, EKS_ERR_BAD_MATRIX, "columns not strictly ascending in row %lld", (long long)(r0 + i));
+      if (c == r0 + i) {
+        if (!(val[p] > 0.0)) return fail(ctx, EKS_ERR_BAD_MATRIX, "non-positive diagonal in row %lld", (long long)(r0 + i));
+        diag = true;
+      }
+    }
+    if (!diag) return fail(ctx, EKS_ERR_BAD_MATRIX, "missing diagonal in row %lld", (long long)(r0 + i));
   }
   // strict-lower L (local columns) and its diagonal
   std::vector<int> dom(n);
@@ -1681,11 +1760,16 @@ eks_status eks_setup_precond(eks_ctx* ctx, eks_precond kind, int nd, const int64
       if (maxe <= eks::kTrsvMaxE)
         for (int W = 2; W <= 4096 && !best; W *= 2) {
           bool ok = true;
+          // every row r owns slot r & (W-1) from its own level until its last reader's level;
+          // the next row of the slot chain (r + W forward, r − W backward, same domain) must
+          // be solved strictly later, for EVERY r (rows without readers included: otherwise
+          // the chain r, r+W, r+2W, … need not be level-monotone and two rows of one level
+          // could share a slot)
           for (int64_t r = 0; r < n && ok; ++r) {
-            if (maxrd[r] < 0) continue;
+            const int need = std::max(lev[r], maxrd[r]);
             const int64_t j = w ? r - W : r + W;
             if (j < 0 || j >= n || dom[j] != dom[r]) continue;
-            ok = lev[j] > maxrd[r];
+            ok = lev[j] > need;
           }
           if (ok) best = W;
         }
@@ -1793,10 +1877,9 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   const int ring = (method == EKS_SRE_CG) ? (restr ? std::max(3, s + 1) : 3) : (method == EKS_CA_SRE_CG ? 2 * s + 1 : 0);
   ctx->ortho = ortho;
   ctx->use_prec = prec;
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  CK(cudaEventRecord(e0, ctx->stream));
+  EventPair ev;
+  CK(ev.create());
+  CK(cudaEventRecord(ev.e0, ctx->stream));
   // r0 = b − A x0, ρ0 = ||r0||  (line 1 of Alg 3/4/6)
   ST(copy_in(ctx, ctx->b, b, ctx->n, where));
   ST(copy_in(ctx, ctx->xv.loc, x, ctx->n, where));
@@ -1808,10 +1891,11 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   int k = 1, nblocks = 0, breakdown_block = -1, max_fit = -1;
   eks_status status = EKS_OK;
   // CUDA-graph replay (eks_options.use_graph): steady-state s-step SRE-CG outer iterations (k ≥ 3:
-  // the 2-block window is full, the fused next-C1 is running, nothing is allocated any more) are
-  // the same stream work up to the ring slots (period 3/gcd(3, s) outer iterations) and the r / r_new
-  // swap (period 2): one graph per phase of the combined period P ∈ {2, 6} is captured from a
-  // normal iteration and replayed after that.
+  // the 2-block window is full, the fused next-C1 is running) are the same stream work up to the
+  // ring slots (period 3/gcd(3, s) outer iterations) and the r / r_new swap (period 2): one graph
+  // per phase of the combined period P ∈ {2, 6} is captured from a normal iteration and replayed
+  // after that.  Everything a steady iteration touches is allocated before the first capture
+  // (prealloc_steady), so no cudaMalloc/cudaFree can happen inside a capture.
   struct PhaseGraph {
     cudaGraphExec_t exec = nullptr;
     int nb0 = 0;             // nblocks when it was captured (block indices baked into the kernels)
@@ -1829,6 +1913,48 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
         if (g[i].exec) cudaGraphExecDestroy(g[i].exec);
     }
   } gguard{pg};
+  if (graphs_on) ST(prealloc_steady(ctx, t, ring));
+  // One outer iteration's stream work (Alg 3/4/6 lines 3-12, or the CA outer iteration).
+  auto outer_body = [&]() -> eks_status {
+    ST(reset_flag(ctx));
+    if (ca) {
+      const int nb0 = nblocks;
+      eks_status cs = ca_outer(ctx, t, s, base, arnoldi, k, nblocks, ring);
+      if (cs == EKS_ERR_OOM) {
+        max_fit = nb0 / s;
+        status = EKS_ERR_OOM;
+        return EKS_OK;
+      }
+      ST(cs);
+    }
+    for (int i = 0; i < (ca ? 0 : s); ++i) {
+      Block *Wn = nullptr, *AWn = nullptr;
+      const int idx = ring ? nblocks % ring : nblocks;
+      eks_status as = slot(ctx, t, idx, &Wn, &AWn);
+      if (as == EKS_ERR_OOM) {
+        max_fit = nblocks / s;
+        status = EKS_ERR_OOM;
+        return EKS_OK;
+      }
+      ST(as);
+      const bool seed = (i == 0) && (method == EKS_MSDO_CG || k == 1);
+      const double* Zsrc = seed ? nullptr : ctx->AWpool[ring ? (nblocks - 1) % ring : nblocks - 1].loc;
+      const int mode = restr ? 4 : (i == 0 ? 1 : 0) | (i == s - 1 ? 2 : 0);
+      ST(make_block(ctx, t, method, ring, nblocks, seed, Zsrc, Wn, AWn, i * t, nblocks, mode));
+      ++nblocks;
+    }
+    if (restr) {  // Alg 1/2 lines 14-17: s sequential updates (skipped on a breakdown flag)
+      for (int i = 0; i < s; ++i) {
+        const int j = nblocks - s + i, idx = ring ? j % ring : j;
+        ST(restructured_update(ctx, t, ctx->Wpool[idx].loc, ctx->AWpool[idx].loc, i == 0 ? ctx->r : ctx->rnew,
+                               ctx->rnew));
+      }
+      ctx->rho_fused = false;
+    }
+    if (ctx->rho_fused) ST(allreduce(ctx, ctx->scal + 1, 1));
+    else ST(reduce_scalar(ctx, ctx->scal + 1));
+    return EKS_OK;
+  };
   int replay_phase = -1;  // phase whose graph ran this outer iteration (for the breakdown index)
   // while (ρ > ε ρ0 and k < k_max)   (reading R7)
   while (rho > tol * rho0 && k < kmax) {
@@ -1841,60 +1967,18 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
       ctx->model_flops += pg[phase].flops;
       replay_phase = phase;
       nblocks += s;
-    } else {
-    const bool capture = phase >= 0;
-    const long long l0 = ctx->launches;
-    const double b0 = ctx->model_bytes, f0 = ctx->model_flops;
-    const int nb0 = nblocks;
-    if (capture) CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    ST(reset_flag(ctx));
-    if (ca) {
+    } else if (phase >= 0) {
+      const long long l0 = ctx->launches;
+      const double b0 = ctx->model_bytes, f0 = ctx->model_flops;
       const int nb0 = nblocks;
-      eks_status cs = ca_outer(ctx, t, s, base, arnoldi, k, nblocks, ring);
-      if (cs == EKS_ERR_OOM) {
-        max_fit = nb0 / s;
-        status = EKS_ERR_OOM;
-        break;
-      }
-      ST(cs);
-    }
-    for (int i = 0; i < (ca ? 0 : s); ++i) {
-      Block *Wn = nullptr, *AWn = nullptr;
-      const int idx = ring ? nblocks % ring : nblocks;
-      eks_status as = slot(ctx, t, idx, &Wn, &AWn);
-      if (as == EKS_ERR_OOM) {
-        max_fit = nblocks / s;
-        status = EKS_ERR_OOM;
-        break;
-      }
-      ST(as);
-      const bool seed = (i == 0) && (method == EKS_MSDO_CG || k == 1);
-      const double* Zsrc = seed ? nullptr : ctx->AWpool[ring ? (nblocks - 1) % ring : nblocks - 1].loc;
-      const int mode = restr ? 4 : (i == 0 ? 1 : 0) | (i == s - 1 ? 2 : 0);
-      ST(make_block(ctx, t, method, ring, nblocks, seed, Zsrc, Wn, AWn, i * t, nblocks, mode));
-      ++nblocks;
-    }
-    if (status == EKS_ERR_OOM) {
-      if (capture) {
-        cudaGraph_t g = nullptr;
-        cudaStreamEndCapture(ctx->stream, &g);
-        if (g) cudaGraphDestroy(g);
-      }
-      break;
-    }
-    if (restr) {  // Alg 1/2 lines 14-17: s sequential updates (skipped on a breakdown flag)
-      for (int i = 0; i < s; ++i) {
-        const int j = nblocks - s + i, idx = ring ? j % ring : j;
-        ST(restructured_update(ctx, t, ctx->Wpool[idx].loc, ctx->AWpool[idx].loc, i == 0 ? ctx->r : ctx->rnew,
-                               ctx->rnew));
-      }
-      ctx->rho_fused = false;
-    }
-    if (ctx->rho_fused) ST(allreduce(ctx, ctx->scal + 1, 1));
-    else ST(reduce_scalar(ctx, ctx->scal + 1));
-    if (capture) {
       cudaGraph_t g = nullptr;
-      CK(cudaStreamEndCapture(ctx->stream, &g));
+      {
+        CaptureGuard cap(ctx->stream);  // ends (and discards) the capture on every exit path
+        CK(cap.begin());
+        ST(outer_body());
+        if (status == EKS_ERR_OOM) break;  // (cannot happen after prealloc_steady)
+        CK(cap.end(&g));
+      }
       cudaError_t ie = cudaGraphInstantiate(&pg[phase].exec, g, 0);
       cudaGraphDestroy(g);
       CK(ie);
@@ -1904,8 +1988,10 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
       pg[phase].flops = ctx->model_flops - f0;
       CK(cudaGraphLaunch(pg[phase].exec, ctx->stream));
       replay_phase = phase;
+    } else {
+      ST(outer_body());
+      if (status == EKS_ERR_OOM) break;
     }
-    }  // graph replay / normal (or capturing) outer iteration
     ST(sync_scalars(ctx, 2));
     const int fl = ctx->h_flag[1];
     if (fl != INT_MAX) {  // A-CholQR breakdown: x stays the last completed iterate
@@ -1918,8 +2004,14 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
     rho = std::sqrt(ctx->h_scal[1]);
     ctx->hist.push_back(rho);
     ++k;
-    if (!std::isfinite(rho)) break;
+    if (!std::isfinite(rho)) {
+      status = EKS_ERR_NONFINITE;
+      break;
+    }
   }
+  ctx->last_t = t;
+  ctx->last_nblocks = nblocks;
+  ctx->last_ring = ring;
   // true residual at exit
   ST(residual(ctx, nullptr, ctx->scal + 2));
   {
@@ -1929,12 +2021,10 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   }
   ST(reduce_scalar(ctx, ctx->scal + 3));
   ST(copy_out(ctx, x, ctx->xv.loc, ctx->n, where));
-  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventRecord(ev.e1, ctx->stream));
   ST(sync_scalars(ctx, 4));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  cudaEventElapsedTime(&ms, ev.e0, ev.e1);
   (void)wall0;
   const bool converged = rho <= tol * rho0;
   if (status == EKS_OK && !converged) status = EKS_ERR_MAXITER;
@@ -1956,6 +2046,8 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   if (status == EKS_ERR_OOM) return fail(ctx, EKS_ERR_OOM, "full basis Q exhausted device memory after %d outer iterations", max_fit);
   if (status == EKS_ERR_BREAKDOWN) return fail(ctx, status, "A-CholQR breakdown in block %d", breakdown_block);
   if (status == EKS_ERR_MAXITER) return fail(ctx, status, "k_max=%d reached, rho/rho0=%.3e", kmax, rho / rho0);
+  if (status == EKS_ERR_NONFINITE)
+    return fail(ctx, status, "non-finite residual norm after outer iteration %d", k - 1);
   return EKS_OK;
 }
 
@@ -1968,10 +2060,9 @@ eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks_total, const double*
   ST(ensure_workspace(ctx, t, 1));
   ctx->use_prec = false;
   ctx->ortho = 0;
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  CK(cudaEventRecord(e0, ctx->stream));
+  EventPair ev;
+  CK(ev.create());
+  CK(cudaEventRecord(ev.e0, ctx->stream));
   ST(reset_flag(ctx));
   const int ring = 3;
   for (int j = 0; j < nblocks_total; ++j) {
@@ -1987,12 +2078,13 @@ eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks_total, const double*
     ST(make_block(ctx, t, EKS_SRE_CG, ring, j, false, Zsrc, Wn, AWn, 0, j, 4));
   }
   ST(copy_out(ctx, W_last, ctx->Wpool[(nblocks_total - 1) % ring].loc, ctx->n * t, where));
-  CK(cudaEventRecord(e1, ctx->stream));
+  ctx->last_t = t;
+  ctx->last_nblocks = nblocks_total;
+  ctx->last_ring = ring;
+  CK(cudaEventRecord(ev.e1, ctx->stream));
   ST(sync_scalars(ctx, 1));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  cudaEventElapsedTime(&ms, ev.e0, ev.e1);
   const int fl = ctx->h_flag[1];
   if (rep) {
     memset(rep, 0, sizeof *rep);
@@ -2201,6 +2293,28 @@ eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, cons
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   *ms = (double)f / reps;
+  return EKS_OK;
+}
+
+eks_status eks_k_last_basis(eks_ctx* ctx, int j, double* W, double* AW) {
+  ST(check_ready(ctx));
+  const int t = ctx->last_t, nb = ctx->last_nblocks, ring = ctx->last_ring;
+  if (!W || t == 0 || j < 0 || j >= nb || (ring && j < nb - ring))
+    return fail(ctx, EKS_ERR_INVALID_ARG, "basis block %d not resident (%d blocks built, ring %d)", j, nb, ring);
+  const int idx = ring ? j % ring : j;
+  if (idx >= (int)ctx->Wpool.size() || !ctx->Wpool[idx].base) return fail(ctx, EKS_ERR_INVALID_ARG, "no basis block %d", j);
+  CK(cudaMemcpyAsync(W, ctx->Wpool[idx].loc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (AW)
+    CK(cudaMemcpyAsync(AW, ctx->AWpool[idx].loc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return EKS_OK;
+}
+
+eks_status eks_k_last_residual(eks_ctx* ctx, double* r) {
+  ST(check_ready(ctx));
+  if (!r || !ctx->r) return fail(ctx, EKS_ERR_INVALID_ARG, "no residual (solve first)");
+  CK(cudaMemcpyAsync(r, ctx->r, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   return EKS_OK;
 }
 

@@ -218,6 +218,11 @@ def test_pre_cholqr_restructured_end_to_end(eks, torch_cuda, oracle_lib, method,
     assert rep["true_relres"] <= 1.5e-8
     assert pre["outer_iters"] == refp["outer_iters"] == 2
     assert rel(host(pre["x"]), refp["x"]) <= 1e-10
+    # and against the oracle's DEFINITION mode (explicit SpMMs Qᵀ(A·Z), u = Vα̃, r −= A·u)
+    dref = oracle_lib.solve(p.A, p.b, method, s_, t, p.tol, ortho=ortho, restructured=restr)
+    assert dref["converged"]
+    assert abs(rep["outer_iters"] - dref["outer_iters"]) <= max(1, round(0.05 * dref["outer_iters"]))
+    assert rel(host(rep["x"]), dref["x"]) <= 1e-6
 
 
 def test_pre_restructured_argument_errors(eks, torch_cuda):
@@ -258,6 +263,11 @@ def test_preconditioned_end_to_end(eks, torch_cuda, oracle_lib, method, s_, t, n
     assert pre["outer_iters"] == refp["outer_iters"] == 2
     assert rel(host(pre["x"]), refp["x"]) <= 1e-9
     assert rep["outer_iters"] < plain["outer_iters"]
+    # and against the oracle's DEFINITION mode (M⁻¹A·W with explicit SpMMs, Qᵀ(A·Z), r −= A·u)
+    dref = oracle_lib.solve(p.A, p.b, method, s_, t, p.tol, L=L)
+    assert dref["converged"]
+    assert abs(rep["outer_iters"] - dref["outer_iters"]) <= max(1, round(0.05 * dref["outer_iters"]))
+    assert rel(host(rep["x"]), dref["x"]) <= 1e-6
 
 
 @pytest.mark.parametrize("method,arnoldi,s_,t", [("ca-sre-cg", 7, 3, 4), ("ca-sre-cg2", 5, 2, 8),
@@ -314,6 +324,46 @@ def test_graph_replay_bitwise(eks, torch_cuda, s_, t, N):
     assert a["gpu_launches"] == g["gpu_launches"]
 
 
+@pytest.mark.parametrize("s_,t", [(1, 4), (1, 16), (2, 8)])
+def test_graph_replay_fresh_solver(eks, torch_cuda, s_, t):
+    """use_graph on a FRESH context (nothing preallocated by an earlier plain solve): every ring
+    slot and partial buffer is allocated before the first capture, so s = 1 (ring slot 2 first used
+    at k = 3) captures and replays; bitwise equal to the plain path on a second fresh context."""
+    A = ei.poisson2d(48)
+    b = dev(torch_cuda, ei.uniform_pm1(78, A.n))
+    S1 = eks.Solver(A)
+    g = S1.solve(b, "sre-cg", s_, t, 1e-10, use_graph=True)
+    S1.close()
+    S2 = eks.Solver(A)
+    a = S2.solve(b, "sre-cg", s_, t, 1e-10)
+    S2.close()
+    assert g["status"] == 0 and g["converged"] and g["outer_iters"] == a["outer_iters"] > 6
+    assert torch_cuda.equal(a["x"], g["x"])
+
+
+def test_trsv_ring_slot_chain(eks, torch_cuda, oracle_lib):
+    """a 9-row preconditioner domain whose rows 3, 7, 8 are isolated and whose edges
+    (1,0),(2,1),(4,2),(5,2),(6,5) make the slot chain r, r+W, r+2W non-monotone in level for rows
+    without readers.  The ring width check now covers every row, so M⁻¹ is deterministic and equal
+    to the oracle's L⁻ᵗL⁻¹ (repeat solves bitwise identical, x = oracle mirror within 1e-12)."""
+    n = 9
+    D = 4.0 * np.eye(n)
+    for i, j in [(1, 0), (2, 1), (4, 2), (5, 2), (6, 5)]:
+        D[i, j] = D[j, i] = -1.0
+    A = ei.csr_from_dense(D)
+    b = ei.uniform_pm1(91, n)
+    st, L = oracle_lib.ic0(A, 1)
+    assert st == 0
+    S = eks.Solver(A)
+    S.setup_precond(1)
+    xs = [host(S.solve(dev(torch_cuda, b), "sre-cg", 1, 1, 1e-12, precond=True)["x"]) for _ in range(5)]
+    S.close()
+    assert all(np.array_equal(xs[0], x) for x in xs[1:])
+    ref = oracle_lib.solve(A, b, "sre-cg", 1, 1, 1e-12, mode=oracle_lib.MODE_MIRROR, L=L)
+    assert rel(xs[0], ref["x"]) <= 1e-12
+    assert rel(xs[0], np.linalg.solve(D, b)) <= 1e-10
+
+
 def test_preconditioner_errors(eks, torch_cuda):
     A = ei.poisson2d(16)
     S = eks.Solver(A)
@@ -362,6 +412,58 @@ def test_cfg4_analog_sre_t64(eks, torch_cuda, oracle_lib):
     assert rep["converged"] and ref["converged"]
     assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
     assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+
+
+def _oracle_iterations(oracle_lib, p, kmax):
+    """Per-outer-iteration V (n×st), x, r of the oracle's DEFINITION mode (callback of or_solve)."""
+    its = {}
+
+    def cb(k, V, alpha, x, r, rho):
+        its[k] = dict(V=V, x=x, r=r, rho=rho)
+    ref = oracle_lib.solve(p.A, p.b, p.method, p.s, p.t, 0.0, kmax=kmax, callback=cb)
+    return ref, its
+
+
+@pytest.mark.parametrize("cfg", ["cfg4", "cfg3"])
+def test_path_size_prefix_vs_definition(eks, torch_cuda, oracle_lib, cfg):
+    """64³ analogs of cfg4 (SRE-CG, t=64, s=2, anisotropic z 1e-2, b=1) and cfg3 (MSDO-CG, t=32, s=4,
+    κ=1e3 subcubes): n = 262,144 rows, i.e. ≈ 28 TR-tiles per CTA of the DMMA/cp.async sweeps and
+    many plane-marching units per CTA at t = 32/64 — the multi-tile paths of the full-size kernels.
+    The first two outer iterations (tol = 0) against the oracle's DEFINITION mode (explicit SpMMs
+    Qᵀ(A·Z), u = Vα̃, r −= A·u; reading R24/R9 give equality in exact arithmetic): every basis block
+    W, x and the recursive r element-wise within 1e-10 (relative to their max-norm)."""
+    torch = torch_cuda
+    p = ei.cfg4(N=64) if cfg == "cfg4" else ei.cfg3(N=64)
+    ref, its = _oracle_iterations(oracle_lib, p, kmax=3)
+    assert ref["outer_iters"] == 2 and sorted(its) == [1, 2]
+    n, t, s_ = p.A.n, p.t, p.s
+    S = eks.Solver(p.A)
+    b = dev(torch, p.b)
+    W = torch.empty(n, t, dtype=torch.float64, device="cuda")
+    r = torch.empty(n, dtype=torch.float64, device="cuda")
+
+    def close(a, o, tol=1e-10):
+        return np.abs(a - o).max() <= tol * np.abs(o).max()
+    seen = set()
+    for k in (1, 2):
+        rep = S.solve(b, p.method, s_, t, 0.0, max_outer=k + 1)
+        assert rep["outer_iters"] == k
+        assert close(host(rep["x"]), its[k]["x"]), (cfg, k, "x")
+        eks.eks_k_last_residual(S.ctx, r)
+        assert close(host(r), its[k]["r"]), (cfg, k, "r")
+        assert abs(rep["rho"] - its[k]["rho"]) <= 1e-10 * its[k]["rho"]
+        for kk in range(1, k + 1):
+            for i in range(s_):
+                j = (kk - 1) * s_ + i
+                try:
+                    eks.eks_k_last_basis(S.ctx, j, W)
+                except eks.EksError:
+                    continue  # SRE-CG ring: block overwritten (it was compared at the earlier k)
+                Vo = its[kk]["V"][:, i * t:(i + 1) * t]
+                assert close(host(W), Vo), (cfg, k, j)
+                seen.add(j)
+    S.close()
+    assert seen == set(range(2 * s_))
 
 
 @pytest.mark.parametrize("t,nblocks", [(8, 4), (16, 8), (32, 6)])
@@ -475,8 +577,18 @@ def test_full_size_spmm_gram_sampled(eks, torch_cuda, oracle_lib, cfg, t):
     Xs = host(X[torch.from_numpy(ucols).cuda()])
     Yo = oracle_lib.spmm(sub, Xs)[: len(rows)]
     assert np.array_equal(host(Y[torch.from_numpy(rows).cuda()]), Yo)
-    assert rel(host(G), host(X.T @ Y)) <= 1e-12
-    assert rel(host(g), host(X.T @ v)) <= 1e-12
+    if cfg == "cfg3":
+        # cfg3 fits the oracle whole (2.1M × 32): every row of Y bitwise, Gram and Xᵀv vs or_xty
+        Xh, vh = host(X), host(v)
+        Yf = oracle_lib.spmm(A, Xh)
+        assert np.array_equal(host(Y), Yf)
+        assert rel(host(G), oracle_lib.xty(Xh, Yf)) <= 1e-12
+        assert rel(host(g), oracle_lib.xty(Xh, vh[:, None])[:, 0]) <= 1e-12
+    else:
+        # cfg4 / cfg5 (8.6 / 7.2 GB blocks): too large for the single-thread oracle's Gram; a cuBLAS
+        # fp64 XᵀY stands in (sampled rows above are the oracle's)
+        assert rel(host(G), host(X.T @ Y)) <= 1e-12
+        assert rel(host(g), host(X.T @ v)) <= 1e-12
     S.close()
 
 
