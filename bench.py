@@ -49,35 +49,96 @@ def workload(name: str):
     raise SystemExit(f"unknown workload {name}")
 
 
-def spmm_block(eks, torch, peak_gbs, N=384, ts=(8, 16, 32), reps=10):
+def spmm_block(eks, torch, peak_gbs, N=384, ts=(8, 16, 32), reps=10, solver=None, A=None):
     """The SpMM-block kernel of the solve (fused Y = A·X + Gram [XᵀY | Xᵀr], tail reduction)
     timed on the cfg5 operator (384³ 7-point Laplacian, BASELINE configs[4]) with CUDA events
     over `reps` back-to-back launches; GB/s of B_spmm = 12·nnz + 4(n+1) + 16·n·t."""
-    A = ei.cfg5_operator(N)
-    s = eks.Solver(A)
+    A = ei.cfg5_operator(N) if A is None else A
+    s = eks.Solver(A) if solver is None else solver
     out = {"workload": f"cfg5 operator {N}^3 7-point Laplacian, n={A.n}, nnz={A.nnz}; fused SpMM+Gram launch "
                        f"as in eks_solve; X uniform, L2 not flushed between the {reps} launches (inputs > L2)",
-           "bytes_formula": "12*nnz + 4*(n+1) + 16*n*t", "peak_gbs": peak_gbs, "t": {}}
+           "bytes_formula": "8*7*n (stencil values) + 16*n*t (X, Y) + 8*n (v); frac_csr_formula uses "
+                            "12*nnz + 4*(n+1) + 16*n*t", "peak_gbs": peak_gbs, "t": {}}
     for t in ts:
         X = torch.rand(A.n, t, dtype=torch.float64, device="cuda") - 0.5
         Y = torch.empty_like(X)
         v = torch.rand(A.n, dtype=torch.float64, device="cuda")
         ms = eks.eks_k_time_spmm(s.ctx, t, X, Y, v, 2, reps)
-        B = 12.0 * A.nnz + 4.0 * (A.n + 1) + 16.0 * A.n * t
+        # algorithmic bytes of the launch: the 7 stencil values per row the plane-marching kernel
+        # streams (no indices), X read, Y written, v read; B_csr = the north_star's CSR formula
+        B = 8.0 * 7 * A.n + 16.0 * A.n * t + 8.0 * A.n
+        Bcsr = 12.0 * A.nnz + 4.0 * (A.n + 1) + 16.0 * A.n * t
         gbs = B / (ms * 1e-3) / 1e9
-        out["t"][str(t)] = {"us_per_launch": ms * 1e3, "gbs": gbs, "frac": gbs / peak_gbs}
+        out["t"][str(t)] = {"us_per_launch": ms * 1e3, "gbs": gbs, "frac": gbs / peak_gbs,
+                            "frac_of_8TBs": gbs / 8000.0, "bytes": B,
+                            "frac_csr_formula": Bcsr / (ms * 1e-3) / 1e9 / peak_gbs}
         del X, Y, v
         torch.cuda.empty_cache()
-    s.close()
+    if solver is None:
+        s.close()
     return out
 
 
+def cfg5_oracle_sample(t: int, s_: int, N: int = 384, planes: int = 4):
+    """The oracle (as it stands, definition mode, one thread) on a bounded sample of the cfg5
+    workload: one outer iteration (s blocks, window 2t, reading R27) of the basis sweep on the first
+    `planes` z-planes of the 384³ grid (a 384×384×planes Dirichlet Laplacian, n_s rows), scaled to
+    the full grid by the row count (the sweep's work is linear in n at fixed t, s).  Returns
+    (outer it/s at full size, seconds, n_s)."""
+    import oracle
+    oracle.build()
+    A = ei.stencil_csr(N, N, planes, ndim=3)
+    X0 = ei.cfg5_start_block(A.n, t)
+    t0 = time.perf_counter()
+    st, _ = oracle.basis_sweep(A, X0, s_)
+    dt = time.perf_counter() - t0
+    if st != 0:
+        raise SystemExit(f"oracle basis sweep failed: {st}")
+    n_full = N ** 3
+    return 1.0 / (dt * n_full / A.n), dt, A.n
+
+
+def roofline_of(agg, c, peaks):
+    """Roofline of kernel class c from the profile pass: algorithmic bytes (flops) per launch ÷ the
+    launch's CUDA-event time on the solve stream."""
+    if agg["ms"].get(c, 0) <= 0:
+        return None
+    n_l = max(1, agg["launches"][c])
+    gbs = agg["bytes"][c] / (agg["ms"][c] * 1e-3) / 1e9
+    tfl = agg["flops"][c] / (agg["ms"][c] * 1e-3) / 1e12
+    intensity = agg["flops"][c] / max(agg["bytes"][c], 1.0)
+    ridge = peaks["dmma_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    common = {"kernel": c, "launches": agg["launches"][c], "avg_launch_us": 1e3 * agg["ms"][c] / n_l,
+              "bytes_per_launch": agg["bytes"][c] / n_l, "flops_per_launch": agg["flops"][c] / n_l,
+              "intensity_flop_per_byte": intensity, "traffic": None}
+    if intensity > ridge:
+        return dict(common, bound="alu", achieved=tfl, peak=peaks["dmma_tflops"], unit="TFLOP/s",
+                    frac=tfl / peaks["dmma_tflops"],
+                    peak_source="measured fp64 DMMA (profiles/fp64_peaks_r01.json, tools/fp64_peaks.cu)")
+    return dict(common, bound="hbm", achieved=gbs, peak=peaks["hbm_gbs"], unit="GB/s", frac=gbs / peaks["hbm_gbs"],
+                peak_source=peaks["source"], frac_of_8TBs=gbs / 8000.0)
+
+
+def attach_traffic(rf, name):
+    """DRAM bytes per launch of the same kernel class from a committed ncu --set full capture."""
+    tf = os.path.join(ROOT, "profiles", name)
+    if rf is None or not os.path.exists(tf):
+        return
+    tr = json.load(open(tf)).get("classes", {})
+    if tr.get(rf["kernel"]):
+        rf["traffic"] = tr[rf["kernel"]]
+        rf["traffic_source"] = f"profiles/{name} (ncu dram__bytes_read.sum + dram__bytes_write.sum per launch)"
+
+
 def run_cfg5(args, eks, torch, dist, world, rank, local):
-    """BASELINE configs[4]: basis-generation sweep only, 20 outer iterations of s blocks on the
-    384³ Laplacian from a seeded unit-norm random block (reading R27); value = outer it/s,
-    plus the GB/s of the sweep's algorithmic bytes."""
+    """BASELINE configs[4] (the bench headline): basis-generation sweep only, 20 outer iterations of
+    s blocks on the 384³ Laplacian from a seeded unit-norm random block (reading R27).  A step = one
+    eks_basis_sweep call (20·s blocks: chained SpMM + CGS2 + A-CholQR, every §8(a) row except the
+    x/r update, which cfg5 does not have); value = outer iterations/s."""
     N, t, s_ = args.cfg5_n, args.t or 16, args.s or 4
+    t_gen = time.perf_counter()
     A = ei.cfg5_operator(N)
+    gen_s = time.perf_counter() - t_gen
     n = A.n
     lo = (rank * (t // world)) * n // t
     hi = ((rank + 1) * (t // world)) * n // t
@@ -88,60 +149,167 @@ def run_cfg5(args, eks, torch, dist, world, rank, local):
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     solver = eks.Solver(None, rank=rank, nranks=world, device=local, nccl_id=uid)
+    t_set = time.perf_counter()
     solver.setup(n, lo, hi, slab.row_ptr, slab.col, slab.val)
-    del A, slab
+    setup_s = time.perf_counter() - t_set
     X0 = ei.cfg5_start_block_torch(n, t, "cuda")[lo:hi].contiguous()
     W = torch.empty_like(X0)
     nblocks = 20 * s_
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
     eks.eks_set_stream(solver.ctx, stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
     for _ in range(args.warmup):
         eks.eks_basis_sweep(solver.ctx, t, nblocks, X0, W)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    barrier()
+    # ---------------- timed region: K steps, CUDA events on the sweep's stream (inputs ≫ L2)
     clocks = ClockSampler(local)
     clocks.start()
-    ms, reps = 0.0, []
-    for _ in range(args.steps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    reps = []
+    barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        evs[k][0].record(stream)
         reps.append(eks.eks_basis_sweep(solver.ctx, t, nblocks, X0, W))
-        b.record(stream)
-        torch.cuda.synchronize()
-        ms += a.elapsed_time(b)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
     clk = clocks.stop()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    prof = eks.eks_basis_sweep(solver.ctx, t, nblocks, X0, W, profile=True)
-    pr = eks.eks_get_profile(solver.ctx)
+    value = 20 * args.steps / (ms * 1e-3)  # every rank builds its slab of the same 20 outer iterations
+    launches = sum(r["gpu_launches"] for r in reps)
+    # ---------------- per-kernel-class device time: one more sweep, CUDA events around every launch
+    prof_rep = eks.eks_basis_sweep(solver.ctx, t, nblocks, X0, W, profile=True)
+    agg = eks.eks_get_profile(solver.ctx)
     peaks = load_peaks()
-    outer = 20 * args.steps
-    model_bytes = reps[0]["model_bytes"] * world
+    classes = [c for c in agg["ms"] if c != "comm" and agg["ms"][c] > 0]
+    dom = max(classes, key=lambda c: agg["ms"][c])
+    roofline = roofline_of(agg, dom, peaks)
+    spmm_roof = roofline_of(agg, "spmm", peaks)
+    for rf in (roofline, spmm_roof):
+        attach_traffic(rf, f"ncu_traffic_cfg5_t{t}_r02.json")
+    share = {c: agg["ms"][c] / max(1e-9, sum(agg["ms"].values())) for c in agg["ms"]}
+    per_class = {c: roofline_of(agg, c, peaks) for c in classes}
+    model_bytes = reps[0]["model_bytes"]
+
+    # ---------------- e2e: the public C ABI with HOST buffers (pinned): eks_setup_csr of the host CSR
+    # slab + eks_basis_sweep(host X0 → host W_last) per step, wall clock (max over ranks)
+    e2e = None
+    if not args.no_e2e:
+        del W
+        torch.cuda.empty_cache()
+
+        def pinned(a):
+            tt = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+            tt.numpy()[...] = a
+            return tt
+        hrp, hcol, hval = pinned(slab.row_ptr), pinned(slab.col), pinned(slab.val)
+        hX0 = X0.cpu().pin_memory()
+        hW = torch.empty_like(hX0).pin_memory()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            solver.setup(n, lo, hi, hrp.numpy(), hcol.numpy(), hval.numpy())
+            eks.eks_set_stream(solver.ctx, stream.cuda_stream)
+            eks.eks_basis_sweep(solver.ctx, t, nblocks, hX0.numpy(), hW.numpy())
+        torch.cuda.synchronize()
+        barrier()
+        wall = time.perf_counter() - t0
+        wt = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        wall = float(wt.item())
+        h2d = hrp.numel() * 8 + hcol.numel() * 4 + hval.numel() * 8 + hX0.numel() * 8
+        e2e = {"value": 20 * args.steps / wall, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(hW.numel() * 8),
+               "note": "eks_setup_csr(pinned host CSR slab) + eks_basis_sweep(pinned host X0 -> pinned host W_last) "
+                       "per step through the C ABI, wall clock; host-side setup (validation, stencil plan) included",
+               "setup_s_first": setup_s}
+        del hrp, hcol, hval, hX0, hW
+    del X0
+    torch.cuda.empty_cache()
+
+    # ---------------- SpMM-block kernel at t = 8/16/32 on this operator (rank 0, N = 1)
+    sblock = None
+    if rank == 0 and world == 1 and not args.no_spmm_block:
+        sblock = spmm_block(eks, torch, peaks["hbm_gbs"], solver=solver, A=A)
+    solver.close()
+    del A, slab
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1; bounded, scaled sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, dt, ns = cfg5_oracle_sample(t, s_, N, args.cpu_planes)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"oracle basis sweep (definition mode, 1 thread of {os.cpu_count()}) of ONE outer "
+                         f"iteration (s={s_} blocks, t={t}) on the first {args.cpu_planes} z-planes of the {N}^3 grid "
+                         f"(n={ns}), {dt:.1f} s, scaled by n_full/n_sample = {n / ns:.0f} to outer it/s at full size"}
+
+    # ---------------- extra workloads (rank 0, N = 1): the cfg2 solve (BASELINE configs[1])
+    extras = {}
+    if rank == 0 and world == 1:
+        for w in [x for x in args.extra.split(",") if x]:
+            extras[w] = solve_summary(eks, torch, w, args)
+
     if rank == 0:
-        spmm_ms = pr["ms"]["spmm"] / max(1, pr["launches"]["spmm"])
-        spmm_b = pr["bytes"]["spmm"] / max(1, pr["launches"]["spmm"])
         line = {
-            "metric": METRIC, "value": outer / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg5: 3D 7-point Laplacian {N}^3 (n={n}), basis-generation sweep only "
-                                   f"(reading R27): 20 outer iterations x s={s_} blocks, t={t}, seeded unit-norm "
-                                   f"U[-1,1) start block", "n": n, "t": t, "s": s_,
-                       "parallelism": f"row-slabs x{world}", "l2": "inputs > L2 (3.6-14.5 GB blocks)"},
-            "sweep_gbs": model_bytes / (ms * 1e-3 / args.steps) / 1e9,
-            "sweep_frac": model_bytes / (ms * 1e-3 / args.steps) / 1e9 / peaks["hbm_gbs"],
-            "spmm_roofline": {"kernel": "spmm", "bound": "hbm", "achieved": spmm_b / (spmm_ms * 1e-3) / 1e9,
-                              "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                              "frac": spmm_b / (spmm_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
-                              "avg_launch_us": spmm_ms * 1e3, "bytes_per_launch": spmm_b},
-            "gpu_launches": sum(r["gpu_launches"] for r in reps), "clocks": clk,
-            "time_share": {c: pr["ms"][c] / max(1e-9, sum(pr["ms"].values())) for c in pr["ms"]},
+            "config": cfg5_config(N, n, t, s_, world),
+            "roofline": roofline, "spmm_roofline": spmm_roof, "spmm_block": sblock,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "sweep": {"model_bytes_per_step": model_bytes * world,
+                      "achieved_model_gbs": model_bytes * world / (ms * 1e-3 / args.steps) / 1e9,
+                      "frac_of_hbm": model_bytes / (ms * 1e-3 / args.steps) / 1e9 / peaks["hbm_gbs"],
+                      "breakdown": reps[0]["breakdown_block"]},
+            "time_share": share, "per_class": per_class, "extras": extras,
+            "host": {"operator_gen_s": gen_s, "setup_csr_s": setup_s},
         }
         print(json.dumps(line), flush=True)
-    solver.close()
+
+
+def slab_nnz(n, N):
+    return n + 6 * N * N * (N - 1)
+
+
+def solve_summary(eks, torch, name, args, steps=3, warmup=2):
+    """A full eks_solve of another BASELINE config (device inputs, graphs on for SRE-CG): outer it/s,
+    outer iterations, convergence — reported beside the headline, not part of it."""
+    p = workload(name)
+    S = eks.Solver(p.A)
+    stream = torch.cuda.Stream()
+    eks.eks_set_stream(S.ctx, stream.cuda_stream)
+    b = torch.from_numpy(p.b).cuda()
+    x = torch.zeros_like(b)
+    for _ in range(warmup):
+        eks.eks_solve_ex(S.ctx, p.method, p.s, p.t, p.tol, b, x, use_graph=True)
+    torch.cuda.synchronize()
+    tot_ms, tot_it, last = 0.0, 0, None
+    for _ in range(steps):
+        x.zero_()
+        a, bb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        st, last = eks.eks_solve_ex(S.ctx, p.method, p.s, p.t, p.tol, b, x, use_graph=True)
+        bb.record(stream)
+        torch.cuda.synchronize()
+        tot_ms += a.elapsed_time(bb)
+        tot_it += last["outer_iters"]
+    S.close()
+    return {"workload": f"{p.name}: {p.note}; s-step {p.method}, s={p.s}, t={p.t}, tol={p.tol:g}",
+            "outer_it_per_s": tot_it / (tot_ms * 1e-3), "outer_iters": last["outer_iters"],
+            "converged": last["converged"], "true_relres": last["true_relres"], "status": int(st),
+            "ms_per_solve": tot_ms / steps, "steps": steps, "warmup": warmup}
 
 
 def load_peaks():
@@ -240,10 +408,47 @@ def problem_of(args):
     return p
 
 
+def cfg5_config(N, n, t, s_, world):
+    return {"workload": f"cfg5 (BASELINE configs[4]): 3D 7-point Laplacian {N}^3 (n={n}, nnz={slab_nnz(n, N)}), "
+                        f"basis-generation sweep only (reading R27): 20 outer iterations x s={s_} blocks, "
+                        f"t={t}, window 2t, seeded unit-norm U[-1,1) start block",
+            "n": n, "t": t, "s": s_, "outer_iters_per_step": 20,
+            "parallelism": f"row-slabs x{world} (t/N domains per GPU)",
+            "l2": "inputs > L2: every block is 8*n*t = %.2f GB, L2 = 126 MB; not flushed" % (8 * n * t / 1e9)}
+
+
+def run_reference_cfg5(args):
+    """Reference arm for the cfg5 headline: the oracle as it stands (one thread), each step one
+    bounded sample (one outer iteration on the first --cpu-planes z-planes), scaled to full n."""
+    N, t, s_ = args.cfg5_n, args.t or 16, args.s or 4
+    for _ in range(args.warmup):
+        cfg5_oracle_sample(t, s_, N, args.cpu_planes)
+    tot_dt, ns = 0.0, 0
+    for _ in range(args.steps):
+        _, dt, ns = cfg5_oracle_sample(t, s_, N, args.cpu_planes)
+        tot_dt += dt
+    n = N ** 3
+    value = args.steps / (tot_dt * n / ns)  # outer it/s at full size
+    sample = (f"oracle basis sweep (definition mode, 1 thread of {os.cpu_count()}) of ONE outer iteration "
+              f"(s={s_} blocks, t={t}) per step on the first {args.cpu_planes} z-planes of the {N}^3 grid (n={ns}), "
+              f"scaled by n_full/n_sample = {n / ns:.0f}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_dt * (n / ns) / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": cfg5_config(N, n, t, s_, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if args.workload == "cfg5":
+        return run_reference_cfg5(args)
     p = problem_of(args)
     per_step = args.ref_iters
     for _ in range(args.warmup):
@@ -289,7 +494,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="eks", choices=["eks", "reference"])
-    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--workload", default="cfg5", help="cfg5 (headline, BASELINE configs[4]) | cfg2 | cfg3 | cfg4 | ...")
     ap.add_argument("--ref-iters", type=int, default=1, help="oracle outer iterations per reference step")
     ap.add_argument("--cpu-iters", type=int, default=2, help="oracle outer iterations for cpu_baseline")
     ap.add_argument("--no-cpu", action="store_true")
@@ -308,6 +513,8 @@ def main():
                     help="split-preconditioned Alg 8-10 with block Jacobi of this many domains (64 in the paper)")
     ap.add_argument("--precond-kind", default="ic0", choices=["ic0", "chol"], help="IC(0) (Table 5) or Cholesky (Table 6)")
     ap.add_argument("--cfg5-n", type=int, default=384, help="cfg5 grid size (384 = BASELINE configs[4])")
+    ap.add_argument("--cpu-planes", type=int, default=2, help="cfg5 cpu_baseline: z-planes of the oracle sample")
+    ap.add_argument("--extra", default="cfg2", help="cfg5: comma-separated solve workloads reported beside the headline")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

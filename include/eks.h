@@ -104,13 +104,19 @@ typedef struct {
                              IC(0) M of eks_setup_precond: seed M⁻¹[T(r)], powers M⁻¹A·W.
                              With a CA method: seed M⁻¹[T(r)] and monomial powers M⁻¹A·W.
                              Restructured: EKS_ERR_INVALID_ARG */
-  int reserved[4];
+  int aq_cache;           /* SRE-CG2 / MSDO-CG (full basis Q): 0 = auto (= off), 1 = keep A·Q
+                             for every block (C = (AQ)ᵀZ, fused CGS sweeps; 2× the memory per outer
+                             iteration), 2 = off: store Q only, C = Qᵀ(A·Z) with two more SpMMs per block
+                             (reading R24).  report.max_outer_fit = outer iterations the device holds */
+  int reserved[3];
 } eks_options;
 
 /* Per-kernel-class device time accumulated while options.profile == 1. */
 typedef enum {
   EKS_K_SPLIT = 0, EKS_K_SPMM = 1, EKS_K_COEF = 2, EKS_K_UPDATE = 3, EKS_K_REDUCE = 4,
-  EKS_K_CHOL = 5, EKS_K_APPLY = 6, EKS_K_COMM = 7, EKS_K_OTHER = 8, EKS_K_NCLASSES = 9
+  EKS_K_CHOL = 5, EKS_K_APPLY = 6, EKS_K_COMM = 7, EKS_K_OTHER = 8,
+  EKS_K_UPCOEF = 9,  /* the fused CGS sweep Z1 = Z − Q·C1 with C2 = (AQ)ᵀZ1 (EKS_K_UPDATE: Z2 = Z1 − Q·C2) */
+  EKS_K_NCLASSES = 10
 } eks_kclass;
 typedef struct {
   double ms[EKS_K_NCLASSES];      /* summed event time per class */
@@ -184,6 +190,17 @@ eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks, const double* X0, d
  * columns are all local, multiplied while the halo is in flight). */
 eks_status eks_plan_halo(int rank, int nranks, const int64_t* ranges, const int64_t* row_ptr,
                          const int32_t* col, int32_t* ext_col, int64_t* need, int64_t* geom);
+
+/* Host-only stencil plan that eks_setup_csr builds on every rank for the plane-marching SpMM
+ * (exported so the multi-rank ghost-plane logic can be tested on CPUs).  Rows [row_begin, row_end)
+ * of a 5-point (2D) / 7-point (3D) lexicographic-grid operator in CSR with GLOBAL columns; halo_before
+ * and halo_after = the ghost rows eks_plan_halo gives this slab.  geom[6] = {nx, ny, nz_local, w,
+ * gb, ga} (gb/ga: ghost plane before/after the local planes), all 0 when the matrix is not
+ * stencil-structured or the slab is not whole planes with one-plane ghosts.  sv (may be NULL):
+ * (row_end-row_begin) × ((w+1)&~1) stencil values per row in ascending column order (slots -plane,
+ * -nx, -1, 0, +1, +nx, +plane; 0 where a neighbour is absent). */
+eks_status eks_plan_grid(int64_t row_begin, int64_t row_end, const int64_t* row_ptr, const int32_t* col,
+                         const double* vals, int64_t halo_before, int64_t halo_after, int64_t* geom, double* sv);
 
 /* Kernel-class timings of the last solve/sweep run with opt.profile = 1. */
 eks_status eks_get_profile(const eks_ctx* ctx, eks_profile* out);

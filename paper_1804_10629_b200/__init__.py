@@ -26,7 +26,7 @@ STATUS = {0: "EKS_OK", 1: "EKS_ERR_INVALID_ARG", 2: "EKS_ERR_STATE", 3: "EKS_ERR
           5: "EKS_ERR_CUDA", 6: "EKS_ERR_NCCL", 7: "EKS_ERR_BREAKDOWN", 8: "EKS_ERR_MAXITER",
           9: "EKS_ERR_NONFINITE"}
 EKS_OK, EKS_ERR_BREAKDOWN, EKS_ERR_MAXITER, EKS_ERR_OOM = 0, 7, 8, 4
-KCLASSES = ["split", "spmm", "coef", "update", "reduce", "chol", "apply", "comm", "other"]
+KCLASSES = ["split", "spmm", "coef", "update", "reduce", "chol", "apply", "comm", "other", "upcoef"]
 
 
 class EksError(RuntimeError):
@@ -48,13 +48,13 @@ class _Report(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("max_outer", C.c_int), ("use_graph", C.c_int), ("profile", C.c_int), ("arnoldi", C.c_int),
-                ("ortho", C.c_int), ("restructured", C.c_int), ("precond", C.c_int),
-                ("reserved", C.c_int * 4)]
+                ("ortho", C.c_int), ("restructured", C.c_int), ("precond", C.c_int), ("aq_cache", C.c_int),
+                ("reserved", C.c_int * 3)]
 
 
 class _Profile(C.Structure):
-    _fields_ = [("ms", C.c_double * 9), ("launches", C.c_longlong * 9), ("bytes", C.c_double * 9),
-                ("flops", C.c_double * 9)]
+    _fields_ = [("ms", C.c_double * 10), ("launches", C.c_longlong * 10), ("bytes", C.c_double * 10),
+                ("flops", C.c_double * 10)]
 
 
 _lib = None
@@ -87,6 +87,7 @@ def lib():
             "eks_k_time_spmm": [vp, i32, vp, vp, vp, i32, i32, C.POINTER(d)],
             "eks_plan_halo": [i32, i32, vp, vp, vp, vp, vp, vp],
             "eks_k_last_basis": [vp, i32, vp, vp],
+            "eks_plan_grid": [i64, i64, vp, vp, vp, i64, i64, vp, vp],
             "eks_k_last_residual": [vp, vp],
         }
         for name, args in sigs.items():
@@ -102,7 +103,7 @@ def lib():
 EXPORTED = ["eks_get_unique_id", "eks_create", "eks_set_stream", "eks_setup_csr", "eks_setup_precond", "eks_solve", "eks_solve_ex",
             "eks_basis_sweep", "eks_get_profile", "eks_destroy", "eks_error_string", "eks_k_split", "eks_k_spmm",
             "eks_k_cgs2", "eks_k_acholqr", "eks_k_chol", "eks_k_time_spmm", "eks_plan_halo", "eks_k_last_basis",
-            "eks_k_last_residual"]
+            "eks_k_last_residual", "eks_plan_grid"]
 
 
 def eks_plan_halo(rank: int, nranks: int, ranges, row_ptr, col):
@@ -118,6 +119,23 @@ def eks_plan_halo(rank: int, nranks: int, ranges, row_ptr, col):
     _check(None, st)
     return ext, need.reshape(nranks, 2), dict(halo_before=int(geom[0]), halo_after=int(geom[1]),
                                               interior_lo=int(geom[2]), interior_hi=int(geom[3]))
+
+
+def eks_plan_grid(row_begin: int, row_end: int, row_ptr, col, val, halo_before: int, halo_after: int):
+    """Host-only stencil plan of a slab (no device): (geom dict, sv (rows × VS) or None)."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cl = np.ascontiguousarray(col, np.int32)
+    vl = np.ascontiguousarray(val, np.float64)
+    geom = np.zeros(6, np.int64)
+    _check(None, lib().eks_plan_grid(int(row_begin), int(row_end), rp.ctypes.data, cl.ctypes.data, vl.ctypes.data,
+                                     int(halo_before), int(halo_after), geom.ctypes.data, None))
+    g = dict(zip(["nx", "ny", "nz", "w", "gb", "ga"], [int(v) for v in geom]))
+    if g["w"] == 0:
+        return g, None
+    sv = np.zeros((row_end - row_begin, (g["w"] + 1) & ~1))
+    _check(None, lib().eks_plan_grid(int(row_begin), int(row_end), rp.ctypes.data, cl.ctypes.data, vl.ctypes.data,
+                                     int(halo_before), int(halo_after), geom.ctypes.data, sv.ctypes.data))
+    return g, sv
 
 
 def _order_after_torch():
@@ -208,15 +226,18 @@ def _report(rep: _Report):
 ORTHO = {"acholqr": 0, "pre-cholqr": 1}
 
 
+AQ_CACHE = {"auto": 0, "on": 1, "off": 2}
+
+
 def eks_solve_ex(ctx, method, s, t, tol, b, x, max_outer=0, profile=False, raise_on=(5, 6, 1, 2, 3), arnoldi=0,
-                 ortho="acholqr", restructured=False, precond=False, use_graph=False):
+                 ortho="acholqr", restructured=False, precond=False, use_graph=False, aq_cache="auto"):
     """Returns (status, report dict).  x holds x0 on entry and the solution on exit.
     arnoldi (CA methods only): 7 = modified CA-Arnoldi (default), 5 = CA-Arnoldi.
     ortho: "acholqr" (default) or "pre-cholqr"; restructured: Alg 2 / Alg 1 (SRE-CG / SRE-CG2)."""
     m = METHODS[method] if isinstance(method, str) else int(method)
     where = _where(b, x)
     opt = _Options(int(max_outer), int(bool(use_graph)), int(bool(profile)), int(arnoldi), ORTHO[ortho],
-                   int(bool(restructured)), int(bool(precond)))
+                   int(bool(restructured)), int(bool(precond)), AQ_CACHE[aq_cache])
     rep = _Report()
     st = lib().eks_solve_ex(ctx, m, int(s), int(t), float(tol), _ptr(b, np.float64), _ptr(x, np.float64), where,
                             C.byref(opt), C.byref(rep))
@@ -332,7 +353,7 @@ class Solver:
         eks_setup_precond(self.ctx, ndomains, *self._csr, kind=kind)
 
     def solve(self, b, method="sre-cg", s=1, t=1, tol=1e-8, x0=None, max_outer=0, profile=False, arnoldi=0,
-              ortho="acholqr", restructured=False, precond=False, use_graph=False):
+              ortho="acholqr", restructured=False, precond=False, use_graph=False, aq_cache="auto"):
         if isinstance(b, np.ndarray):
             b = np.ascontiguousarray(b, np.float64)
             x = np.zeros_like(b) if x0 is None else np.ascontiguousarray(x0, np.float64).copy()
@@ -340,7 +361,7 @@ class Solver:
             x = b.new_zeros(b.shape) if x0 is None else x0.clone()
         st, rep = eks_solve_ex(self.ctx, method, s, t, tol, b, x, max_outer=max_outer, profile=profile,
                                arnoldi=arnoldi, ortho=ortho, restructured=restructured, precond=precond,
-                               use_graph=use_graph)
+                               use_graph=use_graph, aq_cache=aq_cache)
         rep["status"] = st
         rep["x"] = x
         return rep

@@ -38,6 +38,7 @@ struct Send { int peer; int64_t lo, hi; };           // my global rows [lo,hi) â
 struct Block {
   double* base = nullptr;  // ext allocation (ghost rows included) or local allocation
   double* loc = nullptr;   // first local row
+  bool owned = true;       // false: aliases another Block's storage (store-Q-only AW ring)
 };
 
 struct ProfRec { int cls; cudaEvent_t a, b; };
@@ -116,6 +117,11 @@ struct eks_ctx {
   // workspace, keyed by t
   int ws_t = 0;
   std::vector<Block> Wpool, AWpool;  // Wpool ext layout, AWpool local
+  // store-Q-only mode of the full-basis methods (eks_options.aq_cache, reading R24): AÂ·Q is not kept;
+  // AWpool entries alias a ring of two local blocks (AÂ·W of the last two blocks), CGS2 takes
+  // C = Qáµ€(AÂ·Z) with explicit SpMMs of Z and Z1 (scratch: Ze ext, Ysc local)
+  bool aq_off = false, last_aq_off = false;
+  Block AWring[2], Ze, Ysc;
   Block Zs, Z1, xv, tmpv;            // xv: ext vector
   double *b = nullptr, *r = nullptr, *rnew = nullptr, *dx = nullptr;
   double* part = nullptr;
@@ -260,11 +266,15 @@ void free_workspace(eks_ctx* c) {
     *p = nullptr;
   }
   c->ca_cap = 0;
-  for (auto& b : c->Wpool) dfree(b.base);
-  for (auto& b : c->AWpool) dfree(b.base);
+  for (auto& b : c->Wpool) if (b.owned) dfree(b.base);
+  for (auto& b : c->AWpool) if (b.owned) dfree(b.base);
   c->Wpool.clear();
   c->AWpool.clear();
-  for (Block* b : {&c->Zs, &c->Z1, &c->xv, &c->tmpv, &c->Zp, &c->Zq1, &c->Zq2}) { dfree(b->base); *b = Block{}; }
+  for (Block* b : {&c->Zs, &c->Z1, &c->xv, &c->tmpv, &c->Zp, &c->Zq1, &c->Zq2, &c->AWring[0], &c->AWring[1], &c->Ze,
+                   &c->Ysc}) {
+    dfree(b->base);
+    *b = Block{};
+  }
   for (double** p : {&c->b, &c->r, &c->rnew, &c->dx, &c->part, &c->C1, &c->C2, &c->Bg, &c->Rm, &c->Rinv,
                      &c->alpha, &c->scal}) { dfree(*p); *p = nullptr; }
   dfree(c->flag);
@@ -371,8 +381,20 @@ eks_status halo_start(eks_ctx* ctx, const Block& X, int t) {
   return EKS_OK;
 }
 
-// Y = A X with halo exchange overlapped with the interior rows.
+int spmm_path_for(const eks_ctx* ctx, int t);
+
+// Y = A X.  Stencil operators (t â‰¥ 8): the plane-marching kernel without its Gram epilogue, after the
+// ghost-plane exchange.  Otherwise CSR with the halo exchange overlapped with the interior rows.
 eks_status spmm(eks_ctx* ctx, const Block& X, double* Y, int t) {
+  if (eks::sweep_supported(t) && spmm_path_for(ctx, t) == 4) {
+    ST(halo_start(ctx, X, t));
+    if (ctx->nranks > 1) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+    account(ctx, EKS_K_SPMM, 8.0 * ctx->gplan.w * ctx->n + 16.0 * ctx->n * t, 2.0 * ctx->nnz * t);
+    KScope k(ctx, EKS_K_SPMM);
+    CK(eks::launch_spmm_grid(ctx->stream, t, ctx->gplan, X.loc, Y, nullptr, nullptr, ctx->nblk, eks::Tail{},
+                             eks::CholArgs{}, false));
+    return EKS_OK;
+  }
   ST(halo_start(ctx, X, t));
   account(ctx, EKS_K_SPMM, 12.0 * ctx->nnz + 4.0 * (ctx->n + 1) + 16.0 * ctx->n * t, 2.0 * ctx->nnz * t);
   if (ctx->nranks == 1) {
@@ -471,10 +493,10 @@ eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, cons
   ST(ensure_part(ctx, stride * ctx->nblk));
   // algorithmic bytes: read Z, Q_j, AQ_j (once each â€” for SRE-CG Z is AQ_last itself), write Z1
   const bool alias = nq > 0 && AQ[nq - 1] == Z;
-  account(ctx, EKS_K_UPDATE, 8.0 * ctx->n * ((double)2 * nq * t + 2.0 * t - (alias ? t : 0)),
+  account(ctx, EKS_K_UPCOEF, 8.0 * ctx->n * ((double)2 * nq * t + 2.0 * t - (alias ? t : 0)),
           4.0 * ctx->n * t * t * nq);
   {
-    KScope ks(ctx, EKS_K_UPDATE);  // C2 partials reduced by the sweep's last CTAs
+    KScope ks(ctx, EKS_K_UPCOEF);  // C2 partials reduced by the sweep's last CTAs
     CK(eks::launch_sweep(ctx->stream, t, nq, nq, false, ctx->n, Z, Z1, P, C1, nullptr, ctx->part, ctx->nblk,
                          tail(ctx, 0, C2, stride)));
   }
@@ -486,7 +508,7 @@ eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, cons
 // fastest for t â‰¤ 32, then ELL; the segment kernel for t = 64.  EKS_SPMM_PATH=grid|seg|ell|csr
 // forces one for A/B measurements.
 int spmm_path_for(const eks_ctx* ctx, int t) {
-  const bool grid = ctx->grid_ok && ctx->nranks == 1 && eks::spmm_grid_fits(t, ctx->gplan);
+  const bool grid = ctx->grid_ok && eks::spmm_grid_fits(t, ctx->gplan);
   if (grid && (ctx->spmm_path == 4 || ctx->spmm_path == 0)) return 4;
   const bool seg = ctx->seg_ok && eks::spmm_seg_fits(t, ctx->ell_w, ctx->seg.cap);
   if (seg && (ctx->spmm_path == 3 || (ctx->spmm_path == 0 && t == 64))) return 0;
@@ -501,20 +523,28 @@ int spmm_path_for(const eks_ctx* ctx, int t) {
 eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const double* r, double* out,
                      const eks::CholArgs* ch = nullptr, bool ar = true) {
   ctx->chol_fused = false;
-  if (ctx->nranks != 1 || !eks::sweep_supported(t)) {
+  const bool grid_multi = ctx->nranks != 1 && eks::sweep_supported(t) && spmm_path_for(ctx, t) == 4;
+  if ((ctx->nranks != 1 && !grid_multi) || !eks::sweep_supported(t)) {
     ST(spmm(ctx, X, Y, t));
     const double* L[1] = {X.loc};
     return tn_reduce(ctx, t, 1, L, Y, r, out, ar);
   }
+  if (grid_multi) {  // ghost planes first (the persistent kernel occupies every SM: no overlap)
+    ST(halo_start(ctx, X, t));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+  }
   const size_t stride = eks::sweep_part_stride(t, 1, true);
   ST(ensure_part(ctx, stride * ctx->nblk));
-  account(ctx, EKS_K_SPMM, 12.0 * ctx->nnz + 4.0 * (ctx->n + 1) + 16.0 * ctx->n * t, 2.0 * ctx->nnz * t);
-  account(ctx, EKS_K_COEF, r ? 8.0 * ctx->n : 0.0, 2.0 * ctx->n * t * (t + 1));  // epilogue: only r is extra traffic
   eks::CholArgs c{};
   const int path = spmm_path_for(ctx, t);
+  // algorithmic bytes of the representation of A the kernel streams: CSR 12Â·nnz + 4(n+1); the
+  // plane-marching kernel's stencil values 8Â·w per row (no indices); + X read, Y written, r read
+  const double abytes = path == 4 ? 8.0 * ctx->gplan.w * ctx->n : 12.0 * ctx->nnz + 4.0 * (ctx->n + 1);
+  account(ctx, EKS_K_SPMM, abytes + 16.0 * ctx->n * t + (r ? 8.0 * ctx->n : 0.0), 2.0 * ctx->nnz * t);
+  account(ctx, EKS_K_COEF, 0.0, 2.0 * ctx->n * t * (t + 1));  // the Gram epilogue: flops only
   // EKS_CHOL=1: the SpMM kernel's last CTA factors B (measured slower than the separate one-warp
   // launch the solve uses by default: 1894 vs 2085 outer it/s on cfg2)
-  if (ch && ctx->chol_mode == 1 &&
+  if (ch && ctx->chol_mode == 1 && ctx->nranks == 1 &&
       ((path == 4 && eks::spmm_grid_fused_chol(t)) || (path != 4 && eks::spmm_gram_fused_chol(t)))) {
     c = *ch;
     c.on = 1;
@@ -522,7 +552,7 @@ eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const doubl
   {
     KScope k(ctx, EKS_K_SPMM);
     if (path == 4)
-      CK(eks::launch_spmm_grid(ctx->stream, t, ctx->gplan, X.base, Y, r, ctx->part, ctx->nblk,
+      CK(eks::launch_spmm_grid(ctx->stream, t, ctx->gplan, X.loc, Y, r, ctx->part, ctx->nblk,
                                tail(ctx, 2, out, stride), c));
     else if (path == 0)
       CK(eks::launch_spmm_seg(ctx->stream, t, ctx->n, ctx->seg, ctx->ell_w, X.base, Y, r, ctx->part, ctx->nblk,
@@ -538,13 +568,29 @@ eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const doubl
                                c));
   }
   ctx->chol_fused = c.on != 0;
-  return EKS_OK;
+  return (ar && ctx->nranks > 1) ? allreduce(ctx, out, stride) : EKS_OK;
 }
 
 // CGS2 of Z against the window (Q, AQ): two passes of C = (AQ)áµ€Z, Z -= Q C (reading R3/R24).
 eks_status cgs2(eks_ctx* ctx, int t, const std::vector<const double*>& Q, const std::vector<const double*>& AQ,
                 const double* Z, double* Zout) {
   const int nq = (int)Q.size();
+  if (AQ.empty() && nq > 0) {
+    // store-Q-only (reading R24): twice { C = Qáµ€(AÂ·Z) ; Z = Z âˆ’ QÂ·C } with explicit SpMMs â€” the
+    // oracle's definition-mode algebra; Z and Z1 pass through the ext-layout scratch Ze (ghost rows)
+    ST(alloc_block(ctx, &ctx->Ze, t, true));
+    ST(alloc_block(ctx, &ctx->Ysc, t, false));
+    ST(ensure_C(ctx, (size_t)nq * t * t));
+    ctx->c1_ready = false;
+    if (Z != ctx->Ze.loc)
+      CK(cudaMemcpyAsync(ctx->Ze.loc, Z, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
+    ST(spmm(ctx, ctx->Ze, ctx->Ysc.loc, t));
+    ST(tn_reduce(ctx, t, nq, Q.data(), ctx->Ysc.loc, nullptr, ctx->C1));  // C1 = Qáµ€(AÂ·Z)
+    ST(ts_update(ctx, t, nq, Q.data(), ctx->C1, ctx->Ze.loc, ctx->Ze.loc));  // Z1 = Z âˆ’ Q C1 (in place)
+    ST(spmm(ctx, ctx->Ze, ctx->Ysc.loc, t));
+    ST(tn_reduce(ctx, t, nq, Q.data(), ctx->Ysc.loc, nullptr, ctx->C2));  // C2 = Qáµ€(AÂ·Z1)
+    return ts_update(ctx, t, nq, Q.data(), ctx->C2, ctx->Ze.loc, Zout);      // Z2 = Z1 âˆ’ Q C2
+  }
   if (!ctx->c1_ready) {
     ST(ensure_C(ctx, (size_t)nq * t * t));
     ST(tn_reduce(ctx, t, nq, AQ.data(), Z, nullptr, ctx->C1));  // C1 = (AQ)áµ€ Z
@@ -604,10 +650,32 @@ eks_status reduce_scalar(eks_ctx* ctx, double* slot) {
   return allreduce(ctx, slot, 1);
 }
 
+// Wait for the stream.  With NCCL (several ranks) the wait polls ncclCommGetAsyncError: a failed or
+// vanished peer makes the collective on this rank fail with EKS_ERR_NCCL (the communicator is aborted,
+// so the pending kernels return) instead of hanging the solve.
+eks_status stream_wait(eks_ctx* ctx) {
+  if (ctx->nranks == 1 || !ctx->comm) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    return EKS_OK;
+  }
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(ctx->stream);
+    if (q == cudaSuccess) return EKS_OK;
+    if (q != cudaErrorNotReady) CK(q);
+    ncclResult_t ae = ncclSuccess;
+    if (ncclCommGetAsyncError(ctx->comm, &ae) != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress)) {
+      ncclCommAbort(ctx->comm);
+      ctx->comm = nullptr;
+      return fail(ctx, EKS_ERR_NCCL, "NCCL asynchronous error: %s (communicator aborted)", ncclGetErrorString(ae));
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
 eks_status sync_scalars(eks_ctx* ctx, int count) {
   CK(cudaMemcpyAsync(ctx->h_scal, ctx->scal, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(ctx->h_flag + 1, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+  ST(stream_wait(ctx));
   if (ctx->prof_on) prof_harvest(ctx);
   return EKS_OK;
 }
@@ -615,6 +683,7 @@ eks_status sync_scalars(eks_ctx* ctx, int count) {
 eks_status check_ready(eks_ctx* ctx) {
   if (!ctx) return EKS_ERR_INVALID_ARG;
   if (!ctx->have_matrix) return fail(ctx, EKS_ERR_STATE, "eks_setup_csr has not been called");
+  if (ctx->nranks > 1 && !ctx->comm) return fail(ctx, EKS_ERR_NCCL, "the NCCL communicator was aborted");
   CK(cudaSetDevice(ctx->device));
   return EKS_OK;
 }
@@ -639,8 +708,20 @@ eks_status slot(eks_ctx* ctx, int t, int idx, Block** W, Block** AW) {
   }
   eks_status s1 = alloc_block(ctx, &ctx->Wpool[idx], t, true);
   if (s1 != EKS_OK) return s1;
-  s1 = alloc_block(ctx, &ctx->AWpool[idx], t, false);
-  if (s1 != EKS_OK) return s1;
+  if (ctx->aq_off) {  // store-Q-only: AÂ·W lives in a ring of two (the next block's Z and the update)
+    Block& rg = ctx->AWring[idx & 1];
+    s1 = alloc_block(ctx, &rg, t, false);
+    if (s1 != EKS_OK) return s1;
+    Block& aw = ctx->AWpool[idx];
+    if (aw.owned) dfree(aw.base);
+    aw.base = rg.base;
+    aw.loc = rg.loc;
+    aw.owned = false;
+  } else {
+    if (!ctx->AWpool[idx].owned) ctx->AWpool[idx] = Block{};  // was a ring alias of a store-Q-only solve
+    s1 = alloc_block(ctx, &ctx->AWpool[idx], t, false);
+    if (s1 != EKS_OK) return s1;
+  }
   *W = &ctx->Wpool[idx];
   *AW = &ctx->AWpool[idx];
   return EKS_OK;
@@ -658,7 +739,7 @@ Window window_for(eks_ctx* ctx, int method, int nblocks, int ring) {
   for (int j = first; j < nblocks; ++j) {
     int idx = ring ? j % ring : j;
     w.Q.push_back(ctx->Wpool[idx].loc);
-    w.AQ.push_back(ctx->AWpool[idx].loc);
+    if (!ctx->aq_off) w.AQ.push_back(ctx->AWpool[idx].loc);  // store-Q-only: AQ empty
   }
   return w;
 }
@@ -1156,64 +1237,104 @@ eks_status build_seg_plan(eks_ctx* ctx, int64_t n, const std::vector<int64_t>& r
   return EKS_OK;
 }
 
-// Stencil structure for the plane-marching SpMM (eks_grid.cu): the distinct positive column
-// offsets must be {1, b} (2D: nx = b, planes are x-lines) or {1, b, c} with b | c (3D: nx = b,
-// ny = c/b), mirrored by the negative ones, with n a multiple of the plane size, and no Â±1
-// (Â±nx) entry may cross an x-line (y-plane) boundary.  Values are stored per row in ascending
-// offset order, 0 in absent slots.  Otherwise nothing is built (the ELL kernel runs).
-eks_status build_grid_plan(eks_ctx* ctx, int64_t n, const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
-                           const std::vector<double>& val) {
+// Host loops over the rows of a (possibly 56M-row) slab on all host threads: f(lo, hi) per chunk.
+template <typename F>
+void parallel_rows(int64_t n, F&& f) {
+  const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), (int)(n / 65536) + 1));
+  if (nt == 1) {
+    f((int64_t)0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int k = 0; k < nt; ++k) th.emplace_back([&, k] { f(n * k / nt, n * (k + 1) / nt); });
+  for (auto& x : th) x.join();
+}
+
+// Stencil structure for the plane-marching SpMM (eks_grid.cu): the distinct positive column offsets
+// must be {1, b} (2D: nx = b, planes are x-lines) or {1, b, c} with b | c (3D: nx = b, ny = c/b),
+// mirrored by the negative ones, and no Â±1 (Â±nx) entry may cross an x-line (y-plane) boundary.
+// Several ranks: the slab [row_begin, row_begin + n) must be whole planes and the ghost rows of the
+// extended layout exactly the neighbouring planes (halo_before/after âˆˆ {0, plane}); columns are GLOBAL.
+// Values are stored per row in ascending offset order, 0 in absent slots (VS = (w+1)&~1 per row).
+// geom = {nx, ny, nz, w, gb, ga}; false (nothing built, the ELL/CSR kernels run) otherwise.
+bool grid_plan_host(int64_t n, const int64_t* rp, const int32_t* col, const double* val, int64_t row_begin,
+                    int64_t halo_before, int64_t halo_after, int64_t geom[6], std::vector<double>& sv) {
   int64_t pos[3] = {0, 0, 0};
   int np = 0;
-  bool neg_ok = true;
   for (int64_t i = 0; i < n && np <= 3; ++i)
     for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-      const int64_t o = (int64_t)col[p] - i;
+      const int64_t o = (int64_t)col[p] - (row_begin + i);
       if (o <= 0) continue;
       int k = 0;
       while (k < np && pos[k] != o) ++k;
       if (k == np) {
-        if (np == 3) return EKS_OK;
+        if (np == 3) return false;
         pos[np++] = o;
       }
     }
   for (int a2 = 1; a2 < np; ++a2)  // np â‰¤ 3: insertion sort (std::sort trips -Warray-bounds here)
     for (int b2 = a2; b2 > 0 && pos[b2 - 1] > pos[b2]; --b2) std::swap(pos[b2 - 1], pos[b2]);
-  if (np < 2 || pos[0] != 1) return EKS_OK;
+  if (np < 2 || pos[0] != 1) return false;
   const int64_t b = pos[1], c = np == 3 ? pos[2] : 0;
   int64_t nx = b, ny = 1, plane = b;
   if (np == 3) {
-    if (c % b) return EKS_OK;
+    if (c % b) return false;
     ny = c / b;
     plane = c;
   }
-  if (n % plane) return EKS_OK;
+  if (n % plane || row_begin % plane) return false;
+  if ((halo_before != 0 && halo_before != plane) || (halo_after != 0 && halo_after != plane)) return false;
   const int64_t nz = n / plane;
-  if (nx >= INT32_MAX || ny >= INT32_MAX || nz >= INT32_MAX) return EKS_OK;
+  if (nx >= INT32_MAX || ny >= INT32_MAX || nz >= INT32_MAX) return false;
   const int w = np == 3 ? 7 : 5, VS = (w + 1) & ~1;
-  const int64_t offs[7] = {-c, -b, -1, 0, 1, b, c};
-  const int64_t offs2[5] = {-b, -1, 0, 1, b};
-  std::vector<double> sv((size_t)n * VS, 0.0);
-  for (int64_t i = 0; i < n && neg_ok; ++i) {
-    const int64_t x = i % nx, y = (i / nx) % ny;
-    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-      const int64_t o = (int64_t)col[p] - i;
-      int k = -1;
-      for (int q = 0; q < w; ++q)
-        if ((w == 7 ? offs[q] : offs2[q]) == o) k = q;
-      if (k < 0) { neg_ok = false; break; }
-      if ((o == 1 && x + 1 >= nx) || (o == -1 && x == 0)) { neg_ok = false; break; }
-      if (w == 7 && ((o == b && y + 1 >= ny) || (o == -b && y == 0))) { neg_ok = false; break; }
-      sv[(size_t)i * VS + k] = val[p];
+  const int64_t offs7[7] = {-c, -b, -1, 0, 1, b, c};
+  const int64_t offs5[5] = {-b, -1, 0, 1, b};
+  const int64_t* offs = w == 7 ? offs7 : offs5;
+  sv.assign((size_t)n * VS, 0.0);
+  std::atomic<bool> ok{true};
+  parallel_rows(n, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi && ok.load(std::memory_order_relaxed); ++i) {
+      const int64_t x = (row_begin + i) % nx, y = ((row_begin + i) / nx) % ny;
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int64_t o = (int64_t)col[p] - (row_begin + i);
+        int k = -1;
+        for (int q = 0; q < w; ++q)
+          if (offs[q] == o) k = q;
+        const bool bad = k < 0 || (o == 1 && x + 1 >= nx) || (o == -1 && x == 0) ||
+                         (w == 7 && ((o == b && y + 1 >= ny) || (o == -b && y == 0)));
+        if (bad) {
+          ok = false;
+          return;
+        }
+        sv[(size_t)i * VS + k] = val[p];
+      }
     }
-  }
-  if (!neg_ok) return EKS_OK;
+  });
+  if (!ok) return false;
+  geom[0] = nx;
+  geom[1] = ny;
+  geom[2] = nz;
+  geom[3] = w;
+  geom[4] = halo_before ? 1 : 0;
+  geom[5] = halo_after ? 1 : 0;
+  return true;
+}
+
+eks_status build_grid_plan(eks_ctx* ctx, int64_t n, const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
+                           const std::vector<double>& val, int64_t row_begin, int64_t halo_before,
+                           int64_t halo_after) {
+  int64_t g[6];
+  std::vector<double> sv;
+  if (!grid_plan_host(n, rp.data(), col.data(), val.data(), row_begin, halo_before, halo_after, g, sv))
+    return EKS_OK;
   CK(cudaMalloc((void**)&ctx->d_sv, sizeof(double) * sv.size()));
   CK(cudaMemcpy(ctx->d_sv, sv.data(), sizeof(double) * sv.size(), cudaMemcpyHostToDevice));
-  ctx->gplan.nx = (int)nx;
-  ctx->gplan.ny = (int)ny;
-  ctx->gplan.nz = (int)nz;
-  ctx->gplan.w = w;
+  ctx->gplan.nx = (int)g[0];
+  ctx->gplan.ny = (int)g[1];
+  ctx->gplan.nz = (int)g[2];
+  ctx->gplan.w = (int)g[3];
+  ctx->gplan.gb = (int)g[4];
+  ctx->gplan.ga = (int)g[5];
   ctx->gplan.sv = ctx->d_sv;
   ctx->grid_ok = true;
   return EKS_OK;
@@ -1284,6 +1405,7 @@ void begin_run(eks_ctx* ctx, const eks_options* opt) {
   ctx->launches = 0;
   ctx->model_bytes = ctx->model_flops = 0.0;
   ctx->c1_ready = false;
+  ctx->aq_off = false;  // set per solve (full-basis methods)
 }
 
 }  // namespace
@@ -1488,7 +1610,7 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   // the plane-marching plan first: when it applies (one rank, stencil structure) and no path is
   // forced (EKS_SPMM_PATH), the ELL copy and the TMA segment plan are never used, so they are not
   // built (host setup time is part of the end-to-end number)
-  if (ctx->nranks == 1) ST(build_grid_plan(ctx, n, rp, col, val));
+  ST(build_grid_plan(ctx, n, rp, col, val, row_begin, plan.halo_before, plan.halo_after));
   const bool skip_alt = ctx->grid_ok && ctx->spmm_path == 0;
   const int w = skip_alt ? 0 : eks::ell_width((int)ctx->maxrow);
   if (w > 0) {
@@ -1877,6 +1999,23 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   const int ring = (method == EKS_SRE_CG) ? (restr ? std::max(3, s + 1) : 3) : (method == EKS_CA_SRE_CG ? 2 * s + 1 : 0);
   ctx->ortho = ortho;
   ctx->use_prec = prec;
+  // full-basis s-step methods (SRE-CG2, MSDO-CG) keep every W; AÂ·W is cached only with
+  // aq_cache = 1 â€” by default they store Q only (reading R24): the same 4 window sweeps per CGS2, two
+  // more SpMMs per block, half the memory per outer iteration
+  const int aqc = opt ? opt->aq_cache : 0;
+  if (aqc < 0 || aqc > 2) return fail(ctx, EKS_ERR_INVALID_ARG, "aq_cache must be 0 (auto), 1 (on) or 2 (off)");
+  ctx->aq_off = !ring && !ca && !restr && aqc != 1;
+  ctx->last_aq_off = ctx->aq_off;
+  int plan_fit = -1;  // memory planner: outer iterations the device can hold (full-basis methods)
+  if (!ring) {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    double held = 0.0;  // blocks of earlier solves are reused
+    for (auto& bk : ctx->Wpool) if (bk.base && bk.owned) held += 8.0 * n_ext(ctx) * t;
+    for (auto& bk : ctx->AWpool) if (bk.base && bk.owned) held += 8.0 * ctx->n * t;
+    const double per_outer = (double)s * 8.0 * t * ((double)n_ext(ctx) + (ctx->aq_off ? 0.0 : (double)ctx->n));
+    plan_fit = (int)(((double)fr - 64.0 * 1024 * 1024 + held) / per_outer);
+  }
   EventPair ev;
   CK(ev.create());
   CK(cudaEventRecord(ev.e0, ctx->stream));
@@ -1902,8 +2041,10 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
     long long launches = 0;  // this library's kernels in it
     double bytes = 0, flops = 0;
   };
-  const bool graphs_on = opt && opt->use_graph && method == EKS_SRE_CG && !restr && !prec && !ortho &&
-                         ctx->nranks == 1 && !ctx->prof_on;
+  // Several ranks: the NCCL halo exchanges and allreduces are captured with the kernels (the comm
+  // stream forks from and joins the solve stream through events).  Should a capture fail, the outer
+  // iteration (which did not execute while captured) runs uncaptured and graphs stay off.
+  bool graphs_on = opt && opt->use_graph && method == EKS_SRE_CG && !restr && !prec && !ortho && !ctx->prof_on;
   const int gperiod = (s % 3 == 0) ? 2 : 6;
   PhaseGraph pg[6];
   struct GraphGuard {
@@ -1972,16 +2113,35 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
       const double b0 = ctx->model_bytes, f0 = ctx->model_flops;
       const int nb0 = nblocks;
       cudaGraph_t g = nullptr;
+      const bool c1r0 = ctx->c1_ready;
+      eks_status cst = EKS_OK;
+      cudaError_t ie = cudaSuccess;
       {
         CaptureGuard cap(ctx->stream);  // ends (and discards) the capture on every exit path
-        CK(cap.begin());
-        ST(outer_body());
+        ie = cap.begin();
+        if (ie == cudaSuccess) cst = outer_body();
         if (status == EKS_ERR_OOM) break;  // (cannot happen after prealloc_steady)
-        CK(cap.end(&g));
+        if (ie == cudaSuccess && cst == EKS_OK) ie = cap.end(&g);
       }
-      cudaError_t ie = cudaGraphInstantiate(&pg[phase].exec, g, 0);
-      cudaGraphDestroy(g);
-      CK(ie);
+      if (ie == cudaSuccess && cst == EKS_OK) {
+        ie = cudaGraphInstantiate(&pg[phase].exec, g, 0);
+        cudaGraphDestroy(g);
+      } else if (g) {
+        cudaGraphDestroy(g);
+      }
+      if (ie != cudaSuccess || cst != EKS_OK) {  // nothing ran: undo the bookkeeping, run it plainly
+        cudaGetLastError();
+        if (ctx->nranks == 1 && cst != EKS_OK) return cst;  // one rank: a real error
+        graphs_on = false;
+        pg[phase].exec = nullptr;
+        nblocks = nb0;
+        ctx->launches = l0;
+        ctx->model_bytes = b0;
+        ctx->model_flops = f0;
+        ctx->c1_ready = c1r0;  // the fused next-C1 of the last executed block is still in C1
+        ST(outer_body());
+        goto iteration_done;
+      }
       pg[phase].nb0 = nb0;
       pg[phase].launches = ctx->launches - l0;
       pg[phase].bytes = ctx->model_bytes - b0;
@@ -1992,6 +2152,7 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
       ST(outer_body());
       if (status == EKS_ERR_OOM) break;
     }
+  iteration_done:
     ST(sync_scalars(ctx, 2));
     const int fl = ctx->h_flag[1];
     if (fl != INT_MAX) {  // A-CholQR breakdown: x stays the last completed iterate
@@ -2032,7 +2193,7 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
     rep->outer_iters = k - 1;
     rep->converged = converged;
     rep->breakdown_block = breakdown_block;
-    rep->max_outer_fit = (base == EKS_SRE_CG) ? -1 : max_fit;
+    rep->max_outer_fit = (base == EKS_SRE_CG) ? -1 : (max_fit >= 0 ? max_fit : plan_fit);
     rep->rho0 = rho0;
     rep->rho = rho;
     const double nb = std::sqrt(ctx->h_scal[3]);
@@ -2060,6 +2221,7 @@ eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks_total, const double*
   ST(ensure_workspace(ctx, t, 1));
   ctx->use_prec = false;
   ctx->ortho = 0;
+  ctx->last_aq_off = false;
   EventPair ev;
   CK(ev.create());
   CK(cudaEventRecord(ev.e0, ctx->stream));
@@ -2118,6 +2280,18 @@ eks_status eks_plan_halo(int rank, int nranks, const int64_t* ranges, const int6
   geom[1] = P.halo_after;
   geom[2] = P.int_lo;
   geom[3] = P.int_hi;
+  return EKS_OK;
+}
+
+eks_status eks_plan_grid(int64_t row_begin, int64_t row_end, const int64_t* row_ptr, const int32_t* col,
+                         const double* vals, int64_t halo_before, int64_t halo_after, int64_t* geom, double* sv) {
+  if (!row_ptr || !col || !vals || !geom || row_end <= row_begin) return EKS_ERR_INVALID_ARG;
+  std::vector<double> v;
+  if (!grid_plan_host(row_end - row_begin, row_ptr, col, vals, row_begin, halo_before, halo_after, geom, v)) {
+    for (int k = 0; k < 6; ++k) geom[k] = 0;
+    return EKS_OK;
+  }
+  if (sv) memcpy(sv, v.data(), sizeof(double) * v.size());
   return EKS_OK;
 }
 
@@ -2304,6 +2478,8 @@ eks_status eks_k_last_basis(eks_ctx* ctx, int j, double* W, double* AW) {
   const int idx = ring ? j % ring : j;
   if (idx >= (int)ctx->Wpool.size() || !ctx->Wpool[idx].base) return fail(ctx, EKS_ERR_INVALID_ARG, "no basis block %d", j);
   CK(cudaMemcpyAsync(W, ctx->Wpool[idx].loc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (AW && ctx->last_aq_off && !ring && j < nb - 2)
+    return fail(ctx, EKS_ERR_INVALID_ARG, "AÂ·W of block %d is not kept (store-Q-only solve: the last 2 blocks)", j);
   if (AW)
     CK(cudaMemcpyAsync(AW, ctx->AWpool[idx].loc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));

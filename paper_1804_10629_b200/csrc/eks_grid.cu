@@ -48,6 +48,9 @@ struct GrCfg {
   static constexpr int JPW = CG ? (JOBS + NWC - 1) / NWC : 1;
   static_assert(U % NWC == 0, "units");
   static_assert(!CG || UPW == 1, "CTA-level Gram: one unit per warp, the warps' scratches form the Y tile");
+  // PATCH mode (T = 16, 32): GP lanes per row, NG lane groups per warp, patches of up to 2 × 2 rows
+  static constexpr int GP = T / 2, NG = 32 / GP;
+  static constexpr int YR = (NG * 4 > RW) ? NG * 4 : RW;  // rows of a warp's Y scratch
 };
 
 }  // namespace
@@ -60,10 +63,15 @@ __host__ __device__ inline size_t grid_stage_bytes(int bx, int by, int hy, int v
   return (((size_t)(bx + 2) * (by + 2 * hy) * T * 8 + (size_t)K::R * vs * 8 + (size_t)K::R * 8) + 127) & ~(size_t)127;
 }
 
-template <int T, int W>
+// PATCH (t = 16, 32): every group of T/2 lanes (one double2 column pair per lane) forms a PX × PY
+// patch of output rows (2 × 2 in 3D, 2 × 1 in 2D) from one set of loads: the centre-plane x-lines
+// of the patch with their ±1 neighbours, the ±y lines and the ±z planes are each read once —
+// 5 (3D) / 4 (2D) shared-memory row loads per output row instead of 7 / 5.
+template <int T, int W, bool PATCH = false>
 __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
     k_spmm_grid(const GridPlan gp, int bx, int by, int zc, const double* __restrict__ X, double* __restrict__ Y,
-                const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch, int NS) {
+                const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch, int NS,
+                const bool gram) {
   using K = GrCfg<T>;
   pdl_enter();
   constexpr int S = K::S, G = K::G, C = K::C, RW = K::RW, NWC = K::NWC, MT = K::MT, H = T / 2;
@@ -75,8 +83,8 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
   const int PW = bx + 2, PH = by + 2 * hy;     // plane-block extent
   const int64_t plane = (int64_t)nx * ny;
   const size_t SB = grid_stage_bytes<T>(bx, by, hy, VS);
-  double* sYw = reinterpret_cast<double*>(smraw + (size_t)NS * SB);  // [2 (CG)][NWC][RW][S]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sYw + (K::CG ? 2 : 1) * NWC * RW * S);
+  double* sYw = reinterpret_cast<double*>(smraw + (size_t)NS * SB);  // [2 (CG)][NWC][YR][S]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sYw + (K::CG ? 2 : 1) * NWC * K::YR * S);
   uint64_t* empty = full + 8;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q4 = lane & 3;
@@ -125,11 +133,11 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
         // lane l < PH: X line y0 − hy + l of plane p;  lane PH + l < PH + by: values of output line y0 + l, plane p − 1
         uint32_t bytes = 0;
         const int yy = y0 - hy + lane;
-        const bool xline = lane < PH && p >= 0 && p < nz && yy >= 0 && yy < ny;
+        const bool xline = lane < PH && p >= -gp.gb && p < nz + gp.ga && yy >= 0 && yy < ny;
         const int vl = lane - PH, vy = y0 + vl;
         const bool vline = vl >= 0 && vl < by && p - 1 >= z0 && p - 1 < z1 && vy < ny;
         const int rl = lane - PH - by, ry = y0 + rl;  // lanes for the lines of r (16-byte rows: nx even)
-        const bool rline = r != nullptr && rbulk && rl >= 0 && rl < by && p - 1 >= z0 && p - 1 < z1 && ry < ny;
+        const bool rline = gram && r != nullptr && rbulk && rl >= 0 && rl < by && p - 1 >= z0 && p - 1 < z1 && ry < ny;
         if (xline) bytes += (uint32_t)(xb - xa) * T * 8;
         if (vline) bytes += (uint32_t)(ob - x0) * VS * 8;
         if (rline) bytes += (uint32_t)(ob - x0) * 8;
@@ -189,7 +197,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
     // ================= consumers
     const int rw = lane / G, gl = lane % G;
     const int bxs = 31 - __clz(bx);  // bx is a power of two
-    double* yw0 = sYw + (size_t)warp * RW * S;
+    double* yw0 = sYw + (size_t)warp * K::YR * S;
     int cur = 0;        // stage of the current load step
     uint32_t ph = 0;    // its full-barrier phase parity
     for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -206,7 +214,108 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
           const double* Vs = reinterpret_cast<const double*>(smraw + (size_t)cur * SB + (size_t)PW * PH * T * 8);
           const double* Rs = Vs + K::R * VS;
           const int64_t qrow = (int64_t)q * plane + (int64_t)y0 * nx + x0;  // global row of block point (0,0)
-          double* yw = yw0 + (K::CG ? ybuf * NWC * RW * S : 0);
+          double* yw = yw0 + (K::CG ? ybuf * NWC * K::YR * S : 0);
+          if constexpr (PATCH) {
+            constexpr int GP = K::GP, NG = K::NG;
+            constexpr int PX = 2, PY = (W == 7) ? 2 : 1, PR = PX * PY, RPW = NG * PR;
+            const int gi = lane / GP, gl = lane % GP;
+            const int ppx = bx / PX;                 // patches per block line
+            const int nsteps = K::R / (PR * NG * NWC);  // patch steps per warp and plane
+            for (int ps = 0; ps < nsteps; ++ps) {
+              const int pp = (ps * NWC + warp) * NG + gi;  // patch of this lane group
+              const int px0 = (pp % ppx) * PX, py0 = (pp / ppx) * PY;
+              // ---- loads: centre-plane x-lines (with ±1), the ±y lines (3D), the ±z planes
+              double2 xl[PY][PX + 2], ya[PX], yb[PX], zm[PY][PX], zp[PY][PX];
+#pragma unroll
+              for (int dy = 0; dy < PY; ++dy) {
+#pragma unroll
+                for (int i = 0; i < PX + 2; ++i)
+                  xl[dy][i] = *reinterpret_cast<const double2*>(P0 + ((size_t)(py0 + dy + hy) * PW + px0 + i) * T + 2 * gl);
+#pragma unroll
+                for (int dx = 0; dx < PX; ++dx) {
+                  const size_t cen = (size_t)(py0 + dy + hy) * PW + px0 + dx + 1;
+                  zm[dy][dx] = *reinterpret_cast<const double2*>(Pm + cen * T + 2 * gl);
+                  zp[dy][dx] = *reinterpret_cast<const double2*>(Pp + cen * T + 2 * gl);
+                }
+              }
+              if constexpr (W == 7) {
+#pragma unroll
+                for (int dx = 0; dx < PX; ++dx) {
+                  ya[dx] = *reinterpret_cast<const double2*>(P0 + ((size_t)(py0 - 1 + hy) * PW + px0 + dx + 1) * T + 2 * gl);
+                  yb[dx] = *reinterpret_cast<const double2*>(P0 + ((size_t)(py0 + PY + hy) * PW + px0 + dx + 1) * T + 2 * gl);
+                }
+              }
+              // ---- the patch rows, stencil slots in ascending column order (reading R20)
+#pragma unroll
+              for (int dy = 0; dy < PY; ++dy)
+#pragma unroll
+                for (int dx = 0; dx < PX; ++dx) {
+                  const int ir = (py0 + dy) * bx + px0 + dx;
+                  const bool ok = x0 + px0 + dx < nx && y0 + py0 + dy < ny;
+                  const int64_t grow = qrow + (int64_t)(py0 + dy) * nx + px0 + dx;
+                  double2 nb[W];
+                  if constexpr (W == 7) {
+                    nb[0] = zm[dy][dx];
+                    nb[1] = dy == 0 ? ya[dx] : xl[dy > 0 ? dy - 1 : 0][dx + 1];
+                    nb[2] = xl[dy][dx];
+                    nb[3] = xl[dy][dx + 1];
+                    nb[4] = xl[dy][dx + 2];
+                    nb[5] = dy == PY - 1 ? yb[dx] : xl[dy + 1 < PY ? dy + 1 : dy][dx + 1];
+                    nb[6] = zp[dy][dx];
+                  } else {
+                    nb[0] = zm[dy][dx];
+                    nb[1] = xl[dy][dx];
+                    nb[2] = xl[dy][dx + 1];
+                    nb[3] = xl[dy][dx + 2];
+                    nb[4] = zp[dy][dx];
+                  }
+                  double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+                  for (int k = 0; k < VS; k += 2) {
+                    const double2 av = ok ? *reinterpret_cast<const double2*>(Vs + ir * VS + k) : make_double2(0, 0);
+                    y.x = __fma_rn(av.x, nb[k].x, y.x);
+                    y.y = __fma_rn(av.x, nb[k].y, y.y);
+                    if (k + 1 < W) {
+                      y.x = __fma_rn(av.y, nb[k + 1].x, y.x);
+                      y.y = __fma_rn(av.y, nb[k + 1].y, y.y);
+                    }
+                  }
+                  if (!ok) y = make_double2(0.0, 0.0);
+                  else reinterpret_cast<double2*>(Y)[grow * H + gl] = y;
+                  if (gram) *reinterpret_cast<double2*>(yw + (gi * PR + dy * PX + dx) * S + 2 * gl) = y;
+                }
+              if (!gram) continue;
+              __syncwarp();
+              // ---- Gram over the warp's RPW rows on DMMA (k-steps of 4 rows)
+#pragma unroll
+              for (int ks = 0; ks < RPW / 4; ++ks) {
+                const int rq = ks * 4 + q4, gq = rq / PR, wq = rq % PR;
+                const int ppq = (ps * NWC + warp) * NG + gq;
+                const int pxq = (ppq % ppx) * PX + wq % PX, pyq = (ppq / ppx) * PY + wq / PX;
+                const bool okq = x0 + pxq < nx && y0 + pyq < ny;
+                const double* xo = P0 + ((size_t)(pyq + hy) * PW + pxq + 1) * T;
+                double xa[MT], ybv[MT];
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                  xa[i] = okq ? xo[i * 8 + g] : 0.0;
+                  ybv[i] = yw[rq * S + i * 8 + g];
+                }
+                int ut = 0;
+#pragma unroll
+                for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+                  for (int ni = mi; ni < MT; ++ni, ++ut) dmma(acc[ut][0], acc[ut][1], xa[mi], ybv[ni]);
+                if (r != nullptr) {
+                  const int irq = pyq * bx + pxq;
+                  const double br = (g == 0 && okq)
+                                        ? (rbulk ? Rs[irq] : __ldg(r + qrow + (int64_t)pyq * nx + pxq)) : 0.0;
+#pragma unroll
+                  for (int mi = 0; mi < MT; ++mi) dmma(accr[mi][0], accr[mi][1], xa[mi], br);
+                }
+              }
+              __syncwarp();
+            }
+          } else {
 #pragma unroll
           for (int uu = 0; uu < K::UPW; ++uu) {
             const int r0u = (warp + uu * NWC) * RW;  // first row of the unit in the plane-block
@@ -216,7 +325,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
             const int64_t grow = qrow + (int64_t)iy * nx + ix;
             const int cen = (iy + hy) * PW + ix + 1;
             double vr = 0.0;
-            if (r != nullptr && ok) vr = rbulk ? Rs[ir] : __ldg(r + grow);
+            if (gram && r != nullptr && ok) vr = rbulk ? Rs[ir] : __ldg(r + grow);
             double a[VS];
 #pragma unroll
             for (int k = 0; k < VS; k += 2) {
@@ -254,8 +363,9 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
               }
               if (!ok) y = make_double2(0.0, 0.0);
               else reinterpret_cast<double2*>(Y)[grow * H + gl + G * c2] = y;
-              *reinterpret_cast<double2*>(yw + rw * S + 2 * (gl + G * c2)) = y;
+              if (gram) *reinterpret_cast<double2*>(yw + rw * S + 2 * (gl + G * c2)) = y;
             }
+            if (!gram) continue;
             __syncwarp();
             // ---- Gram over the unit's RW rows on DMMA: A = own X rows (plane q), B = [Y rows | r]
             // (t = 64: over the whole block below instead)
@@ -286,11 +396,12 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
             }
             __syncwarp();
           }
-          if constexpr (K::CG) {
+          }  // PATCH / unit consumers
+          if (K::CG && gram) {
             // ---- CTA-level Gram: all consumer warps' Y rows are in the Y tile; each warp
             // accumulates its tiles over the block's R rows (k-steps of 4 rows)
             asm volatile("bar.sync 1, %0;" ::"n"(32 * NWC) : "memory");
-            const double* Yt = sYw + ybuf * NWC * RW * S;
+            const double* Yt = sYw + ybuf * NWC * K::YR * S;
 #pragma unroll 2
             for (int kk = 0; kk < K::R; kk += 4) {  // the warp's jobs interleaved: independent DMMA chains
               const int irq = kk + q4, ixq = irq & (bx - 1), iyq = irq >> bxs;
@@ -322,6 +433,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
     }
   }
   // ================= epilogue (as k_spmm_seg): consumer warps' partials in warp order, lower half mirrored
+  if (!gram) return;
   __syncthreads();
   double* red = reinterpret_cast<double*>(smraw);
   constexpr int PER = T * T + T;
@@ -411,7 +523,7 @@ static void grid_shape(const GridPlan& gp, int& bx, int& by, int& zc, int sms) {
 
 template <int T, int W>
 static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, double* Y, const double* r,
-                          double* part, int nblk, const Tail& tl, const CholArgs& ch) {
+                          double* part, int nblk, const Tail& tl, const CholArgs& ch, bool gram) {
   using K = GrCfg<T>;
   static int sms = 0;
   if (!sms) {
@@ -423,15 +535,28 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
   grid_shape<T>(gp, bx, by, zc, sms);
   const int hy = gp.ny > 1 ? 1 : 0, vs = (W + 1) & ~1;
   const size_t SB = grid_stage_bytes<T>(bx, by, hy, vs);
-  const size_t fixed = (size_t)(K::CG ? 2 : 1) * K::NWC * K::RW * K::S * 8 + 16 * 8 + 128;
+  const size_t fixed = (size_t)(K::CG ? 2 : 1) * K::NWC * K::YR * K::S * 8 + 16 * 8 + 128;
+  static const bool patch_env = [] {  // EKS_GRID_PATCH=0: the per-row consumer (A/B measurements)
+    const char* e = getenv("EKS_GRID_PATCH");
+    return !(e && atoi(e) == 0);
+  }();
+  constexpr bool PATCH_T = (T == 16 || T == 32);
+  const bool patch = PATCH_T && patch_env && bx % 2 == 0 && (W == 5 || by % 2 == 0);
   int ns = (int)((220 * 1024 - fixed) / SB);
   if (ns > 8) ns = 8;
   if (ns < 4) return cudaErrorInvalidConfiguration;
   size_t sm = (size_t)ns * SB + fixed;
   if (sm < (size_t)(T * T + T) * 8) sm = (size_t)(T * T + T) * 8;
-  cudaFuncSetAttribute(k_spmm_grid<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   nblk = nblk < sms ? nblk : sms;  // one persistent CTA per SM
-  return launch_k(k_spmm_grid<T, W>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns);
+  if constexpr (PATCH_T) {
+    if (patch) {
+      cudaFuncSetAttribute(k_spmm_grid<T, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      return launch_k(k_spmm_grid<T, W, true>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns,
+                      gram);
+    }
+  }
+  cudaFuncSetAttribute(k_spmm_grid<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  return launch_k(k_spmm_grid<T, W>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns, gram);
 }
 
 bool spmm_grid_fused_chol(int t) { return t == 8 || t == 16; }
@@ -452,11 +577,11 @@ bool spmm_grid_fits(int t, const GridPlan& gp) {
 }
 
 cudaError_t launch_spmm_grid(cudaStream_t st, int t, const GridPlan& gp, const double* X, double* Y, const double* r,
-                             double* part, int nblk, const Tail& tl, const CholArgs& ch) {
-  if (ch.on && !spmm_grid_fused_chol(t)) return cudaErrorInvalidValue;
+                             double* part, int nblk, const Tail& tl, const CholArgs& ch, bool gram) {
+  if (ch.on && (!spmm_grid_fused_chol(t) || !gram)) return cudaErrorInvalidValue;
 #define EKS_GRID_W(TT)                                                                  \
-  return gp.w == 7 ? grid_t<TT, 7>(st, gp, X, Y, r, part, nblk, tl, ch)                 \
-                   : grid_t<TT, 5>(st, gp, X, Y, r, part, nblk, tl, ch);
+  return gp.w == 7 ? grid_t<TT, 7>(st, gp, X, Y, r, part, nblk, tl, ch, gram)           \
+                   : grid_t<TT, 5>(st, gp, X, Y, r, part, nblk, tl, ch, gram);
   switch (t) {
     case 8: EKS_GRID_W(8)
     case 16: EKS_GRID_W(16)

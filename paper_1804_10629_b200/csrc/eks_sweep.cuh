@@ -66,14 +66,20 @@ cudaError_t launch_spmm_seg(cudaStream_t st, int t, int64_t n, const SegPlan& pl
 // x-lines), every entry at offset 0, ±1, ±nx (3D), ±nx·ny inside the grid; sv holds per row the
 // w = 7 (3D) or 5 (2D) stencil values in ascending column order, 0 in absent slots, padded to
 // (w+1)&~1 doubles per row.  Single rank only.
+// Several ranks: the slab is whole planes; X points at the first LOCAL row and the ghost planes
+// z = -1 (gb = 1) and z = nz (ga = 1) of the neighbouring ranks sit right before / after the local
+// rows (the extended layout of eks.cu), so the kernel reads them like local planes.
 struct GridPlan {
   int nx = 0, ny = 0, nz = 0, w = 0;
+  int gb = 0, ga = 0;  // ghost planes before / after the local ones (0 or 1)
   const double* sv = nullptr;
 };
 bool spmm_grid_fits(int t, const GridPlan& gp);
 bool spmm_grid_fused_chol(int t);  // ch.on allowed: the last CTA runs the solve-path Cholesky
+// gram = false: Y = A·X only (no Y scratch, no DMMA, no partials; part and tl unused) — the plain
+// SpMM of the CA monomial powers, the store-Q-only CGS2 products and the residual.
 cudaError_t launch_spmm_grid(cudaStream_t st, int t, const GridPlan& gp, const double* X, double* Y, const double* r,
-                             double* part, int nblk, const Tail& tl, const CholArgs& ch);
+                             double* part, int nblk, const Tail& tl, const CholArgs& ch, bool gram = true);
 // maxrow = longest CSR row (selects the register-resident fast path; longer rows still work).
 cudaError_t launch_spmm_gram(cudaStream_t st, int t, int64_t n, const int* rp, const int* col, const double* val,
                              int maxrow, const double* Xext, int64_t xoff, double* Y, const double* r, double* part,

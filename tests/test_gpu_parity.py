@@ -398,6 +398,31 @@ def test_cfg2_full_size_prefix(eks, torch_cuda, oracle_lib):
     assert abs(rep["rho"] - ref["rho"]) <= 1e-8 * ref["rho"]
 
 
+@pytest.mark.parametrize("method,s_,t", [("sre-cg2", 2, 4), ("msdo-cg", 3, 8), ("msdo-cg", 2, 16), ("sre-cg2", 3, 32)])
+def test_store_q_only(eks, torch_cuda, oracle_lib, method, s_, t):
+    """Full-basis methods with and without the A·Q cache (eks_options.aq_cache, reading R24): store-Q-only
+    (the default) takes C = Qᵀ(A·Z) with explicit SpMMs — the oracle's definition algebra — and holds
+    twice the outer iterations in memory.  Both agree with the oracle's definition mode (counts within
+    5 %, x within 1e-6; two-iteration prefix within 1e-10) and the planner reports max_outer_fit."""
+    p = ei.cfg1()
+    S = eks.Solver(p.A)
+    b = dev(torch_cuda, p.b)
+    off = S.solve(b, method, s_, t, p.tol)                       # auto = store Q only
+    on = S.solve(b, method, s_, t, p.tol, aq_cache="on")
+    pre_off = S.solve(b, method, s_, t, 0.0, max_outer=3, aq_cache="off")
+    S.close()
+    ref = oracle_lib.solve(p.A, p.b, method, s_, t, p.tol)
+    refp = oracle_lib.solve(p.A, p.b, method, s_, t, 0.0, kmax=3)
+    for rep in (off, on):
+        assert rep["converged"] and rep["status"] == 0
+        assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"]))
+        assert rel(host(rep["x"]), ref["x"]) <= 1e-6
+        assert rep["max_outer_fit"] > rep["outer_iters"]
+    assert off["max_outer_fit"] > 1.5 * on["max_outer_fit"]  # A·W no longer stored per block
+    assert pre_off["outer_iters"] == refp["outer_iters"] == 2
+    assert rel(host(pre_off["x"]), refp["x"]) <= 1e-10
+
+
 def test_cfg3_analog_msdo(eks, torch_cuda, oracle_lib):
     p = ei.cfg3(N=16)  # 16³ analog of the 128³ subcube problem, t=32 (a domain = 8 rows... 128 rows), s=4
     rep, ref = _e2e(eks, torch_cuda, oracle_lib, p.A, p.b, "msdo-cg", p.s, p.t, p.tol)

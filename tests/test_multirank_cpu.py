@@ -112,10 +112,31 @@ def _worker(rank, world, port, kind, t, q):
         dist.all_reduce(G)
         Gref = X.T @ oracle.spmm(A, X)
         gram_err = float(np.abs(G.numpy() - Gref).max() / np.abs(Gref).max())
+        # ghost-plane plan of the plane-marching SpMM (eks_plan_grid, what eks_setup_csr builds on every
+        # rank): stencil operators with whole-plane slabs get one ghost plane per neighbour rank; the
+        # SpMM from the slot values over [ghost plane | local planes | ghost plane] (absent neighbours:
+        # value 0 on the row's own column, fma(0, x, y) = y) is bitwise the global one
+        grid_ok = None
+        if kind != "general":
+            g, sv = eks.eks_plan_grid(lo, hi, S.row_ptr, S.col, S.val, geom["halo_before"], geom["halo_after"])
+            plane = g["nx"] * g["ny"]
+            grid_ok = g["w"] == (7 if kind == "aniso3d" else 5) and g["nz"] * plane == nloc
+            grid_ok &= g["gb"] == (1 if rank > 0 else 0) and g["ga"] == (1 if rank < world - 1 else 0)
+            grid_ok &= geom["halo_before"] == g["gb"] * plane and geom["halo_after"] == g["ga"] * plane
+            offs = [-plane, -g["nx"], -1, 0, 1, g["nx"], plane] if g["w"] == 7 else [-g["nx"], -1, 0, 1, g["nx"]]
+            rows = np.arange(nloc)
+            cols = np.empty((nloc, g["w"]), np.int64)
+            for k, o in enumerate(offs):
+                c = geom["halo_before"] + rows + o
+                inside = (c >= 0) & (c < next_) & (sv[:, k] != 0.0)
+                cols[:, k] = np.where(inside, c, geom["halo_before"] + rows)
+            Ag = ei.Csr(nloc, np.arange(0, nloc * g["w"] + 1, g["w"], dtype=np.int64),
+                        cols.reshape(-1).astype(np.int32), np.ascontiguousarray(sv[:, :g["w"]]).reshape(-1))
+            grid_ok &= bool(np.array_equal(oracle.spmm(Ag, Xext)[:nloc], Yglob))
         # max-over-ranks timing aggregation used by bench.py
         tt = torch.tensor([float(rank + 1)])
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        q.put((rank, bitwise, interior_ok, gram_err, float(tt.item()), int(nloc), geom))
+        q.put((rank, bitwise, interior_ok, gram_err, float(tt.item()), int(nloc), geom, grid_ok))
     except Exception as e:  # report instead of leaving the parent waiting
         q.put((rank, f"error: {e!r}"))
         raise
@@ -144,8 +165,9 @@ def test_distributed_spmm_gram_protocol(world, kind, t):
     res.sort()
     n = _matrix(kind).n
     assert sum(r[5] for r in res) == n
-    for rank, bitwise, interior_ok, gram_err, tmax, nloc, geom in res:
+    for rank, bitwise, interior_ok, gram_err, tmax, nloc, geom, grid_ok in res:
         assert bitwise, (rank, kind)
+        assert grid_ok is None if kind == "general" else grid_ok, (rank, kind)
         assert interior_ok
         assert gram_err <= 1e-13
         assert tmax == float(world)

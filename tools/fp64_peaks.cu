@@ -37,6 +37,28 @@ __global__ void dmma_kernel(double* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// DMMA and DFMA issued by the same warps: is the fp64 tensor path a separate pipe from the FMA pipe?
+// Per iteration: 4 DMMA (4·512 flop per warp) and 32 DFMA per thread (32·2·32 = 2048 flop per warp).
+__global__ void mixed_kernel(double* out, int iters, double a, double b) {
+  double ma = 1.0 + threadIdx.x * 1e-9, mb = 1.0 - threadIdx.x * 1e-9;
+  double c[4][2];
+  for (int k = 0; k < 4; ++k) { c[k][0] = 0; c[k][1] = 0; }
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+  double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[k][0]), "+d"(c[k][1]) : "d"(ma), "d"(mb));
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void read_kernel(const double2* __restrict__ x, size_t n2, double* out) {
   double s = 0;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x) {
@@ -86,6 +108,20 @@ int main() {
       if (fl / (ms * 1e-3) > best) best = fl / (ms * 1e-3);
     }
     printf("{\"dmma_tflops\": %.3f}\n", best / 1e12);
+  }
+  // DMMA + DFMA interleaved in the same warps
+  {
+    int iters = 4096, blocks = sms * 8, threads = 256;
+    mixed_kernel<<<blocks, threads>>>(out, 16, 1.0000001, 1e-9);
+    CK(cudaDeviceSynchronize());
+    double best = 0;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0); mixed_kernel<<<blocks, threads>>>(out, iters, 1.0000001, 1e-9); cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+      double fl = (512.0 * 4 + 2.0 * 32 * 32) * iters * (double)blocks * (threads / 32);
+      if (fl / (ms * 1e-3) > best) best = fl / (ms * 1e-3);
+    }
+    printf("{\"mixed_dmma_dfma_tflops\": %.3f}\n", best / 1e12);
   }
   // fp64 read and copy bandwidth over 4 GiB
   {

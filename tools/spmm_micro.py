@@ -53,7 +53,10 @@ def main():
             X = torch.rand(A.n, t, dtype=torch.float64, device="cuda") - 0.5
             Y = torch.empty_like(X)
             v = torch.rand(A.n, dtype=torch.float64, device="cuda")
-            B = 12.0 * A.nnz + 4.0 * (A.n + 1) + 16.0 * A.n * t
+            # algorithmic bytes: A in the representation the kernel streams (stencil operators on the
+            # plane-marching path: 8·7 B of values per row; CSR otherwise) + X read + Y written + v read
+            B = 8.0 * 7 * A.n + 16.0 * A.n * t + 8.0 * A.n
+            Bcsr = 12.0 * A.nnz + 4.0 * (A.n + 1) + 16.0 * A.n * t
             res = {}
             for var in [int(x) for x in a.variants.split(",")]:
                 ms = eks.eks_k_time_spmm(s.ctx, t, X, Y, v, var, a.reps)
