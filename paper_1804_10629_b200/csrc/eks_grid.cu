@@ -63,10 +63,10 @@ __host__ __device__ inline size_t grid_stage_bytes(int bx, int by, int hy, int v
   return (((size_t)(bx + 2) * (by + 2 * hy) * T * 8 + (size_t)K::R * vs * 8 + (size_t)K::R * 8) + 127) & ~(size_t)127;
 }
 
-// PATCH (t = 16, 32): every group of T/2 lanes (one double2 column pair per lane) forms a PX × PY
-// patch of output rows (2 × 2 in 3D, 2 × 1 in 2D) from one set of loads: the centre-plane x-lines
-// of the patch with their ±1 neighbours, the ±y lines and the ±z planes are each read once —
-// 5 (3D) / 4 (2D) shared-memory row loads per output row instead of 7 / 5.
+// PATCH (3D, t = 16, 32): every group of T/2 lanes (one double2 column pair per lane) forms a 1 × 4
+// patch of output rows (4 consecutive y-lines at one x) from one set of loads: the centre-plane
+// rows with their ±1 x-neighbours, the ±y lines outside the patch and the ±z planes are each read
+// once — 5.5 shared-memory row loads per output row instead of 7.
 template <int T, int W, bool PATCH = false>
 __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
     k_spmm_grid(const GridPlan gp, int bx, int by, int zc, const double* __restrict__ X, double* __restrict__ Y,
@@ -217,73 +217,52 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
           double* yw = yw0 + (K::CG ? ybuf * NWC * K::YR * S : 0);
           if constexpr (PATCH) {
             constexpr int GP = K::GP, NG = K::NG;
-            constexpr int PX = 2, PY = (W == 7) ? 2 : 1, PR = PX * PY, RPW = NG * PR;
+            // 1 × 4 patches (a column of 4 y-lines): the 4 lane groups of a warp take x-adjacent
+            // columns, so their rows' stencil values (64 B per row) fall in both bank halves
+            // (2 × 2 patches put them 128 B apart: 4-way conflicts that cancelled the gain)
+            constexpr int PX = 1, PY = 4, LPX = 0, PR = PX * PY, RPW = NG * PR;
             const int gi = lane / GP, gl = lane % GP;
-            const int ppx = bx / PX;                 // patches per block line
+            const int ppx = bx / PX;                 // patches per block line (a power of 2)
             const int nsteps = K::R / (PR * NG * NWC);  // patch steps per warp and plane
             for (int ps = 0; ps < nsteps; ++ps) {
               const int pp = (ps * NWC + warp) * NG + gi;  // patch of this lane group
-              const int px0 = (pp % ppx) * PX, py0 = (pp / ppx) * PY;
-              // ---- loads: centre-plane x-lines (with ±1), the ±y lines (3D), the ±z planes
-              double2 xl[PY][PX + 2], ya[PX], yb[PX], zm[PY][PX], zp[PY][PX];
+              const int px0 = (pp & (ppx - 1)) * PX, py0 = (pp >> (bxs - LPX)) * PY;
+              // ---- the patch's 4 rows, sliding up the y-lines: the centre of line dy+1 is loaded once
+              // (as the +y neighbour of line dy and the centre of the next row); ±x and ±z per row.
+              // Stencil slots in ascending column order (reading R20).
+              const double* c0p = P0 + ((size_t)(py0 + hy) * PW + px0 + 1) * T + 2 * gl;  // centre, line 0
+              double2 cm = *reinterpret_cast<const double2*>(c0p - (size_t)PW * T);       // line −1 (−y of row 0)
+              double2 c0 = *reinterpret_cast<const double2*>(c0p);
 #pragma unroll
               for (int dy = 0; dy < PY; ++dy) {
+                const double* cp = c0p + (size_t)dy * PW * T;
+                const double2 cn = *reinterpret_cast<const double2*>(cp + (size_t)PW * T);  // +y (line dy+1)
+                const double2 xm = *reinterpret_cast<const double2*>(cp - T);
+                const double2 xp = *reinterpret_cast<const double2*>(cp + T);
+                const size_t zo = (size_t)(cp - P0);
+                const double2 zm = *reinterpret_cast<const double2*>(Pm + zo);
+                const double2 zp = *reinterpret_cast<const double2*>(Pp + zo);
+                const int ir = (py0 + dy) * bx + px0;
+                const bool ok = x0 + px0 < nx && y0 + py0 + dy < ny;
+                const int64_t grow = qrow + (int64_t)(py0 + dy) * nx + px0;
+                const double2 nb[7] = {zm, cm, xm, c0, xp, cn, zp};
+                double2 y = make_double2(0.0, 0.0);
 #pragma unroll
-                for (int i = 0; i < PX + 2; ++i)
-                  xl[dy][i] = *reinterpret_cast<const double2*>(P0 + ((size_t)(py0 + dy + hy) * PW + px0 + i) * T + 2 * gl);
-#pragma unroll
-                for (int dx = 0; dx < PX; ++dx) {
-                  const size_t cen = (size_t)(py0 + dy + hy) * PW + px0 + dx + 1;
-                  zm[dy][dx] = *reinterpret_cast<const double2*>(Pm + cen * T + 2 * gl);
-                  zp[dy][dx] = *reinterpret_cast<const double2*>(Pp + cen * T + 2 * gl);
-                }
-              }
-              if constexpr (W == 7) {
-#pragma unroll
-                for (int dx = 0; dx < PX; ++dx) {
-                  ya[dx] = *reinterpret_cast<const double2*>(P0 + ((size_t)(py0 - 1 + hy) * PW + px0 + dx + 1) * T + 2 * gl);
-                  yb[dx] = *reinterpret_cast<const double2*>(P0 + ((size_t)(py0 + PY + hy) * PW + px0 + dx + 1) * T + 2 * gl);
-                }
-              }
-              // ---- the patch rows, stencil slots in ascending column order (reading R20)
-#pragma unroll
-              for (int dy = 0; dy < PY; ++dy)
-#pragma unroll
-                for (int dx = 0; dx < PX; ++dx) {
-                  const int ir = (py0 + dy) * bx + px0 + dx;
-                  const bool ok = x0 + px0 + dx < nx && y0 + py0 + dy < ny;
-                  const int64_t grow = qrow + (int64_t)(py0 + dy) * nx + px0 + dx;
-                  double2 nb[W];
-                  if constexpr (W == 7) {
-                    nb[0] = zm[dy][dx];
-                    nb[1] = dy == 0 ? ya[dx] : xl[dy > 0 ? dy - 1 : 0][dx + 1];
-                    nb[2] = xl[dy][dx];
-                    nb[3] = xl[dy][dx + 1];
-                    nb[4] = xl[dy][dx + 2];
-                    nb[5] = dy == PY - 1 ? yb[dx] : xl[dy + 1 < PY ? dy + 1 : dy][dx + 1];
-                    nb[6] = zp[dy][dx];
-                  } else {
-                    nb[0] = zm[dy][dx];
-                    nb[1] = xl[dy][dx];
-                    nb[2] = xl[dy][dx + 1];
-                    nb[3] = xl[dy][dx + 2];
-                    nb[4] = zp[dy][dx];
+                for (int k = 0; k < VS; k += 2) {
+                  const double2 av = ok ? *reinterpret_cast<const double2*>(Vs + ir * VS + k) : make_double2(0, 0);
+                  y.x = __fma_rn(av.x, nb[k].x, y.x);
+                  y.y = __fma_rn(av.x, nb[k].y, y.y);
+                  if (k + 1 < 7) {
+                    y.x = __fma_rn(av.y, nb[k + 1].x, y.x);
+                    y.y = __fma_rn(av.y, nb[k + 1].y, y.y);
                   }
-                  double2 y = make_double2(0.0, 0.0);
-#pragma unroll
-                  for (int k = 0; k < VS; k += 2) {
-                    const double2 av = ok ? *reinterpret_cast<const double2*>(Vs + ir * VS + k) : make_double2(0, 0);
-                    y.x = __fma_rn(av.x, nb[k].x, y.x);
-                    y.y = __fma_rn(av.x, nb[k].y, y.y);
-                    if (k + 1 < W) {
-                      y.x = __fma_rn(av.y, nb[k + 1].x, y.x);
-                      y.y = __fma_rn(av.y, nb[k + 1].y, y.y);
-                    }
-                  }
-                  if (!ok) y = make_double2(0.0, 0.0);
-                  else reinterpret_cast<double2*>(Y)[grow * H + gl] = y;
-                  if (gram) *reinterpret_cast<double2*>(yw + (gi * PR + dy * PX + dx) * S + 2 * gl) = y;
                 }
+                if (!ok) y = make_double2(0.0, 0.0);
+                else reinterpret_cast<double2*>(Y)[grow * H + gl] = y;
+                if (gram) *reinterpret_cast<double2*>(yw + (gi * PR + dy) * S + 2 * gl) = y;
+                cm = c0;
+                c0 = cn;
+              }
               if (!gram) continue;
               __syncwarp();
               // ---- Gram over the warp's RPW rows on DMMA (k-steps of 4 rows)
@@ -291,7 +270,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
               for (int ks = 0; ks < RPW / 4; ++ks) {
                 const int rq = ks * 4 + q4, gq = rq / PR, wq = rq % PR;
                 const int ppq = (ps * NWC + warp) * NG + gq;
-                const int pxq = (ppq % ppx) * PX + wq % PX, pyq = (ppq / ppx) * PY + wq / PX;
+                const int pxq = (ppq & (ppx - 1)) * PX + wq % PX, pyq = (ppq >> (bxs - LPX)) * PY + wq / PX;
                 const bool okq = x0 + pxq < nx && y0 + pyq < ny;
                 const double* xo = P0 + ((size_t)(pyq + hy) * PW + pxq + 1) * T;
                 double xa[MT], ybv[MT];
@@ -540,8 +519,8 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
     const char* e = getenv("EKS_GRID_PATCH");
     return !(e && atoi(e) == 0);
   }();
-  constexpr bool PATCH_T = (T == 16 || T == 32);
-  const bool patch = PATCH_T && patch_env && bx % 2 == 0 && (W == 5 || by % 2 == 0);
+  constexpr bool PATCH_T = (T == 16 || T == 32) && W == 7;
+  const bool patch = PATCH_T && W == 7 && patch_env && by % 4 == 0;
   int ns = (int)((220 * 1024 - fixed) / SB);
   if (ns > 8) ns = 8;
   if (ns < 4) return cudaErrorInvalidConfiguration;

@@ -367,8 +367,10 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
     for (int ni = 0; ni < K::NT; ++ni) {
       double w0 = 0.0, w1 = 0.0, y0 = 0.0, y1 = 0.0;
+      // R⁻¹ is upper triangular: rows k > 8·ni + 7 of column tile ni are exact zeros (skipped: the
+      // same result, 1/4 (t = 16) to 7/16 (t = 64) fewer DMMAs)
 #pragma unroll
-      for (int kk = 0; kk < T; kk += 4) {
+      for (int kk = 0; kk < (T < 8 * (ni + 1) ? T : 8 * (ni + 1)); kk += 4) {
         const double b = RREG ? rf[ni * (T / 4) + kk / 4] : sRi[(kk + q4) * SR + ni * 8 + g];
         dmma(w0, w1, sZ[rr * S + kk + q4], b);
         dmma(y0, y1, sY[rr * S + kk + q4], b);
