@@ -45,7 +45,9 @@ eks_status eks_k_chol(eks_ctx* ctx, int t, const double* B, double* R);
  * selects for this t, per-CTA partials only; 2: + the tail reduction of the partials (what
  * eks_solve launches); 3: + the block's Cholesky; 4: the ELL gather kernel forced; 5: the CSR
  * gather kernel forced, 6: the plane-marching stencil kernel forced (4-6 with the tail; 6 needs a
- * stencil-structured matrix).  v may be NULL.  Variants 1-6 need t in {8,16,32,64}. */
+ * stencil-structured matrix), 7: exactly the step eks_solve runs (the fused kernel, or at t = 64 the
+ * Gram-free plane-marching SpMM followed by the Gram sweep).  v may be NULL.  Variants 1-7 need t in
+ * {8,16,32,64}. */
 eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, const double* v, int variant, int reps,
                            double* ms);
 

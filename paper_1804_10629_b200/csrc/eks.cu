@@ -22,6 +22,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <atomic>
 #include <string>
@@ -121,6 +122,11 @@ struct eks_ctx {
   // AWpool entries alias a ring of two local blocks (A·W of the last two blocks), CGS2 takes
   // C = Qᵀ(A·Z) with explicit SpMMs of Z and Z1 (scratch: Ze ext, Ysc local)
   bool aq_off = false, last_aq_off = false;
+  // lazy basis (s-step SRE-CG and the basis sweep, t ≥ 8): a ring slot keeps Z2 (not W = Z2 R⁻¹), its
+  // A·W and R⁻¹ (Rslot, t×t per slot); Q·C products use R⁻¹C (folded by the sweeps)
+  bool lazy = false, last_lazy = false;
+  double* Rslot = nullptr;
+  int rslot_cap = 0;
   Block AWring[2], Ze, Ysc;
   Block Zs, Z1, xv, tmpv;            // xv: ext vector
   double *b = nullptr, *r = nullptr, *rnew = nullptr, *dx = nullptr;
@@ -276,7 +282,8 @@ void free_workspace(eks_ctx* c) {
     *b = Block{};
   }
   for (double** p : {&c->b, &c->r, &c->rnew, &c->dx, &c->part, &c->C1, &c->C2, &c->Bg, &c->Rm, &c->Rinv,
-                     &c->alpha, &c->scal}) { dfree(*p); *p = nullptr; }
+                     &c->alpha, &c->scal, &c->Rslot}) { dfree(*p); *p = nullptr; }
+  c->rslot_cap = 0;
   dfree(c->flag);
   c->flag = nullptr;
   dfree(c->cnt);
@@ -303,6 +310,12 @@ eks_status ensure_workspace(eks_ctx* ctx, int t, int s) {
   ST(dalloc(ctx, &ctx->Bg, (size_t)t * t + t));
   ST(dalloc(ctx, &ctx->Rm, (size_t)t * t));
   ST(dalloc(ctx, &ctx->Rinv, (size_t)t * t));
+  if (ctx->rslot_cap < 3) {  // R⁻¹ of the 3 ring slots of the lazy basis
+    dfree(ctx->Rslot);
+    ctx->Rslot = nullptr;
+    ST(dalloc(ctx, &ctx->Rslot, (size_t)3 * t * t));
+    ctx->rslot_cap = 3;
+  }
   ST(dalloc(ctx, &ctx->pre, (size_t)3 * t * t + t));
   ST(dalloc(ctx, &ctx->scal, 16));
   if (!ctx->flag) CK(cudaMalloc((void**)&ctx->flag, sizeof(int) * 4));
@@ -383,6 +396,14 @@ eks_status halo_start(eks_ctx* ctx, const Block& X, int t) {
 
 int spmm_path_for(const eks_ctx* ctx, int t);
 
+bool gram_split_env() {
+  static const bool on = [] {  // EKS_GRAM64=fused: the in-kernel CTA-level Gram at t = 64 (A/B measurements)
+    const char* e = getenv("EKS_GRAM64");
+    return !(e && !strcmp(e, "fused"));
+  }();
+  return on;
+}
+
 // Y = A X.  Stencil operators (t ≥ 8): the plane-marching kernel without its Gram epilogue, after the
 // ghost-plane exchange.  Otherwise CSR with the halo exchange overlapped with the interior rows.
 eks_status spmm(eks_ctx* ctx, const Block& X, double* Y, int t) {
@@ -460,13 +481,16 @@ eks_status tn_reduce(eks_ctx* ctx, int t, int nl, const double* const* L, const 
 
 // Zout = Zin − Σ_j Q_j C_j  (CGS update)
 eks_status ts_update(eks_ctx* ctx, int t, int nq, const double* const* Q, const double* C, const double* Zin,
-                     double* Zout) {
+                     double* Zout, const double* const* RQ = nullptr) {
   if (eks::sweep_supported(t)) {
     const int maxb = eks::sweep_max_blocks(t);
     for (int j0 = 0; j0 < nq;) {
       const int k = std::min(maxb, nq - j0);
       eks::SweepPtrs P{};
-      for (int j = 0; j < k; ++j) P.q[j] = Q[j0 + j];
+      for (int j = 0; j < k; ++j) {
+        P.q[j] = Q[j0 + j];
+        P.rq[j] = RQ ? RQ[j0 + j] : nullptr;  // lazy blocks: Q_j = Z2_j R_j⁻¹
+      }
       account(ctx, EKS_K_UPDATE, 8.0 * ctx->n * ((double)k * t + 2.0 * t), 2.0 * ctx->n * t * t * k);
       KScope ks(ctx, EKS_K_UPDATE);
       CK(eks::launch_sweep(ctx->stream, t, k, 0, false, ctx->n, j0 == 0 ? Zin : Zout, Zout, P,
@@ -483,11 +507,13 @@ eks_status ts_update(eks_ctx* ctx, int t, int nq, const double* const* Q, const 
 
 // Fused CGS pass: Z1 = Z − Q C1 and C2 = (AQ)ᵀ Z1 in one sweep (nq ≤ 2 window of SRE-CG).
 eks_status update_coef(eks_ctx* ctx, int t, int nq, const double* const* Q, const double* const* AQ,
-                       const double* C1, const double* Z, double* Z1, double* C2, bool ar = true) {
+                       const double* C1, const double* Z, double* Z1, double* C2, bool ar = true,
+                       const double* const* RQ = nullptr) {
   eks::SweepPtrs P{};
   for (int j = 0; j < nq; ++j) {
     P.q[j] = Q[j];
     P.l[j] = AQ[j];
+    P.rq[j] = RQ ? RQ[j] : nullptr;
   }
   const size_t stride = eks::sweep_part_stride(t, nq, false);
   ST(ensure_part(ctx, stride * ctx->nblk));
@@ -528,6 +554,20 @@ eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const doubl
     ST(spmm(ctx, X, Y, t));
     const double* L[1] = {X.loc};
     return tn_reduce(ctx, t, 1, L, Y, r, out, ar);
+  }
+  if (t == 64 && spmm_path_for(ctx, t) == 4 && gram_split_env()) {
+    // t = 64: the plane-marching SpMM without its Gram, then the Gram [Z2ᵀ(AZ2) (upper tiles) | Z2ᵀr]
+    // as its own DMMA sweep over Z2 and AZ2 — the in-kernel CTA-level Gram was LSU/latency-bound
+    // (0.20 of HBM); measured faster together (profiles/spmm_micro_r02.txt)
+    ST(spmm(ctx, X, Y, t));
+    const size_t stride = eks::sweep_part_stride(t, 1, r != nullptr);
+    ST(ensure_part(ctx, stride * ctx->nblk));
+    account(ctx, EKS_K_COEF, 8.0 * ctx->n * (2.0 * t + (r ? 1.0 : 0.0)), ctx->n * t * (t + 8.0) + 2.0 * ctx->n * t);
+    {
+      KScope k(ctx, EKS_K_COEF);
+      CK(eks::launch_gram_upper(ctx->stream, t, ctx->n, X.loc, Y, r, ctx->part, ctx->nblk, tail(ctx, 2, out, stride)));
+    }
+    return (ar && ctx->nranks > 1) ? allreduce(ctx, out, stride) : EKS_OK;
   }
   if (grid_multi) {  // ghost planes first (the persistent kernel occupies every SM: no overlap)
     ST(halo_start(ctx, X, t));
@@ -573,8 +613,9 @@ eks_status spmm_gram(eks_ctx* ctx, const Block& X, double* Y, int t, const doubl
 
 // CGS2 of Z against the window (Q, AQ): two passes of C = (AQ)ᵀZ, Z -= Q C (reading R3/R24).
 eks_status cgs2(eks_ctx* ctx, int t, const std::vector<const double*>& Q, const std::vector<const double*>& AQ,
-                const double* Z, double* Zout) {
+                const double* Z, double* Zout, const std::vector<const double*>* RQv = nullptr) {
   const int nq = (int)Q.size();
+  const double* const* RQ = (RQv && !RQv->empty()) ? RQv->data() : nullptr;
   if (AQ.empty() && nq > 0) {
     // store-Q-only (reading R24): twice { C = Qᵀ(A·Z) ; Z = Z − Q·C } with explicit SpMMs — the
     // oracle's definition-mode algebra; Z and Z1 pass through the ext-layout scratch Ze (ghost rows)
@@ -597,12 +638,12 @@ eks_status cgs2(eks_ctx* ctx, int t, const std::vector<const double*>& Q, const 
   }
   ctx->c1_ready = false;  // (else C1 came fused from the previous block's R⁻¹ kernel)
   if (eks::sweep_supported(t) && eks::sweep_fused_supported(t, nq)) {
-    ST(update_coef(ctx, t, nq, Q.data(), AQ.data(), ctx->C1, Z, ctx->Z1.loc, ctx->C2));  // Z1, C2 = (AQ)ᵀ Z1
+    ST(update_coef(ctx, t, nq, Q.data(), AQ.data(), ctx->C1, Z, ctx->Z1.loc, ctx->C2, true, RQ));  // Z1, C2 = (AQ)ᵀ Z1
   } else {
-    ST(ts_update(ctx, t, nq, Q.data(), ctx->C1, Z, ctx->Z1.loc));
+    ST(ts_update(ctx, t, nq, Q.data(), ctx->C1, Z, ctx->Z1.loc, RQ));
     ST(tn_reduce(ctx, t, nq, AQ.data(), ctx->Z1.loc, nullptr, ctx->C2));
   }
-  ST(ts_update(ctx, t, nq, Q.data(), ctx->C2, ctx->Z1.loc, Zout));  // Z2 = Z1 − Q C2
+  ST(ts_update(ctx, t, nq, Q.data(), ctx->C2, ctx->Z1.loc, Zout, RQ));  // Z2 = Z1 − Q C2
   return EKS_OK;
 }
 
@@ -728,18 +769,19 @@ eks_status slot(eks_ctx* ctx, int t, int idx, Block** W, Block** AW) {
 }
 
 struct Window {
-  std::vector<const double*> Q, AQ;
+  std::vector<const double*> Q, AQ, RQ;  // RQ: R⁻¹ of lazy blocks (Q holds Z2), empty otherwise
 };
 
 // Window of the next block: SRE-CG → last min(2,#) blocks (Alg 4, reading R11);
 // SRE-CG2 / MSDO-CG → all blocks (Alg 3 P:151/Alg 6).
-Window window_for(eks_ctx* ctx, int method, int nblocks, int ring) {
+Window window_for(eks_ctx* ctx, int t, int method, int nblocks, int ring) {
   Window w;
   int first = (method == EKS_SRE_CG) ? std::max(0, nblocks - 2) : 0;
   for (int j = first; j < nblocks; ++j) {
     int idx = ring ? j % ring : j;
     w.Q.push_back(ctx->Wpool[idx].loc);
     if (!ctx->aq_off) w.AQ.push_back(ctx->AWpool[idx].loc);  // store-Q-only: AQ empty
+    if (ctx->lazy) w.RQ.push_back(ctx->Rslot + (size_t)idx * t * t);
   }
   return w;
 }
@@ -828,7 +870,7 @@ eks_status restructured_update(eks_ctx* ctx, int t, const double* W, const doubl
 // One A-orthonormalized block: Zsrc (or the split of r) → W_new, AW_new, R⁻¹, alpha_b.
 eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bool seed_from_r, const double* Zsrc,
                       Block* Wn, Block* AWn, int alpha_off, int gb, int mode) {
-  Window w = window_for(ctx, method, nblocks, ring);
+  Window w = window_for(ctx, t, method, nblocks, ring);
   if (seed_from_r) {
     double* dst = (w.Q.empty() && !ctx->use_prec) ? Wn->loc : ctx->Zs.loc;
     {
@@ -844,16 +886,19 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
     Zsrc = ctx->Zp.loc;
   }
   if (!w.Q.empty()) {
-    ST(cgs2(ctx, t, w.Q, w.AQ, Zsrc, Wn->loc));  // "A-orthonormalize W against Q"
+    ST(cgs2(ctx, t, w.Q, w.AQ, Zsrc, Wn->loc, &w.RQ));  // "A-orthonormalize W against Q"
   } else if (Zsrc != Wn->loc) {
     CK(cudaMemcpyAsync(Wn->loc, Zsrc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   if (ctx->ortho == 1) ST(pre_euclid(ctx, t, *Wn, AWn->loc, gb));  // Pre-CholQR (reading R30)
   // "A-orthonormalize W": A-CholQR with one SpMM of Z2 (AW = (A Z2) R⁻¹)
   const bool with_update = !(mode & 4);
+  // lazy basis: this block's R⁻¹ lives in its ring slot (the later windows fold it into their
+  // coefficients) and the R⁻¹ kernel leaves Z2 in the slot instead of W
+  double* Rinv = ctx->lazy ? ctx->Rslot + (size_t)(nblocks % ring) * t * t : ctx->Rinv;
   eks::CholArgs ch{};
   ch.R = ctx->Rm;
-  ch.Rinv = ctx->Rinv;
+  ch.Rinv = Rinv;
   ch.alpha = with_update ? ctx->alpha + alpha_off : nullptr;
   ch.flag = ctx->flag;
   ch.gblock = gb;
@@ -862,7 +907,7 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
   ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg, &ch));
   if (!ctx->chol_fused) {  // default: one-warp Cholesky launch (rsqrt pivots for t ≤ 32)
     KScope k(ctx, EKS_K_CHOL);
-    CK(eks::launch_chol_fast(ctx->stream, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, ctx->Rinv,
+    CK(eks::launch_chol_fast(ctx->stream, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, Rinv,
                              with_update ? ctx->alpha + alpha_off : nullptr, ctx->flag, gb));
   }
   // SRE-CG: the next block's window is {W_prev, W_new} and its Z is AW_new, so the R⁻¹ kernel
@@ -879,17 +924,21 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
   ctx->rho_fused = false;
   {
     KScope k(ctx, EKS_K_APPLY);
-    account(ctx, EKS_K_APPLY, 8.0 * ctx->n * (4.0 * t + 4.0 + (c1n == 2 ? t : 0)),
-            2.0 * ctx->n * t * (t + 2 + c1n * t));
+    // bytes: AZ2 read + AW written, Z2 read (eager or x update) + W written (eager), AW_prev (fused
+    // next-C1), the x/r vectors; flops: the triangular products (1 lazy, 2 eager), next-C1, x/r
+    const double nblk_io = (ctx->lazy ? 2.0 + (with_update ? 1.0 : 0.0) : 4.0) * t + (c1n == 2 ? t : 0) +
+                           (with_update ? 4.0 : 0.0);
+    account(ctx, EKS_K_APPLY, 8.0 * ctx->n * nblk_io,
+            (ctx->lazy ? 1.0 : 2.0) * ctx->n * t * (t + 8.0) + 2.0 * c1n * ctx->n * t * t + 4.0 * ctx->n * t);
     if (eks::sweep_supported(t)) {
       // partials [C1 | ‖rnew‖²] reduced by the kernel's last CTAs into C1 and scal[1]
       const size_t cnt1 = (size_t)c1n * t * t;
       const eks::Tail tl = (cnt1 + (last ? 1 : 0)) ? tail(ctx, 3, ctx->C1, cnt1 + (last ? 1 : 0), ctx->scal + 1,
                                                            (int)cnt1)
                                                     : eks::Tail{};
-      CK(eks::launch_apply_tc(ctx->stream, t, ctx->n, Wn->loc, AWn->loc, ctx->Rinv,
+      CK(eks::launch_apply_tc(ctx->stream, t, ctx->n, Wn->loc, AWn->loc, Rinv,
                               with_update ? ctx->alpha + alpha_off : nullptr, ctx->xv.loc, ctx->dx, ctx->r, ctx->rnew,
-                              ctx->flag, mode, ctx->nblk, c1n,
+                              ctx->flag, mode | (ctx->lazy ? 8 : 0), ctx->nblk, c1n,
                               c1n == 2 ? ctx->AWpool[(nblocks - 1) % ring].loc : nullptr, ctx->part2, tl));
       ctx->rho_fused = last;
     } else {
@@ -904,6 +953,24 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
     ctx->c1_ready = true;
   }
   return EKS_OK;
+}
+
+// lazy basis: W = Z2·R⁻¹ of ring slot idx into out (device, n×t): 0 − Z2·(−R⁻¹) on the update sweep.
+eks_status materialize_w(eks_ctx* ctx, int t, int idx, double* out) {
+  double* pack = ctx->pre + (size_t)2 * t * t;  // [G | R1⁻¹ | pack | g] scratch of Pre-CholQR
+  CK(eks::launch_ca_pack(ctx->stream, t, 1, ctx->Rslot + (size_t)idx * t * t, pack));
+  eks::SweepPtrs P{};
+  P.q[0] = ctx->Wpool[idx].loc;
+  CK(eks::launch_sweep(ctx->stream, t, 1, 0, false, ctx->n, nullptr, out, P, pack, nullptr, nullptr, ctx->nblk));
+  return EKS_OK;
+}
+
+bool lazy_env() {
+  static const bool on = [] {  // EKS_LAZY_W=0: materialize W in every block (A/B measurements)
+    const char* e = getenv("EKS_LAZY_W");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
 }
 
 // A-CholQR of one block in place (the Alg 7 seed): B = Zᵀ(AZ), R, W = Z R⁻¹, AW = (AZ) R⁻¹.
@@ -1093,6 +1160,12 @@ void plan_halo(int rank, int nranks, const int64_t* ranges, int64_t n, const int
                HaloPlan& P) {
   const int64_t row_begin = ranges[2 * rank], row_end = ranges[2 * rank + 1];
   const int64_t nnz = rp[n];
+  if (nranks == 1) {  // no ghosts: the extended columns are the columns (P.ecol left empty), all rows interior
+    P = HaloPlan{};
+    P.need.assign(2, 0);
+    P.int_hi = n;
+    return;
+  }
   auto owner = [&](int64_t c) {
     int q = 0;
     while (q < nranks && !(c >= ranges[2 * q] && c < ranges[2 * q + 1])) ++q;
@@ -1261,7 +1334,10 @@ bool grid_plan_host(int64_t n, const int64_t* rp, const int32_t* col, const doub
                     int64_t halo_before, int64_t halo_after, int64_t geom[6], std::vector<double>& sv) {
   int64_t pos[3] = {0, 0, 0};
   int np = 0;
-  for (int64_t i = 0; i < n && np <= 3; ++i)
+  // the offsets from the first rows (a stencil shows all of them within a few planes); an offset
+  // first appearing later is caught by the full check below (not a stencil: nothing built)
+  const int64_t scan = std::min<int64_t>(n, (int64_t)1 << 22);
+  for (int64_t i = 0; i < scan && np <= 3; ++i)
     for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
       const int64_t o = (int64_t)col[p] - (row_begin + i);
       if (o <= 0) continue;
@@ -1320,13 +1396,11 @@ bool grid_plan_host(int64_t n, const int64_t* rp, const int32_t* col, const doub
   return true;
 }
 
-eks_status build_grid_plan(eks_ctx* ctx, int64_t n, const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
-                           const std::vector<double>& val, int64_t row_begin, int64_t halo_before,
-                           int64_t halo_after) {
+eks_status build_grid_plan(eks_ctx* ctx, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
+                           int64_t row_begin, int64_t halo_before, int64_t halo_after) {
   int64_t g[6];
   std::vector<double> sv;
-  if (!grid_plan_host(n, rp.data(), col.data(), val.data(), row_begin, halo_before, halo_after, g, sv))
-    return EKS_OK;
+  if (!grid_plan_host(n, rp, col, val, row_begin, halo_before, halo_after, g, sv)) return EKS_OK;
   CK(cudaMalloc((void**)&ctx->d_sv, sizeof(double) * sv.size()));
   CK(cudaMemcpy(ctx->d_sv, sv.data(), sizeof(double) * sv.size(), cudaMemcpyHostToDevice));
   ctx->gplan.nx = (int)g[0];
@@ -1406,6 +1480,7 @@ void begin_run(eks_ctx* ctx, const eks_options* opt) {
   ctx->model_bytes = ctx->model_flops = 0.0;
   ctx->c1_ready = false;
   ctx->aq_off = false;  // set per solve (full-basis methods)
+  ctx->lazy = false;    // set per solve / sweep (s-step SRE-CG, t ≥ 8)
 }
 
 }  // namespace
@@ -1494,39 +1569,72 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   if (n_global >= INT_MAX) return fail(ctx, EKS_ERR_INVALID_ARG, "n_global must be < 2^31 (int32 columns)");
   CK(cudaSetDevice(ctx->device));
   const int64_t n = row_end - row_begin;
-  std::vector<int64_t> rp(n + 1);
-  if (where == EKS_MEM_HOST) memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1));
-  else CK(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
-  if (rp[0] != 0) return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr[0] != 0");
-  for (int64_t i = 0; i < n; ++i)
-    if (rp[i + 1] < rp[i]) return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr not monotone at row %lld", (long long)i);
-  const int64_t nnz = rp[n];
-  if (nnz >= INT_MAX) return fail(ctx, EKS_ERR_INVALID_ARG, "local nnz must be < 2^31");
-  std::vector<int32_t> col(nnz);
-  std::vector<double> val(nnz);
-  if (where == EKS_MEM_HOST) {
-    memcpy(col.data(), col_idx, sizeof(int32_t) * nnz);
-    memcpy(val.data(), vals, sizeof(double) * nnz);
-  } else {
-    CK(cudaMemcpy(col.data(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(val.data(), vals, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+  // host views of the caller's arrays (EKS_MEM_HOST: used in place, no copy; device: copied down)
+  std::vector<int64_t> rpv;
+  std::vector<int32_t> colv;
+  std::vector<double> valv;
+  const int64_t* RP = row_ptr;
+  if (where != EKS_MEM_HOST) {
+    rpv.resize(n + 1);
+    CK(cudaMemcpy(rpv.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+    RP = rpv.data();
   }
-  // validation (SPEC S:30-33 invariants): sorted unique columns in range, positive diagonal
-  for (int64_t i = 0; i < n; ++i) {
-    bool diag = false;
-    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-      const int64_t c = col[p];
-      if (c < 0 || c >= n_global) return fail(ctx, EKS_ERR_BAD_MATRIX, "column %lld out of range in row %lld",
-                                              (long long)c, (long long)(row_begin + i));
-      if (p > rp[i] && col[p - 1] >= c)
-        return fail(ctx, EKS_ERR_BAD_MATRIX, "columns not strictly ascending in row %lld", (long long)(row_begin + i));
-      if (c == row_begin + i) {
-        if (!(val[p] > 0.0)) return fail(ctx, EKS_ERR_BAD_MATRIX, "non-positive diagonal in row %lld",
-                                         (long long)(row_begin + i));
-        diag = true;
+  if (RP[0] != 0) return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr[0] != 0");
+  for (int64_t i = 0; i < n; ++i)
+    if (RP[i + 1] < RP[i]) return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr not monotone at row %lld", (long long)i);
+  const int64_t nnz = RP[n];
+  if (nnz >= INT_MAX) return fail(ctx, EKS_ERR_INVALID_ARG, "local nnz must be < 2^31");
+  const int32_t* COL = col_idx;
+  const double* VAL = vals;
+  if (where != EKS_MEM_HOST) {
+    colv.resize(nnz);
+    valv.resize(nnz);
+    CK(cudaMemcpy(colv.data(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(valv.data(), vals, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+    COL = colv.data();
+    VAL = valv.data();
+  }
+  // validation (SPEC S:30-33 invariants): sorted unique columns in range, positive diagonal — on all
+  // host threads; the first failing row (lowest index) is reported
+  {
+    std::mutex mu;
+    int64_t bad_row = INT64_MAX;
+    int bad_kind = 0;
+    int64_t maxrow = 0;
+    parallel_rows(n, [&](int64_t lo, int64_t hi) {
+      int64_t mr = 0;
+      for (int64_t i = lo; i < hi; ++i) {
+        mr = std::max(mr, RP[i + 1] - RP[i]);
+        int kind = 0;
+        bool diag = false;
+        for (int64_t p = RP[i]; p < RP[i + 1] && !kind; ++p) {
+          const int64_t c = COL[p];
+          if (c < 0 || c >= n_global) kind = 1;
+          else if (p > RP[i] && COL[p - 1] >= c) kind = 2;
+          else if (c == row_begin + i) {
+            if (!(VAL[p] > 0.0)) kind = 3;
+            diag = true;
+          }
+        }
+        if (!kind && !diag) kind = 4;
+        if (kind) {
+          std::lock_guard<std::mutex> g(mu);
+          if (i < bad_row) {
+            bad_row = i;
+            bad_kind = kind;
+          }
+          break;
+        }
       }
+      std::lock_guard<std::mutex> g(mu);
+      maxrow = std::max(maxrow, mr);
+    });
+    if (bad_kind) {
+      static const char* what[] = {"", "column out of range", "columns not strictly ascending",
+                                   "non-positive diagonal", "missing diagonal"};
+      return fail(ctx, EKS_ERR_BAD_MATRIX, "%s in row %lld", what[bad_kind], (long long)(row_begin + bad_row));
     }
-    if (!diag) return fail(ctx, EKS_ERR_BAD_MATRIX, "missing diagonal in row %lld", (long long)(row_begin + i));
+    ctx->maxrow = maxrow;
   }
   // ---- slab table of all ranks
   std::vector<int64_t> ranges(2 * ctx->nranks);
@@ -1546,7 +1654,7 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   }
   // ---- halo plan (host-only, also exported as eks_plan_halo for the multi-rank CPU tests)
   HaloPlan plan;
-  plan_halo(ctx->rank, ctx->nranks, ranges.data(), n, rp.data(), col.data(), plan);
+  plan_halo(ctx->rank, ctx->nranks, ranges.data(), n, RP, COL, plan);
   const int64_t old_before = ctx->halo_before, old_after = ctx->halo_after;
   ctx->recvs = plan.recvs;
   ctx->sends.clear();
@@ -1570,11 +1678,9 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
       if (hi > lo) ctx->sends.push_back({q, lo, hi});
     }
   }
-  const std::vector<int32_t>& ecol = plan.ecol;
+  const int32_t* ECOL = plan.ecol.empty() ? COL : plan.ecol.data();  // one rank: the columns themselves
   ctx->int_lo = plan.int_lo;
   ctx->int_hi = plan.int_hi;
-  ctx->maxrow = 0;
-  for (int64_t i = 0; i < n; ++i) ctx->maxrow = std::max<int64_t>(ctx->maxrow, rp[i + 1] - rp[i]);
   // ---- upload (the block workspace survives when the slab geometry is unchanged)
   if (!ctx->have_matrix || ctx->n != n || old_before != ctx->halo_before || old_after != ctx->halo_after)
     free_workspace(ctx);
@@ -1597,23 +1703,28 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   ctx->ell_w = 0;
   ctx->have_matrix = false;
   std::vector<int32_t> rp32(n + 1);
-  for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)rp[i];
+  parallel_rows(n + 1, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) rp32[i] = (int32_t)RP[i];
+  });
   // +16 bytes of padding: the fused SpMM copies aligned 16-byte chunks that may run past the end
   CK(cudaMalloc((void**)&ctx->d_rp, sizeof(int) * (n + 1) + 16));
   CK(cudaMalloc((void**)&ctx->d_col, sizeof(int) * nnz + 16));
   CK(cudaMalloc((void**)&ctx->d_val, sizeof(double) * nnz + 16));
   CK(cudaMemcpy(ctx->d_rp, rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->d_col, ecol.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->d_val, val.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_col, ECOL, sizeof(int) * nnz, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_val, VAL, sizeof(double) * nnz, cudaMemcpyHostToDevice));
   // ELL copy for the fused SpMM+Gram when every row has ≤ 8 entries (tiles of kEllTR rows,
   // slot-major inside a tile; padding: value 0 and the row's own column)
   // the plane-marching plan first: when it applies (one rank, stencil structure) and no path is
   // forced (EKS_SPMM_PATH), the ELL copy and the TMA segment plan are never used, so they are not
   // built (host setup time is part of the end-to-end number)
-  ST(build_grid_plan(ctx, n, rp, col, val, row_begin, plan.halo_before, plan.halo_after));
+  ST(build_grid_plan(ctx, n, RP, COL, VAL, row_begin, plan.halo_before, plan.halo_after));
   const bool skip_alt = ctx->grid_ok && ctx->spmm_path == 0;
   const int w = skip_alt ? 0 : eks::ell_width((int)ctx->maxrow);
   if (w > 0) {
+    const std::vector<int64_t> rp(RP, RP + n + 1);
+    const std::vector<int32_t> ecol(ECOL, ECOL + nnz);
+    const std::vector<double> val(VAL, VAL + nnz);
     const int64_t TR = eks::kEllTR, ntiles = (n + TR - 1) / TR;
     std::vector<int32_t> ec((size_t)ntiles * TR * w), tmax((size_t)ntiles, 0);
     std::vector<double> ev((size_t)ntiles * TR * w, 0.0);
@@ -2006,6 +2117,8 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   if (aqc < 0 || aqc > 2) return fail(ctx, EKS_ERR_INVALID_ARG, "aq_cache must be 0 (auto), 1 (on) or 2 (off)");
   ctx->aq_off = !ring && !ca && !restr && aqc != 1;
   ctx->last_aq_off = ctx->aq_off;
+  ctx->lazy = method == EKS_SRE_CG && !restr && eks::sweep_supported(t) && lazy_env();
+  ctx->last_lazy = ctx->lazy;
   int plan_fit = -1;  // memory planner: outer iterations the device can hold (full-basis methods)
   if (!ring) {
     size_t fr = 0, tot = 0;
@@ -2222,6 +2335,8 @@ eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks_total, const double*
   ctx->use_prec = false;
   ctx->ortho = 0;
   ctx->last_aq_off = false;
+  ctx->lazy = eks::sweep_supported(t) && lazy_env();
+  ctx->last_lazy = ctx->lazy;
   EventPair ev;
   CK(ev.create());
   CK(cudaEventRecord(ev.e0, ctx->stream));
@@ -2239,7 +2354,12 @@ eks_status eks_basis_sweep(eks_ctx* ctx, int t, int nblocks_total, const double*
     }
     ST(make_block(ctx, t, EKS_SRE_CG, ring, j, false, Zsrc, Wn, AWn, 0, j, 4));
   }
-  ST(copy_out(ctx, W_last, ctx->Wpool[(nblocks_total - 1) % ring].loc, ctx->n * t, where));
+  if (ctx->lazy) {  // W_last = Z2 R⁻¹ of the last slot (through the scratch block Zs)
+    ST(materialize_w(ctx, t, (nblocks_total - 1) % ring, ctx->Zs.loc));
+    ST(copy_out(ctx, W_last, ctx->Zs.loc, ctx->n * t, where));
+  } else {
+    ST(copy_out(ctx, W_last, ctx->Wpool[(nblocks_total - 1) % ring].loc, ctx->n * t, where));
+  }
   ctx->last_t = t;
   ctx->last_nblocks = nblocks_total;
   ctx->last_ring = ring;
@@ -2274,7 +2394,8 @@ eks_status eks_plan_halo(int rank, int nranks, const int64_t* ranges, const int6
     if (col[p] < 0 || col[p] >= ranges[2 * nranks - 1]) return EKS_ERR_BAD_MATRIX;
   HaloPlan P;
   plan_halo(rank, nranks, ranges, n, row_ptr, col, P);
-  memcpy(ext_col, P.ecol.data(), sizeof(int32_t) * P.ecol.size());
+  if (P.ecol.empty()) memcpy(ext_col, col, sizeof(int32_t) * row_ptr[n]);  // one rank: unchanged
+  else memcpy(ext_col, P.ecol.data(), sizeof(int32_t) * P.ecol.size());
   memcpy(need, P.need.data(), sizeof(int64_t) * P.need.size());
   geom[0] = P.halo_before;
   geom[1] = P.halo_after;
@@ -2405,7 +2526,7 @@ eks_status eks_k_acholqr(eks_ctx* ctx, int t, const double* Z, double* W, double
 eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, const double* v, int variant, int reps,
                            double* ms) {
   ST(k_ready(ctx, t));
-  if (!X || !Y || !ms || reps < 1 || variant < 0 || variant > 6)
+  if (!X || !Y || !ms || reps < 1 || variant < 0 || variant > 7)
     return fail(ctx, EKS_ERR_INVALID_ARG, "bad eks_k_time_spmm arguments");
   if (variant > 0 && !eks::sweep_supported(t))
     return fail(ctx, EKS_ERR_INVALID_ARG, "fused SpMM+Gram needs t in {8,16,32,64}");
@@ -2426,7 +2547,12 @@ eks_status eks_k_time_spmm(eks_ctx* ctx, int t, const double* X, double* Y, cons
     path = 4;
   }
   const bool use_seg = path == 0, use_ell = path == 1;
+  Block xb7;
+  xb7.base = const_cast<double*>(X);
+  xb7.loc = xb7.base;
   auto run = [&]() -> cudaError_t {
+    if (variant == 7)  // exactly the solve's SpMM-block step (spmm_gram): fused, or SpMM + Gram sweep at t = 64
+      return spmm_gram(ctx, xb7, Y, t, v, ctx->Bg) == EKS_OK ? cudaSuccess : cudaErrorUnknown;
     if (variant == 0)
       return eks::launch_spmm(ctx->stream, t, 0, (int)ctx->n, ctx->d_rp, ctx->d_col, ctx->d_val, X, Y, ctx->sms);
     if (path == 4) {
@@ -2477,7 +2603,8 @@ eks_status eks_k_last_basis(eks_ctx* ctx, int j, double* W, double* AW) {
     return fail(ctx, EKS_ERR_INVALID_ARG, "basis block %d not resident (%d blocks built, ring %d)", j, nb, ring);
   const int idx = ring ? j % ring : j;
   if (idx >= (int)ctx->Wpool.size() || !ctx->Wpool[idx].base) return fail(ctx, EKS_ERR_INVALID_ARG, "no basis block %d", j);
-  CK(cudaMemcpyAsync(W, ctx->Wpool[idx].loc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (ctx->last_lazy) ST(materialize_w(ctx, t, idx, W));  // the slot holds Z2 and R⁻¹
+  else CK(cudaMemcpyAsync(W, ctx->Wpool[idx].loc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
   if (AW && ctx->last_aq_off && !ring && j < nb - 2)
     return fail(ctx, EKS_ERR_INVALID_ARG, "A·W of block %d is not kept (store-Q-only solve: the last 2 blocks)", j);
   if (AW)

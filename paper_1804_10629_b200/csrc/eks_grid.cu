@@ -519,7 +519,7 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
     const char* e = getenv("EKS_GRID_PATCH");
     return !(e && atoi(e) == 0);
   }();
-  constexpr bool PATCH_T = (T == 16 || T == 32) && W == 7;
+  constexpr bool PATCH_T = T == 16 && W == 7;  // t = 32: measured slower (0.57 vs 0.63, profiles/spmm_micro_r02.txt)
   const bool patch = PATCH_T && W == 7 && patch_env && by % 4 == 0;
   int ns = (int)((220 * 1024 - fixed) / SB);
   if (ns > 8) ns = 8;

@@ -71,7 +71,9 @@ __device__ __forceinline__ void vec_async(double* dst, const double* src, int64_
 // ----------------------------------------------------------------------------
 // AL: the last left block is Zin itself (SRE-CG: Z = A·W_{j−1} = AQ_last), so it is streamed
 // once and R goes to a separate (unstaged) tile.
-template <int T, int NQ, int NL, bool V, bool AL = false>
+// UP (NQ = 0, NL = 1): only the upper 8×8 tiles of L_0ᵀR (the A-CholQR Gram, whose lower triangle is never
+// read, reading R4), the lower ones mirrored into the partial.
+template <int T, int NQ, int NL, bool V, bool AL = false, bool UP = false>
 struct SwCfg {
   static constexpr int TR = (T == 8) ? 64 : 32;  // rows per tile
   static constexpr int S = T + 4;                // padded smem row stride (doubles)
@@ -90,9 +92,10 @@ struct SwCfg {
   static constexpr int UPW = UT / 8;
   // partial products: NL·(T/8)² output tiles; WS row slices when fewer than 8
   static constexpr int MT = T / 8;
-  static constexpr int OT = NL * MT * MT;
+  static constexpr int OT = UP ? MT * (MT + 1) / 2 : NL * MT * MT;
   static constexpr int WS = (NL == 0) ? 1 : (OT >= 8 ? 1 : 8 / OT);
-  static constexpr int TPW = (NL == 0) ? 0 : (OT >= 8 ? OT / 8 : 1);
+  static constexpr int TPW = (NL == 0) ? 0 : (OT >= 8 ? (OT + 7) / 8 : 1);
+  static_assert(!UP || (NQ == 0 && NL == 1 && OT >= 8), "upper Gram: one left block, t >= 32");
   static constexpr int PER = NL * T * T + (V ? T : 0);  // partial doubles per CTA
   static constexpr int RED = (WS > 1 ? 8 * NL * T * T : 0) + (V ? 8 * T : 0);
   static constexpr int SMEM0 = NS * STAGE + CDBL;
@@ -102,11 +105,21 @@ struct SwCfg {
   static constexpr bool CREG = NQ > 0 && NCF <= 16;
 };
 
-template <int T, int NQ, int NL, bool V, bool AL = false>
+// upper 8×8 tile number u (row-major over mi ≤ ni) → (mi, ni)
+__device__ __forceinline__ void upper_tile(int u, int mt, int& mi, int& ni) {
+  mi = 0;
+  while (u >= mt - mi) {
+    u -= mt - mi;
+    ++mi;
+  }
+  ni = mi + u;
+}
+
+template <int T, int NQ, int NL, bool V, bool AL = false, bool UP = false>
 __global__ void __launch_bounds__(256, 1)
     k_sweep(int64_t n, const double* Zin, double* Zout, const SweepPtrs P,
             const double* __restrict__ Cm, const double* __restrict__ v, double* __restrict__ part, const Tail tl) {
-  using K = SwCfg<T, NQ, NL, V, AL>;
+  using K = SwCfg<T, NQ, NL, V, AL, UP>;
   static_assert(!AL || (NQ > 0 && NL > 0 && !V), "alias needs an update and left blocks");
   pdl_enter();
   constexpr int S = K::S;
@@ -118,8 +131,34 @@ __global__ void __launch_bounds__(256, 1)
   double* sC = sm + K::NS * K::STAGE;
   double* sRb = sC + NQ * T * K::SC;  // R tile (AL only)
 
-  if constexpr (NQ > 0)
+  if constexpr (NQ > 0) {
     for (int e = tid; e < NQ * T * T; e += 256) sC[(e / T) * K::SC + e % T] = Cm[e];
+    // lazy basis blocks: C_j ← R_j⁻¹ C_j (R⁻¹ upper triangular, ascending k, fma), the stage area as
+    // scratch before the first tiles are issued — every CTA computes the same folded coefficients
+    bool lazy = false;
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) lazy = lazy || P.rq[j] != nullptr;
+    if (lazy) {
+      double* tR = sm;
+      double* tO = sm + T * T;
+#pragma unroll 1
+      for (int j = 0; j < NQ; ++j) {
+        if (P.rq[j] == nullptr) continue;
+        __syncthreads();
+        for (int e = tid; e < T * T; e += 256) tR[e] = P.rq[j][e];
+        __syncthreads();
+        for (int e = tid; e < T * T; e += 256) {
+          const int i = e / T, c = e % T;
+          double v = 0.0;
+          for (int k = i; k < T; ++k) v = fma(tR[i * T + k], sC[(j * T + k) * K::SC + c], v);
+          tO[e] = v;
+        }
+        __syncthreads();
+        for (int e = tid; e < T * T; e += 256) sC[(j * T + e / T) * K::SC + e % T] = tO[e];
+      }
+      __syncthreads();
+    }
+  }
   double cf[K::CREG ? K::NCF : 1];
   if constexpr (K::CREG) {
     __syncthreads();
@@ -156,6 +195,14 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
   for (int j = 0; j < (K::TPW > 0 ? K::TPW : 1); ++j) acc[j][0] = acc[j][1] = 0.0;
   double accv[2] = {0.0, 0.0};
+  int umi[UP ? K::TPW : 1], uni[UP ? K::TPW : 1];  // UP: this warp's upper tiles, decoded once
+  if constexpr (UP) {
+#pragma unroll
+    for (int u = 0; u < K::TPW; ++u) {
+      const int tile = (warp / K::WS) * K::TPW + u;
+      upper_tile(tile < K::OT ? tile : 0, K::MT, umi[u], uni[u]);
+    }
+  }
 
   for (int i = 0; i < ntiles; ++i) {
     cp_wait<K::NS - 2>();
@@ -197,7 +244,13 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int u = 0; u < K::TPW; ++u) {
         const int tile = (warp / K::WS) * K::TPW + u;
-        const int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
+        int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
+        if constexpr (UP) {
+          if (tile >= K::OT) continue;
+          l = 0;
+          mi = umi[u];
+          ni = uni[u];
+        }
         const double* sL = (AL && l == NL - 1) ? sZ : st + (1 + NQ + l) * K::TILE;
         const double* sR = AL ? sRb : sZ;
         double d0 = acc[u][0], d1 = acc[u][1];
@@ -229,7 +282,16 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int u = 0; u < K::TPW; ++u) {
         const int tile = warp * K::TPW + u;
-        const int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
+        int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
+        if constexpr (UP) {
+          if (tile >= K::OT) continue;
+          l = 0;
+          upper_tile(tile, K::MT, mi, ni);
+          if (mi < ni) {  // mirrored lower tile
+            out[(ni * 8 + 2 * q4) * T + mi * 8 + g] = acc[u][0];
+            out[(ni * 8 + 2 * q4 + 1) * T + mi * 8 + g] = acc[u][1];
+          }
+        }
         *reinterpret_cast<double2*>(out + l * T * T + (mi * 8 + g) * T + ni * 8 + 2 * q4) =
             make_double2(acc[u][0], acc[u][1]);
       }
@@ -308,10 +370,19 @@ __global__ void __launch_bounds__(256, 1)
   const int ntiles = (int)((hi - lo + K::TR - 1) / K::TR);
   double* sRi = sm + K::NS * K::STAGE;
   double* sA = sRi + T * SR;
-  const bool first = mode & 1, last = mode & 2, basis = mode & 4;
+  const bool first = mode & 1, last = mode & 2, basis = mode & 4, lazy = mode & 8;
   const bool skip = basis || (flag != nullptr && *flag != INT_MAX);
   for (int e = tid; e < T * T; e += 256) sRi[(e / T) * SR + e % T] = Rinv[e];
-  for (int e = tid; e < T; e += 256) sA[e] = alpha ? alpha[e] : 0.0;
+  // lazy: x += W α̃ = Z2 β with β = R⁻¹ α̃ (R⁻¹ upper triangular)
+  for (int e = tid; e < T; e += 256) {
+    double v = 0.0;
+    if (alpha && lazy)
+      for (int k = e; k < T; ++k) v = fma(Rinv[e * T + k], alpha[k], v);
+    else if (alpha)
+      v = alpha[e];
+    sA[e] = v;
+  }
+  const bool zread = !(lazy && basis);  // Z2 tiles are needed for W (eager) or for x += Z2 β (lazy)
   constexpr int VOFF = (C1N == 2 ? 3 : 2) * K::TILE;  // vectors after the tiles
   auto issue = [&](int i) {
     if (i < ntiles) {
@@ -319,7 +390,7 @@ __global__ void __launch_bounds__(256, 1)
       const int64_t row = lo + (int64_t)i * K::TR;
       const int rows = (int)((hi - row) < K::TR ? (hi - row) : K::TR);
       double* st = sm + s * K::STAGE;
-      tile_async<T, S, K::TR>(st, Z2W, row, rows);
+      if (zread) tile_async<T, S, K::TR>(st, Z2W, row, rows);
       tile_async<T, S, K::TR>(st + K::TILE, AZ2AW, row, rows);
       if constexpr (C1N == 2) tile_async<T, S, K::TR>(st + 2 * K::TILE, AWprev, row, rows);
       if (!skip) {
@@ -372,12 +443,16 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int kk = 0; kk < (T < 8 * (ni + 1) ? T : 8 * (ni + 1)); kk += 4) {
         const double b = RREG ? rf[ni * (T / 4) + kk / 4] : sRi[(kk + q4) * SR + ni * 8 + g];
-        dmma(w0, w1, sZ[rr * S + kk + q4], b);
+        if (!lazy) dmma(w0, w1, sZ[rr * S + kk + q4], b);
         dmma(y0, y1, sY[rr * S + kk + q4], b);
       }
       const int c = ni * 8 + 2 * q4;
+      if (lazy && zread) {  // the x update multiplies Z2 by β (no W)
+        w0 = sZ[rr * S + c];
+        w1 = sZ[rr * S + c + 1];
+      }
       if (rr < rows) {
-        *reinterpret_cast<double2*>(Z2W + (row + rr) * T + c) = make_double2(w0, w1);
+        if (!lazy) *reinterpret_cast<double2*>(Z2W + (row + rr) * T + c) = make_double2(w0, w1);
         *reinterpret_cast<double2*>(AZ2AW + (row + rr) * T + c) = make_double2(y0, y1);
       }
       yk[ni][0] = y0;
@@ -1127,21 +1202,35 @@ static int grid_for(int nblk_max, int occ) {
   const int g = sms * occ;
   return g < nblk_max ? g : nblk_max;
 }
-template <int T, int NQ, int NL, bool V, bool AL = false>
+template <int T, int NQ, int NL, bool V, bool AL = false, bool UP = false>
 static cudaError_t launch_sweep_t(cudaStream_t st, int64_t n, const double* Zin, double* Zout, const SweepPtrs& P,
                                   const double* C, const double* v, double* part, int nblk, const Tail& tl) {
-  using K = SwCfg<T, NQ, NL, V, AL>;
+  using K = SwCfg<T, NQ, NL, V, AL, UP>;
   const size_t sm = (size_t)K::SMEM * 8;
   if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
   static int occ = 0;
   if (!occ) {
-    cudaFuncSetAttribute(k_sweep<T, NQ, NL, V, AL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<T, NQ, NL, V, AL>, 256, sm);
+    cudaFuncSetAttribute(k_sweep<T, NQ, NL, V, AL, UP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<T, NQ, NL, V, AL, UP>, 256, sm);
     if (occ < 1) occ = 1;
   }
   nblk = grid_for(nblk, occ);
   t_last_grid = nblk;
-  return launch_k(k_sweep<T, NQ, NL, V, AL>, nblk, 256, sm, st, n, Zin, Zout, P, C, v, part, NL > 0 ? tl : Tail{});
+  return launch_k(k_sweep<T, NQ, NL, V, AL, UP>, nblk, 256, sm, st, n, Zin, Zout, P, C, v, part,
+                  NL > 0 ? tl : Tail{});
+}
+
+cudaError_t launch_gram_upper(cudaStream_t st, int t, int64_t n, const double* X, const double* Y, const double* v,
+                              double* part, int nblk, const Tail& tl) {
+  SweepPtrs P{};
+  P.l[0] = X;
+  switch (t) {
+    case 32: return v ? launch_sweep_t<32, 0, 1, true, false, true>(st, n, Y, nullptr, P, nullptr, v, part, nblk, tl)
+                      : launch_sweep_t<32, 0, 1, false, false, true>(st, n, Y, nullptr, P, nullptr, v, part, nblk, tl);
+    case 64: return v ? launch_sweep_t<64, 0, 1, true, false, true>(st, n, Y, nullptr, P, nullptr, v, part, nblk, tl)
+                      : launch_sweep_t<64, 0, 1, false, false, true>(st, n, Y, nullptr, P, nullptr, v, part, nblk, tl);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 #define EKS_SW_T(t, ...)                                   \

@@ -11,6 +11,9 @@ constexpr int kSweepMaxBlocks = 8;
 struct SweepPtrs {
   const double* q[kSweepMaxBlocks];  // update blocks Q_j (Zout = Zin − Σ_j Q_j C_j)
   const double* l[kSweepMaxBlocks];  // left blocks L_j of the partial products L_jᵀ R
+  // lazy basis blocks (W_j = Z2_j R_j⁻¹ never formed): q[j] holds Z2_j and rq[j] its R_j⁻¹ (t×t,
+  // upper triangular); the sweep uses the coefficient R_j⁻¹ C_j (folded in its prologue).  NULL: q[j] is W_j.
+  const double* rq[kSweepMaxBlocks];
 };
 
 bool sweep_supported(int t);
@@ -75,6 +78,10 @@ struct GridPlan {
   const double* sv = nullptr;
 };
 bool spmm_grid_fits(int t, const GridPlan& gp);
+// The A-CholQR Gram [XᵀY (upper 8×8 tiles, lower mirrored) | Xᵀv] as a separate sweep over X and Y
+// (t ∈ {32, 64}; per-CTA partials of layout sweep_part_stride(t,1,v), tail-reduced into tl.out).
+cudaError_t launch_gram_upper(cudaStream_t st, int t, int64_t n, const double* X, const double* Y, const double* v,
+                              double* part, int nblk, const Tail& tl);
 bool spmm_grid_fused_chol(int t);  // ch.on allowed: the last CTA runs the solve-path Cholesky
 // gram = false: Y = A·X only (no Y scratch, no DMMA, no partials; part and tl unused) — the plain
 // SpMM of the CA monomial powers, the store-Q-only CGS2 products and the residual.
@@ -90,6 +97,8 @@ cudaError_t launch_spmm_gram(cudaStream_t st, int t, int64_t n, const int* rp, c
 // [AW_prev, AW]ᵀ AW (c1n = 2) or AWᵀAW (c1n = 1) — the SRE-CG window — then ‖rnew‖² (last block).
 // They are reduced by the grid's tail into tl (tl.count = c1n·t·t [+1]); tl.cnt == NULL: none.
 bool apply_c1_supported(int t, int c1n);
+// mode bit 8 (lazy basis, SRE-CG): W = Z2·R⁻¹ is NOT written (Z2 stays the stored block); x += Z2 (R⁻¹α̃);
+// with bit 4 (no x/r update) Z2 is not even read.  AW = AZ2·R⁻¹ is always formed (in place).
 cudaError_t launch_apply_tc(cudaStream_t st, int t, int64_t n, double* Z2W, double* AZ2AW, const double* Rinv,
                             const double* alpha, double* x, double* dx, const double* r, double* rnew, const int* flag,
                             int mode, int nblk, int c1n, const double* AWprev, double* part, const Tail& tl);
