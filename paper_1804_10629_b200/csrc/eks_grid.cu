@@ -20,8 +20,12 @@
 #include "eks_device.cuh"
 #include "eks_sweep.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 namespace eks {
 
@@ -57,10 +61,28 @@ struct GrCfg {
 
 // Stage bytes: X plane-block (bx+2)·(by+2·hy) rows, then R rows of VS stencil values, then R
 // entries of r.
+// SWZ (the t = 16 patch kernel): the X plane-block arrives by 2D tensor-map TMA with the 128-byte
+// swizzle — every X row is one 128-byte line whose 16-byte chunks are permuted by (point & 7) —
+// each y-line padded to a multiple of 8 points (PWP) so that every line starts on a 1024-byte
+// swizzle atom; stages are 1024-byte aligned.
+__host__ __device__ inline int grid_pwp(int bx, bool swz) { return swz ? ((bx + 2 + 7) & ~7) : bx + 2; }
 template <int T>
-__host__ __device__ inline size_t grid_stage_bytes(int bx, int by, int hy, int vs) {
+__host__ __device__ inline size_t grid_xbytes(int bx, int by, int hy, bool swz) {
+  return (size_t)grid_pwp(bx, swz) * (by + 2 * hy) * T * 8;
+}
+template <int T>
+__host__ __device__ inline size_t grid_stage_bytes(int bx, int by, int hy, int vs, bool swz = false) {
   using K = GrCfg<T>;
-  return (((size_t)(bx + 2) * (by + 2 * hy) * T * 8 + (size_t)K::R * vs * 8 + (size_t)K::R * 8) + 127) & ~(size_t)127;
+  const size_t a = swz ? 1023 : 127;
+  return ((grid_xbytes<T>(bx, by, hy, swz) + (size_t)K::R * vs * 8 + (size_t)K::R * 8) + a) & ~a;
+}
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          saddr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(saddr(bar))
+      : "memory");
 }
 
 // PATCH (3D, t = 16, 32): every group of T/2 lanes (one double2 column pair per lane) forms a 1 × 4
@@ -71,18 +93,23 @@ template <int T, int W, bool PATCH = false>
 __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
     k_spmm_grid(const GridPlan gp, int bx, int by, int zc, const double* __restrict__ X, double* __restrict__ Y,
                 const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch, int NS,
-                const bool gram) {
+                const bool gram, const __grid_constant__ CUtensorMap tmX) {
   using K = GrCfg<T>;
   pdl_enter();
   constexpr int S = K::S, G = K::G, C = K::C, RW = K::RW, NWC = K::NWC, MT = K::MT, H = T / 2;
   constexpr int VS = (W + 1) & ~1;
   static_assert(W == 5 || W == 7, "2D 5-point or 3D 7-point stencil");
-  extern __shared__ __align__(128) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw_[];
+  constexpr bool SWZ = PATCH;  // the patch kernel streams X by swizzled tensor-map TMA
+  unsigned char* smraw =
+      SWZ ? reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw_) + 1023) & ~(uintptr_t)1023) : smraw_;
   const int nx = gp.nx, ny = gp.ny, nz = gp.nz;
   const int hy = ny > 1 ? 1 : 0;               // y halo (3D only)
   const int PW = bx + 2, PH = by + 2 * hy;     // plane-block extent
+  const int PWP = grid_pwp(bx, SWZ);           // points per y-line in shared memory
   const int64_t plane = (int64_t)nx * ny;
-  const size_t SB = grid_stage_bytes<T>(bx, by, hy, VS);
+  const size_t SB = grid_stage_bytes<T>(bx, by, hy, VS, SWZ);
+  const size_t XB = grid_xbytes<T>(bx, by, hy, SWZ);  // X plane-block bytes of a stage
   double* sYw = reinterpret_cast<double*>(smraw + (size_t)NS * SB);  // [2 (CG)][NWC][YR][S]
   uint64_t* full = reinterpret_cast<uint64_t*>(sYw + (K::CG ? 2 : 1) * NWC * K::YR * S);
   uint64_t* empty = full + 8;
@@ -138,7 +165,11 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
         const bool vline = vl >= 0 && vl < by && p - 1 >= z0 && p - 1 < z1 && vy < ny;
         const int rl = lane - PH - by, ry = y0 + rl;  // lanes for the lines of r (16-byte rows: nx even)
         const bool rline = gram && r != nullptr && rbulk && rl >= 0 && rl < by && p - 1 >= z0 && p - 1 < z1 && ry < ny;
-        if (xline) bytes += (uint32_t)(xb - xa) * T * 8;
+        // SWZ: every line of a plane in [−gb, nz + ga) as a full (bx+2)-point box; rows outside the
+        // tensor are zero-filled, rows of a neighbouring line / plane are finite and meet stencil
+        // slots of value 0 (fma(0, x, y) = y)
+        const bool pin = p >= -gp.gb && p < nz + gp.ga;
+        if (SWZ ? (lane < PH && pin) : xline) bytes += SWZ ? (uint32_t)PW * T * 8 : (uint32_t)(xb - xa) * T * 8;
         if (vline) bytes += (uint32_t)(ob - x0) * VS * 8;
         if (rline) bytes += (uint32_t)(ob - x0) * 8;
 #pragma unroll
@@ -148,19 +179,24 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
           mbar_expect_tx(full + s, bytes);  // 0 bytes (plane outside the grid): the phase completes at once
         }
         __syncwarp();
-        if (xline) {
+        if constexpr (SWZ) {
+          if (lane < PH && pin) {  // tensor rows from the first ghost plane: (p + gb)·plane + yy·nx + x0 − 1
+            const int row = (int)((int64_t)(p + gp.gb) * plane + (int64_t)yy * nx + x0 - 1);
+            tma_2d(st + (size_t)lane * PWP * T * 8, &tmX, 0, row, full + s);
+          }
+        } else if (xline) {
           const int64_t row = (int64_t)p * plane + (int64_t)yy * nx + xa;
           double* dst = reinterpret_cast<double*>(st) + ((size_t)lane * PW + (xa - x0 + 1)) * T;
           bulk_g2s(dst, X + row * T, (uint32_t)(xb - xa) * T * 8, full + s);
         }
         if (vline) {
           const int64_t row = (int64_t)(p - 1) * plane + (int64_t)vy * nx + x0;
-          double* dst = reinterpret_cast<double*>(st + (size_t)PW * PH * T * 8) + (size_t)vl * bx * VS;
+          double* dst = reinterpret_cast<double*>(st + XB) + (size_t)vl * bx * VS;
           bulk_g2s(dst, gp.sv + row * VS, (uint32_t)(ob - x0) * VS * 8, full + s);
         }
         if (rline) {
           const int64_t row = (int64_t)(p - 1) * plane + (int64_t)ry * nx + x0;
-          double* dst = reinterpret_cast<double*>(st + (size_t)PW * PH * T * 8 + (size_t)K::R * VS * 8) + (size_t)rl * bx;
+          double* dst = reinterpret_cast<double*>(st + XB + (size_t)K::R * VS * 8) + (size_t)rl * bx;
           bulk_g2s(dst, r + row, (uint32_t)(ob - x0) * 8, full + s);
         }
       }
@@ -211,7 +247,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
           const double* Pm = reinterpret_cast<const double*>(smraw + (size_t)sm2 * SB);
           const double* P0 = reinterpret_cast<const double*>(smraw + (size_t)sm1 * SB);
           const double* Pp = reinterpret_cast<const double*>(smraw + (size_t)cur * SB);
-          const double* Vs = reinterpret_cast<const double*>(smraw + (size_t)cur * SB + (size_t)PW * PH * T * 8);
+          const double* Vs = reinterpret_cast<const double*>(smraw + (size_t)cur * SB + XB);
           const double* Rs = Vs + K::R * VS;
           const int64_t qrow = (int64_t)q * plane + (int64_t)y0 * nx + x0;  // global row of block point (0,0)
           double* yw = yw0 + (K::CG ? ybuf * NWC * K::YR * S : 0);
@@ -230,16 +266,19 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
               // ---- the patch's 4 rows, sliding up the y-lines: the centre of line dy+1 is loaded once
               // (as the +y neighbour of line dy and the centre of the next row); ±x and ±z per row.
               // Stencil slots in ascending column order (reading R20).
-              const double* c0p = P0 + ((size_t)(py0 + hy) * PW + px0 + 1) * T + 2 * gl;  // centre, line 0
-              double2 cm = *reinterpret_cast<const double2*>(c0p - (size_t)PW * T);       // line −1 (−y of row 0)
-              double2 c0 = *reinterpret_cast<const double2*>(c0p);
-#pragma unroll
+              // swizzled 128-byte X rows: column pair gl of point P sits at chunk gl ^ (P & 7)
+              const int Pc = px0 + 1;  // the patch's point in its line
+              const int sc = 2 * (gl ^ (Pc & 7)), sm_ = 2 * (gl ^ ((Pc - 1) & 7)), sp_ = 2 * (gl ^ ((Pc + 1) & 7));
+              const double* c0p = P0 + ((size_t)(py0 + hy) * PWP + Pc) * T;  // centre row, line 0 (unswizzled base)
+              double2 cm = *reinterpret_cast<const double2*>(c0p - (size_t)PWP * T + sc);  // line −1 (−y of row 0)
+              double2 c0 = *reinterpret_cast<const double2*>(c0p + sc);
+#pragma unroll 2
               for (int dy = 0; dy < PY; ++dy) {
-                const double* cp = c0p + (size_t)dy * PW * T;
-                const double2 cn = *reinterpret_cast<const double2*>(cp + (size_t)PW * T);  // +y (line dy+1)
-                const double2 xm = *reinterpret_cast<const double2*>(cp - T);
-                const double2 xp = *reinterpret_cast<const double2*>(cp + T);
-                const size_t zo = (size_t)(cp - P0);
+                const double* cp = c0p + (size_t)dy * PWP * T;
+                const double2 cn = *reinterpret_cast<const double2*>(cp + (size_t)PWP * T + sc);  // +y (line dy+1)
+                const double2 xm = *reinterpret_cast<const double2*>(cp - T + sm_);
+                const double2 xp = *reinterpret_cast<const double2*>(cp + T + sp_);
+                const size_t zo = (size_t)(cp - P0) + sc;
                 const double2 zm = *reinterpret_cast<const double2*>(Pm + zo);
                 const double2 zp = *reinterpret_cast<const double2*>(Pp + zo);
                 const int ir = (py0 + dy) * bx + px0;
@@ -272,11 +311,12 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
                 const int ppq = (ps * NWC + warp) * NG + gq;
                 const int pxq = (ppq & (ppx - 1)) * PX + wq % PX, pyq = (ppq >> (bxs - LPX)) * PY + wq / PX;
                 const bool okq = x0 + pxq < nx && y0 + pyq < ny;
-                const double* xo = P0 + ((size_t)(pyq + hy) * PW + pxq + 1) * T;
+                const int Pq = pxq + 1;
+                const double* xo = P0 + ((size_t)(pyq + hy) * PWP + Pq) * T;
                 double xa[MT], ybv[MT];
 #pragma unroll
-                for (int i = 0; i < MT; ++i) {
-                  xa[i] = okq ? xo[i * 8 + g] : 0.0;
+                for (int i = 0; i < MT; ++i) {  // column 8i + g: chunk (4i + g/2) ^ (Pq & 7), half g & 1
+                  xa[i] = okq ? xo[2 * ((4 * i + (g >> 1)) ^ (Pq & 7)) + (g & 1)] : 0.0;
                   ybv[i] = yw[rq * S + i * 8 + g];
                 }
                 int ut = 0;
@@ -476,6 +516,21 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
 // ----------------------------------------------------------------------------
 // host side
 // ----------------------------------------------------------------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
 template <int T>
 static void grid_shape(const GridPlan& gp, int& bx, int& by, int& zc, int sms) {
   using K = GrCfg<T>;
@@ -513,14 +568,28 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
   int bx, by, zc;
   grid_shape<T>(gp, bx, by, zc, sms);
   const int hy = gp.ny > 1 ? 1 : 0, vs = (W + 1) & ~1;
-  const size_t SB = grid_stage_bytes<T>(bx, by, hy, vs);
-  const size_t fixed = (size_t)(K::CG ? 2 : 1) * K::NWC * K::YR * K::S * 8 + 16 * 8 + 128;
   static const bool patch_env = [] {  // EKS_GRID_PATCH=0: the per-row consumer (A/B measurements)
     const char* e = getenv("EKS_GRID_PATCH");
     return !(e && atoi(e) == 0);
   }();
   constexpr bool PATCH_T = T == 16 && W == 7;  // t = 32: measured slower (0.57 vs 0.63, profiles/spmm_micro_r02.txt)
-  const bool patch = PATCH_T && W == 7 && patch_env && by % 4 == 0;
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof tm);
+  bool patch = PATCH_T && patch_env && by % 4 == 0 && bx + 2 <= 256;
+  if (patch) {  // the X tensor from the first ghost plane: T columns × (gb + nz + ga)·plane rows, 128-byte swizzle
+    const PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    const int64_t plane = (int64_t)gp.nx * gp.ny, rows = (int64_t)(gp.gb + gp.nz + gp.ga) * plane;
+    const cuuint64_t gdim[2] = {(cuuint64_t)T, (cuuint64_t)rows};
+    const cuuint64_t gstride[1] = {(cuuint64_t)T * 8};
+    const cuuint32_t box[2] = {(cuuint32_t)T, (cuuint32_t)(bx + 2)};
+    const cuuint32_t es[2] = {1, 1};
+    patch = enc != nullptr && rows < INT32_MAX &&
+            enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X - (int64_t)gp.gb * plane * T), gdim,
+                gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  const size_t SB = grid_stage_bytes<T>(bx, by, hy, vs, patch);
+  const size_t fixed = (size_t)(K::CG ? 2 : 1) * K::NWC * K::YR * K::S * 8 + 16 * 8 + 128 + (patch ? 1024 : 0);
   int ns = (int)((220 * 1024 - fixed) / SB);
   if (ns > 8) ns = 8;
   if (ns < 4) return cudaErrorInvalidConfiguration;
@@ -531,11 +600,11 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
     if (patch) {
       cudaFuncSetAttribute(k_spmm_grid<T, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       return launch_k(k_spmm_grid<T, W, true>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns,
-                      gram);
+                      gram, tm);
     }
   }
   cudaFuncSetAttribute(k_spmm_grid<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  return launch_k(k_spmm_grid<T, W>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns, gram);
+  return launch_k(k_spmm_grid<T, W>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns, gram, tm);
 }
 
 bool spmm_grid_fused_chol(int t) { return t == 8 || t == 16; }

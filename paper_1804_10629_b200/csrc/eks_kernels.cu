@@ -958,53 +958,59 @@ __device__ __forceinline__ void trsv_load(TrsvItem<E>& f, int pos, int c, int t,
   f.z = Zp[(int64_t)pos * t + c];
 }
 
+// cl: column within the CTA's column group (ring stride rs), c: global column (Y stride t)
 template <int E>
-__device__ __forceinline__ void trsv_solve(const TrsvItem<E>& f, int c, double* ring, int wmask, int t, double* Y) {
+__device__ __forceinline__ void trsv_solve(const TrsvItem<E>& f, int cl, int c, double* ring, int wmask, int rs, int t,
+                                           double* Y) {
   double v = f.z;
 #pragma unroll
   for (int e = 0; e < E; ++e)
-    if (e < f.ne) v = __fma_rn(-f.v[e], ring[(f.k[e] & wmask) * t + c], v);
+    if (e < f.ne) v = __fma_rn(-f.v[e], ring[(f.k[e] & wmask) * rs + cl], v);
   v = v * f.rd;
-  ring[(f.i & wmask) * t + c] = v;
+  ring[(f.i & wmask) * rs + cl] = v;
   Y[(int64_t)f.o * t + c] = v;
 }
 
+// The t columns of the block are independent right-hand sides: CTA b solves domain b / ngrp for the
+// column group (b % ngrp)·cpg … +cpg.  With a level's items (rows × cpg) within one warp the CTA is
+// one warp and the per-level barrier is a warp barrier.
 template <int E>
-__global__ void __launch_bounds__(256) k_trsv_ring(int t, int wmask, const TrsvSched S,
+__global__ void __launch_bounds__(256) k_trsv_ring(int t, int cpg, int ngrp, int wmask, const TrsvSched S,
                                                    const int* __restrict__ dom_lev,
                                                    const int* __restrict__ lev_ptr, const double* Zp, double* Y) {
   pdl_enter();
-  extern __shared__ double ring[];  // (wmask + 1) × t doubles, then the domain's level bounds
-  int* slev = reinterpret_cast<int*>(ring + (size_t)(wmask + 1) * t);
-  const int d = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
+  extern __shared__ double ring[];  // (wmask + 1) × cpg doubles, then the domain's level bounds
+  int* slev = reinterpret_cast<int*>(ring + (size_t)(wmask + 1) * cpg);
+  const int d = blockIdx.x / ngrp, c0 = (blockIdx.x % ngrp) * cpg, tid = threadIdx.x, nth = blockDim.x;
   const int l0 = dom_lev[d], l1 = dom_lev[d + 1];
   for (int e = tid; e <= l1 - l0; e += nth) slev[e] = lev_ptr[l0 + e];
   __syncthreads();
-  const int prow = tid / t, c = tid % t;  // this thread's (row in level, column) of a level's first nth items
+  const int prow = tid / cpg, cl = tid % cpg;  // this thread's (row in level, column) of a level's first nth items
   TrsvItem<E> q[kTrsvD];
   bool h[kTrsvD];
 #pragma unroll
   for (int u = 0; u < kTrsvD; ++u) {
     const int L = l0 + u;
     h[u] = L < l1 && prow < slev[L - l0 + 1] - slev[L - l0];
-    if (h[u]) trsv_load(q[u], slev[L - l0] + prow, c, t, S, Zp);
+    if (h[u]) trsv_load(q[u], slev[L - l0] + prow, c0 + cl, t, S, Zp);
   }
   for (int lv = l0; lv < l1; lv += kTrsvD) {
 #pragma unroll
     for (int u = 0; u < kTrsvD; ++u) {
       const int L = lv + u;
       if (L < l1) {  // uniform across the CTA
-        if (h[u]) trsv_solve(q[u], c, ring, wmask, t, Y);
-        const int b = slev[L - l0], items = (slev[L - l0 + 1] - b) * t;
+        if (h[u]) trsv_solve(q[u], cl, c0 + cl, ring, wmask, cpg, t, Y);
+        const int b = slev[L - l0], items = (slev[L - l0 + 1] - b) * cpg;
         for (int it = tid + nth; it < items; it += nth) {  // wide levels: the rest without prefetch
           TrsvItem<E> f;
-          trsv_load(f, b + it / t, it % t, t, S, Zp);
-          trsv_solve(f, it % t, ring, wmask, t, Y);
+          trsv_load(f, b + it / cpg, c0 + it % cpg, t, S, Zp);
+          trsv_solve(f, it % cpg, c0 + it % cpg, ring, wmask, cpg, t, Y);
         }
         const int Ln = L + kTrsvD;
         h[u] = Ln < l1 && prow < slev[Ln - l0 + 1] - slev[Ln - l0];
-        if (h[u]) trsv_load(q[u], slev[Ln - l0] + prow, c, t, S, Zp);
-        __syncthreads();
+        if (h[u]) trsv_load(q[u], slev[Ln - l0] + prow, c0 + cl, t, S, Zp);
+        if (nth == 32) __syncwarp();
+        else __syncthreads();
       }
     }
   }
@@ -1030,6 +1036,19 @@ cudaError_t launch_perm_gather(cudaStream_t st, int64_t npos, int t, const int* 
   return launch_k(k_perm_gather, (int)blocks, 256, 0, st, npos, t, pos_row, Z, Zp);
 }
 
+// columns per CTA: the largest power-of-two divisor of t with a level's items (maxrows × cpg) in one
+// warp (EKS_TRSV_CPG overrides, A/B measurements); t itself when even one column's level exceeds a warp
+static int trsv_cpg(int t, int maxrows) {
+  static const int env = [] {
+    const char* e = getenv("EKS_TRSV_CPG");
+    return e ? atoi(e) : 0;
+  }();
+  if (env > 0 && env <= t && t % env == 0) return env;
+  int cpg = t;
+  while (cpg > 1 && maxrows * cpg > 32) cpg /= 2;
+  return maxrows * cpg <= 32 ? cpg : t;
+}
+
 size_t trsv_ring_smem(int wrows, int t, int maxlev) { return (size_t)wrows * t * 8 + (size_t)(maxlev + 1) * 4; }
 
 cudaError_t launch_trsv_ring(cudaStream_t st, int ndom, int t, int wrows, int maxlev, int maxrows,
@@ -1037,17 +1056,18 @@ cudaError_t launch_trsv_ring(cudaStream_t st, int ndom, int t, int wrows, int ma
                              const int* pos_col, const double* pos_val, int E, const int* dom_lev, const int* lev_ptr,
                              const double* Zp, double* Y) {
   if (ndom < 1 || t < 1 || wrows < 1 || (wrows & (wrows - 1))) return cudaErrorInvalidValue;
-  const size_t sm = trsv_ring_smem(wrows, t, maxlev);
+  const int cpg = trsv_cpg(t, maxrows), ngrp = t / cpg;
+  const size_t sm = trsv_ring_smem(wrows, cpg, maxlev);
   if (sm > 220 * 1024) return cudaErrorInvalidValue;
-  // threads: a level's items (rows × t), rounded to warps, at most 256; wider levels loop
-  int nth = ((maxrows * t + 31) / 32) * 32;
+  // threads: a level's items (rows × cpg), rounded to warps, at most 256; wider levels loop
+  int nth = ((maxrows * cpg + 31) / 32) * 32;
   if (nth > 256) nth = 256;
   if (nth < 32) nth = 32;
   const TrsvSched S{pos_row, pos_out, pos_ne, pos_rdiag, pos_col, pos_val};
 #define EKS_TRSV_E(EE)                                                                                            \
   case EE:                                                                                                        \
     if (sm > 48 * 1024) cudaFuncSetAttribute(k_trsv_ring<EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    return launch_k(k_trsv_ring<EE>, ndom, nth, sm, st, t, wrows - 1, S, dom_lev, lev_ptr, Zp, Y);
+    return launch_k(k_trsv_ring<EE>, ndom * ngrp, nth, sm, st, t, cpg, ngrp, wrows - 1, S, dom_lev, lev_ptr, Zp, Y);
   switch (E) {
     EKS_TRSV_E(1)
     EKS_TRSV_E(2)

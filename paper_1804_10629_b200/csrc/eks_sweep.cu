@@ -458,8 +458,10 @@ __global__ void __launch_bounds__(256, 1)
       yk[ni][0] = y0;
       yk[ni][1] = y1;
       const double a0 = RREG ? af[2 * ni] : sA[c], a1 = RREG ? af[2 * ni + 1] : sA[c + 1];
+      // r −= AW α̃; lazy: a = β = R⁻¹α̃, so the residual update takes AZ2 (the sY tile, still unchanged) · β
+      const double q0 = lazy ? sY[rr * S + c] : y0, q1 = lazy ? sY[rr * S + c + 1] : y1;
       double tu = fma(w0, a0, w1 * a1);
-      double tq = fma(y0, a0, y1 * a1);
+      double tq = fma(q0, a0, q1 * a1);
       tu += __shfl_xor_sync(0xffffffffu, tu, 1);
       tq += __shfl_xor_sync(0xffffffffu, tq, 1);
       tu += __shfl_xor_sync(0xffffffffu, tu, 2);
