@@ -89,7 +89,7 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
 // patch of output rows (4 consecutive y-lines at one x) from one set of loads: the centre-plane
 // rows with their ±1 x-neighbours, the ±y lines outside the patch and the ±z planes are each read
 // once — 5.5 shared-memory row loads per output row instead of 7.
-template <int T, int W, bool PATCH = false>
+template <int T, int W, bool PATCH = false, bool SWZ_ = false>
 __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
     k_spmm_grid(const GridPlan gp, int bx, int by, int zc, const double* __restrict__ X, double* __restrict__ Y,
                 const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch, int NS,
@@ -100,7 +100,9 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
   constexpr int VS = (W + 1) & ~1;
   static_assert(W == 5 || W == 7, "2D 5-point or 3D 7-point stencil");
   extern __shared__ __align__(128) unsigned char smraw_[];
-  constexpr bool SWZ = PATCH;  // the patch kernel streams X by swizzled tensor-map TMA
+  // SWZ (EKS_GRID_SWZ=1): the t = 16 patch kernel streams X by swizzled tensor-map TMA.  Measured slower
+  // than the linear 1D bulk copies (0.57 vs 0.67 of HBM at 384³, profiles/spmm_micro_r02.txt): off by default
+  constexpr bool SWZ = PATCH && T == 16 && SWZ_;
   unsigned char* smraw =
       SWZ ? reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw_) + 1023) & ~(uintptr_t)1023) : smraw_;
   const int nx = gp.nx, ny = gp.ny, nz = gp.nz;
@@ -268,7 +270,8 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
               // Stencil slots in ascending column order (reading R20).
               // swizzled 128-byte X rows: column pair gl of point P sits at chunk gl ^ (P & 7)
               const int Pc = px0 + 1;  // the patch's point in its line
-              const int sc = 2 * (gl ^ (Pc & 7)), sm_ = 2 * (gl ^ ((Pc - 1) & 7)), sp_ = 2 * (gl ^ ((Pc + 1) & 7));
+              const int sc = SWZ ? 2 * (gl ^ (Pc & 7)) : 2 * gl;
+              const int sm_ = SWZ ? 2 * (gl ^ ((Pc - 1) & 7)) : 2 * gl, sp_ = SWZ ? 2 * (gl ^ ((Pc + 1) & 7)) : 2 * gl;
               const double* c0p = P0 + ((size_t)(py0 + hy) * PWP + Pc) * T;  // centre row, line 0 (unswizzled base)
               double2 cm = *reinterpret_cast<const double2*>(c0p - (size_t)PWP * T + sc);  // line −1 (−y of row 0)
               double2 c0 = *reinterpret_cast<const double2*>(c0p + sc);
@@ -304,7 +307,8 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
               }
               if (!gram) continue;
               __syncwarp();
-              // ---- Gram over the warp's RPW rows on DMMA (k-steps of 4 rows)
+              // ---- Gram over the warp's RPW rows on DMMA (k-steps of 4 rows); t = 64 runs Gram-free only
+              if constexpr (!K::CG) {
 #pragma unroll
               for (int ks = 0; ks < RPW / 4; ++ks) {
                 const int rq = ks * 4 + q4, gq = rq / PR, wq = rq % PR;
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
                 double xa[MT], ybv[MT];
 #pragma unroll
                 for (int i = 0; i < MT; ++i) {  // column 8i + g: chunk (4i + g/2) ^ (Pq & 7), half g & 1
-                  xa[i] = okq ? xo[2 * ((4 * i + (g >> 1)) ^ (Pq & 7)) + (g & 1)] : 0.0;
+                  xa[i] = okq ? xo[SWZ ? 2 * ((4 * i + (g >> 1)) ^ (Pq & 7)) + (g & 1) : i * 8 + g] : 0.0;
                   ybv[i] = yw[rq * S + i * 8 + g];
                 }
                 int ut = 0;
@@ -332,6 +336,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
                   for (int mi = 0; mi < MT; ++mi) dmma(accr[mi][0], accr[mi][1], xa[mi], br);
                 }
               }
+              }  // !CG
               __syncwarp();
             }
           } else {
@@ -572,11 +577,17 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
     const char* e = getenv("EKS_GRID_PATCH");
     return !(e && atoi(e) == 0);
   }();
-  constexpr bool PATCH_T = T == 16 && W == 7;  // t = 32: measured slower (0.57 vs 0.63, profiles/spmm_micro_r02.txt)
+  // t = 16 (swizzled TMA) and the Gram-free t = 64 launches; t = 32: measured slower (0.57 vs 0.63,
+  // profiles/spmm_micro_r02.txt)
+  constexpr bool PATCH_T = (T == 16 || T == 64) && W == 7;
   CUtensorMap tm;
   memset(&tm, 0, sizeof tm);
-  bool patch = PATCH_T && patch_env && by % 4 == 0 && bx + 2 <= 256;
-  if (patch) {  // the X tensor from the first ghost plane: T columns × (gb + nz + ga)·plane rows, 128-byte swizzle
+  static const bool swz_env = [] {
+    const char* e = getenv("EKS_GRID_SWZ");
+    return e && atoi(e) == 1;
+  }();
+  bool patch = PATCH_T && patch_env && by % 4 == 0 && bx + 2 <= 256 && (T == 16 || !gram);
+  if (patch && T == 16 && swz_env) {  // the X tensor from the first ghost plane: T columns × (gb + nz + ga)·plane rows, 128B swizzle
     const PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     const int64_t plane = (int64_t)gp.nx * gp.ny, rows = (int64_t)(gp.gb + gp.nz + gp.ga) * plane;
     const cuuint64_t gdim[2] = {(cuuint64_t)T, (cuuint64_t)rows};
@@ -588,8 +599,9 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
                 gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
-  const size_t SB = grid_stage_bytes<T>(bx, by, hy, vs, patch);
-  const size_t fixed = (size_t)(K::CG ? 2 : 1) * K::NWC * K::YR * K::S * 8 + 16 * 8 + 128 + (patch ? 1024 : 0);
+  const bool swz = patch && T == 16 && swz_env;
+  const size_t SB = grid_stage_bytes<T>(bx, by, hy, vs, swz);
+  const size_t fixed = (size_t)(K::CG ? 2 : 1) * K::NWC * K::YR * K::S * 8 + 16 * 8 + 128 + (swz ? 1024 : 0);
   int ns = (int)((220 * 1024 - fixed) / SB);
   if (ns > 8) ns = 8;
   if (ns < 4) return cudaErrorInvalidConfiguration;
@@ -597,6 +609,11 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
   if (sm < (size_t)(T * T + T) * 8) sm = (size_t)(T * T + T) * 8;
   nblk = nblk < sms ? nblk : sms;  // one persistent CTA per SM
   if constexpr (PATCH_T) {
+    if (patch && swz) {
+      cudaFuncSetAttribute(k_spmm_grid<T, W, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      return launch_k(k_spmm_grid<T, W, true, true>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch,
+                      ns, gram, tm);
+    }
     if (patch) {
       cudaFuncSetAttribute(k_spmm_grid<T, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       return launch_k(k_spmm_grid<T, W, true>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns,

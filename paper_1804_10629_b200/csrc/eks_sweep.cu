@@ -495,6 +495,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int u = 0; u < K::TPW; ++u) {
         const int tile = (warp / K::WS) * K::TPW + u;
         const int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
+        if (K::WS == 1 && l == C1N - 1 && mi > ni) continue;  // AWᵀAW is symmetric: upper tiles, mirrored below
         const double* sL = (C1N == 2 && l == 0) ? sZ + 2 * K::TILE : sY;
         double d0 = acc[u][0], d1 = acc[u][1];
 #pragma unroll
@@ -526,6 +527,11 @@ __global__ void __launch_bounds__(256, 1)
       for (int u = 0; u < K::TPW; ++u) {
         const int tile = warp * K::TPW + u;
         const int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
+        if (l == C1N - 1 && mi > ni) continue;  // written by its mirror tile
+        if (l == C1N - 1 && mi < ni) {
+          out[l * T * T + (ni * 8 + 2 * q4) * T + mi * 8 + g] = acc[u][0];
+          out[l * T * T + (ni * 8 + 2 * q4 + 1) * T + mi * 8 + g] = acc[u][1];
+        }
         *reinterpret_cast<double2*>(out + l * T * T + (mi * 8 + g) * T + ni * 8 + 2 * q4) =
             make_double2(acc[u][0], acc[u][1]);
       }
