@@ -331,13 +331,17 @@ __global__ void __launch_bounds__(256, 1)
 // W = Z2·R⁻¹, AW = AZ2·R⁻¹ (in place) and the fused x/r update of the block
 // (see launch_apply).  Same pipeline; both products on DMMA.
 // ----------------------------------------------------------------------------
-template <int T, int C1N>
+// ZT = false: the lazy basis without x/r update (mode bits 4 | 8): no Z2 tile and no vectors in a stage,
+// so more stages fit (more bytes in flight per SM)
+template <int T, int C1N, bool ZT = true>
 struct ApCfg {
   static constexpr int TR = 64;  // 8 warps × 8 rows: every warp owns complete rows
   static constexpr int S = T + 4;
   static constexpr int TILE = TR * S;
-  // Z2, AZ2 tiles (+ AW_prev tile when C1N == 2) + r_in, dx, x vectors
-  static constexpr int STAGE = (C1N == 2 ? 3 : 2) * TILE + 3 * TR;
+  // [Z2 tile (ZT)], AZ2 tile, [AW_prev tile (C1N == 2)], [r_in, dx, x vectors (ZT)]
+  static constexpr int NTL = (C1N == 2 ? 3 : 2) - (ZT ? 0 : 1);
+  static constexpr int OY = ZT ? TILE : 0, OPREV = OY + TILE, VOFF = NTL * TILE;
+  static constexpr int STAGE = NTL * TILE + (ZT ? 3 * TR : 0);
   static constexpr int NSA = (100 * 1024 / 8 - T * (T + 4)) / STAGE;
   static constexpr int NS0 = NSA >= 3 ? NSA : (200 * 1024 / 8 - T * (T + 4)) / STAGE;
   static constexpr int NS = NS0 > 8 ? 8 : (NS0 < 2 ? 2 : NS0);
@@ -352,13 +356,13 @@ struct ApCfg {
   static constexpr int SMEM = SMEM0 > RED ? SMEM0 : RED;
 };
 
-template <int T, int C1N>
+template <int T, int C1N, bool ZT = true>
 __global__ void __launch_bounds__(256, 1)
     k_apply_tc(int64_t n, double* Z2W, double* AZ2AW, const double* __restrict__ Rinv,
                const double* __restrict__ alpha, double* __restrict__ x, double* __restrict__ dx,
                const double* __restrict__ r, double* __restrict__ rnew, const int* __restrict__ flag, int mode,
                const double* __restrict__ AWprev, double* __restrict__ part, const Tail tl) {
-  using K = ApCfg<T, C1N>;
+  using K = ApCfg<T, C1N, ZT>;
   pdl_enter();
   constexpr int PS = C1N * T * T + 2;  // per-CTA partial: [C1 (C1N·T·T) | ‖rnew‖² | pad] (16-byte rows)
   constexpr int S = K::S, SR = T + 4;
@@ -382,8 +386,8 @@ __global__ void __launch_bounds__(256, 1)
       v = alpha[e];
     sA[e] = v;
   }
-  const bool zread = !(lazy && basis);  // Z2 tiles are needed for W (eager) or for x += Z2 β (lazy)
-  constexpr int VOFF = (C1N == 2 ? 3 : 2) * K::TILE;  // vectors after the tiles
+  const bool zread = ZT && !(lazy && basis);  // Z2 tiles are needed for W (eager) or for x += Z2 β (lazy)
+  constexpr int VOFF = K::VOFF;  // vectors after the tiles
   auto issue = [&](int i) {
     if (i < ntiles) {
       const int s = i % K::NS;
@@ -391,9 +395,9 @@ __global__ void __launch_bounds__(256, 1)
       const int rows = (int)((hi - row) < K::TR ? (hi - row) : K::TR);
       double* st = sm + s * K::STAGE;
       if (zread) tile_async<T, S, K::TR>(st, Z2W, row, rows);
-      tile_async<T, S, K::TR>(st + K::TILE, AZ2AW, row, rows);
-      if constexpr (C1N == 2) tile_async<T, S, K::TR>(st + 2 * K::TILE, AWprev, row, rows);
-      if (!skip) {
+      tile_async<T, S, K::TR>(st + K::OY, AZ2AW, row, rows);
+      if constexpr (C1N == 2) tile_async<T, S, K::TR>(st + K::OPREV, AWprev, row, rows);
+      if (ZT && !skip) {
         double* sv = st + VOFF;
         vec_async<K::TR>(sv, first ? r : rnew, row, rows);
         if (!first) vec_async<K::TR>(sv + K::TR, dx, row, rows);
@@ -427,7 +431,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     issue(i + K::NS - 1);
     double* sZ = sm + (i % K::NS) * K::STAGE;
-    double* sY = sZ + K::TILE;
+    double* sY = sZ + K::OY;
     const double* sv = sZ + VOFF;
     const int64_t row = lo + (int64_t)i * K::TR;
     const int rows = (int)((hi - row) < K::TR ? (hi - row) : K::TR);
@@ -443,16 +447,16 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int kk = 0; kk < (T < 8 * (ni + 1) ? T : 8 * (ni + 1)); kk += 4) {
         const double b = RREG ? rf[ni * (T / 4) + kk / 4] : sRi[(kk + q4) * SR + ni * 8 + g];
-        if (!lazy) dmma(w0, w1, sZ[rr * S + kk + q4], b);
+        if (ZT && !lazy) dmma(w0, w1, sZ[rr * S + kk + q4], b);
         dmma(y0, y1, sY[rr * S + kk + q4], b);
       }
       const int c = ni * 8 + 2 * q4;
-      if (lazy && zread) {  // the x update multiplies Z2 by β (no W)
+      if (ZT && lazy && zread) {  // the x update multiplies Z2 by β (no W)
         w0 = sZ[rr * S + c];
         w1 = sZ[rr * S + c + 1];
       }
       if (rr < rows) {
-        if (!lazy) *reinterpret_cast<double2*>(Z2W + (row + rr) * T + c) = make_double2(w0, w1);
+        if (ZT && !lazy) *reinterpret_cast<double2*>(Z2W + (row + rr) * T + c) = make_double2(w0, w1);
         *reinterpret_cast<double2*>(AZ2AW + (row + rr) * T + c) = make_double2(y0, y1);
       }
       yk[ni][0] = y0;
@@ -496,7 +500,7 @@ __global__ void __launch_bounds__(256, 1)
         const int tile = (warp / K::WS) * K::TPW + u;
         const int l = tile / (K::MT * K::MT), mi = (tile / K::MT) % K::MT, ni = tile % K::MT;
         if (K::WS == 1 && l == C1N - 1 && mi > ni) continue;  // AWᵀAW is symmetric: upper tiles, mirrored below
-        const double* sL = (C1N == 2 && l == 0) ? sZ + 2 * K::TILE : sY;
+        const double* sL = (C1N == 2 && l == 0) ? sZ + K::OPREV : sY;
         double d0 = acc[u][0], d1 = acc[u][1];
 #pragma unroll
         for (int kk = slice * 4; kk < K::TR; kk += 4 * K::WS)
@@ -1432,22 +1436,24 @@ cudaError_t launch_spmm_gram(cudaStream_t st, int t, int64_t n, const int* rp, c
   return cudaErrorInvalidValue;
 }
 
-template <int T, int C1N>
+template <int T, int C1N, bool ZT = true>
 static cudaError_t apply_t(cudaStream_t st, int64_t n, double* Z2W, double* AZ2AW, const double* Rinv,
                            const double* alpha, double* x, double* dx, const double* r, double* rnew, const int* flag,
                            int mode, const double* AWprev, double* part, int nblk, const Tail& tl) {
-  using K = ApCfg<T, C1N>;
+  if (ZT && (mode & 12) == 12)  // lazy basis without update: the stage layout without Z2 and vectors
+    return apply_t<T, C1N, false>(st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode, AWprev, part, nblk, tl);
+  using K = ApCfg<T, C1N, ZT>;
   const size_t sm = (size_t)K::SMEM * 8;
   if (sm > 227 * 1024) return cudaErrorInvalidConfiguration;
   static int occ = 0;
   if (!occ) {
-    cudaFuncSetAttribute(k_apply_tc<T, C1N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_tc<T, C1N>, 256, sm);
+    cudaFuncSetAttribute(k_apply_tc<T, C1N, ZT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_tc<T, C1N, ZT>, 256, sm);
     if (occ < 1) occ = 1;
   }
   nblk = grid_for(nblk, occ);
   t_last_grid = nblk;
-  return launch_k(k_apply_tc<T, C1N>, nblk, 256, sm, st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode,
+  return launch_k(k_apply_tc<T, C1N, ZT>, nblk, 256, sm, st, n, Z2W, AZ2AW, Rinv, alpha, x, dx, r, rnew, flag, mode,
                   AWprev, part, tl);
 }
 
