@@ -1401,21 +1401,8 @@ eks_status build_grid_plan(eks_ctx* ctx, int64_t n, const int64_t* rp, const int
   int64_t g[6];
   std::vector<double> sv;
   if (!grid_plan_host(n, rp, col, val, row_begin, halo_before, halo_after, g, sv)) return EKS_OK;
-  // device layout slot-pair-major per grid line: [line][VS/2][nx] of double2 (a line's values of one
-  // slot pair are one contiguous run for the producer; adjacent rows' pairs 16 bytes apart for the
-  // consumers' loads)
-  const int64_t nx = g[0], VS = (g[3] + 1) & ~1, KP = VS / 2, lines = n / nx;
-  std::vector<double> svT(sv.size());
-  parallel_rows(lines, [&](int64_t lo, int64_t hi) {
-    for (int64_t L = lo; L < hi; ++L)
-      for (int64_t kp = 0; kp < KP; ++kp)
-        for (int64_t x = 0; x < nx; ++x) {
-          svT[((L * KP + kp) * nx + x) * 2] = sv[(L * nx + x) * VS + 2 * kp];
-          svT[((L * KP + kp) * nx + x) * 2 + 1] = sv[(L * nx + x) * VS + 2 * kp + 1];
-        }
-  });
-  CK(cudaMalloc((void**)&ctx->d_sv, sizeof(double) * svT.size()));
-  CK(cudaMemcpy(ctx->d_sv, svT.data(), sizeof(double) * svT.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc((void**)&ctx->d_sv, sizeof(double) * sv.size()));
+  CK(cudaMemcpy(ctx->d_sv, sv.data(), sizeof(double) * sv.size(), cudaMemcpyHostToDevice));
   ctx->gplan.nx = (int)g[0];
   ctx->gplan.ny = (int)g[1];
   ctx->gplan.nz = (int)g[2];

@@ -159,58 +159,21 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
           if (gstep >= NS) eph ^= 1u;  // lap L ≥ 1 waits for release phase (L − 1) & 1
         }
         unsigned char* st = smraw + (size_t)s * SB;
-        // copy jobs of this load step, dealt to the producer's lanes: [0, PH) the X lines y0 − hy + j of
-        // plane p; then by·VS/2 stencil-value runs (output line y0 + l of plane p − 1, slot pair kp: the
-        // values are stored slot-pair-major per line, gp.sv[((line)·VS/2 + kp)·nx + x] as double2, so a
-        // line's bx rows of one slot pair are one run); then the by lines of r
+        // lane l < PH: X line y0 − hy + l of plane p;  lane PH + l < PH + by: values of output line y0 + l, plane p − 1
+        uint32_t bytes = 0;
+        const int yy = y0 - hy + lane;
+        const bool xline = lane < PH && p >= -gp.gb && p < nz + gp.ga && yy >= 0 && yy < ny;
+        const int vl = lane - PH, vy = y0 + vl;
+        const bool vline = vl >= 0 && vl < by && p - 1 >= z0 && p - 1 < z1 && vy < ny;
+        const int rl = lane - PH - by, ry = y0 + rl;  // lanes for the lines of r (16-byte rows: nx even)
+        const bool rline = gram && r != nullptr && rbulk && rl >= 0 && rl < by && p - 1 >= z0 && p - 1 < z1 && ry < ny;
         // SWZ: every line of a plane in [−gb, nz + ga) as a full (bx+2)-point box; rows outside the
         // tensor are zero-filled, rows of a neighbouring line / plane are finite and meet stencil
         // slots of value 0 (fma(0, x, y) = y)
-        constexpr int KP = VS / 2;
-        const int nvj = by * KP, njobs = PH + nvj + by;
         const bool pin = p >= -gp.gb && p < nz + gp.ga;
-        const bool pval = p - 1 >= z0 && p - 1 < z1;
-        auto job = [&](int j, bool issue) -> uint32_t {
-          if (j < PH) {
-            const int yy = y0 - hy + j;
-            if constexpr (SWZ) {
-              if (!pin) return 0;
-              if (issue) {  // tensor rows from the first ghost plane: (p + gb)·plane + yy·nx + x0 − 1
-                const int row = (int)((int64_t)(p + gp.gb) * plane + (int64_t)yy * nx + x0 - 1);
-                tma_2d(st + (size_t)j * PWP * T * 8, &tmX, 0, row, full + s);
-              }
-              return (uint32_t)PW * T * 8;
-            } else {
-              if (!(pin && yy >= 0 && yy < ny)) return 0;
-              if (issue) {
-                const int64_t row = (int64_t)p * plane + (int64_t)yy * nx + xa;
-                double* dst = reinterpret_cast<double*>(st) + ((size_t)j * PW + (xa - x0 + 1)) * T;
-                bulk_g2s(dst, X + row * T, (uint32_t)(xb - xa) * T * 8, full + s);
-              }
-              return (uint32_t)(xb - xa) * T * 8;
-            }
-          }
-          if (j < PH + nvj) {
-            const int vl = (j - PH) / KP, kp = (j - PH) % KP, vy = y0 + vl;
-            if (!(pval && vy < ny)) return 0;
-            if (issue) {
-              const int64_t line = (int64_t)(p - 1) * ny + vy;
-              double* dst = reinterpret_cast<double*>(st + XB) + ((size_t)vl * KP + kp) * bx * 2;
-              bulk_g2s(dst, gp.sv + ((line * KP + kp) * nx + x0) * 2, (uint32_t)(ob - x0) * 16, full + s);
-            }
-            return (uint32_t)(ob - x0) * 16;
-          }
-          const int rl = j - PH - nvj, ry = y0 + rl;  // lines of r (16-byte rows: nx even)
-          if (!(gram && r != nullptr && rbulk && pval && ry < ny)) return 0;
-          if (issue) {
-            const int64_t row = (int64_t)(p - 1) * plane + (int64_t)ry * nx + x0;
-            double* dst = reinterpret_cast<double*>(st + XB + (size_t)K::R * VS * 8) + (size_t)rl * bx;
-            bulk_g2s(dst, r + row, (uint32_t)(ob - x0) * 8, full + s);
-          }
-          return (uint32_t)(ob - x0) * 8;
-        };
-        uint32_t bytes = 0;
-        for (int j = lane; j < njobs; j += 32) bytes += job(j, false);
+        if (SWZ ? (lane < PH && pin) : xline) bytes += SWZ ? (uint32_t)PW * T * 8 : (uint32_t)(xb - xa) * T * 8;
+        if (vline) bytes += (uint32_t)(ob - x0) * VS * 8;
+        if (rline) bytes += (uint32_t)(ob - x0) * 8;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
         if (lane == 0) {
@@ -218,7 +181,26 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
           mbar_expect_tx(full + s, bytes);  // 0 bytes (plane outside the grid): the phase completes at once
         }
         __syncwarp();
-        for (int j = lane; j < njobs; j += 32) job(j, true);
+        if constexpr (SWZ) {
+          if (lane < PH && pin) {  // tensor rows from the first ghost plane: (p + gb)·plane + yy·nx + x0 − 1
+            const int row = (int)((int64_t)(p + gp.gb) * plane + (int64_t)yy * nx + x0 - 1);
+            tma_2d(st + (size_t)lane * PWP * T * 8, &tmX, 0, row, full + s);
+          }
+        } else if (xline) {
+          const int64_t row = (int64_t)p * plane + (int64_t)yy * nx + xa;
+          double* dst = reinterpret_cast<double*>(st) + ((size_t)lane * PW + (xa - x0 + 1)) * T;
+          bulk_g2s(dst, X + row * T, (uint32_t)(xb - xa) * T * 8, full + s);
+        }
+        if (vline) {
+          const int64_t row = (int64_t)(p - 1) * plane + (int64_t)vy * nx + x0;
+          double* dst = reinterpret_cast<double*>(st + XB) + (size_t)vl * bx * VS;
+          bulk_g2s(dst, gp.sv + row * VS, (uint32_t)(ob - x0) * VS * 8, full + s);
+        }
+        if (rline) {
+          const int64_t row = (int64_t)(p - 1) * plane + (int64_t)ry * nx + x0;
+          double* dst = reinterpret_cast<double*>(st + XB + (size_t)K::R * VS * 8) + (size_t)rl * bx;
+          bulk_g2s(dst, r + row, (uint32_t)(ob - x0) * 8, full + s);
+        }
       }
     }
   }
@@ -302,14 +284,14 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
                 const size_t zo = (size_t)(cp - P0) + sc;
                 const double2 zm = *reinterpret_cast<const double2*>(Pm + zo);
                 const double2 zp = *reinterpret_cast<const double2*>(Pp + zo);
+                const int ir = (py0 + dy) * bx + px0;
                 const bool ok = x0 + px0 < nx && y0 + py0 + dy < ny;
                 const int64_t grow = qrow + (int64_t)(py0 + dy) * nx + px0;
                 const double2 nb[7] = {zm, cm, xm, c0, xp, cn, zp};
                 double2 y = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int k = 0; k < VS; k += 2) {
-                  const double2 av = ok ? reinterpret_cast<const double2*>(Vs)[((py0 + dy) * (VS / 2) + k / 2) * bx + px0]
-                                        : make_double2(0, 0);
+                  const double2 av = ok ? *reinterpret_cast<const double2*>(Vs + ir * VS + k) : make_double2(0, 0);
                   y.x = __fma_rn(av.x, nb[k].x, y.x);
                   y.y = __fma_rn(av.x, nb[k].y, y.y);
                   if (k + 1 < 7) {
@@ -371,8 +353,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
             double a[VS];
 #pragma unroll
             for (int k = 0; k < VS; k += 2) {
-              const double2 av = ok ? reinterpret_cast<const double2*>(Vs)[(iy * (VS / 2) + k / 2) * bx + ix]
-                                    : make_double2(0, 0);
+              const double2 av = ok ? *reinterpret_cast<const double2*>(Vs + ir * VS + k) : make_double2(0, 0);
               a[k] = av.x;
               a[k + 1] = av.y;
             }

@@ -18,4 +18,10 @@ if [ $rc -ne 0 ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sweep|k_apply_tc|k_spmm_grid" -s 8 -c 5 -o gpurun_out/i_cfg4size_full python tools/sweep_once.py --N 256 --t 16 --nblocks 4 > gpurun_out/i_ncu_full256.log 2>&1
   echo "full256 rc=$?" >> gpurun_out/i_rc.txt
 fi
+for T in 32 64; do
+  SK=1; [ $T -eq 64 ] && SK=2
+  timeout 600 python tools/spmm_once.py --N 384 --t $T > gpurun_out/i_spmm${T}_plain.txt 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_spmm_grid|k_sweep" -s $SK -c $SK -o gpurun_out/i_spmm${T}_full python tools/spmm_once.py --N 384 --t $T > gpurun_out/i_ncu_spmm$T.log 2>&1
+  echo "spmm$T rc=$?" >> gpurun_out/i_rc.txt
+done
 exit 0
