@@ -259,6 +259,8 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
             // columns, so their rows' stencil values (64 B per row) fall in both bank halves
             // (2 × 2 patches put them 128 B apart: 4-way conflicts that cancelled the gain)
             constexpr int PX = 1, PY = 4, LPX = 0, PR = PX * PY, RPW = NG * PR;
+            // the Gram from registers: t = 16 (4 lane groups = the 4 rows of a k-step), linear layout
+            constexpr bool RGRAM = T == 16 && !SWZ;
             const int gi = lane / GP, gl = lane % GP;
             const int ppx = bx / PX;                 // patches per block line (a power of 2)
             const int nsteps = K::R / (PR * NG * NWC);  // patch steps per warp and plane
@@ -301,11 +303,43 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
                 }
                 if (!ok) y = make_double2(0.0, 0.0);
                 else reinterpret_cast<double2*>(Y)[grow * H + gl] = y;
-                if (gram) *reinterpret_cast<double2*>(yw + (gi * PR + dy) * S + 2 * gl) = y;
+                if constexpr (RGRAM) {
+                  // Gram k-step over the 4 lane groups' rows of line dy (row q4 = group q4's row), its
+                  // fragments gathered from the groups' registers by shuffles (no Y scratch round trip):
+                  // lane (g, q4) takes column 8i + g of group q4's row from lane q4·GP + 4i + g/2
+                  if (gram) {
+                    const int ppq = (ps * NWC + warp) * NG + q4;
+                    const int pxq = ppq & (ppx - 1), pyq = (ppq >> bxs) * PY + dy;
+                    const bool okq = x0 + pxq < nx && y0 + pyq < ny;
+                    double xa[MT], ybv[MT];
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) {
+                      const int src = q4 * GP + 4 * i + (g >> 1);
+                      const double cx = __shfl_sync(0xffffffffu, c0.x, src), cy = __shfl_sync(0xffffffffu, c0.y, src);
+                      const double yx = __shfl_sync(0xffffffffu, y.x, src), yy2 = __shfl_sync(0xffffffffu, y.y, src);
+                      xa[i] = okq ? ((g & 1) ? cy : cx) : 0.0;
+                      ybv[i] = (g & 1) ? yy2 : yx;
+                    }
+                    int ut = 0;
+#pragma unroll
+                    for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+                      for (int ni = mi; ni < MT; ++ni, ++ut) dmma(acc[ut][0], acc[ut][1], xa[mi], ybv[ni]);
+                    if (r != nullptr) {
+                      const double br = (g == 0 && okq)
+                                            ? (rbulk ? Rs[pyq * bx + pxq] : __ldg(r + qrow + (int64_t)pyq * nx + pxq))
+                                            : 0.0;
+#pragma unroll
+                      for (int mi = 0; mi < MT; ++mi) dmma(accr[mi][0], accr[mi][1], xa[mi], br);
+                    }
+                  }
+                } else {
+                  if (gram) *reinterpret_cast<double2*>(yw + (gi * PR + dy) * S + 2 * gl) = y;
+                }
                 cm = c0;
                 c0 = cn;
               }
-              if (!gram) continue;
+              if (!gram || RGRAM) continue;
               __syncwarp();
               // ---- Gram over the warp's RPW rows on DMMA (k-steps of 4 rows); t = 64 runs Gram-free only
               if constexpr (!K::CG) {
