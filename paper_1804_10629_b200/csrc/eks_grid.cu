@@ -89,7 +89,9 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
 // patch of output rows (4 consecutive y-lines at one x) from one set of loads: the centre-plane
 // rows with their ±1 x-neighbours, the ±y lines outside the patch and the ±z planes are each read
 // once — 5.5 shared-memory row loads per output row instead of 7.
-template <int T, int W, bool PATCH = false, bool SWZ_ = false>
+// PV (t = 16 patch variants, EKS_GRID_PV): 0 = Gram fragments from a per-warp Y scratch (default,
+// measured best), 1 = X by swizzled tensor-map TMA, 2 = Gram fragments gathered by shuffles
+template <int T, int W, bool PATCH = false, int PV = 0>
 __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
     k_spmm_grid(const GridPlan gp, int bx, int by, int zc, const double* __restrict__ X, double* __restrict__ Y,
                 const double* __restrict__ r, double* __restrict__ part, const Tail tl, const CholArgs ch, int NS,
@@ -100,9 +102,9 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
   constexpr int VS = (W + 1) & ~1;
   static_assert(W == 5 || W == 7, "2D 5-point or 3D 7-point stencil");
   extern __shared__ __align__(128) unsigned char smraw_[];
-  // SWZ (EKS_GRID_SWZ=1): the t = 16 patch kernel streams X by swizzled tensor-map TMA.  Measured slower
+  // SWZ (EKS_GRID_PV=1): the t = 16 patch kernel streams X by swizzled tensor-map TMA.  Measured slower
   // than the linear 1D bulk copies (0.57 vs 0.67 of HBM at 384³, profiles/spmm_micro_r02.txt): off by default
-  constexpr bool SWZ = PATCH && T == 16 && SWZ_;
+  constexpr bool SWZ = PATCH && T == 16 && PV == 1;
   unsigned char* smraw =
       SWZ ? reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw_) + 1023) & ~(uintptr_t)1023) : smraw_;
   const int nx = gp.nx, ny = gp.ny, nz = gp.nz;
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
             // (2 × 2 patches put them 128 B apart: 4-way conflicts that cancelled the gain)
             constexpr int PX = 1, PY = 4, LPX = 0, PR = PX * PY, RPW = NG * PR;
             // the Gram from registers: t = 16 (4 lane groups = the 4 rows of a k-step), linear layout
-            constexpr bool RGRAM = T == 16 && !SWZ;
+            constexpr bool RGRAM = T == 16 && PV == 2;  // measured slower than the scratch (0.61 vs 0.67)
             const int gi = lane / GP, gl = lane % GP;
             const int ppx = bx / PX;                 // patches per block line (a power of 2)
             const int nsteps = K::R / (PR * NG * NWC);  // patch steps per warp and plane
@@ -616,10 +618,11 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
   constexpr bool PATCH_T = (T == 16 || T == 64) && W == 7;
   CUtensorMap tm;
   memset(&tm, 0, sizeof tm);
-  static const bool swz_env = [] {
-    const char* e = getenv("EKS_GRID_SWZ");
-    return e && atoi(e) == 1;
+  static const int pv_env = [] {
+    const char* e = getenv("EKS_GRID_PV");
+    return e ? atoi(e) : 0;
   }();
+  const bool swz_env = pv_env == 1;
   bool patch = PATCH_T && patch_env && by % 4 == 0 && bx + 2 <= 256 && (T == 16 || !gram);
   if (patch && T == 16 && swz_env) {  // the X tensor from the first ghost plane: T columns × (gb + nz + ga)·plane rows, 128B swizzle
     const PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
@@ -644,8 +647,13 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
   nblk = nblk < sms ? nblk : sms;  // one persistent CTA per SM
   if constexpr (PATCH_T) {
     if (patch && swz) {
-      cudaFuncSetAttribute(k_spmm_grid<T, W, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      return launch_k(k_spmm_grid<T, W, true, true>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch,
+      cudaFuncSetAttribute(k_spmm_grid<T, W, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      return launch_k(k_spmm_grid<T, W, true, 1>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch,
+                      ns, gram, tm);
+    }
+    if (patch && pv_env == 2 && T == 16) {
+      cudaFuncSetAttribute(k_spmm_grid<T, W, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      return launch_k(k_spmm_grid<T, W, true, 2>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch,
                       ns, gram, tm);
     }
     if (patch) {

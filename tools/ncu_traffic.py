@@ -33,7 +33,10 @@ def kclass(name):
 
 
 def main(path, note):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):  # a raw-page export (ncu -i x.ncu-rep --page raw --csv)
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
     h, u = r[0], r[1]
     per_kernel = collections.defaultdict(list)
