@@ -22,7 +22,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 SRE_CG, SRE_CG2, MSDO_CG = 0, 1, 2
 METHODS = {"sre-cg": SRE_CG, "sre-cg2": SRE_CG2, "msdo-cg": MSDO_CG}
 OK, BADARG, BREAKDOWN, MAXITER = 0, 1, 7, 8
-MODE_DEFINITION, MODE_MIRROR = 0, 1
+MODE_DEFINITION, MODE_MIRROR, MODE_ONESYNCH = 0, 1, 2
 
 
 def build(force: bool = False) -> str:

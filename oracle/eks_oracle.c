@@ -423,6 +423,9 @@ int or_solve_pc(const or_csr* A, const double* b, double* x, int method, int s, 
   if (ortho != OR_ORTHO_ACHOLQR && ortho != OR_ORTHO_PRE) return OR_BADARG;
   /* restructured Alg 1/2 exist for SRE-CG2 / SRE-CG only (no restructured MSDO-CG) */
   if (restructured && method == OR_MSDO_CG) return OR_BADARG;
+  if (mode < OR_MODE_DEFINITION || mode > OR_MODE_ONESYNCH) return OR_BADARG;
+  /* one-synch CGS2 (reading R36): A-CholQR only, not with the restructured update */
+  if (mode == OR_MODE_ONESYNCH && (ortho != OR_ORTHO_ACHOLQR || restructured)) return OR_BADARG;
   size_t blk = (size_t)n * (size_t)t;
 
   double* r = dalloc((size_t)n);
@@ -469,7 +472,7 @@ int or_solve_pc(const or_csr* A, const double* b, double* x, int method, int s, 
         }
       } else {
         const double* Wprev = Q.W[Q.count - 1];
-        if (mode == OR_MODE_MIRROR) memcpy(Z, Q.AW[Q.count - 1], sizeof(double) * blk);
+        if (mode != OR_MODE_DEFINITION) memcpy(Z, Q.AW[Q.count - 1], sizeof(double) * blk);
         else or_spmm(A, t, Wprev, Z);
         if (L) { /* Alg 8-10: W_{j} = M⁻¹ A W_{j-1} = L⁻ᵗ L⁻¹ (A W_{j-1}) */
           or_lsolve(L, t, Z, Z);
@@ -489,31 +492,79 @@ int or_solve_pc(const or_csr* A, const double* b, double* x, int method, int s, 
         /* Mirror of the GPU algebra: C = (AQ)ᵀZ with cached AQ, one SpMM of Z2,
          * AW = (A Z2) R⁻¹, alpha_b = R⁻ᵀ (Z2ᵀ r_{k-1}). Equal to the definition in
          * exact arithmetic (A symmetric, reading R24). */
+        double* AZ = dalloc(blk);
+        int synched = 0; /* one-synch: B, g, Z2 and A·Z2 already formed below */
         if (nq > 0) {
           Cb = (double*)realloc(Cb, sizeof(double) * (size_t)nq * t * t);
-          for (int pass = 0; pass < 2; ++pass)
+          for (int pass = 0; pass < (mode == OR_MODE_ONESYNCH ? 1 : 2); ++pass)
             cgs_pass_from_AZ(n, t, nq, (const double* const*)(Q.W + w0),
                              (const double* const*)(Q.AW + w0), Z, Z, Cb);
+        }
+        if (nq > 0 && mode == OR_MODE_ONESYNCH) {
+          /* One-synch CGS2 (DESIGN reading R36): the SpMM runs on Z1 and
+           * C2 = (AQ)ᵀZ1, B1 = Z1ᵀ(A Z1), g1 = Z1ᵀr_{k-1} are reduced together; then, since
+           * QᵀAQ = I and QᵀAZ1 = C2 (A-orthonormal window):
+           *   Z2ᵀAZ2 = B1 − C2ᵀC2,   Z2ᵀr = g1 − C2ᵀ(Qᵀr_{k-1}),
+           *   Z2 = Z1 − Q C2,        A Z2 = A Z1 − (AQ) C2,
+           * where Qᵀr_{k-1} stacks alpha~ = W_qᵀr_{k-1} of the window blocks built in this outer
+           * iteration and 0 for older blocks (r_{k-1} ⊥ the earlier search space). */
+          or_spmm(A, t, Z, AZ);
+          for (int q = 0; q < nq; ++q)
+            or_xty(n, t, Q.AW[w0 + q], t, Z, Cb + (size_t)q * t * t);
+          or_xty(n, t, Z, t, AZ, B);
+          or_xty(n, t, Z, 1, r, g);
+          for (int a = 0; a < t; ++a)
+            for (int c = a; c < t; ++c) {
+              double v = B[a * t + c];
+              for (int qa = 0; qa < nq * t; ++qa) v = v - Cb[(size_t)qa * t + a] * Cb[(size_t)qa * t + c];
+              B[a * t + c] = v;
+            }
+          for (int a = 0; a < t; ++a)
+            for (int c = 0; c < a; ++c) B[a * t + c] = 0.0;
+          for (int q = 0; q < nq; ++q) {
+            int cur = (w0 + q) - (Q.count - i); /* position in this outer iteration, < 0: older */
+            if (cur < 0) continue;
+            const double* aq = alpha + (size_t)cur * t;
+            for (int c = 0; c < t; ++c) {
+              double v = g[c];
+              for (int a = 0; a < t; ++a) v = v - Cb[((size_t)q * t + a) * t + c] * aq[a];
+              g[c] = v;
+            }
+          }
+          for (int64_t row = 0; row < n; ++row)
+            for (int c = 0; c < t; ++c) {
+              double dz = 0.0, daz = 0.0;
+              for (int q = 0; q < nq; ++q)
+                for (int a = 0; a < t; ++a) {
+                  double cc = Cb[((size_t)q * t + a) * t + c];
+                  dz += Q.W[w0 + q][row * t + a] * cc;
+                  daz += Q.AW[w0 + q][row * t + a] * cc;
+                }
+              Z[row * t + c] -= dz;
+              AZ[row * t + c] -= daz;
+            }
+          synched = 1;
         }
         if (ortho == OR_ORTHO_PRE) {
           /* Pre-CholQR's Euclidean stage on the explicit block: Z ← Z R1⁻¹ (reading R30) */
           or_xty(n, t, Z, t, Z, B);
           for (int a = 0; a < t; ++a)
             for (int c = 0; c < a; ++c) B[a * t + c] = 0.0;
-          if (or_chol(t, B, R) != OR_OK) { status = OR_BREAKDOWN; free(Z); free(W); ok = 0; break; }
+          if (or_chol(t, B, R) != OR_OK) { status = OR_BREAKDOWN; free(Z); free(W); free(AZ); ok = 0; break; }
           rsolve_rows(n, t, R, Z, W);
           memcpy(Z, W, sizeof(double) * blk);
         }
-        double* AZ = dalloc(blk);
-        or_spmm(A, t, Z, AZ);
-        or_xty(n, t, Z, t, AZ, B);
-        for (int a = 0; a < t; ++a)
-          for (int c = 0; c < a; ++c) B[a * t + c] = 0.0;
+        if (!synched) {
+          or_spmm(A, t, Z, AZ);
+          or_xty(n, t, Z, t, AZ, B);
+          for (int a = 0; a < t; ++a)
+            for (int c = 0; c < a; ++c) B[a * t + c] = 0.0;
+          or_xty(n, t, Z, 1, r, g);
+        }
         if (or_chol(t, B, R) != OR_OK) { status = OR_BREAKDOWN; free(Z); free(W); free(AZ); ok = 0; break; }
         AW = dalloc(blk);
         rsolve_rows(n, t, R, Z, W);
         rsolve_rows(n, t, R, AZ, AW);
-        or_xty(n, t, Z, 1, r, g);
         rtsolve_vec(t, R, g, alpha + (size_t)i * t);
         free(AZ);
       }

@@ -29,7 +29,10 @@ typedef struct {
 
 enum { OR_SRE_CG = 0, OR_SRE_CG2 = 1, OR_MSDO_CG = 2 };
 enum { OR_OK = 0, OR_BREAKDOWN = 7, OR_MAXITER = 8, OR_BADARG = 1 };
-enum { OR_MODE_DEFINITION = 0, OR_MODE_MIRROR = 1 };
+/* DEFINITION: the paper's algebra (explicit SpMMs Qᵀ(A·Z), u = Vα̃, r −= A·u);  MIRROR: the GPU's
+ * algebra (cached A·Q, C = (AQ)ᵀZ, r −= Σ (AW)α̃);  ONESYNCH: MIRROR with the one-synch CGS2 of
+ * reading R36 (SpMM of Z1, Z2ᵀAZ2 = Z1ᵀAZ1 − C2ᵀC2, A·Z2 = A·Z1 − (AQ)C2). */
+enum { OR_MODE_DEFINITION = 0, OR_MODE_MIRROR = 1, OR_MODE_ONESYNCH = 2 };
 enum { OR_ORTHO_ACHOLQR = 0, OR_ORTHO_PRE = 1 };
 
 /* Per-outer-iteration hook for the invariant pins (tests only).

@@ -92,10 +92,14 @@ def test_tiny_dense_spd_exact_termination(oracle_lib, method, n, s, t):
 
 
 # ---------------------------------------------------------------- per-iteration invariants
-@pytest.mark.parametrize("method,s,t", [("sre-cg", 3, 4), ("sre-cg2", 2, 8), ("msdo-cg", 4, 4)])
-def test_invariants_per_outer_iteration(oracle_lib, method, s, t):
+@pytest.mark.parametrize("method,s,t,mode,hi", [("sre-cg", 3, 4, 0, 10.0), ("sre-cg2", 2, 8, 0, 10.0),
+                                                ("msdo-cg", 4, 4, 0, 10.0),
+                                                # one-synch CGS2 (reading R36) on harder bands
+                                                ("sre-cg", 3, 4, 2, 1e4), ("sre-cg2", 2, 8, 2, 1e4),
+                                                ("msdo-cg", 4, 4, 2, 1e4)])
+def test_invariants_per_outer_iteration(oracle_lib, method, s, t, mode, hi):
     N = 24
-    A = ei.stencil_csr(N, N, ndim=2, kappa=ei.bands_kappa(N, band=4, hi=10.0))
+    A = ei.stencil_csr(N, N, ndim=2, kappa=ei.bands_kappa(N, band=4, hi=hi))
     D = A.to_dense()
     xstar = ei.uniform01(3, A.n)
     b = D @ xstar
@@ -120,7 +124,7 @@ def test_invariants_per_outer_iteration(oracle_lib, method, s, t):
             Qm = np.hstack(state["Q"])
             assert np.abs(Qm.T @ r).max() <= 1e-8 * state["rho0"]
 
-    out = oracle_lib.solve(A, b, method, s=s, t=t, tol=1e-8, callback=cb)
+    out = oracle_lib.solve(A, b, method, s=s, t=t, tol=1e-8, callback=cb, mode=mode)
     assert out["converged"] and state["count"] == out["outer_iters"] > 3
     assert out["true_relres"] <= 1e-7
 
@@ -177,6 +181,30 @@ def test_mirror_mode_agrees_with_definition(oracle_lib):
     assert d["converged"] and m["converged"]
     assert abs(d["outer_iters"] - m["outer_iters"]) <= 1
     assert np.linalg.norm(d["x"] - m["x"]) <= 1e-7 * np.linalg.norm(d["x"])
+
+
+@pytest.mark.parametrize("method,s,t,N,hi", [("sre-cg", 3, 16, 48, 1e3), ("sre-cg2", 2, 8, 32, 1e3),
+                                            ("msdo-cg", 4, 4, 32, 1e3), ("sre-cg", 1, 1, 32, 1.0)])
+def test_onesynch_agrees_with_definition(oracle_lib, method, s, t, N, hi):
+    """One-synch CGS2 (reading R36: SpMM of Z1, Z2ᵀAZ2 = Z1ᵀAZ1 − C2ᵀC2, A·Z2 = A·Z1 − (AQ)C2) against
+    the definition mode (two explicit CGS passes Qᵀ(A·Z), R3): the first two outer iterations'
+    x within 1e-10, converged x within 1e-7, outer-iteration counts within 1."""
+    A = ei.stencil_csr(N, N, ndim=2, kappa=ei.bands_kappa(N, band=4, hi=hi))
+    b = ei.uniform_pm1(1806, A.n)
+    pre = [oracle_lib.solve(A, b, method, s, t, 0.0, kmax=3, mode=m) for m in (0, 2)]
+    assert pre[0]["outer_iters"] == pre[1]["outer_iters"] == 2
+    assert np.linalg.norm(pre[1]["x"] - pre[0]["x"]) <= 1e-10 * np.linalg.norm(pre[0]["x"])
+    d, o = (oracle_lib.solve(A, b, method, s, t, 1e-8, mode=m) for m in (0, 2))
+    assert d["converged"] and o["converged"]
+    assert abs(d["outer_iters"] - o["outer_iters"]) <= 1
+    assert np.linalg.norm(o["x"] - d["x"]) <= 1e-7 * np.linalg.norm(d["x"])
+    assert o["true_relres"] <= 2e-8
+
+
+def test_onesynch_rejects_pre_cholqr_and_restructured(oracle_lib):
+    p = ei.cfg1()
+    for kw in (dict(ortho="pre-cholqr"), dict(restructured=True)):
+        assert oracle_lib.solve(p.A, p.b, "sre-cg", 2, 4, 1e-8, mode=2, **kw)["status"] == oracle_lib.BADARG
 
 
 # ---------------------------------------------------------------- degenerate cases
