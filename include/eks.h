@@ -108,7 +108,14 @@ typedef struct {
                              for every block (C = (AQ)ᵀZ, fused CGS sweeps; 2× the memory per outer
                              iteration), 2 = off: store Q only, C = Qᵀ(A·Z) with two more SpMMs per block
                              (reading R24).  report.max_outer_fit = outer iterations the device holds */
-  int reserved[3];
+  int onesynch;           /* 1: one-synch CGS2 (DESIGN reading R36) for the s-step methods with
+                             A-CholQR: the SpMM of each block runs on Z1 (after CGS pass 1) and [C2 | B1 | g1]
+                             is reduced in ONE collective; B = B1 − C2ᵀC2, g = g1 − C2ᵀ(Qᵀr),
+                             Z2 = Z1 − QC2, A·Z2 = A·Z1 − (AQ)C2 (QᵀAQ = I).  2 reductions per block
+                             (C1, [C2|B1|g1]) + ρ²: 2s+1 collectives per outer iteration instead of 3s+1.
+                             Needs A·Q (SRE-CG2/MSDO-CG: aq_cache 0 or 1); CA methods, Pre-CholQR and
+                             restructured: EKS_ERR_INVALID_ARG */
+  int reserved[2];
 } eks_options;
 
 /* Per-kernel-class device time accumulated while options.profile == 1. */

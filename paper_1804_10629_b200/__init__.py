@@ -49,7 +49,7 @@ class _Report(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("max_outer", C.c_int), ("use_graph", C.c_int), ("profile", C.c_int), ("arnoldi", C.c_int),
                 ("ortho", C.c_int), ("restructured", C.c_int), ("precond", C.c_int), ("aq_cache", C.c_int),
-                ("reserved", C.c_int * 3)]
+                ("onesynch", C.c_int), ("reserved", C.c_int * 2)]
 
 
 class _Profile(C.Structure):
@@ -230,14 +230,16 @@ AQ_CACHE = {"auto": 0, "on": 1, "off": 2}
 
 
 def eks_solve_ex(ctx, method, s, t, tol, b, x, max_outer=0, profile=False, raise_on=(5, 6, 1, 2, 3), arnoldi=0,
-                 ortho="acholqr", restructured=False, precond=False, use_graph=False, aq_cache="auto"):
+                 ortho="acholqr", restructured=False, precond=False, use_graph=False, aq_cache="auto",
+                 onesynch=False):
     """Returns (status, report dict).  x holds x0 on entry and the solution on exit.
     arnoldi (CA methods only): 7 = modified CA-Arnoldi (default), 5 = CA-Arnoldi.
-    ortho: "acholqr" (default) or "pre-cholqr"; restructured: Alg 2 / Alg 1 (SRE-CG / SRE-CG2)."""
+    ortho: "acholqr" (default) or "pre-cholqr"; restructured: Alg 2 / Alg 1 (SRE-CG / SRE-CG2).
+    onesynch: one-synch CGS2 (2s+1 collectives per outer iteration, DESIGN reading R36)."""
     m = METHODS[method] if isinstance(method, str) else int(method)
     where = _where(b, x)
     opt = _Options(int(max_outer), int(bool(use_graph)), int(bool(profile)), int(arnoldi), ORTHO[ortho],
-                   int(bool(restructured)), int(bool(precond)), AQ_CACHE[aq_cache])
+                   int(bool(restructured)), int(bool(precond)), AQ_CACHE[aq_cache], int(bool(onesynch)))
     rep = _Report()
     st = lib().eks_solve_ex(ctx, m, int(s), int(t), float(tol), _ptr(b, np.float64), _ptr(x, np.float64), where,
                             C.byref(opt), C.byref(rep))
@@ -250,9 +252,10 @@ def eks_solve(ctx, method, s, t, tol, b, x, max_outer=0):
     return eks_solve_ex(ctx, method, s, t, tol, b, x, max_outer=max_outer)
 
 
-def eks_basis_sweep(ctx, t, nblocks, X0, W_last, profile=False):
+def eks_basis_sweep(ctx, t, nblocks, X0, W_last, profile=False, onesynch=False):
     where = _where(X0, W_last)
     opt = _Options(0, 0, int(bool(profile)))
+    opt.onesynch = int(bool(onesynch))
     rep = _Report()
     st = lib().eks_basis_sweep(ctx, int(t), int(nblocks), _ptr(X0, np.float64), _ptr(W_last, np.float64), where,
                                C.byref(opt), C.byref(rep))
@@ -353,7 +356,8 @@ class Solver:
         eks_setup_precond(self.ctx, ndomains, *self._csr, kind=kind)
 
     def solve(self, b, method="sre-cg", s=1, t=1, tol=1e-8, x0=None, max_outer=0, profile=False, arnoldi=0,
-              ortho="acholqr", restructured=False, precond=False, use_graph=False, aq_cache="auto"):
+              ortho="acholqr", restructured=False, precond=False, use_graph=False, aq_cache="auto",
+              onesynch=False):
         if isinstance(b, np.ndarray):
             b = np.ascontiguousarray(b, np.float64)
             x = np.zeros_like(b) if x0 is None else np.ascontiguousarray(x0, np.float64).copy()
@@ -361,7 +365,7 @@ class Solver:
             x = b.new_zeros(b.shape) if x0 is None else x0.clone()
         st, rep = eks_solve_ex(self.ctx, method, s, t, tol, b, x, max_outer=max_outer, profile=profile,
                                arnoldi=arnoldi, ortho=ortho, restructured=restructured, precond=precond,
-                               use_graph=use_graph, aq_cache=aq_cache)
+                               use_graph=use_graph, aq_cache=aq_cache, onesynch=onesynch)
         rep["status"] = st
         rep["x"] = x
         return rep

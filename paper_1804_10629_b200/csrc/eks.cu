@@ -137,6 +137,11 @@ struct eks_ctx {
   double* part2 = nullptr;  // per-CTA partials of the fused next-block C1
   size_t part2_cap = 0;
   bool c1_ready = false;    // C1 of the next CGS pass already reduced into C1
+  // one-synch CGS2 (eks_options.onesynch, reading R36): [C2 | B1 | g1] of a block in one buffer, one
+  // stacked reduction per block (2 per block with C1, 2s+1 per outer iteration with ρ²)
+  bool onesynch = false;
+  double* os = nullptr;
+  size_t os_cap = 0;
   double *Bg = nullptr, *Rm = nullptr, *Rinv = nullptr, *alpha = nullptr, *scal = nullptr;
   int alpha_cap = 0;
   int* flag = nullptr;
@@ -282,8 +287,9 @@ void free_workspace(eks_ctx* c) {
     *b = Block{};
   }
   for (double** p : {&c->b, &c->r, &c->rnew, &c->dx, &c->part, &c->C1, &c->C2, &c->Bg, &c->Rm, &c->Rinv,
-                     &c->alpha, &c->scal, &c->Rslot}) { dfree(*p); *p = nullptr; }
+                     &c->alpha, &c->scal, &c->Rslot, &c->os}) { dfree(*p); *p = nullptr; }
   c->rslot_cap = 0;
+  c->os_cap = 0;
   dfree(c->flag);
   c->flag = nullptr;
   dfree(c->cnt);
@@ -360,6 +366,15 @@ eks_status ensure_C(eks_ctx* ctx, size_t doubles) {
 }
 
 // Tail reduction of a producer kernel's per-CTA partials into out[0..count) (eks_device.cuh).
+eks_status ensure_os(eks_ctx* ctx, size_t doubles) {
+  if (ctx->os_cap >= doubles) return EKS_OK;
+  dfree(ctx->os);
+  ctx->os = nullptr;
+  ST(dalloc(ctx, &ctx->os, doubles));
+  ctx->os_cap = doubles;
+  return EKS_OK;
+}
+
 eks::Tail tail(eks_ctx* ctx, int slot, double* out, size_t count, double* out2 = nullptr, int split = INT_MAX) {
   eks::Tail tl;
   tl.cnt = ctx->cnt + slot;
@@ -867,6 +882,47 @@ eks_status restructured_update(eks_ctx* ctx, int t, const double* W, const doubl
   return EKS_OK;
 }
 
+// One-synch CGS2 of Z against the window (DESIGN reading R36; the oracle's
+// MODE_ONESYNCH): pass 1 as in cgs2() (C1 = (AQ)ᵀZ, fused from the previous block's R⁻¹ kernel for
+// SRE-CG), Z1 = Z − Q C1 with C2 = (AQ)ᵀZ1 (NOT reduced yet); the SpMM runs on Z1: A·Z1, B1 = Z1ᵀAZ1,
+// g1 = Z1ᵀr; ONE stacked allreduce of [C2 | B1 | g1]; then, since QᵀAQ = I and QᵀAZ1 = C2,
+//   Z2ᵀAZ2 = B1 − C2ᵀC2,  Z2ᵀr = g1 − C2ᵀ(Qᵀr)  (k_onesynch_fix, into Bg),
+//   Z2 = Z1 − Q C2,  A·Z2 = A·Z1 − (AQ) C2     (two update sweeps, in place).
+// Leaves Z2 in Z (the block's slot), A·Z2 in AZ and [B | g] in Bg for the Cholesky and R⁻¹ kernels.
+eks_status onesynch_block(eks_ctx* ctx, int t, const Window& w, const double* Zsrc, Block& Z, double* AZ,
+                          bool with_update, int i) {
+  const int nq = (int)w.Q.size();
+  const size_t cb = (size_t)nq * t * t;
+  const double* const* RQ = w.RQ.empty() ? nullptr : w.RQ.data();
+  ST(ensure_C(ctx, cb));
+  ST(ensure_os(ctx, cb + (size_t)t * t + t));
+  if (!ctx->c1_ready) ST(tn_reduce(ctx, t, nq, w.AQ.data(), Zsrc, nullptr, ctx->C1));  // C1 = (AQ)ᵀZ (synch 1)
+  ctx->c1_ready = false;
+  double* C2 = ctx->os;
+  double* Bg1 = ctx->os + cb;
+  if (eks::sweep_supported(t) && eks::sweep_fused_supported(t, nq)) {
+    ST(update_coef(ctx, t, nq, w.Q.data(), w.AQ.data(), ctx->C1, Zsrc, Z.loc, C2, false, RQ));
+  } else {
+    ST(ts_update(ctx, t, nq, w.Q.data(), ctx->C1, Zsrc, Z.loc, RQ));
+    ST(tn_reduce(ctx, t, nq, w.AQ.data(), Z.loc, nullptr, C2, false));
+  }
+  ST(spmm_gram(ctx, Z, AZ, t, with_update ? ctx->r : nullptr, Bg1, nullptr, false));
+  ST(allreduce(ctx, ctx->os, cb + (size_t)t * t + t));  // synch 2: [C2 | B1 | g1]
+  // window blocks of this outer iteration (block i of it): the last i' = min(i, nq); their
+  // α̃ = Wᵀr_{k−1} start at alpha + (i − i')·t
+  const int ic = std::min(i, nq);
+  {
+    KScope k(ctx, EKS_K_CHOL);
+    account(ctx, EKS_K_CHOL, 0.0, (double)nq * t * t * (t + 1) + 2.0 * ic * t * t);
+    CK(eks::launch_onesynch_fix(ctx->stream, t, nq, nq - ic, C2, Bg1,
+                                (with_update && ic > 0) ? ctx->alpha + (size_t)(i - ic) * t : nullptr,
+                                ctx->Bg));
+  }
+  ST(ts_update(ctx, t, nq, w.Q.data(), C2, Z.loc, Z.loc, RQ));  // Z2 = Z1 − Q C2
+  ST(ts_update(ctx, t, nq, w.AQ.data(), C2, AZ, AZ));           // A·Z2 = A·Z1 − (AQ) C2
+  return EKS_OK;
+}
+
 // One A-orthonormalized block: Zsrc (or the split of r) → W_new, AW_new, R⁻¹, alpha_b.
 eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bool seed_from_r, const double* Zsrc,
                       Block* Wn, Block* AWn, int alpha_off, int gb, int mode) {
@@ -885,17 +941,20 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
     ST(prec_apply(ctx, t, Zsrc, ctx->Zp.loc));
     Zsrc = ctx->Zp.loc;
   }
-  if (!w.Q.empty()) {
+  const bool with_update = !(mode & 4);
+  // lazy basis: this block's R⁻¹ lives in its ring slot (the later windows fold it into their
+  // coefficients) and the R⁻¹ kernel leaves Z2 in the slot instead of W
+  double* Rinv = ctx->lazy ? ctx->Rslot + (size_t)(nblocks % ring) * t * t : ctx->Rinv;
+  const bool os = ctx->onesynch && !w.Q.empty() && !w.AQ.empty();
+  if (os) {
+    ST(onesynch_block(ctx, t, w, Zsrc, *Wn, AWn->loc, with_update, alpha_off / t));
+  } else if (!w.Q.empty()) {
     ST(cgs2(ctx, t, w.Q, w.AQ, Zsrc, Wn->loc, &w.RQ));  // "A-orthonormalize W against Q"
   } else if (Zsrc != Wn->loc) {
     CK(cudaMemcpyAsync(Wn->loc, Zsrc, sizeof(double) * ctx->n * t, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   if (ctx->ortho == 1) ST(pre_euclid(ctx, t, *Wn, AWn->loc, gb));  // Pre-CholQR (reading R30)
   // "A-orthonormalize W": A-CholQR with one SpMM of Z2 (AW = (A Z2) R⁻¹)
-  const bool with_update = !(mode & 4);
-  // lazy basis: this block's R⁻¹ lives in its ring slot (the later windows fold it into their
-  // coefficients) and the R⁻¹ kernel leaves Z2 in the slot instead of W
-  double* Rinv = ctx->lazy ? ctx->Rslot + (size_t)(nblocks % ring) * t * t : ctx->Rinv;
   eks::CholArgs ch{};
   ch.R = ctx->Rm;
   ch.Rinv = Rinv;
@@ -904,7 +963,8 @@ eks_status make_block(eks_ctx* ctx, int t, int method, int ring, int nblocks, bo
   ch.gblock = gb;
   // t ≤ 32: the R⁻¹ kernel factors the Gram itself (every CTA, identical inputs on every rank);
   // otherwise the last CTA of the SpMM+Gram kernel or a separate Cholesky launch does it.
-  ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg, &ch));
+  if (!os) ST(spmm_gram(ctx, *Wn, AWn->loc, t, with_update ? ctx->r : nullptr, ctx->Bg, &ch));
+  else ctx->chol_fused = false;  // B, g corrected by onesynch_block
   if (!ctx->chol_fused) {  // default: one-warp Cholesky launch (rsqrt pivots for t ≤ 32)
     KScope k(ctx, EKS_K_CHOL);
     CK(eks::launch_chol_fast(ctx->stream, t, ctx->Bg, with_update ? ctx->Bg + t * t : nullptr, ctx->Rm, Rinv,
@@ -1460,6 +1520,7 @@ eks_status prealloc_steady(eks_ctx* ctx, int t, int ring) {
     ST(slot(ctx, t, idx, &W, &AW));
   }
   ST(ensure_C(ctx, (size_t)2 * t * t));
+  if (ctx->onesynch) ST(ensure_os(ctx, (size_t)3 * t * t + t));
   size_t stride = std::max(eks::tn_partials_stride(t, 2, false), eks::tn_partials_stride(t, 1, true));
   if (eks::sweep_supported(t))
     stride = std::max({stride, eks::sweep_part_stride(t, 2, false), eks::sweep_part_stride(t, 1, true)});
@@ -1481,6 +1542,7 @@ void begin_run(eks_ctx* ctx, const eks_options* opt) {
   ctx->c1_ready = false;
   ctx->aq_off = false;  // set per solve (full-basis methods)
   ctx->lazy = false;    // set per solve / sweep (s-step SRE-CG, t ≥ 8)
+  ctx->onesynch = opt && opt->onesynch;
 }
 
 }  // namespace
@@ -2115,7 +2177,11 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   // more SpMMs per block, half the memory per outer iteration
   const int aqc = opt ? opt->aq_cache : 0;
   if (aqc < 0 || aqc > 2) return fail(ctx, EKS_ERR_INVALID_ARG, "aq_cache must be 0 (auto), 1 (on) or 2 (off)");
-  ctx->aq_off = !ring && !ca && !restr && aqc != 1;
+  // one-synch CGS2 (reading R36) forms A·Z2 = A·Z1 − (AQ)C2: it needs A·Q (auto turns the cache on)
+  if (ctx->onesynch && (ca || ortho || restr || aqc == 2))
+    return fail(ctx, EKS_ERR_INVALID_ARG, "onesynch is for the s-step methods with A-CholQR, not restructured, "
+                                          "with A·Q cached (aq_cache != 2)");
+  ctx->aq_off = !ring && !ca && !restr && aqc != 1 && !ctx->onesynch;
   ctx->last_aq_off = ctx->aq_off;
   ctx->lazy = method == EKS_SRE_CG && !restr && eks::sweep_supported(t) && lazy_env();
   ctx->last_lazy = ctx->lazy;

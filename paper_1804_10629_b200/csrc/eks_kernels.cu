@@ -1119,6 +1119,50 @@ cudaError_t launch_wtv(cudaStream_t st, int64_t n, int t, const double* W, const
   return launch_k(k_wtv, nblk, 256, 0, st, n, t, W, v, part);
 }
 
+// One-synch CGS2 (DESIGN reading R36): after the single stacked reduction of
+// [C2 | B1 | g1] (C2 = (AQ)ᵀZ1, B1 = Z1ᵀ(A·Z1), g1 = Z1ᵀr), with QᵀAQ = I and QᵀAZ1 = C2:
+//   B = Z2ᵀAZ2 = B1 − C2ᵀC2   (upper entries, mirrored),   g = Z2ᵀr = g1 − Σ_{q ≥ qcur} C2_qᵀ α̃_q,
+// where α̃_q = W_qᵀ r_{k−1} of the window blocks built in this outer iteration (abase = that of
+// window block qcur; the older blocks' Wᵀr_{k−1} = 0).  One warp per output entry; its lanes
+// stride the nq·t-long sum and reduce with a fixed butterfly (run-to-run reproducible).
+__global__ void __launch_bounds__(256) k_onesynch_fix(int t, int nq, int qcur, const double* __restrict__ C,
+                                                      const double* __restrict__ Bg1, const double* __restrict__ abase,
+                                                      double* __restrict__ Bg) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int e = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nU = t * (t + 1) / 2, m = nq * t;
+  if (e < nU) {
+    int a = 0, rem = e;
+    while (rem >= t - a) {
+      rem -= t - a;
+      ++a;
+    }
+    const int c = a + rem;
+    double v = 0.0;
+    for (int qa = lane; qa < m; qa += 32) v = fma(C[(size_t)qa * t + a], C[(size_t)qa * t + c], v);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+      const double b = Bg1[a * t + c] - v;
+      Bg[a * t + c] = b;
+      Bg[c * t + a] = b;
+    }
+  } else if (e < nU + t) {
+    const int c = e - nU;
+    double v = 0.0;
+    if (abase)
+      for (int qa = qcur * t + lane; qa < m; qa += 32) v = fma(C[(size_t)qa * t + c], abase[qa - qcur * t], v);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) Bg[t * t + c] = Bg1[t * t + c] - v;
+  }
+}
+
+cudaError_t launch_onesynch_fix(cudaStream_t st, int t, int nq, int qcur, const double* C, const double* Bg1,
+                                const double* abase, double* Bg) {
+  const int warps = t * (t + 1) / 2 + t;
+  return launch_k(k_onesynch_fix, (warps + 7) / 8, 256, 0, st, t, nq, qcur, C, Bg1, abase, Bg);
+}
+
 // Column block j of −R⁻¹ packed for the update sweeps (W_j = 0 − Σ_{i≤j} V_i·(−R⁻¹_ij)):
 // pack + (j(j+1)/2)·t·t holds the t×t blocks −R⁻¹_ij, i = 0..j, each row-major (row = column of V_i).
 __global__ void __launch_bounds__(256) k_ca_pack(int t, int s, const double* __restrict__ Rinv,

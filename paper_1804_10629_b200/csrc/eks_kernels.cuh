@@ -106,6 +106,12 @@ cudaError_t launch_ca_pack(cudaStream_t st, int t, int s, const double* Rinv, do
 cudaError_t launch_ca_update(cudaStream_t st, int64_t n, int t, int s, const CaPtrs& P, const double* alpha,
                              double* x, const double* r, double* rnew, double* part, int nblk);
 
+// ---- one-synch CGS2 (reading R36): Bg[0..t·t) = B1 − C2ᵀC2 (symmetric), Bg[t·t..t·t+t) = g1 − Σ_{q ≥ qcur}
+// C2_qᵀ α̃_q (abase = α̃ of window block qcur, contiguous per block; NULL: g = g1).  C2 is (nq·t)×t
+// row-major, Bg1 = [B1 (upper read) | g1].
+cudaError_t launch_onesynch_fix(cudaStream_t st, int t, int nq, int qcur, const double* C, const double* Bg1,
+                                const double* abase, double* Bg);
+
 // ---- vector kernels
 // out = b − Ax (y holds A·x): r = b − y; partial Σ r² per CTA
 cudaError_t launch_residual(cudaStream_t st, int64_t n, const double* b, const double* y, double* r,

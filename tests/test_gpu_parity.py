@@ -754,3 +754,87 @@ def test_ca_breakdown_reported(eks, torch_cuda, oracle_lib):
     S.close()
     assert rep["status"] == eks.EKS_ERR_BREAKDOWN and rep["outer_iters"] == 0
     assert float(rep["x"].abs().max()) == 0.0
+
+
+# ------------------------------------------------------------------ (a3) one-synch CGS2 (reading R36)
+@pytest.mark.parametrize("method,s_,t,N,aq", [("sre-cg", 3, 16, 64, "auto"), ("sre-cg", 2, 4, 48, "auto"),
+                                              ("sre-cg", 1, 1, 32, "auto"), ("sre-cg", 2, 32, 48, "auto"),
+                                              ("sre-cg2", 2, 8, 48, "on"), ("msdo-cg", 4, 4, 32, "auto"),
+                                              ("msdo-cg", 2, 16, 48, "on")])
+def test_onesynch_end_to_end(eks, torch_cuda, oracle_lib, method, s_, t, N, aq):
+    """eks_options.onesynch (SpMM of Z1, one stacked reduction of [C2 | B1 | g1], B = B1 − C2ᵀC2,
+    A·Z2 = A·Z1 − (AQ)C2) against the oracle's MODE_ONESYNCH and its DEFINITION mode on κ = 1e3
+    bands: counts within max(5 %, 1), x within 1e-6 after convergence; the first two outer
+    iterations (tol = 0) within 1e-10 of both (equal in exact arithmetic)."""
+    A = ei.stencil_csr(N, N, ndim=2, kappa=ei.bands_kappa(N, band=4, hi=1e3))
+    bh = ei.uniform_pm1(1806, A.n)
+    S = eks.Solver(A)
+    b = dev(torch_cuda, bh)
+    rep = S.solve(b, method, s_, t, 1e-8, onesynch=True, aq_cache=aq)
+    pre = S.solve(b, method, s_, t, 0.0, max_outer=3, onesynch=True, aq_cache=aq)
+    S.close()
+    for mode in (oracle_lib.MODE_ONESYNCH, oracle_lib.MODE_DEFINITION):
+        ref = oracle_lib.solve(A, bh, method, s_, t, 1e-8, mode=mode)
+        refp = oracle_lib.solve(A, bh, method, s_, t, 0.0, kmax=3, mode=mode)
+        assert rep["status"] == 0 and rep["converged"] and ref["converged"]
+        assert abs(rep["outer_iters"] - ref["outer_iters"]) <= max(1, round(0.05 * ref["outer_iters"])), \
+            (mode, rep["outer_iters"], ref["outer_iters"])
+        assert rel(host(rep["x"]), ref["x"]) <= 1e-6, mode
+        assert pre["outer_iters"] == refp["outer_iters"] == 2
+        assert rel(host(pre["x"]), refp["x"]) <= 1e-10, mode
+    assert rep["true_relres"] <= 2e-8
+
+
+def test_onesynch_graph_replay_bitwise_and_errors(eks, torch_cuda):
+    """One-synch under CUDA-graph replay: bitwise the plain one-synch path; the options it does not
+    combine with are rejected (EKS_ERR_INVALID_ARG)."""
+    A = ei.poisson2d(64)
+    b = dev(torch_cuda, ei.uniform_pm1(79, A.n))
+    S = eks.Solver(A)
+    a = S.solve(b, "sre-cg", 3, 16, 1e-10, onesynch=True)
+    g = S.solve(b, "sre-cg", 3, 16, 1e-10, onesynch=True, use_graph=True)
+    assert a["converged"] and g["converged"] and a["outer_iters"] == g["outer_iters"] > 8
+    assert torch_cuda.equal(a["x"], g["x"])
+    for method, kw in [("ca-sre-cg", {}), ("sre-cg", dict(ortho="pre-cholqr")), ("sre-cg", dict(restructured=True)),
+                       ("msdo-cg", dict(aq_cache="off"))]:
+        with pytest.raises(eks.EksError) as e:
+            S.solve(b, method, 2, 4, 1e-8, onesynch=True, **kw)
+        assert e.value.status == 1
+    S.close()
+
+
+@pytest.mark.parametrize("cfg", ["cfg4", "cfg3"])
+def test_onesynch_path_size_prefix(eks, torch_cuda, oracle_lib, cfg):
+    """One-synch at the 64³ analogs of cfg4 (SRE-CG t=64 s=2) and cfg3 (MSDO-CG t=32 s=4, A·Q cached):
+    after two outer iterations x and r agree with the oracle's DEFINITION mode within 1e-10 of their
+    max-norm (multi-tile sweeps and plane-marching units at t = 32/64)."""
+    torch = torch_cuda
+    p = ei.cfg4(N=64) if cfg == "cfg4" else ei.cfg3(N=64)
+    ref, its = _oracle_iterations(oracle_lib, p, kmax=3)
+    S = eks.Solver(p.A)
+    b = dev(torch, p.b)
+    r = torch.empty(p.A.n, dtype=torch.float64, device="cuda")
+    rep = S.solve(b, p.method, p.s, p.t, 0.0, max_outer=3, onesynch=True, aq_cache="on")
+    assert rep["outer_iters"] == 2
+    eks.eks_k_last_residual(S.ctx, r)
+    S.close()
+    for got, exp in ((host(rep["x"]), its[2]["x"]), (host(r), its[2]["r"])):
+        assert np.abs(got - exp).max() <= 1e-10 * np.abs(exp).max()
+
+
+@pytest.mark.parametrize("t", [8, 16, 32])
+def test_onesynch_basis_sweep(eks, torch_cuda, oracle_lib, t):
+    """cfg5's basis sweep with one-synch CGS2: W_last within 1e-9 of the oracle's sweep and
+    A-orthonormal to 1e-10."""
+    torch = torch_cuda
+    A = ei.stencil_csr(12, 12, 12, ndim=3)
+    X0 = ei.cfg5_start_block(A.n, t)
+    S = eks.Solver(A)
+    W = torch.empty(A.n, t, dtype=torch.float64, device="cuda")
+    rep = eks.eks_basis_sweep(S.ctx, t, 8, dev(torch, X0), W, onesynch=True)
+    S.close()
+    st, Wo = oracle_lib.basis_sweep(A, X0, 8)
+    assert st == 0 and rep["outer_iters"] == 8
+    assert rel(host(W), Wo) <= 1e-9
+    Wh = host(W)
+    assert np.abs(oracle_lib.xty(Wh, oracle_lib.spmm(A, Wh)) - np.eye(t)).max() <= 1e-10

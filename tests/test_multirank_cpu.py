@@ -196,3 +196,75 @@ def test_plan_halo_single_rank_is_identity():
     ext, need, geom = eks.eks_plan_halo(0, 1, np.array([0, A.n]), A.row_ptr, A.col)
     assert np.array_equal(ext, A.col) and not need.any()
     assert geom == dict(halo_before=0, halo_after=0, interior_lo=0, interior_hi=A.n)
+
+
+def _onesynch_worker(rank, world, port, t, q):
+    """One block of one-synch CGS2 (DESIGN reading R36) on row slabs: rank-local partials, exactly two
+    allreduces (C1, then the stacked [C2 | B1 | g1]), the local B/g correction — compared with the
+    two-pass CGS2 + A-CholQR Gram of the whole block (R3/R4) computed on one process."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        A = ei.stencil_csr(20, 20, ndim=2, kappa=ei.bands_kappa(20, band=4, hi=1e2))
+        n = A.n
+        lo, hi = slab(rank, world, n, t)
+        # a window Q of two A-orthonormal blocks (A-CholQR of a random n×2t block), Z, r, α of block 1
+        V = ei.uniform_pm1(21, n * 2 * t).reshape(n, 2 * t)
+        L = np.linalg.cholesky(V.T @ oracle.spmm(A, V))
+        Q = np.linalg.solve(L, V.T).T
+        AQ = oracle.spmm(A, Q)
+        Z = ei.uniform_pm1(22, n * t).reshape(n, t)
+        r = ei.uniform_pm1(23, n)
+        alpha1 = Q[:, t:].T @ r  # α̃ of the window block built in this outer iteration (the older one: 0)
+        ncoll = 0
+
+        def allreduce(a):
+            nonlocal ncoll
+            ncoll += 1
+            tt = torch.from_numpy(np.ascontiguousarray(a))
+            dist.all_reduce(tt)
+            return tt.numpy()
+        sl = slice(lo, hi)
+        C1 = allreduce(AQ[sl].T @ Z[sl])                       # synch 1
+        Z1 = Z - Q @ C1                                         # (every rank: its rows; all rows kept here
+        AZ1 = oracle.spmm(A, Z1)                                #  only to form A·Z1 without a halo exchange)
+        stacked = np.concatenate([(AQ[sl].T @ Z1[sl]).ravel(), (Z1[sl].T @ AZ1[sl]).ravel(), Z1[sl].T @ r[sl]])
+        red = allreduce(stacked)                                # synch 2: [C2 | B1 | g1]
+        C2 = red[:2 * t * t].reshape(2 * t, t)
+        B1 = red[2 * t * t:3 * t * t].reshape(t, t)
+        g1 = red[3 * t * t:]
+        B = B1 - C2.T @ C2
+        g = g1 - C2[t:].T @ alpha1
+        Z2 = Z1[sl] - Q[sl] @ C2
+        AZ2 = AZ1[sl] - AQ[sl] @ C2
+        # reference: two explicit CGS passes Qᵀ(A·Z) on one process, then the Gram of Z2
+        Zr = Z - Q @ (Q.T @ oracle.spmm(A, Z))
+        Zr = Zr - Q @ (Q.T @ oracle.spmm(A, Zr))
+        AZr = oracle.spmm(A, Zr)
+        Bref, gref = Zr.T @ AZr, Zr.T @ r
+        errs = (float(np.abs(B - Bref).max() / np.abs(Bref).max()), float(np.abs(g - gref).max() / np.abs(gref).max()),
+                float(np.abs(Z2 - Zr[sl]).max() / np.abs(Zr).max()), float(np.abs(AZ2 - AZr[sl]).max() / np.abs(AZr).max()))
+        q.put((rank, ncoll, errs))
+    except Exception as e:
+        q.put((rank, f"error: {e!r}"))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,t", [(2, 4), (4, 8)])
+def test_onesynch_protocol_two_collectives(world, t):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_onesynch_worker, args=(r, world, port, t, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(not isinstance(r[1], str) for r in res), res
+    for rank, ncoll, errs in res:
+        assert ncoll == 2, (rank, ncoll)
+        assert max(errs) <= 1e-10, (rank, errs)
