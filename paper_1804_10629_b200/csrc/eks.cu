@@ -1390,8 +1390,10 @@ void parallel_rows(int64_t n, F&& f) {
 // extended layout exactly the neighbouring planes (halo_before/after ∈ {0, plane}); columns are GLOBAL.
 // Values are stored per row in ascending offset order, 0 in absent slots (VS = (w+1)&~1 per row).
 // geom = {nx, ny, nz, w, gb, ga}; false (nothing built, the ELL/CSR kernels run) otherwise.
-bool grid_plan_host(int64_t n, const int64_t* rp, const int32_t* col, const double* val, int64_t row_begin,
-                    int64_t halo_before, int64_t halo_after, int64_t geom[6], std::vector<double>& sv) {
+// Detection only: geom = {nx, ny, nz, w, gb, ga} and the positive offsets b = nx, c = nx·ny (2D: c = 0)
+// from the offsets of the first rows; the per-entry check comes with the fill (host or device).
+bool grid_detect(int64_t n, const int64_t* rp, const int32_t* col, int64_t row_begin, int64_t halo_before,
+                 int64_t halo_after, int64_t geom[6], int64_t& b, int64_t& c) {
   int64_t pos[3] = {0, 0, 0};
   int np = 0;
   // the offsets from the first rows (a stencil shows all of them within a few planes); an offset
@@ -1411,7 +1413,8 @@ bool grid_plan_host(int64_t n, const int64_t* rp, const int32_t* col, const doub
   for (int a2 = 1; a2 < np; ++a2)  // np ≤ 3: insertion sort (std::sort trips -Warray-bounds here)
     for (int b2 = a2; b2 > 0 && pos[b2 - 1] > pos[b2]; --b2) std::swap(pos[b2 - 1], pos[b2]);
   if (np < 2 || pos[0] != 1) return false;
-  const int64_t b = pos[1], c = np == 3 ? pos[2] : 0;
+  b = pos[1];
+  c = np == 3 ? pos[2] : 0;
   int64_t nx = b, ny = 1, plane = b;
   if (np == 3) {
     if (c % b) return false;
@@ -1422,7 +1425,21 @@ bool grid_plan_host(int64_t n, const int64_t* rp, const int32_t* col, const doub
   if ((halo_before != 0 && halo_before != plane) || (halo_after != 0 && halo_after != plane)) return false;
   const int64_t nz = n / plane;
   if (nx >= INT32_MAX || ny >= INT32_MAX || nz >= INT32_MAX) return false;
-  const int w = np == 3 ? 7 : 5, VS = (w + 1) & ~1;
+  geom[0] = nx;
+  geom[1] = ny;
+  geom[2] = nz;
+  geom[3] = np == 3 ? 7 : 5;
+  geom[4] = halo_before ? 1 : 0;
+  geom[5] = halo_after ? 1 : 0;
+  return true;
+}
+
+bool grid_plan_host(int64_t n, const int64_t* rp, const int32_t* col, const double* val, int64_t row_begin,
+                    int64_t halo_before, int64_t halo_after, int64_t geom[6], std::vector<double>& sv) {
+  int64_t b = 0, c = 0;
+  if (!grid_detect(n, rp, col, row_begin, halo_before, halo_after, geom, b, c)) return false;
+  const int64_t nx = geom[0], ny = geom[1];
+  const int w = (int)geom[3], VS = (w + 1) & ~1;
   const int64_t offs7[7] = {-c, -b, -1, 0, 1, b, c};
   const int64_t offs5[5] = {-b, -1, 0, 1, b};
   const int64_t* offs = w == 7 ? offs7 : offs5;
@@ -1446,23 +1463,32 @@ bool grid_plan_host(int64_t n, const int64_t* rp, const int32_t* col, const doub
       }
     }
   });
-  if (!ok) return false;
-  geom[0] = nx;
-  geom[1] = ny;
-  geom[2] = nz;
-  geom[3] = w;
-  geom[4] = halo_before ? 1 : 0;
-  geom[5] = halo_after ? 1 : 0;
-  return true;
+  return ok.load();
 }
 
 eks_status build_grid_plan(eks_ctx* ctx, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
                            int64_t row_begin, int64_t halo_before, int64_t halo_after) {
-  int64_t g[6];
-  std::vector<double> sv;
-  if (!grid_plan_host(n, rp, col, val, row_begin, halo_before, halo_after, g, sv)) return EKS_OK;
-  CK(cudaMalloc((void**)&ctx->d_sv, sizeof(double) * sv.size()));
-  CK(cudaMemcpy(ctx->d_sv, sv.data(), sizeof(double) * sv.size(), cudaMemcpyHostToDevice));
+  (void)val;
+  int64_t g[6], b = 0, c = 0;
+  if (!grid_detect(n, rp, col, row_begin, halo_before, halo_after, g, b, c)) return EKS_OK;
+  // the stencil values are scattered from the uploaded CSR by a device kernel (columns in the extended
+  // layout: offset = ecol − halo_before − i); an entry outside the stencil leaves the plan unbuilt
+  const int VS = ((int)g[3] + 1) & ~1;
+  CK(cudaMalloc((void**)&ctx->d_sv, sizeof(double) * (size_t)n * VS));
+  int* d_bad = nullptr;
+  CK(cudaMalloc((void**)&d_bad, sizeof(int)));
+  CK(cudaMemset(d_bad, 0, sizeof(int)));
+  CK(eks::launch_grid_sv(ctx->stream, n, ctx->d_rp, ctx->d_col, ctx->d_val, row_begin, halo_before, g[0], g[1], b, c,
+                         (int)g[3], ctx->d_sv, d_bad, ctx->sms));
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_bad);
+  if (bad) {
+    dfree(ctx->d_sv);
+    ctx->d_sv = nullptr;
+    return EKS_OK;
+  }
   ctx->gplan.nx = (int)g[0];
   ctx->gplan.ny = (int)g[1];
   ctx->gplan.nz = (int)g[2];

@@ -666,6 +666,45 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
   return launch_k(k_spmm_grid<T, W>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch, ns, gram, tm);
 }
 
+// Setup: the stencil values per row from the uploaded CSR (columns in the extended layout, so the offset
+// of entry p of local row i is col[p] − halo_before − i in both the one-rank and the ghost-plane case):
+// sv[i][k] = val[p] for the slot k of that offset (ascending: −c, −b, −1, 0, 1, b, c; 2D without ±c),
+// 0 in absent slots; an entry at no slot or crossing an x-line (y-plane) boundary sets *bad.
+__global__ void __launch_bounds__(256) k_grid_sv(int64_t n, const int* __restrict__ rp, const int* __restrict__ col,
+                                                 const double* __restrict__ val, int64_t row_begin, int64_t halo_before,
+                                                 int64_t nx, int64_t ny, int64_t b, int64_t c, int w,
+                                                 double* __restrict__ sv, int* __restrict__ bad) {
+  const int VS = (w + 1) & ~1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gi = row_begin + i, x = gi % nx, y = (gi / nx) % ny;
+    double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool ok = true;
+    for (int p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t o = (int64_t)col[p] - halo_before - i;
+      int k;
+      if (w == 7) k = o == -c ? 0 : o == -b ? 1 : o == -1 ? 2 : o == 0 ? 3 : o == 1 ? 4 : o == b ? 5 : o == c ? 6 : -1;
+      else k = o == -b ? 0 : o == -1 ? 1 : o == 0 ? 2 : o == 1 ? 3 : o == b ? 4 : -1;
+      if (k < 0 || (o == 1 && x + 1 >= nx) || (o == -1 && x == 0) ||
+          (w == 7 && ((o == b && y + 1 >= ny) || (o == -b && y == 0))))
+        ok = false;
+      else
+        v[k] = val[p];
+    }
+    if (!ok) atomicExch(bad, 1);
+#pragma unroll
+    for (int k = 0; k < 8; k += 2)
+      if (k < VS) *reinterpret_cast<double2*>(sv + i * VS + k) = make_double2(v[k], v[k + 1]);
+  }
+}
+
+cudaError_t launch_grid_sv(cudaStream_t st, int64_t n, const int* rp, const int* col, const double* val,
+                           int64_t row_begin, int64_t halo_before, int64_t nx, int64_t ny, int64_t b, int64_t c, int w,
+                           double* sv, int* bad, int sms) {
+  if (w != 5 && w != 7) return cudaErrorInvalidValue;
+  k_grid_sv<<<sms * 8, 256, 0, st>>>(n, rp, col, val, row_begin, halo_before, nx, ny, b, c, w, sv, bad);
+  return cudaGetLastError();
+}
+
 bool spmm_grid_fused_chol(int t) { return t == 8 || t == 16; }
 
 bool spmm_grid_fits(int t, const GridPlan& gp) {

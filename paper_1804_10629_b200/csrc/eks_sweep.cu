@@ -351,13 +351,18 @@ struct ApCfg {
   static constexpr int OT = C1N * MT * MT;
   static constexpr int WS = (C1N == 0) ? 1 : (OT >= 8 ? 1 : 8 / OT);
   static constexpr int TPW = (C1N == 0) ? 1 : (OT >= 8 ? OT / 8 : 1);
-  static constexpr int RED = (WS > 1 ? 8 * C1N * T * T : 0);
+  // WOWN (T ≤ 16): every warp accumulates ALL C1 tiles over its own 8 rows (k-steps of 4 rows) from
+  // fragments loaded once per k-step (AW column tiles serve as both operands of the AWᵀAW tiles) — no
+  // CTA barrier between the R⁻¹ product and C1, ≈2.5× fewer shared loads; per-warp partials summed at the end
+  static constexpr bool WOWN = T <= 16 && C1N > 0;
+  static constexpr int NAW = WOWN ? (C1N == 2 ? MT * MT : 0) + MT * (MT + 1) / 2 : 0;
+  static constexpr int RED = WOWN ? 8 * C1N * T * T : (WS > 1 ? 8 * C1N * T * T : 0);
   static constexpr int SMEM0 = NS * STAGE + T * (T + 4) + T;
   static constexpr int SMEM = SMEM0 > RED ? SMEM0 : RED;
 };
 
 template <int T, int C1N, bool ZT = true>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, (T <= 16 ? 2 : 1))
     k_apply_tc(int64_t n, double* Z2W, double* AZ2AW, const double* __restrict__ Rinv,
                const double* __restrict__ alpha, double* __restrict__ x, double* __restrict__ dx,
                const double* __restrict__ r, double* __restrict__ rnew, const int* __restrict__ flag, int mode,
@@ -423,9 +428,10 @@ __global__ void __launch_bounds__(256, 1)
   }
 
   double rr_acc = 0.0;
-  double acc[K::TPW][2];
+  constexpr int NACC = K::WOWN ? K::NAW : K::TPW;
+  double acc[NACC][2];
 #pragma unroll
-  for (int u = 0; u < K::TPW; ++u) acc[u][0] = acc[u][1] = 0.0;
+  for (int u = 0; u < NACC; ++u) acc[u][0] = acc[u][1] = 0.0;
   for (int i = 0; i < ntiles; ++i) {
     cp_wait<K::NS - 2>();
     __syncthreads();
@@ -461,17 +467,19 @@ __global__ void __launch_bounds__(256, 1)
       }
       yk[ni][0] = y0;
       yk[ni][1] = y1;
-      const double a0 = RREG ? af[2 * ni] : sA[c], a1 = RREG ? af[2 * ni + 1] : sA[c + 1];
-      // r −= AW α̃; lazy: a = β = R⁻¹α̃, so the residual update takes AZ2 (the sY tile, still unchanged) · β
-      const double q0 = lazy ? sY[rr * S + c] : y0, q1 = lazy ? sY[rr * S + c + 1] : y1;
-      double tu = fma(w0, a0, w1 * a1);
-      double tq = fma(q0, a0, q1 * a1);
-      tu += __shfl_xor_sync(0xffffffffu, tu, 1);
-      tq += __shfl_xor_sync(0xffffffffu, tq, 1);
-      tu += __shfl_xor_sync(0xffffffffu, tu, 2);
-      tq += __shfl_xor_sync(0xffffffffu, tq, 2);
-      pu += tu;
-      pq += tq;
+      if (!skip) {  // (warp-uniform) the row products with α̃ / β of the x and r updates
+        const double a0 = RREG ? af[2 * ni] : sA[c], a1 = RREG ? af[2 * ni + 1] : sA[c + 1];
+        // r −= AW α̃; lazy: a = β = R⁻¹α̃, so the residual update takes AZ2 (the sY tile, still unchanged) · β
+        const double q0 = lazy ? sY[rr * S + c] : y0, q1 = lazy ? sY[rr * S + c + 1] : y1;
+        double tu = fma(w0, a0, w1 * a1);
+        double tq = fma(q0, a0, q1 * a1);
+        tu += __shfl_xor_sync(0xffffffffu, tu, 1);
+        tq += __shfl_xor_sync(0xffffffffu, tq, 1);
+        tu += __shfl_xor_sync(0xffffffffu, tu, 2);
+        tq += __shfl_xor_sync(0xffffffffu, tq, 2);
+        pu += tu;
+        pq += tq;
+      }
     }
     if (!skip && q4 == 0 && rr < rows) {
       const int64_t rg = row + rr;
@@ -492,6 +500,31 @@ __global__ void __launch_bounds__(256, 1)
       for (int ni = 0; ni < K::NT; ++ni) {
         sY[rr * S + ni * 8 + 2 * q4] = yk[ni][0];
         sY[rr * S + ni * 8 + 2 * q4 + 1] = yk[ni][1];
+      }
+      if constexpr (K::WOWN) {
+        __syncwarp();  // the warp's own rows only
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int kr = warp * 8 + ks * 4 + q4;
+          double fa[K::MT], fp[K::MT];
+#pragma unroll
+          for (int i2 = 0; i2 < K::MT; ++i2) {
+            fa[i2] = sY[kr * S + i2 * 8 + g];
+            fp[i2] = C1N == 2 ? sZ[K::OPREV + kr * S + i2 * 8 + g] : 0.0;
+          }
+          int u = 0;
+          if constexpr (C1N == 2) {
+#pragma unroll
+            for (int mi = 0; mi < K::MT; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < K::MT; ++ni, ++u) dmma(acc[u][0], acc[u][1], fp[mi], fa[ni]);
+          }
+#pragma unroll
+          for (int mi = 0; mi < K::MT; ++mi)
+#pragma unroll
+            for (int ni = mi; ni < K::MT; ++ni, ++u) dmma(acc[u][0], acc[u][1], fa[mi], fa[ni]);
+        }
+        continue;
       }
       __syncthreads();
       const int slice = warp % K::WS;
@@ -526,7 +559,36 @@ __global__ void __launch_bounds__(256, 1)
   if constexpr (C1N > 0) {
     double* out = part + (size_t)blockIdx.x * PS;
     __syncthreads();
-    if constexpr (K::WS == 1) {
+    if constexpr (K::WOWN) {  // per-warp partials (lower half of AWᵀAW mirrored), summed in warp order
+      double* red = sm;
+      double* dst = red + (size_t)warp * C1N * T * T;
+      int u = 0;
+      if constexpr (C1N == 2) {
+#pragma unroll
+        for (int mi = 0; mi < K::MT; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < K::MT; ++ni, ++u)
+            *reinterpret_cast<double2*>(dst + (mi * 8 + g) * T + ni * 8 + 2 * q4) = make_double2(acc[u][0], acc[u][1]);
+      }
+      double* d1 = dst + (C1N - 1) * T * T;
+#pragma unroll
+      for (int mi = 0; mi < K::MT; ++mi)
+#pragma unroll
+        for (int ni = mi; ni < K::MT; ++ni, ++u) {
+          *reinterpret_cast<double2*>(d1 + (mi * 8 + g) * T + ni * 8 + 2 * q4) = make_double2(acc[u][0], acc[u][1]);
+          if (mi < ni) {
+            d1[(ni * 8 + 2 * q4) * T + mi * 8 + g] = acc[u][0];
+            d1[(ni * 8 + 2 * q4 + 1) * T + mi * 8 + g] = acc[u][1];
+          }
+        }
+      __syncthreads();
+      for (int e = tid; e < C1N * T * T; e += 256) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sacc += red[(size_t)w * C1N * T * T + e];
+        out[e] = sacc;
+      }
+    } else if constexpr (K::WS == 1) {
 #pragma unroll
       for (int u = 0; u < K::TPW; ++u) {
         const int tile = warp * K::TPW + u;
@@ -1198,6 +1260,182 @@ __global__ void __launch_bounds__(SsCfg<T>::NTH, 1)
 }
 
 // ----------------------------------------------------------------------------
+// The SRE-CG fused CGS pass at T = 16 (k_sweep<16,2,2,·,AL> semantics: Z1 = Zin − Q_0C_0 − Q_1C_1 written
+// to Zout, per-CTA partial [L_0, Zin]ᵀ Z1 with Zin = A·Q_1 the last left block) restructured for B200:
+//  * tiles of 64 rows, warp w owns rows 8w..8w+7 of every tile: its update DMMAs (both column tiles from
+//    one A fragment), its Z1 rows (kept in its own rows of the Q_0 tile) and its partial-product k-steps
+//    use only its rows — one CTA barrier per tile (the ring), none between the update and the products;
+//  * rows stored unpadded (128 B) with the 16-byte chunks XOR-swizzled by f(r) = ((r&1)<<2)|(r&2): every
+//    cp.async chunk row is one aligned 128-byte line and every fragment / double2 access is conflict-free;
+//  * 3 stages of 4 tiles (96 KB) → 2 CTAs per SM.
+// The arithmetic (DMMA k order, Z1 = Zin − D) is that of k_sweep; the partial sums are accumulated per warp
+// over its rows and summed over the 8 warps in order (a fixed order: run-to-run reproducible).
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ int sw16(int r, int c) {
+  return r * 16 + (((c >> 1) ^ (((r & 1) << 2) | (r & 2))) << 1) + (c & 1);
+}
+
+constexpr int kU16NS = 3, kU16TR = 64, kU16TILE = kU16TR * 16, kU16STAGE = 4 * kU16TILE;
+constexpr int kU16SMEM = kU16NS * kU16STAGE + 2 * 16 * 20;  // doubles: ring + C (padded stride 20)
+
+__global__ void __launch_bounds__(256, 2)
+    k_upcoef16(int64_t n, const double* Zin, double* Zout, const SweepPtrs P, const double* __restrict__ Cm,
+               double* __restrict__ part, const Tail tl) {
+  constexpr int T = 16, TR = kU16TR, TILE = kU16TILE, STAGE = kU16STAGE, NS = kU16NS, SC = 20;
+  pdl_enter();
+  extern __shared__ __align__(128) double sm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q4 = lane & 3;
+  const int64_t lo = chunk_lo(n, blockIdx.x, gridDim.x), hi = chunk_lo(n, blockIdx.x + 1, gridDim.x);
+  const int ntiles = (int)((hi - lo + TR - 1) / TR);
+  double* sC = sm + NS * STAGE;
+  // C (2T×T); lazy blocks: C_j ← R_j⁻¹ C_j (as k_sweep), the ring as scratch before the first copies
+  for (int e = tid; e < 2 * T * T; e += 256) sC[(e / T) * SC + e % T] = Cm[e];
+  if (P.rq[0] != nullptr || P.rq[1] != nullptr) {
+    double* tR = sm;
+    double* tO = sm + T * T;
+#pragma unroll 1
+    for (int j = 0; j < 2; ++j) {
+      if (P.rq[j] == nullptr) continue;
+      __syncthreads();
+      for (int e = tid; e < T * T; e += 256) tR[e] = P.rq[j][e];
+      __syncthreads();
+      for (int e = tid; e < T * T; e += 256) {
+        const int i = e / T, c = e % T;
+        double v = 0.0;
+        for (int k = i; k < T; ++k) v = fma(tR[i * T + k], sC[(j * T + k) * SC + c], v);
+        tO[e] = v;
+      }
+      __syncthreads();
+      for (int e = tid; e < T * T; e += 256) sC[(j * T + e / T) * SC + e % T] = tO[e];
+    }
+  }
+  __syncthreads();
+  // B fragments of the update in registers: cf[j][ni][ks] = C_j[4ks + q4][8ni + g]
+  double cf[2][2][4];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) cf[j][ni][ks] = sC[(j * T + ks * 4 + q4) * SC + ni * 8 + g];
+  __syncthreads();  // the scratch rows of the ring are reused by the copies below
+
+  const double* src[4] = {Zin, P.q[0], P.q[1], P.l[0]};
+  auto issue = [&](int i) {
+    if (i < ntiles) {
+      const int64_t row = lo + (int64_t)i * TR;
+      const int rows = (int)((hi - row) < TR ? (hi - row) : TR);
+      double* st = sm + (i % NS) * STAGE;
+      for (int e = tid; e < TR * 8; e += 256) {
+        const int r = e >> 3, j = e & 7;
+        const bool ok = r < rows;
+        const int d = r * 16 + ((j ^ (((r & 1) << 2) | (r & 2))) << 1);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+          cp16(st + a * TILE + d, ok ? (const void*)(src[a] + (row + r) * T + 2 * j) : (const void*)src[a], ok ? 16 : 0);
+      }
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int i = 0; i < NS - 1; ++i) issue(i);
+
+  double acc[8][2];  // [L_0ᵀZ1 (mi, ni) | Zinᵀ Z1 (mi, ni)]
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0;
+  const int r = warp * 8 + g;  // this lane's update row
+  for (int i = 0; i < ntiles; ++i) {
+    cp_wait<NS - 2>();
+    __syncthreads();
+    issue(i + NS - 1);
+    double* st = sm + (i % NS) * STAGE;
+    const double* sZ = st;
+    double* sQ0 = st + TILE;
+    const double* sQ1 = st + 2 * TILE;
+    const double* sL = st + 3 * TILE;
+    const int64_t row = lo + (int64_t)i * TR;
+    const int rows = (int)((hi - row) < TR ? (hi - row) : TR);
+    // ---- update: D = Q_0 C_0 + Q_1 C_1 over the warp's 8 rows (both column tiles per A fragment)
+    double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double* sQ = j ? sQ1 : sQ0;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const double a = sQ[sw16(r, ks * 4 + q4)];
+        dmma(d[0][0], d[0][1], a, cf[j][0][ks]);
+        dmma(d[1][0], d[1][1], a, cf[j][1][ks]);
+      }
+    }
+    __syncwarp();  // the warp's Q_0 rows are read: they now take its Z1 rows
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int c = ni * 8 + 2 * q4;
+      const double2 z = *reinterpret_cast<const double2*>(sZ + sw16(r, c));
+      const double2 z1 = make_double2(z.x - d[ni][0], z.y - d[ni][1]);
+      *reinterpret_cast<double2*>(sQ0 + sw16(r, c)) = z1;
+      if (r < rows) *reinterpret_cast<double2*>(Zout + (row + r) * T + c) = z1;
+    }
+    __syncwarp();
+    // ---- partial [L_0, Zin]ᵀ Z1 over the warp's rows: k-steps of 4 rows
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kr = warp * 8 + ks * 4 + q4;
+      double fl[2], fz[2], fy[2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        fl[mi] = sL[sw16(kr, mi * 8 + g)];
+        fz[mi] = sZ[sw16(kr, mi * 8 + g)];
+        fy[mi] = sQ0[sw16(kr, mi * 8 + g)];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          dmma(acc[mi * 2 + ni][0], acc[mi * 2 + ni][1], fl[mi], fy[ni]);
+          dmma(acc[4 + mi * 2 + ni][0], acc[4 + mi * 2 + ni][1], fz[mi], fy[ni]);
+        }
+    }
+  }
+  cp_wait<0>();
+  // ---- per-CTA partial: the warps' sums in warp order
+  constexpr int PER = 2 * T * T;
+  __syncthreads();
+  double* red = sm;
+  {
+    double* dst = red + (size_t)warp * PER;
+#pragma unroll
+    for (int l = 0; l < 2; ++l)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          const int u = l * 4 + mi * 2 + ni;
+          *reinterpret_cast<double2*>(dst + l * T * T + (mi * 8 + g) * T + ni * 8 + 2 * q4) =
+              make_double2(acc[u][0], acc[u][1]);
+        }
+  }
+  __syncthreads();
+  double* out = part + (size_t)blockIdx.x * PER;
+  for (int e = tid; e < PER; e += 256) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += red[(size_t)w * PER + e];
+    out[e] = v;
+  }
+  if (tl.cnt != nullptr) tail_reduce(part, PER, tl);
+}
+
+static bool upcoef16_env() {
+  static const bool on = [] {  // EKS_UPCOEF16=0: the generic k_sweep<16,2,2,·,AL> (A/B measurements)
+    const char* e = getenv("EKS_UPCOEF16");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+// ----------------------------------------------------------------------------
 // host side
 // ----------------------------------------------------------------------------
 static thread_local int t_last_grid = 0;
@@ -1292,6 +1530,18 @@ cudaError_t launch_sweep(cudaStream_t st, int t, int nq, int nl, bool v, int64_t
     if (v) return cudaErrorInvalidValue;
     if (nq == 1 && nl == 1) return launch_sweep_t<T, 1, 1, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
     if (nq == 2 && nl == 2) {
+      if (T == 16 && P.l[1] == Zin && upcoef16_env()) {
+        const size_t sm = (size_t)kU16SMEM * 8;
+        static int occ = 0;
+        if (!occ) {
+          cudaFuncSetAttribute(k_upcoef16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_upcoef16, 256, sm);
+          if (occ < 1) occ = 1;
+        }
+        nblk = grid_for(nblk, occ);
+        t_last_grid = nblk;
+        return launch_k(k_upcoef16, nblk, 256, sm, st, n, Zin, Zout, P, C, part, tl);
+      }
       if (P.l[1] == Zin) return launch_sweep_t<T, 2, 2, false, true>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
       return launch_sweep_t<T, 2, 2, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
     }

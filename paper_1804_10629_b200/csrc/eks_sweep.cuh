@@ -83,6 +83,11 @@ bool spmm_grid_fits(int t, const GridPlan& gp);
 // (t ∈ {32, 64}; per-CTA partials of layout sweep_part_stride(t,1,v), tail-reduced into tl.out).
 cudaError_t launch_gram_upper(cudaStream_t st, int t, int64_t n, const double* X, const double* Y, const double* v,
                               double* part, int nblk, const Tail& tl);
+// Setup: stencil values per row (layout of GridPlan::sv) scattered from the uploaded CSR (int32 row
+// pointers, extended-layout columns); *bad (zeroed by the caller) is set when an entry is not a stencil slot.
+cudaError_t launch_grid_sv(cudaStream_t st, int64_t n, const int* rp, const int* col, const double* val,
+                           int64_t row_begin, int64_t halo_before, int64_t nx, int64_t ny, int64_t b, int64_t c, int w,
+                           double* sv, int* bad, int sms);
 bool spmm_grid_fused_chol(int t);  // ch.on allowed: the last CTA runs the solve-path Cholesky
 // gram = false: Y = A·X only (no Y scratch, no DMMA, no partials; part and tl unused) — the plain
 // SpMM of the CA monomial powers, the store-Q-only CGS2 products and the residual.
