@@ -269,74 +269,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
             const int gi = lane / GP, gl = lane % GP;
             const int ppx = bx / PX;                 // patches per block line (a power of 2)
             const int nsteps = K::R / (PR * NG * NWC);  // patch steps per warp and plane
-            if constexpr (PV == 3 && T == 16) {
-              // FRAG layout (t = 16): lane (fg = lane>>2, fq = lane&3) holds columns fg and fg+8 of lane
-              // group fq's row — exactly its A / B fragments of a Gram k-step over the 4 groups' rows
-              // (row fq of the k-step), so the Gram needs no Y scratch and no fragment loads.  The 4 groups'
-              // rows are 128 B apart (the same banks), so odd groups load the two 64-byte halves in
-              // swapped order (2 wavefronts per 256-byte load instead of 4); Y accumulates in that order
-              // (the same slot order per element: bitwise the CSR order) and is un-swapped for the Gram.
-              const int fg = lane >> 2, fq = lane & 3;
-              const bool odd = (fq & 1) != 0;
-              const int ca = odd ? fg + 8 : fg, cb = odd ? fg : fg + 8;
-              const int LS = PWP * T;  // doubles per y-line
-              for (int ps = 0; ps < nsteps; ++ps) {
-                const int pp = (ps * NWC + warp) * NG + fq;
-                const int px0 = pp & (ppx - 1), py0 = (pp >> bxs) * PY;
-                const double* c0p = P0 + ((size_t)(py0 + hy) * PWP + px0 + 1) * T;
-                double cma = c0p[ca - LS], cmb = c0p[cb - LS];
-                double c0a = c0p[ca], c0b = c0p[cb];
-#pragma unroll
-                for (int dy = 0; dy < PY; ++dy) {
-                  const double* cp = c0p + dy * LS;
-                  const double cna = cp[LS + ca], cnb = cp[LS + cb];
-                  const double xma = cp[ca - T], xmb = cp[cb - T];
-                  const double xpa = cp[T + ca], xpb = cp[T + cb];
-                  const size_t zo = (size_t)(cp - P0);
-                  const double zma = Pm[zo + ca], zmb = Pm[zo + cb];
-                  const double zpa = Pp[zo + ca], zpb = Pp[zo + cb];
-                  const int ir = (py0 + dy) * bx + px0;
-                  const bool ok = x0 + px0 < nx && y0 + py0 + dy < ny;
-                  const int64_t grow = qrow + (int64_t)(py0 + dy) * nx + px0;
-                  const double na[7] = {zma, cma, xma, c0a, xpa, cna, zpa};
-                  const double nb2[7] = {zmb, cmb, xmb, c0b, xpb, cnb, zpb};
-                  double ya = 0.0, yb = 0.0;
-#pragma unroll
-                  for (int k = 0; k < VS; k += 2) {
-                    const double2 av = ok ? *reinterpret_cast<const double2*>(Vs + ir * VS + k) : make_double2(0, 0);
-                    ya = __fma_rn(av.x, na[k], ya);
-                    yb = __fma_rn(av.x, nb2[k], yb);
-                    if (k + 1 < 7) {
-                      ya = __fma_rn(av.y, na[k + 1], ya);
-                      yb = __fma_rn(av.y, nb2[k + 1], yb);
-                    }
-                  }
-                  if (!ok) {
-                    ya = 0.0;
-                    yb = 0.0;
-                  } else {
-                    Y[grow * T + ca] = ya;
-                    Y[grow * T + cb] = yb;
-                  }
-                  if (gram) {  // k-step over the 4 groups' rows: tiles (0,0), (0,1), (1,1) and the r tiles
-                    const double xf0 = ok ? (odd ? c0b : c0a) : 0.0, xf1 = ok ? (odd ? c0a : c0b) : 0.0;
-                    const double yf0 = odd ? yb : ya, yf1 = odd ? ya : yb;
-                    dmma(acc[0][0], acc[0][1], xf0, yf0);
-                    dmma(acc[1][0], acc[1][1], xf0, yf1);
-                    dmma(acc[2][0], acc[2][1], xf1, yf1);
-                    if (r != nullptr) {
-                      const double br = (fg == 0 && ok) ? (rbulk ? Rs[ir] : __ldg(r + grow)) : 0.0;
-                      dmma(accr[0][0], accr[0][1], xf0, br);
-                      dmma(accr[1][0], accr[1][1], xf1, br);
-                    }
-                  }
-                  cma = c0a;
-                  cmb = c0b;
-                  c0a = cna;
-                  c0b = cnb;
-                }
-              }
-            } else {
+            {
             for (int ps = 0; ps < nsteps; ++ps) {
               const int pp = (ps * NWC + warp) * NG + gi;  // patch of this lane group
               const int px0 = (pp & (ppx - 1)) * PX, py0 = (pp >> (bxs - LPX)) * PY;
@@ -446,7 +379,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
               }  // !CG
               __syncwarp();
             }
-            }  // PV
+            }
           } else {
 #pragma unroll
           for (int uu = 0; uu < K::UPW; ++uu) {
@@ -721,11 +654,6 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
     if (patch && swz) {
       cudaFuncSetAttribute(k_spmm_grid<T, W, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       return launch_k(k_spmm_grid<T, W, true, 1>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch,
-                      ns, gram, tm);
-    }
-    if (patch && pv_env == 3 && T == 16) {
-      cudaFuncSetAttribute(k_spmm_grid<T, W, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      return launch_k(k_spmm_grid<T, W, true, 3>, nblk, K::NTH, sm, st, gp, bx, by, zc, X, Y, r, part, tl, ch,
                       ns, gram, tm);
     }
     if (patch && pv_env == 2 && T == 16) {

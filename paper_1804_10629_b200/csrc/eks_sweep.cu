@@ -354,7 +354,7 @@ struct ApCfg {
   // WOWN (T ≤ 16): every warp accumulates ALL C1 tiles over its own 8 rows (k-steps of 4 rows) from
   // fragments loaded once per k-step (AW column tiles serve as both operands of the AWᵀAW tiles) — no
   // CTA barrier between the R⁻¹ product and C1, ≈2.5× fewer shared loads; per-warp partials summed at the end
-  static constexpr bool WOWN = T <= 16 && C1N > 0;
+  static constexpr bool WOWN = T <= 32 && C1N > 0;
   static constexpr int NAW = WOWN ? (C1N == 2 ? MT * MT : 0) + MT * (MT + 1) / 2 : 0;
   static constexpr int RED = WOWN ? 8 * C1N * T * T : (WS > 1 ? 8 * C1N * T * T : 0);
   static constexpr int SMEM0 = NS * STAGE + T * (T + 4) + T;
@@ -1271,17 +1271,24 @@ __global__ void __launch_bounds__(SsCfg<T>::NTH, 1)
 // The arithmetic (DMMA k order, Z1 = Zin − D) is that of k_sweep; the partial sums are accumulated per warp
 // over its rows and summed over the 8 warps in order (a fixed order: run-to-run reproducible).
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ int sw16(int r, int c) {
-  return r * 16 + (((c >> 1) ^ (((r & 1) << 2) | (r & 2))) << 1) + (c & 1);
+template <int T>
+__device__ __forceinline__ int swz(int r, int c) {  // element (r, c) of an unpadded swizzled T-column tile
+  return r * T + (((c >> 1) ^ (((r & 1) << 2) | (r & 2))) << 1) + (c & 1);
 }
 
-constexpr int kU16NS = 3, kU16TR = 64, kU16TILE = kU16TR * 16, kU16STAGE = 4 * kU16TILE;
-constexpr int kU16SMEM = kU16NS * kU16STAGE + 2 * 16 * 20;  // doubles: ring + C (padded stride 20)
+template <int T>
+struct UcCfg {
+  static constexpr int NS = 3, TR = 64, TILE = TR * T, STAGE = 4 * TILE, SC = T + 4;
+  static constexpr int SMEM = NS * STAGE + 2 * T * SC;  // doubles: ring + C (padded)
+  static constexpr int NT = T / 8, KS = T / 4;          // column tiles, k-steps per window block
+};
 
-__global__ void __launch_bounds__(256, 2)
-    k_upcoef16(int64_t n, const double* Zin, double* Zout, const SweepPtrs P, const double* __restrict__ Cm,
+template <int T>
+__global__ void __launch_bounds__(256, (T == 16 ? 2 : 1))
+    k_upcoef_w(int64_t n, const double* Zin, double* Zout, const SweepPtrs P, const double* __restrict__ Cm,
                double* __restrict__ part, const Tail tl) {
-  constexpr int T = 16, TR = kU16TR, TILE = kU16TILE, STAGE = kU16STAGE, NS = kU16NS, SC = 20;
+  using K = UcCfg<T>;
+  constexpr int TR = K::TR, TILE = K::TILE, STAGE = K::STAGE, NS = K::NS, SC = K::SC, NT = K::NT, KS = K::KS;
   pdl_enter();
   extern __shared__ __align__(128) double sm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1311,14 +1318,18 @@ __global__ void __launch_bounds__(256, 2)
     }
   }
   __syncthreads();
-  // B fragments of the update in registers: cf[j][ni][ks] = C_j[4ks + q4][8ni + g]
-  double cf[2][2][4];
+  // B fragments of the update in registers for t = 16 (cf[j][ni][ks] = C_j[4ks + q4][8ni + g]); t = 32 reads
+  // them from the padded sC (64 more registers would spill next to the 32 partial tiles)
+  constexpr bool CREG = T <= 16;
+  double cf[2][CREG ? NT : 1][CREG ? KS : 1];
+  if constexpr (CREG) {
 #pragma unroll
-  for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < 2; ++j)
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
+      for (int ni = 0; ni < NT; ++ni)
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) cf[j][ni][ks] = sC[(j * T + ks * 4 + q4) * SC + ni * 8 + g];
+        for (int ks = 0; ks < KS; ++ks) cf[j][ni][ks] = sC[(j * T + ks * 4 + q4) * SC + ni * 8 + g];
+  }
   __syncthreads();  // the scratch rows of the ring are reused by the copies below
 
   const double* src[4] = {Zin, P.q[0], P.q[1], P.l[0]};
@@ -1327,10 +1338,11 @@ __global__ void __launch_bounds__(256, 2)
       const int64_t row = lo + (int64_t)i * TR;
       const int rows = (int)((hi - row) < TR ? (hi - row) : TR);
       double* st = sm + (i % NS) * STAGE;
-      for (int e = tid; e < TR * 8; e += 256) {
-        const int r = e >> 3, j = e & 7;
+      constexpr int CPR = T / 2;  // 16-byte chunks per row
+      for (int e = tid; e < TR * CPR; e += 256) {
+        const int r = e / CPR, j = e % CPR;
         const bool ok = r < rows;
-        const int d = r * 16 + ((j ^ (((r & 1) << 2) | (r & 2))) << 1);
+        const int d = r * T + ((j ^ (((r & 1) << 2) | (r & 2))) << 1);
 #pragma unroll
         for (int a = 0; a < 4; ++a)
           cp16(st + a * TILE + d, ok ? (const void*)(src[a] + (row + r) * T + 2 * j) : (const void*)src[a], ok ? 16 : 0);
@@ -1341,9 +1353,13 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
   for (int i = 0; i < NS - 1; ++i) issue(i);
 
-  double acc[8][2];  // [L_0ᵀZ1 (mi, ni) | Zinᵀ Z1 (mi, ni)]
+  double acc[2][NT][NT][2];  // [L_0ᵀZ1 | Zinᵀ Z1] tiles (mi, ni)
 #pragma unroll
-  for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0;
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int mi = 0; mi < NT; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) acc[l][mi][ni][0] = acc[l][mi][ni][1] = 0.0;
   const int r = warp * 8 + g;  // this lane's update row
   for (int i = 0; i < ntiles; ++i) {
     cp_wait<NS - 2>();
@@ -1356,25 +1372,28 @@ __global__ void __launch_bounds__(256, 2)
     const double* sL = st + 3 * TILE;
     const int64_t row = lo + (int64_t)i * TR;
     const int rows = (int)((hi - row) < TR ? (hi - row) : TR);
-    // ---- update: D = Q_0 C_0 + Q_1 C_1 over the warp's 8 rows (both column tiles per A fragment)
-    double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    // ---- update: D = Q_0 C_0 + Q_1 C_1 over the warp's 8 rows (every column tile per A fragment)
+    double d[NT][2];
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) d[ni][0] = d[ni][1] = 0.0;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const double* sQ = j ? sQ1 : sQ0;
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const double a = sQ[sw16(r, ks * 4 + q4)];
-        dmma(d[0][0], d[0][1], a, cf[j][0][ks]);
-        dmma(d[1][0], d[1][1], a, cf[j][1][ks]);
+      for (int ks = 0; ks < KS; ++ks) {
+        const double a = sQ[swz<T>(r, ks * 4 + q4)];
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni)
+          dmma(d[ni][0], d[ni][1], a, CREG ? cf[j][CREG ? ni : 0][CREG ? ks : 0] : sC[(j * T + ks * 4 + q4) * SC + ni * 8 + g]);
       }
     }
     __syncwarp();  // the warp's Q_0 rows are read: they now take its Z1 rows
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni) {
+    for (int ni = 0; ni < NT; ++ni) {
       const int c = ni * 8 + 2 * q4;
-      const double2 z = *reinterpret_cast<const double2*>(sZ + sw16(r, c));
+      const double2 z = *reinterpret_cast<const double2*>(sZ + swz<T>(r, c));
       const double2 z1 = make_double2(z.x - d[ni][0], z.y - d[ni][1]);
-      *reinterpret_cast<double2*>(sQ0 + sw16(r, c)) = z1;
+      *reinterpret_cast<double2*>(sQ0 + swz<T>(r, c)) = z1;
       if (r < rows) *reinterpret_cast<double2*>(Zout + (row + r) * T + c) = z1;
     }
     __syncwarp();
@@ -1382,19 +1401,19 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       const int kr = warp * 8 + ks * 4 + q4;
-      double fl[2], fz[2], fy[2];
+      double fl[NT], fz[NT], fy[NT];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        fl[mi] = sL[sw16(kr, mi * 8 + g)];
-        fz[mi] = sZ[sw16(kr, mi * 8 + g)];
-        fy[mi] = sQ0[sw16(kr, mi * 8 + g)];
+      for (int mi = 0; mi < NT; ++mi) {
+        fl[mi] = sL[swz<T>(kr, mi * 8 + g)];
+        fz[mi] = sZ[swz<T>(kr, mi * 8 + g)];
+        fy[mi] = sQ0[swz<T>(kr, mi * 8 + g)];
       }
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int mi = 0; mi < NT; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-          dmma(acc[mi * 2 + ni][0], acc[mi * 2 + ni][1], fl[mi], fy[ni]);
-          dmma(acc[4 + mi * 2 + ni][0], acc[4 + mi * 2 + ni][1], fz[mi], fy[ni]);
+        for (int ni = 0; ni < NT; ++ni) {
+          dmma(acc[0][mi][ni][0], acc[0][mi][ni][1], fl[mi], fy[ni]);
+          dmma(acc[1][mi][ni][0], acc[1][mi][ni][1], fz[mi], fy[ni]);
         }
     }
   }
@@ -1408,13 +1427,11 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
     for (int l = 0; l < 2; ++l)
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int mi = 0; mi < NT; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-          const int u = l * 4 + mi * 2 + ni;
+        for (int ni = 0; ni < NT; ++ni)
           *reinterpret_cast<double2*>(dst + l * T * T + (mi * 8 + g) * T + ni * 8 + 2 * q4) =
-              make_double2(acc[u][0], acc[u][1]);
-        }
+              make_double2(acc[l][mi][ni][0], acc[l][mi][ni][1]);
   }
   __syncthreads();
   double* out = part + (size_t)blockIdx.x * PER;
@@ -1428,7 +1445,7 @@ __global__ void __launch_bounds__(256, 2)
 }
 
 static bool upcoef16_env() {
-  static const bool on = [] {  // EKS_UPCOEF16=0: the generic k_sweep<16,2,2,·,AL> (A/B measurements)
+  static const bool on = [] {  // EKS_UPCOEF16=0: the generic k_sweep<T,2,2,·,AL> at t = 16/32 (A/B measurements)
     const char* e = getenv("EKS_UPCOEF16");
     return !(e && atoi(e) == 0);
   }();
@@ -1452,6 +1469,21 @@ static int grid_for(int nblk_max, int occ) {
   const int g = sms * occ;
   return g < nblk_max ? g : nblk_max;
 }
+template <int T>
+static cudaError_t launch_upcoef_w(cudaStream_t st, int64_t n, const double* Zin, double* Zout, const SweepPtrs& P,
+                                   const double* C, double* part, int nblk, const Tail& tl) {
+  const size_t sm = (size_t)UcCfg<T>::SMEM * 8;
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(k_upcoef_w<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_upcoef_w<T>, 256, sm);
+    if (occ < 1) occ = 1;
+  }
+  nblk = grid_for(nblk, occ);
+  t_last_grid = nblk;
+  return launch_k(k_upcoef_w<T>, nblk, 256, sm, st, n, Zin, Zout, P, C, part, tl);
+}
+
 template <int T, int NQ, int NL, bool V, bool AL = false, bool UP = false>
 static cudaError_t launch_sweep_t(cudaStream_t st, int64_t n, const double* Zin, double* Zout, const SweepPtrs& P,
                                   const double* C, const double* v, double* part, int nblk, const Tail& tl) {
@@ -1530,18 +1562,8 @@ cudaError_t launch_sweep(cudaStream_t st, int t, int nq, int nl, bool v, int64_t
     if (v) return cudaErrorInvalidValue;
     if (nq == 1 && nl == 1) return launch_sweep_t<T, 1, 1, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
     if (nq == 2 && nl == 2) {
-      if (T == 16 && P.l[1] == Zin && upcoef16_env()) {
-        const size_t sm = (size_t)kU16SMEM * 8;
-        static int occ = 0;
-        if (!occ) {
-          cudaFuncSetAttribute(k_upcoef16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_upcoef16, 256, sm);
-          if (occ < 1) occ = 1;
-        }
-        nblk = grid_for(nblk, occ);
-        t_last_grid = nblk;
-        return launch_k(k_upcoef16, nblk, 256, sm, st, n, Zin, Zout, P, C, part, tl);
-      }
+      if constexpr (T == 16 || T == 32)
+        if (P.l[1] == Zin && upcoef16_env()) return launch_upcoef_w<T>(st, n, Zin, Zout, P, C, part, nblk, tl);
       if (P.l[1] == Zin) return launch_sweep_t<T, 2, 2, false, true>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
       return launch_sweep_t<T, 2, 2, false>(st, n, Zin, Zout, P, C, vec, part, nblk, tl);
     }
