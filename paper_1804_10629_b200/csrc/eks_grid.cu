@@ -118,7 +118,12 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
   const size_t XB = grid_xbytes<T>(bx, by, hy, SWZ);  // X plane-block bytes of a stage
   double* sYw = reinterpret_cast<double*>(smraw + (size_t)NS * SB);  // [2 (CG)][NWC][YR][S]
   constexpr int YR = K::yr(PATCH);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sYw + (K::CG ? 2 : 1) * NWC * YR * S);
+  // XSCR (t = 16 patch consumer): the Gram's X fragments from a padded per-warp copy of the centre rows
+  // (written with the Y rows) instead of the plane-block, whose 4 rows of a k-step are whole 128-byte
+  // lines apart — the same banks: ncu showed 8 wavefronts per fragment load instead of 2
+  // (t = 8: rows 64 B apart, 2-way only, and the scratch would cost the ring its fifth stage)
+  constexpr bool XSCR = !K::CG && T >= 16 && (PATCH ? (T == 16 && PV == 0) : true);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sYw + ((K::CG ? 2 : 1) + (XSCR ? 1 : 0)) * NWC * YR * S);
   uint64_t* empty = full + 8;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q4 = lane & 3;
@@ -241,6 +246,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
     const int rw = lane / G, gl = lane % G;
     const int bxs = 31 - __clz(bx);  // bx is a power of two
     double* yw0 = sYw + (size_t)warp * YR * S;
+    double* xw0 = sYw + (size_t)(NWC + warp) * YR * S;  // XSCR only
     int cur = 0;        // stage of the current load step
     uint32_t ph = 0;    // its full-barrier phase parity
     for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -340,7 +346,11 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
                     }
                   }
                 } else {
-                  if (gram) *reinterpret_cast<double2*>(yw + (gi * PR + dy) * S + 2 * gl) = y;
+                  if (gram) {
+                    *reinterpret_cast<double2*>(yw + (gi * PR + dy) * S + 2 * gl) = y;
+                    if constexpr (XSCR)
+                      *reinterpret_cast<double2*>(xw0 + (gi * PR + dy) * S + 2 * gl) = ok ? c0 : make_double2(0.0, 0.0);
+                  }
                 }
                 cm = c0;
                 c0 = cn;
@@ -360,7 +370,8 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
                 double xa[MT], ybv[MT];
 #pragma unroll
                 for (int i = 0; i < MT; ++i) {  // column 8i + g: chunk (4i + g/2) ^ (Pq & 7), half g & 1
-                  xa[i] = okq ? xo[SWZ ? 2 * ((4 * i + (g >> 1)) ^ (Pq & 7)) + (g & 1) : i * 8 + g] : 0.0;
+                  xa[i] = XSCR ? xw0[rq * S + i * 8 + g]
+                               : (okq ? xo[SWZ ? 2 * ((4 * i + (g >> 1)) ^ (Pq & 7)) + (g & 1) : i * 8 + g] : 0.0);
                   ybv[i] = yw[rq * S + i * 8 + g];
                 }
                 int ut = 0;
@@ -428,7 +439,11 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
               }
               if (!ok) y = make_double2(0.0, 0.0);
               else reinterpret_cast<double2*>(Y)[grow * H + gl + G * c2] = y;
-              if (gram) *reinterpret_cast<double2*>(yw + rw * S + 2 * (gl + G * c2)) = y;
+              if (gram) {
+                *reinterpret_cast<double2*>(yw + rw * S + 2 * (gl + G * c2)) = y;
+                if constexpr (XSCR)
+                  *reinterpret_cast<double2*>(xw0 + rw * S + 2 * (gl + G * c2)) = ok ? xv[W / 2] : make_double2(0.0, 0.0);
+              }
             }
             if (!gram) continue;
             __syncwarp();
@@ -442,7 +457,7 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
               double xa[MT], yb[MT];
 #pragma unroll
               for (int i = 0; i < MT; ++i) {
-                xa[i] = okq ? xo[i * 8 + g] : 0.0;
+                xa[i] = XSCR ? xw0[rq * S + i * 8 + g] : (okq ? xo[i * 8 + g] : 0.0);
                 yb[i] = yw[rq * S + i * 8 + g];
               }
               if constexpr (!K::CG) {
@@ -643,7 +658,9 @@ static cudaError_t grid_t(cudaStream_t st, const GridPlan& gp, const double* X, 
   }
   const bool swz = patch && T == 16 && swz_env;
   const size_t SB = grid_stage_bytes<T>(bx, by, hy, vs, swz);
-  const size_t fixed = (size_t)(K::CG ? 2 : 1) * K::NWC * K::yr(patch) * K::S * 8 + 16 * 8 + 128 + (swz ? 1024 : 0);
+  const bool xscr = !K::CG && T >= 16 && (patch ? (T == 16 && !swz && pv_env != 2) : true);  // the kernel's XSCR
+  const size_t fixed = (size_t)((K::CG ? 2 : 1) + (xscr ? 1 : 0)) * K::NWC * K::yr(patch) * K::S * 8 + 16 * 8 + 128 +
+                       (swz ? 1024 : 0);
   int ns = (int)((220 * 1024 - fixed) / SB);
   if (ns > 8) ns = 8;
   if (ns < 4) return cudaErrorInvalidConfiguration;
