@@ -1444,6 +1444,128 @@ __global__ void __launch_bounds__(256, (T == 16 ? 2 : 1))
   if (tl.cnt != nullptr) tail_reduce(part, PER, tl);
 }
 
+// ----------------------------------------------------------------------------
+// The A-CholQR Gram [XᵀY (upper 8×8 tiles, lower mirrored) | Xᵀv] of the t = 64 split SpMM step (R35) with
+// warp-owned rows: warp w owns rows 8w..8w+7 of every 64-row tile and accumulates ALL 36 upper tiles and the
+// 8 v tiles over them (k-steps of 4 rows; each X / Y column-tile fragment loaded once feeds up to 8 DMMAs:
+// 16 shared loads per 44 DMMAs instead of 2 per DMMA); swizzled unpadded rows (aligned cp.async lines,
+// conflict-free fragments); 3 stages of 2 tiles = 192 KB → 1 CTA per SM.  The warps' sums are added in warp
+// order (fixed: run-to-run reproducible).
+// ----------------------------------------------------------------------------
+template <int T>
+struct GwCfg {
+  static constexpr int NS = 3, TR = 64, TILE = TR * T, STAGE = 2 * TILE + TR;
+  static constexpr int MT = T / 8, NUT = MT * (MT + 1) / 2;
+  static constexpr int SMEM = NS * STAGE > T * T + T ? NS * STAGE : T * T + T;
+};
+
+template <int T, bool V>
+__global__ void __launch_bounds__(256, 1)
+    k_gram_w(int64_t n, const double* __restrict__ X, const double* __restrict__ Y, const double* __restrict__ v,
+             double* __restrict__ part, const Tail tl) {
+  using K = GwCfg<T>;
+  constexpr int TR = K::TR, TILE = K::TILE, STAGE = K::STAGE, NS = K::NS, MT = K::MT, NUT = K::NUT;
+  pdl_enter();
+  extern __shared__ __align__(128) double sm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q4 = lane & 3;
+  const int64_t lo = chunk_lo(n, blockIdx.x, gridDim.x), hi = chunk_lo(n, blockIdx.x + 1, gridDim.x);
+  const int ntiles = (int)((hi - lo + TR - 1) / TR);
+  auto issue = [&](int i) {
+    if (i < ntiles) {
+      const int64_t row = lo + (int64_t)i * TR;
+      const int rows = (int)((hi - row) < TR ? (hi - row) : TR);
+      double* st = sm + (i % NS) * STAGE;
+      constexpr int CPR = T / 2;
+      for (int e = tid; e < TR * CPR; e += 256) {
+        const int r = e / CPR, j = e % CPR;
+        const bool ok = r < rows;
+        const int d = r * T + ((j ^ (((r & 1) << 2) | (r & 2))) << 1);
+        cp16(st + d, ok ? (const void*)(X + (row + r) * T + 2 * j) : (const void*)X, ok ? 16 : 0);
+        cp16(st + TILE + d, ok ? (const void*)(Y + (row + r) * T + 2 * j) : (const void*)Y, ok ? 16 : 0);
+      }
+      if constexpr (V) vec_async<TR>(st + 2 * TILE, v, row, rows);
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int i = 0; i < NS - 1; ++i) issue(i);
+  double acc[NUT][2], accv[MT][2];
+#pragma unroll
+  for (int u = 0; u < NUT; ++u) acc[u][0] = acc[u][1] = 0.0;
+#pragma unroll
+  for (int u = 0; u < MT; ++u) accv[u][0] = accv[u][1] = 0.0;
+  for (int i = 0; i < ntiles; ++i) {
+    cp_wait<NS - 2>();
+    __syncthreads();
+    issue(i + NS - 1);
+    const double* st = sm + (i % NS) * STAGE;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kr = warp * 8 + ks * 4 + q4;
+      double fx[MT], fy[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        fx[m] = st[swz<T>(kr, m * 8 + g)];
+        fy[m] = st[TILE + swz<T>(kr, m * 8 + g)];
+      }
+      int u = 0;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = mi; ni < MT; ++ni, ++u) dmma(acc[u][0], acc[u][1], fx[mi], fy[ni]);
+      if constexpr (V) {
+        const double bv = g == 0 ? st[2 * TILE + kr] : 0.0;  // v as column 0 of a tile
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) dmma(accv[mi][0], accv[mi][1], fx[mi], bv);
+      }
+    }
+  }
+  cp_wait<0>();
+  // ---- per-CTA partial: the warps' tiles added into shared memory in warp order, lower half mirrored
+  constexpr int PER = T * T + (V ? T : 0);
+  double* red = sm;
+  __syncthreads();
+  for (int w = 0; w < 8; ++w) {
+    if (warp == w) {
+      int u = 0;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = mi; ni < MT; ++ni, ++u) {
+          double* d = red + (mi * 8 + g) * T + ni * 8 + 2 * q4;
+          d[0] = w == 0 ? acc[u][0] : d[0] + acc[u][0];
+          d[1] = w == 0 ? acc[u][1] : d[1] + acc[u][1];
+        }
+      if constexpr (V) {
+        if (q4 == 0)
+#pragma unroll
+          for (int mi = 0; mi < MT; ++mi) {
+            double* d = red + T * T + mi * 8 + g;
+            *d = w == 0 ? accv[mi][0] : *d + accv[mi][0];
+          }
+      }
+    }
+    __syncthreads();
+  }
+  double* out = part + (size_t)blockIdx.x * PER;
+  for (int e = tid; e < T * T; e += 256) {
+    const int rI = e / T, cI = e % T;
+    out[e] = (rI / 8 <= cI / 8) ? red[e] : red[cI * T + rI];
+  }
+  if constexpr (V)
+    for (int e = tid; e < T; e += 256) out[T * T + e] = red[T * T + e];
+  if (tl.cnt != nullptr) tail_reduce(part, PER, tl);
+}
+
+static bool gramw_env() {
+  static const bool on = [] {  // EKS_GRAMW=0: the generic k_sweep<64,0,1,·,·,UP> Gram (A/B measurements)
+    const char* e = getenv("EKS_GRAMW");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 static bool upcoef16_env() {
   static const bool on = [] {  // EKS_UPCOEF16=0: the generic k_sweep<T,2,2,·,AL> at t = 16/32 (A/B measurements)
     const char* e = getenv("EKS_UPCOEF16");
@@ -1509,7 +1631,22 @@ cudaError_t launch_gram_upper(cudaStream_t st, int t, int64_t n, const double* X
   switch (t) {
     case 32: return v ? launch_sweep_t<32, 0, 1, true, false, true>(st, n, Y, nullptr, P, nullptr, v, part, nblk, tl)
                       : launch_sweep_t<32, 0, 1, false, false, true>(st, n, Y, nullptr, P, nullptr, v, part, nblk, tl);
-    case 64: return v ? launch_sweep_t<64, 0, 1, true, false, true>(st, n, Y, nullptr, P, nullptr, v, part, nblk, tl)
+    case 64:
+      if (gramw_env()) {
+        const size_t sm = (size_t)GwCfg<64>::SMEM * 8;
+        auto kern = v ? k_gram_w<64, true> : k_gram_w<64, false>;
+        static int occ = 0;
+        if (!occ) {
+          cudaFuncSetAttribute(k_gram_w<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          cudaFuncSetAttribute(k_gram_w<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gram_w<64, true>, 256, sm);
+          if (occ < 1) occ = 1;
+        }
+        nblk = grid_for(nblk, occ);
+        t_last_grid = nblk;
+        return launch_k(kern, nblk, 256, sm, st, n, X, Y, v, part, tl);
+      }
+      return v ? launch_sweep_t<64, 0, 1, true, false, true>(st, n, Y, nullptr, P, nullptr, v, part, nblk, tl)
                       : launch_sweep_t<64, 0, 1, false, false, true>(st, n, Y, nullptr, P, nullptr, v, part, nblk, tl);
     default: return cudaErrorInvalidValue;
   }
