@@ -25,6 +25,10 @@ def kclass(name):
         if nq > 0 and nl > 0:
             return "upcoef"
         return "update" if nq > 0 else "coef"
+    if name.startswith("k_upcoef"):
+        return "upcoef"
+    if name.startswith("k_gram_w"):
+        return "coef"
     if name.startswith("k_apply"):
         return "apply"
     if name.startswith("k_chol"):
