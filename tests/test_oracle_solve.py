@@ -246,3 +246,69 @@ def test_cfg1_oracle_full_solve(oracle_lib):
     # s=1 vs s=2 on a Poisson matrix: ceil relation
     r1 = oracle_lib.solve(p.A, p.b, p.method, 1, p.t, p.tol)
     assert r["outer_iters"] == math.ceil(r1["outer_iters"] / 2)
+
+
+def _dense(A):
+    D = np.zeros((A.n, A.n))
+    for i in range(A.n):
+        D[i, A.col[A.row_ptr[i]:A.row_ptr[i + 1]]] = A.val[A.row_ptr[i]:A.row_ptr[i + 1]]
+    return D
+
+
+@pytest.mark.parametrize("t", [4, 8])
+def test_basis_sweep_pinned_by_krylov_structure(oracle_lib, t):
+    """or_basis_sweep (cfg5, reading R27) against what Alg 4 fixes, independently of the oracle's solve:
+    block 1 is the A-CholQR of X0 (numpy Cholesky of X0ᵀAX0, P:380 R4); every block is A-orthonormal and
+    A-orthogonal to the two before it; A·W_{j−1} lies in span{W_{j−2}, W_{j−1}, W_j} (the
+    three-block recurrence of the SRE-CG basis) — so a dropped CGS term, a wrong window or
+    a transposed coefficient fails one of these."""
+    A = ei.stencil_csr(7, 6, 5, ndim=3)
+    X0 = ei.cfg5_start_block(A.n, t)
+    D = _dense(A)
+    W = [oracle_lib.basis_sweep(A, X0, j)[1] for j in range(1, 7)]
+    # block 1 = X0 R⁻¹ with RᵀR = X0ᵀAX0
+    R = np.linalg.cholesky(X0.T @ D @ X0).T
+    assert np.abs(W[0] - np.linalg.solve(R.T, X0.T).T).max() <= 1e-12 * np.abs(W[0]).max()
+    for j, Wj in enumerate(W):
+        assert np.abs(Wj.T @ D @ Wj - np.eye(t)).max() <= 1e-10
+        for k in (j - 1, j - 2):
+            if k >= 0:
+                assert np.abs(W[k].T @ D @ Wj).max() <= 1e-10, (j, k)
+        if j >= 1:
+            Z = D @ W[j - 1]
+            Pz = sum(W[k] @ (W[k].T @ D @ Z) for k in range(max(0, j - 2), j + 1))
+            assert np.linalg.norm(Z - Pz) <= 1e-9 * np.linalg.norm(Z), j
+
+
+@pytest.mark.parametrize("method,s,t,kw", [("sre-cg", 3, 8, {}), ("sre-cg2", 2, 4, {}), ("msdo-cg", 3, 4, {}),
+                                         ("sre-cg", 2, 4, dict(ortho="pre-cholqr")),
+                                         ("sre-cg2", 2, 4, dict(restructured=True)),
+                                         ("sre-cg", 2, 8, dict(precond=16)), ("msdo-cg", 2, 4, dict(precond=16))])
+def test_mirror_mode_prefix_pinned(oracle_lib, method, s, t, kw):
+    """The oracle's MIRROR mode (the GPU's algebra: cached A·Q, C = (AQ)ᵀZ, r −= Σ(AW)α̃; reading R24/R9)
+    against the DEFINITION mode step by step, not only at convergence: after each of the first three outer
+    iterations x, the recursive residual r and ρ agree within 1e-10 (equal in exact arithmetic), and
+    every basis block of the mirror run is A-orthonormal — on κ = 1e3 bands."""
+    A = ei.stencil_csr(24, 24, ndim=2, kappa=ei.bands_kappa(24, band=4, hi=1e3))
+    b = ei.uniform_pm1(1806, A.n)
+    L = None
+    if "precond" in kw:
+        st, L = oracle_lib.ic0(A, kw.pop("precond"))
+        assert st == 0
+    its = {0: {}, 1: {}}
+    D = _dense(A)
+    for mode in (0, 1):
+        def cb(k, V, alpha, x, r, rho, m=mode):
+            its[m][k] = (x.copy(), r.copy(), rho, V.copy())
+        res = oracle_lib.solve(A, b, method, s, t, 0.0, kmax=4, mode=mode, callback=cb, L=L, **kw)
+        assert res["outer_iters"] == 3
+    for k in (1, 2, 3):
+        xd, rd, rhod, _ = its[0][k]
+        xm, rm, rhom, Vm = its[1][k]
+        assert np.abs(xm - xd).max() <= 1e-10 * np.abs(xd).max(), (k, "x")
+        assert np.abs(rm - rd).max() <= 1e-10 * np.abs(rd).max(), (k, "r")
+        assert abs(rhom - rhod) <= 1e-10 * rhod
+        for i in range(s):
+            Wi = Vm[:, i * t:(i + 1) * t]
+            if not kw.get("restructured"):
+                assert np.abs(Wi.T @ D @ Wi - np.eye(t)).max() <= 1e-9, (k, i)
