@@ -90,7 +90,12 @@ typedef struct {
                              steady-state outer iterations (k ≥ 3) are captured once per phase of
                              their slot/pointer period as CUDA graphs and replayed (launch-bound
                              small problems); results are bitwise those of the plain path.
-                             Ignored where it does not apply. */
+                             2: in addition, once every phase is captured the rest of the solve
+                             is ONE graph launch: a while node (the loop test of P:146/P:177,
+                             evaluated on the device by k_loop_check after each outer iteration)
+                             around a switch node over the phase graphs — no host synchronisation
+                             per outer iteration; falls back to 1 if the driver
+                             rejects the conditional graph.  Ignored where it does not apply. */
   int profile;            /* 1: record per-kernel-class CUDA events (see eks_profile) */
   int arnoldi;            /* CA methods: 7 = modified CA-Arnoldi (Alg 7, default when 0),
                              5 = CA-Arnoldi (Alg 5) */

@@ -238,7 +238,7 @@ def eks_solve_ex(ctx, method, s, t, tol, b, x, max_outer=0, profile=False, raise
     onesynch: one-synch CGS2 (2s+1 collectives per outer iteration, DESIGN reading R36)."""
     m = METHODS[method] if isinstance(method, str) else int(method)
     where = _where(b, x)
-    opt = _Options(int(max_outer), int(bool(use_graph)), int(bool(profile)), int(arnoldi), ORTHO[ortho],
+    opt = _Options(int(max_outer), int(use_graph), int(bool(profile)), int(arnoldi), ORTHO[ortho],
                    int(bool(restructured)), int(bool(precond)), AQ_CACHE[aq_cache], int(bool(onesynch)))
     rep = _Report()
     st = lib().eks_solve_ex(ctx, m, int(s), int(t), float(tol), _ptr(b, np.float64), _ptr(x, np.float64), where,

@@ -151,6 +151,10 @@ struct eks_ctx {
   double* h_scal = nullptr;  // pinned: [0..3] doubles, [4] flag as double
   int* h_flag = nullptr;     // pinned INT_MAX source
   std::vector<double> hist;
+  // device-resident loop control (eks_options.use_graph = 2): loop state and ρ history on the device
+  eks::LoopState* d_loop = nullptr;
+  double* d_hist = nullptr;
+  size_t hist_cap = 0;
   // profiling
   bool prof_on = false;
   std::vector<ProfRec> prof_pending;
@@ -324,7 +328,10 @@ eks_status ensure_workspace(eks_ctx* ctx, int t, int s) {
   }
   ST(dalloc(ctx, &ctx->pre, (size_t)3 * t * t + t));
   ST(dalloc(ctx, &ctx->scal, 16));
-  if (!ctx->flag) CK(cudaMalloc((void**)&ctx->flag, sizeof(int) * 4));
+  if (!ctx->flag) {  // flag[0]: breakdown block (atomicMin); flag[3]: INT_MAX, the device-side reset source
+    CK(cudaMalloc((void**)&ctx->flag, sizeof(int) * 4));
+    CK(cudaMemcpy(ctx->flag + 3, ctx->h_flag, sizeof(int), cudaMemcpyHostToDevice));
+  }
   if (!ctx->cnt) {
     CK(cudaMalloc((void**)&ctx->cnt, sizeof(unsigned) * 16));
     CK(cudaMemset(ctx->cnt, 0, sizeof(unsigned) * 16));
@@ -692,8 +699,8 @@ eks_status chol(eks_ctx* ctx, int t, const double* B, const double* g, double* R
   return EKS_OK;
 }
 
-eks_status reset_flag(eks_ctx* ctx) {
-  CK(cudaMemcpyAsync(ctx->flag, ctx->h_flag, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+eks_status reset_flag(eks_ctx* ctx) {  // device to device (capturable into a conditional graph body)
+  CK(cudaMemcpyAsync(ctx->flag, ctx->flag + 3, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
   return EKS_OK;
 }
 
@@ -2151,6 +2158,78 @@ eks_status eks_setup_precond(eks_ctx* ctx, eks_precond kind, int nd, const int64
   return EKS_OK;
 }
 
+// One captured phase of the steady-state s-step SRE-CG outer iteration (eks_options.use_graph).
+struct PhaseGraph {
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;  // kept for the device-resident loop (use_graph = 2)
+  int nb0 = 0;                  // nblocks when it was captured (block indices baked into the kernels)
+  long long launches = 0;       // this library's kernels in it
+  double bytes = 0, flops = 0;
+};
+
+// use_graph value of the options (0 off, 1 phase-graph replay, 2 also the device-resident loop)
+static int graphs_on_req(const eks_options* opt) { return opt ? opt->use_graph : 0; }
+
+eks_status ensure_hist(eks_ctx* ctx, size_t count) {
+  if (!ctx->d_loop) CK(cudaMalloc((void**)&ctx->d_loop, sizeof(eks::LoopState)));
+  if (ctx->hist_cap < count) {
+    dfree(ctx->d_hist);
+    ctx->hist_cap = 0;
+    CK(cudaMalloc((void**)&ctx->d_hist, sizeof(double) * count));
+    ctx->hist_cap = count;
+  }
+  return EKS_OK;
+}
+
+// The device-resident loop graph: while(hw) { switch(hs) { phase 0 … P−1 } ; k_loop_check }.
+// hw defaults to 1 and hs to 0 at every launch (the host launches it at a phase-0 iteration whose
+// loop test it has just evaluated).  Conditional bodies allow kernels, memcpy/memset and child
+// graphs (CUDA 12.4+), which is everything a one-rank phase graph holds.
+eks_status build_loop_graph(eks_ctx* ctx, const PhaseGraph* pg, int nphase, cudaGraphExec_t* out) {
+  *out = nullptr;
+  if (!ctx->d_loop || !ctx->d_hist) return fail(ctx, EKS_ERR_STATE, "loop state not allocated");
+  cudaGraph_t top = nullptr;
+  CK(cudaGraphCreate(&top, 0));
+  struct TopGuard {
+    cudaGraph_t g;
+    ~TopGuard() { cudaGraphDestroy(g); }
+  } tg{top};
+  cudaGraphConditionalHandle hw, hs;
+  CK(cudaGraphConditionalHandleCreate(&hw, top, 1, cudaGraphCondAssignDefault));
+  CK(cudaGraphConditionalHandleCreate(&hs, top, 0, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams wp{};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  CK(cudaGraphAddNode(&wn, top, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  cudaGraphNodeParams sp{};
+  sp.type = cudaGraphNodeTypeConditional;
+  sp.conditional.handle = hs;
+  sp.conditional.type = cudaGraphCondTypeSwitch;
+  sp.conditional.size = (unsigned)nphase;
+  cudaGraphNode_t sn;
+  CK(cudaGraphAddNode(&sn, body, nullptr, 0, &sp));
+  for (int p = 0; p < nphase; ++p) {
+    const cudaGraph_t pgraph = pg[p].graph;
+    if (!pgraph) return fail(ctx, EKS_ERR_STATE, "phase graph %d missing", p);
+    cudaGraphNode_t cn;
+    CK(cudaGraphAddChildGraphNode(&cn, sp.conditional.phGraph_out[p], nullptr, 0, pgraph));
+  }
+  // the check kernel after the switch, captured into the body
+  cudaStream_t cs = ctx->stream;
+  CK(cudaStreamBeginCaptureToGraph(cs, body, &sn, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+  const cudaError_t le = eks::launch_loop_check(cs, hw, hs, ctx->d_loop, ctx->scal, ctx->flag, ctx->d_hist);
+  cudaGraph_t cap = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(cs, &cap);
+  CK(le);
+  CK(ee);
+  CK(cudaGraphInstantiate(out, top, 0));
+  return EKS_OK;
+}
+
 eks_status eks_solve(eks_ctx* ctx, eks_method method, int s, int t, double tol, const double* b, double* x,
                      eks_mem where, int max_outer, eks_report* rep) {
   eks_options o{};
@@ -2240,25 +2319,29 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   // per phase of the combined period P ∈ {2, 6} is captured from a normal iteration and replayed
   // after that.  Everything a steady iteration touches is allocated before the first capture
   // (prealloc_steady), so no cudaMalloc/cudaFree can happen inside a capture.
-  struct PhaseGraph {
-    cudaGraphExec_t exec = nullptr;
-    int nb0 = 0;             // nblocks when it was captured (block indices baked into the kernels)
-    long long launches = 0;  // this library's kernels in it
-    double bytes = 0, flops = 0;
-  };
   // Several ranks: the NCCL halo exchanges and allreduces are captured with the kernels (the comm
   // stream forks from and joins the solve stream through events).  Should a capture fail, the outer
   // iteration (which did not execute while captured) runs uncaptured and graphs stay off.
   bool graphs_on = opt && opt->use_graph && method == EKS_SRE_CG && !restr && !prec && !ortho && !ctx->prof_on;
   const int gperiod = (s % 3 == 0) ? 2 : 6;
   PhaseGraph pg[6];
+  // Device-resident loop control (use_graph = 2): once every phase is captured, the
+  // rest of the solve is ONE graph launch — a while node (condition: the loop test of P:146) around a
+  // switch node over the phase graphs (child graphs) followed by k_loop_check, which evaluates the
+  // test on the device and selects the next phase.  No host synchronisation per outer iteration.
+  bool dloop_on = graphs_on_req(opt) == 2;
+  cudaGraphExec_t loop_exec = nullptr;
   struct GraphGuard {
     PhaseGraph* g;
+    cudaGraphExec_t* lx;
     ~GraphGuard() {
-      for (int i = 0; i < 6; ++i)
+      for (int i = 0; i < 6; ++i) {
         if (g[i].exec) cudaGraphExecDestroy(g[i].exec);
+        if (g[i].graph) cudaGraphDestroy(g[i].graph);
+      }
+      if (*lx) cudaGraphExecDestroy(*lx);
     }
-  } gguard{pg};
+  } gguard{pg, &loop_exec};
   if (graphs_on) ST(prealloc_steady(ctx, t, ring));
   // One outer iteration's stream work (Alg 3/4/6 lines 3-12, or the CA outer iteration).
   auto outer_body = [&]() -> eks_status {
@@ -2306,6 +2389,48 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   while (rho > tol * rho0 && k < kmax) {
     const int phase = (graphs_on && k >= 3) ? (k - 3) % gperiod : -1;
     replay_phase = -1;
+    if (phase == 0 && dloop_on && pg[gperiod - 1].exec) {
+      ST(ensure_hist(ctx, (size_t)kmax + 1));  // before the build: the graph bakes d_hist in
+      if (!loop_exec) {
+        const eks_status bs = build_loop_graph(ctx, pg, gperiod, &loop_exec);
+        if (bs != EKS_OK || !loop_exec) {  // not supported here: keep the host-checked replay
+          dloop_on = false;
+          loop_exec = nullptr;
+          cudaGetLastError();
+          continue;
+        }
+      }
+      // the rest of the solve on the device: one graph launch, one synchronisation
+      eks::LoopState ls{};
+      ls.k = k;
+      ls.kmax = kmax;
+      ls.nphase = gperiod;
+      ls.thr = tol * rho0;
+      CK(cudaMemcpyAsync(ctx->d_loop, &ls, sizeof(ls), cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaGraphLaunch(loop_exec, ctx->stream));
+      CK(cudaMemcpyAsync(&ls, ctx->d_loop, sizeof(ls), cudaMemcpyDeviceToHost, ctx->stream));
+      ST(stream_wait(ctx));
+      const int k0 = k;
+      ctx->hist.resize((size_t)ls.k);
+      if (ls.k > k0)
+        CK(cudaMemcpy(ctx->hist.data() + k0, ctx->d_hist + k0, sizeof(double) * (ls.k - k0), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < ls.iters; ++i) {  // iteration i ran phase i % gperiod
+        const PhaseGraph& q = pg[i % gperiod];
+        ctx->launches += q.launches + 1;
+        ctx->model_bytes += q.bytes;
+        ctx->model_flops += q.flops;
+      }
+      nblocks += s * ls.iters;
+      if (ls.stop == 2) {  // breakdown in the last iteration the graph ran (its phase: (iters-1) % P)
+        breakdown_block = ls.fl + (nblocks - s - pg[(ls.iters - 1) % gperiod].nb0);
+        status = EKS_ERR_BREAKDOWN;
+      }
+      if ((ls.k - k0) % 2) std::swap(ctx->r, ctx->rnew);
+      k = ls.k;
+      rho = ctx->hist.back();
+      if (ls.stop == 3) status = EKS_ERR_NONFINITE;
+      break;
+    }
     if (phase >= 0 && pg[phase].exec) {
       CK(cudaGraphLaunch(pg[phase].exec, ctx->stream));
       ctx->launches += pg[phase].launches;
@@ -2330,7 +2455,8 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
       }
       if (ie == cudaSuccess && cst == EKS_OK) {
         ie = cudaGraphInstantiate(&pg[phase].exec, g, 0);
-        cudaGraphDestroy(g);
+        if (dloop_on) pg[phase].graph = g;
+        else cudaGraphDestroy(g);
       } else if (g) {
         cudaGraphDestroy(g);
       }
@@ -2541,6 +2667,8 @@ eks_status eks_destroy(eks_ctx* ctx) {
   if (ctx->own) cudaStreamDestroy(ctx->own);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
   if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
+  dfree(ctx->d_hist);
+  if (ctx->d_loop) cudaFree(ctx->d_loop);
   delete ctx;
   return EKS_OK;
 }

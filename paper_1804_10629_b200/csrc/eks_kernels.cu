@@ -1360,4 +1360,37 @@ cudaError_t launch_sumsq(cudaStream_t st, int64_t n, const double* v, double* pa
   return cudaGetLastError();
 }
 
+// (a6) one thread: the loop test of Alg 3/4/6 on the device, in the host
+// loop's order — breakdown flag first (x stays the last completed iterate), then ρ = √(ρ²)
+// (IEEE-rounded, the host's std::sqrt), hist[k] = ρ, k += 1, non-finite ρ stops (EKS_ERR_NONFINITE).
+__global__ void k_loop_check(cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hs, LoopState* st,
+                             const double* __restrict__ scal, const int* __restrict__ flag, double* hist) {
+  LoopState s = *st;
+  s.iters += 1;
+  const int fl = flag[0];
+  unsigned int cont = 0;
+  if (fl != 0x7fffffff) {
+    s.stop = 2;
+    s.fl = fl;
+  } else {
+    const double rho = sqrt(scal[1]);
+    hist[s.k] = rho;
+    s.k += 1;
+    if (!isfinite(rho)) s.stop = 3;
+    else if (rho > s.thr && s.k < s.kmax) cont = 1;
+    else s.stop = 1;
+  }
+  s.phase = (s.phase + 1) % s.nphase;
+  *st = s;
+  cudaGraphSetConditional(hs, (unsigned int)s.phase);
+  cudaGraphSetConditional(hw, cont);
+}
+
+cudaError_t launch_loop_check(cudaStream_t st, unsigned long long hwhile, unsigned long long hswitch,
+                              LoopState* state, const double* scal, const int* flag, double* hist) {
+  k_loop_check<<<1, 1, 0, st>>>((cudaGraphConditionalHandle)hwhile, (cudaGraphConditionalHandle)hswitch, state,
+                                scal, flag, hist);
+  return cudaGetLastError();
+}
+
 }  // namespace eks

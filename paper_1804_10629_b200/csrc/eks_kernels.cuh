@@ -119,4 +119,23 @@ cudaError_t launch_residual(cudaStream_t st, int64_t n, const double* b, const d
 // partial Σ v² per CTA
 cudaError_t launch_sumsq(cudaStream_t st, int64_t n, const double* v, double* part, int nblk);
 
+// ---- (a6) device-resident loop control (P:146/"while ρ > ε ρ0 and k < k_max"):
+// the state of a steady-state solve that runs as ONE CUDA graph (a while node around a switch
+// over the captured outer-iteration phases, eks_options.use_graph = 2).  After each outer
+// iteration k_loop_check reads ρ² (scal[1]) and the breakdown flag, appends ρ to hist, and sets
+// the while condition (ρ > thr and k < kmax and no breakdown and ρ finite) and the next phase.
+struct LoopState {
+  int k;        // next outer-iteration index (host's k): hist[k] receives ρ_k
+  int kmax;     // k_max
+  int nphase;   // phases of the captured period
+  int phase;    // phase of the next iteration
+  int iters;    // outer iterations executed in the graph (the breakdown one included)
+  int stop;     // 0 running, 1 converged or k_max, 2 breakdown (flag in fl), 3 non-finite ρ
+  int fl;       // breakdown flag value (block index baked into the phase graph)
+  int pad;
+  double thr;   // ε ρ0
+};
+cudaError_t launch_loop_check(cudaStream_t st, unsigned long long hwhile, unsigned long long hswitch,
+                              LoopState* state, const double* scal, const int* flag, double* hist);
+
 }  // namespace eks

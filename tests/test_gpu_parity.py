@@ -324,6 +324,48 @@ def test_graph_replay_bitwise(eks, torch_cuda, s_, t, N):
     assert a["gpu_launches"] == g["gpu_launches"]
 
 
+@pytest.mark.parametrize("s_,t,N", [(3, 16, 64), (2, 4, 64), (4, 8, 48), (1, 16, 48)])
+def test_device_loop_bitwise(eks, torch_cuda, s_, t, N):
+    """use_graph = 2 ("while ρ > ε ρ0 and k < k_max" on the device): after the
+    phases are captured the rest of the solve is ONE graph launch (while node → switch over the
+    phase graphs → k_loop_check).  Bitwise the plain path's x, counts and ρ history; the graph ran
+    (one k_loop_check launch per device-loop iteration on top of the plain path's launches)."""
+    A = ei.poisson2d(N)
+    b = dev(torch_cuda, ei.uniform_pm1(77, A.n))
+    S = eks.Solver(A)
+    a = S.solve(b, "sre-cg", s_, t, 1e-10)
+    g = S.solve(b, "sre-cg", s_, t, 1e-10, use_graph=2)
+    S.close()
+    assert a["converged"] and g["converged"] and a["outer_iters"] == g["outer_iters"] > 12
+    assert torch_cuda.equal(a["x"], g["x"])
+    assert np.array_equal(a["hist"], g["hist"])
+    period = 2 if s_ % 3 == 0 else 6
+    ndev = g["gpu_launches"] - a["gpu_launches"]  # k_loop_check launches = device-loop iterations
+    assert 0 < ndev <= a["outer_iters"] - 2 - period
+
+
+@pytest.mark.parametrize("tol,max_outer", [(0.0, 40), (1e-10, 14)])
+def test_device_loop_stop_reasons(eks, torch_cuda, tol, max_outer):
+    """The device loop stops where the host loop stops: k_max (MAXITER), or, driven past
+    convergence with tol = 0 on a 64-row problem, the same breakdown block / non-finite ρ.
+    Status, counts, breakdown block, x and ρ history identical to the plain path."""
+    A = ei.poisson2d(8 if tol == 0.0 else 64)
+    b = dev(torch_cuda, ei.uniform_pm1(5, A.n))
+    S = eks.Solver(A)
+    out = []
+    for ug in (0, 2):
+        x = torch_cuda.zeros_like(b)
+        st, rep = eks.eks_solve_ex(S.ctx, "sre-cg", 2, 4, tol, b, x, max_outer=max_outer, raise_on=(),
+                                   use_graph=ug)
+        out.append((st, rep, x))
+    S.close()
+    (sa, ra, xa), (sg, rg, xg) = out
+    assert sa == sg and sa != 0
+    assert ra["outer_iters"] == rg["outer_iters"] and ra["breakdown_block"] == rg["breakdown_block"]
+    assert torch_cuda.equal(xa, xg)
+    assert np.array_equal(ra["hist"], rg["hist"], equal_nan=True)
+
+
 @pytest.mark.parametrize("s_,t", [(1, 4), (1, 16), (2, 8)])
 def test_graph_replay_fresh_solver(eks, torch_cuda, s_, t):
     """use_graph on a FRESH context (nothing preallocated by an earlier plain solve): every ring

@@ -1,4 +1,5 @@
-"""cfg1 (2D Poisson 64², launch-bound) and cfg2 solve time with and without CUDA-graph replay."""
+"""cfg1 (2D Poisson 64², launch-bound) and cfg2 solve time: plain (0), CUDA-graph replay with a host loop
+test per outer iteration (1), and the device-resident loop (2: one graph launch for the steady solve)."""
 import os
 import sys
 import time
@@ -12,7 +13,7 @@ import paper_1804_10629_b200 as eks  # noqa: E402
 for name, p in (("cfg1", ei.cfg1()), ("cfg2", ei.cfg2())):
     S = eks.Solver(p.A)
     b = torch.from_numpy(p.b).cuda()
-    for g in (False, True, False, True):
+    for g in (0, 1, 2, 0, 1, 2, 1, 2):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         reps = 5 if name == "cfg1" else 2
