@@ -214,6 +214,13 @@ eks_status eks_plan_halo(int rank, int nranks, const int64_t* ranges, const int6
 eks_status eks_plan_grid(int64_t row_begin, int64_t row_end, const int64_t* row_ptr, const int32_t* col,
                          const double* vals, int64_t halo_before, int64_t halo_after, int64_t* geom, double* sv);
 
+/* Host-only plan of the matrix-powers kernel the CA variants run on several ranks (P:1092-1097,
+ * reading R37): a slab of nz planes with db / da ghost planes below / above (d = s − 1 next to a
+ * neighbour rank, 0 at the grid boundary).  steps[4·(i−1) .. 4·(i−1)+3] = {zlo, zhi, gb, ga} for
+ * power i = 1..d: A^i·V is computed on planes [zlo, zhi) (slab-relative, zlo = −min(db, d−i),
+ * zhi = nz + min(da, d−i)) and reads one further plane below / above iff gb / ga = 1. */
+eks_status eks_plan_mpk(int nz, int d, int db, int da, int* steps);
+
 /* Kernel-class timings of the last solve/sweep run with opt.profile = 1. */
 eks_status eks_get_profile(const eks_ctx* ctx, eks_profile* out);
 

@@ -23,6 +23,16 @@ eks_status eks_k_split(eks_ctx* ctx, int t, const double* r, double* Z);
  * If G != NULL: G = XᵀY (t×t, full, fixed-order sums).  If v and g != NULL: g = Xᵀv (t). */
 eks_status eks_k_spmm(eks_ctx* ctx, int t, const double* X, double* Y, double* G, const double* v, double* g);
 
+/* §8(f)1 at N > 1, the matrix-powers kernel with depth-(s−1) ghost zones (reading
+ * R37) on ONE GPU: planes [z0, z1) of the context's stencil operator play a rank's slab; its
+ * d = s − 1 ghost planes on each side (fewer next to the grid boundary) are copied from X (n×t device,
+ * the whole block) as the one exchange would deliver them, and power i = 1..d is computed on the slab
+ * plus (d − i) ghost planes by the same launches the multi-rank CA outer iteration issues.
+ * V (device, d × (z1−z0)·nx·ny × t) receives the slab rows of A·X, …, A^d·X — bitwise the rows of the
+ * global powers.  Rows a power must not read are NaN in the scratch.  Needs the plane-marching
+ * SpMM (stencil operator, t ∈ {8,16,32,64}); EKS_ERR_INVALID_ARG otherwise. */
+eks_status eks_k_matrix_powers(eks_ctx* ctx, int t, int s, int z0, int z1, const double* X, double* V);
+
 /* (a3) CGS2: twice { C = (AQ)ᵀZ ; Z = Z − Q·C } against nq window blocks (
  * readings R3, R24).  Q and AQ are HOST arrays of nq DEVICE pointers (each an n×t block,
  * AQ[j] = A·Q[j]).  Z is updated in place; C1, C2 ((nq·t)×t device, may be NULL) receive the

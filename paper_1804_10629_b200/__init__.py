@@ -89,6 +89,8 @@ def lib():
             "eks_k_last_basis": [vp, i32, vp, vp],
             "eks_plan_grid": [i64, i64, vp, vp, vp, i64, i64, vp, vp],
             "eks_k_last_residual": [vp, vp],
+            "eks_plan_mpk": [i32, i32, i32, i32, vp],
+            "eks_k_matrix_powers": [vp, i32, i32, i32, i32, vp, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -103,7 +105,7 @@ def lib():
 EXPORTED = ["eks_get_unique_id", "eks_create", "eks_set_stream", "eks_setup_csr", "eks_setup_precond", "eks_solve", "eks_solve_ex",
             "eks_basis_sweep", "eks_get_profile", "eks_destroy", "eks_error_string", "eks_k_split", "eks_k_spmm",
             "eks_k_cgs2", "eks_k_acholqr", "eks_k_chol", "eks_k_time_spmm", "eks_plan_halo", "eks_k_last_basis",
-            "eks_k_last_residual", "eks_plan_grid"]
+            "eks_k_last_residual", "eks_plan_grid", "eks_plan_mpk", "eks_k_matrix_powers"]
 
 
 def eks_plan_halo(rank: int, nranks: int, ranges, row_ptr, col):
@@ -289,6 +291,17 @@ def eks_k_split(ctx, t, r, Z):
 def eks_k_spmm(ctx, t, X, Y, G=None, v=None, g=None):
     _check(ctx, lib().eks_k_spmm(ctx, int(t), _ptr(X, None), _ptr(Y, None), _ptr(G, None), _ptr(v, None),
                                  _ptr(g, None)))
+
+
+def eks_plan_mpk(nz: int, d: int, db: int, da: int):
+    """Host-only matrix-powers plan (include/eks.h): d rows of (zlo, zhi, gb, ga)."""
+    steps = np.zeros(4 * d, np.int32)
+    _check(None, lib().eks_plan_mpk(int(nz), int(d), int(db), int(da), _ptr(steps, np.int32)))
+    return steps.reshape(d, 4)
+
+
+def eks_k_matrix_powers(ctx, t, s, z0, z1, X, V):
+    _check(ctx, lib().eks_k_matrix_powers(ctx, int(t), int(s), int(z0), int(z1), _ptr(X, None), _ptr(V, None)))
 
 
 def eks_k_cgs2(ctx, t, Q, AQ, Z, C1=None, C2=None):

@@ -40,6 +40,7 @@ struct Block {
   double* base = nullptr;  // ext allocation (ghost rows included) or local allocation
   double* loc = nullptr;   // first local row
   bool owned = true;       // false: aliases another Block's storage (store-Q-only AW ring)
+  double* alloc = nullptr; // deep-ghost blocks of the matrix-powers kernel: the allocation (base = loc − halo rows)
 };
 
 struct ProfRec { int cls; cudaEvent_t a, b; };
@@ -81,6 +82,13 @@ struct eks_ctx {
   bool grid_ok = false;
   eks::GridPlan gplan{};
   double* d_sv = nullptr;
+  // matrix-powers kernel of the CA variants at N > 1: stencil values of the
+  // slab plus mpk_d ghost planes of each neighbour (exchanged once), slab table of all ranks
+  std::vector<int64_t> ranges;
+  double* mpk_sv = nullptr;
+  int mpk_d = 0;           // ghost depth mpk_sv holds (0: not built)
+  int mpk_ok_t = 0, mpk_ok_d = 0, mpk_ok = -1;  // cached all-ranks decision for (t, d): −1 unknown
+  int ca_deep = 0;         // ghost depth (planes) the Vca blocks were allocated with
   // communication-avoiding outer iteration: the s monomial blocks, their A-products, the st×st
   // Gram / factor / inverse, g = Vᵀr and α̃
   std::vector<Block> Vca, AVca;
@@ -272,7 +280,7 @@ eks_status alloc_block(eks_ctx* ctx, Block* B, int t, bool ext) {
 }
 
 void free_workspace(eks_ctx* c) {
-  for (auto& b : c->Vca) dfree(b.base);
+  for (auto& b : c->Vca) dfree(b.alloc ? b.alloc : b.base);
   for (auto& b : c->AVca) dfree(b.base);
   c->Vca.clear();
   c->AVca.clear();
@@ -1057,6 +1065,133 @@ eks_status acholqr_block(eks_ctx* ctx, int t, Block& Z, double* AZ, int gb) {
   return EKS_OK;
 }
 
+// ---- Matrix-powers kernel with depth-d ghost zones (reading R37) ----
+// The CA variants need V_i = A^i V_0, i = 1..d (d = s − 1), of a block whose rows are spread over the
+// ranks.  Instead of one ghost-plane exchange per product, V_0's d boundary planes are exchanged ONCE
+// and power i is computed on the slab plus (d − i) ghost planes of each neighbour (redundant work on
+// the ghost planes), so that power i + 1 finds its ghost plane already there.  The ghost
+// rows of A (their stencil values) are exchanged once per operator.  Every product is a launch of the
+// plane-marching SpMM on a sub-range of planes, so each row is the same fma chain as in the global
+// product (bitwise equal powers).
+//
+// Host plan: the slab has nz planes; db / da ghost planes exist below / above (d next to another rank,
+// 0 at the boundary of the grid; in between only for a virtual slab whose distance to the boundary is
+// < d).  Power i computes planes [zlo, zhi) (slab-relative, zlo ≤ 0) and reads one plane further
+// where gb / ga = 1.
+struct MpkStep { int zlo, zhi, gb, ga; };
+
+void mpk_plan(int nz, int d, int db, int da, MpkStep* st) {
+  for (int i = 1; i <= d; ++i) {
+    const int below = std::min(db, d - i), above = std::min(da, d - i);
+    st[i - 1] = MpkStep{-below, nz + above, db > below ? 1 : 0, da > above ? 1 : 0};
+  }
+}
+
+// V[i] = A·V[i−1], i = 1..d, on the shrinking plane ranges of mpk_plan.  V[i] points at slab plane 0
+// of a buffer holding planes [−db, nz + da); sv_ext = stencil values from plane −db on.
+eks_status mpk_local(eks_ctx* ctx, int t, int d, int nz, int db, int da, const double* sv_ext, double* const* V) {
+  std::vector<MpkStep> st(d);
+  mpk_plan(nz, d, db, da, st.data());
+  const int64_t plane = (int64_t)ctx->gplan.nx * ctx->gplan.ny;
+  const int VS = (ctx->gplan.w + 1) & ~1;
+  for (int i = 1; i <= d; ++i) {
+    const MpkStep& m = st[i - 1];
+    eks::GridPlan gp = ctx->gplan;
+    gp.nz = m.zhi - m.zlo;
+    gp.gb = m.gb;
+    gp.ga = m.ga;
+    gp.sv = sv_ext + (size_t)(m.zlo + db) * plane * VS;
+    if (!eks::spmm_grid_fits(t, gp)) return fail(ctx, EKS_ERR_INVALID_ARG, "matrix powers: plane range does not fit");
+    const int64_t rows = (int64_t)gp.nz * plane;
+    account(ctx, EKS_K_SPMM, 8.0 * gp.w * rows + 16.0 * rows * t, 2.0 * gp.w * rows * t);
+    KScope k(ctx, EKS_K_SPMM);
+    CK(eks::launch_spmm_grid(ctx->stream, t, gp, V[i - 1] + m.zlo * plane * t, V[i] + m.zlo * plane * t, nullptr,
+                             nullptr, ctx->nblk, eks::Tail{}, eks::CholArgs{}, false));
+  }
+  return EKS_OK;
+}
+
+// Can the CA powers of this solve run as the matrix-powers kernel?  Several ranks, the plane-marching
+// SpMM on every rank, no preconditioner (M⁻¹ couples rows of a domain: no ghost rows for it), every
+// slab at least d planes thick (the ghost planes then come from the two neighbour ranks only).  The
+// answer must be the same on all ranks (the exchanges pair up): one MIN allreduce per (t, d), cached.
+// EKS_MPK=0 keeps the one-exchange-per-product path.
+eks_status mpk_usable(eks_ctx* ctx, int t, int d, bool& on) {
+  on = false;
+  if (ctx->nranks == 1 || d < 1) return EKS_OK;
+  static const bool env_on = [] {
+    const char* e = getenv("EKS_MPK");
+    return !(e && !strcmp(e, "0"));
+  }();
+  if (ctx->mpk_ok >= 0 && ctx->mpk_ok_t == t && ctx->mpk_ok_d == d) {
+    on = ctx->mpk_ok == 1;
+    return EKS_OK;
+  }
+  bool mine = env_on && !ctx->use_prec && eks::sweep_supported(t) && spmm_path_for(ctx, t) == 4;
+  if (mine) {
+    const int64_t plane = (int64_t)ctx->gplan.nx * ctx->gplan.ny;
+    for (int q = 0; q < ctx->nranks; ++q) mine = mine && ctx->ranges[2 * q + 1] - ctx->ranges[2 * q] >= d * plane;
+  }
+  double v = mine ? 1.0 : 0.0;  // MIN over ranks through the fp64 scratch of the Cholesky flag's neighbours
+  double* dv = nullptr;
+  ST(dalloc(ctx, &dv, 1));
+  CK(cudaMemcpyAsync(dv, &v, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  NK(ncclAllReduce(dv, dv, 1, ncclDouble, ncclMin, ctx->comm, ctx->stream));
+  CK(cudaMemcpyAsync(&v, dv, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  dfree(dv);
+  ctx->mpk_ok = v == 1.0 ? 1 : 0;
+  ctx->mpk_ok_t = t;
+  ctx->mpk_ok_d = d;
+  on = ctx->mpk_ok == 1;
+  return EKS_OK;
+}
+
+// Send my d lowest planes to rank − 1 and my d highest to rank + 1; receive theirs into the ghost
+// zones right before / after the slab (row width `w` doubles: t for a block, VS for stencil values).
+eks_status mpk_exchange(eks_ctx* ctx, double* loc, int w, int d) {
+  const int64_t plane = (int64_t)ctx->gplan.nx * ctx->gplan.ny;
+  const size_t cnt = (size_t)d * plane * w;
+  KScope k(ctx, EKS_K_COMM);
+  CK(cudaEventRecord(ctx->ev_ready, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_ready, 0));
+  NK(ncclGroupStart());
+  if (ctx->rank > 0) {
+    NK(ncclSend(loc, cnt, ncclDouble, ctx->rank - 1, ctx->comm, ctx->comm_stream));
+    NK(ncclRecv(loc - cnt, cnt, ncclDouble, ctx->rank - 1, ctx->comm, ctx->comm_stream));
+  }
+  if (ctx->rank + 1 < ctx->nranks) {
+    NK(ncclSend(loc + (size_t)ctx->n * w - cnt, cnt, ncclDouble, ctx->rank + 1, ctx->comm, ctx->comm_stream));
+    NK(ncclRecv(loc + (size_t)ctx->n * w, cnt, ncclDouble, ctx->rank + 1, ctx->comm, ctx->comm_stream));
+  }
+  NK(ncclGroupEnd());
+  CK(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+  return EKS_OK;
+}
+
+// The d monomial powers V[1..d] of V[0] (deep-ghost blocks) on several ranks: stencil values of the
+// ghost planes once per operator and depth, ONE exchange of V[0]'s boundary planes, d local products.
+eks_status mpk_powers(eks_ctx* ctx, int t, int d, std::vector<Block>& V) {
+  const int64_t plane = (int64_t)ctx->gplan.nx * ctx->gplan.ny;
+  const int VS = (ctx->gplan.w + 1) & ~1;
+  const int db = ctx->rank > 0 ? d : 0, da = ctx->rank + 1 < ctx->nranks ? d : 0;
+  if (ctx->mpk_d != d) {
+    dfree(ctx->mpk_sv);
+    ctx->mpk_sv = nullptr;
+    ctx->mpk_d = 0;
+    ST(dalloc(ctx, &ctx->mpk_sv, (size_t)(db + da) * plane * VS + (size_t)ctx->n * VS));
+    double* mid = ctx->mpk_sv + (size_t)db * plane * VS;
+    CK(cudaMemcpyAsync(mid, ctx->gplan.sv, sizeof(double) * ctx->n * VS, cudaMemcpyDeviceToDevice, ctx->stream));
+    ST(mpk_exchange(ctx, mid, VS, d));
+    ctx->mpk_d = d;
+  }
+  ST(mpk_exchange(ctx, V[0].loc, t, d));
+  std::vector<double*> L(d + 1);
+  for (int i = 0; i <= d; ++i) L[i] = V[i].loc;
+  return mpk_local(ctx, t, d, (int)(ctx->n / plane), db, da, ctx->mpk_sv, L.data());
+}
+
 // One outer iteration of CA SRE-CG / CA SRE-CG2 / CA MSDO-CG (base = the s-step method):
 //   W = T(r_{k−1}) (k = 1, or every k for MSDO) or A·W_last;  Alg 7: A-orthonormalize W
 //   against the window and itself;  V = [W, AW, …, A^{s−1}W];  CGS2 of every V_i
@@ -1068,8 +1203,11 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
   const int st = s * t;
   ctx->rho_fused = false;  // ‖r_k‖² comes from k_ca_update's per-CTA partials
   ctx->c1_ready = false;
-  if (ctx->ca_cap != st || (int)ctx->Vca.size() != s) {
-    for (auto& b : ctx->Vca) dfree(b.base);
+  bool mpk = false;
+  ST(mpk_usable(ctx, t, s - 1, mpk));
+  const int deep = mpk ? s - 1 : 0;
+  if (ctx->ca_cap != st || (int)ctx->Vca.size() != s || ctx->ca_deep != deep) {
+    for (auto& b : ctx->Vca) dfree(b.alloc ? b.alloc : b.base);
     for (auto& b : ctx->AVca) dfree(b.base);
     for (double** p : {&ctx->Bca, &ctx->gca, &ctx->Rca, &ctx->Rinvca, &ctx->alphaca, &ctx->Btmp, &ctx->cawork}) {
       dfree(*p);
@@ -1078,9 +1216,19 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
     ctx->Vca.assign(s, Block{});
     ctx->AVca.assign(s, Block{});
     for (int i = 0; i < s; ++i) {
-      ST(alloc_block(ctx, &ctx->Vca[i], t, true));
+      if (deep) {  // `deep` ghost planes next to each neighbour rank (≥ the one plane of the halo layout)
+        Block& B = ctx->Vca[i];
+        const int64_t plane = (int64_t)ctx->gplan.nx * ctx->gplan.ny;
+        const int64_t rb = ctx->rank > 0 ? deep * plane : 0, ra = ctx->rank + 1 < ctx->nranks ? deep * plane : 0;
+        ST(dalloc(ctx, &B.alloc, (size_t)(rb + ctx->n + ra) * t));
+        B.loc = B.alloc + rb * t;
+        B.base = B.loc - ctx->halo_before * t;
+      } else {
+        ST(alloc_block(ctx, &ctx->Vca[i], t, true));
+      }
       ST(alloc_block(ctx, &ctx->AVca[i], t, false));
     }
+    ctx->ca_deep = deep;
     ST(dalloc(ctx, &ctx->Bca, (size_t)st * st));
     ST(dalloc(ctx, &ctx->gca, (size_t)st));
     ST(dalloc(ctx, &ctx->Rca, (size_t)st * st));
@@ -1115,9 +1263,13 @@ eks_status ca_outer(eks_ctx* ctx, int t, int s, int base, int arnoldi, int k, in
     if (!Q.empty()) ST(cgs2(ctx, t, Q, AQ, V[0].loc, V[0].loc));
     ST(acholqr_block(ctx, t, V[0], AV[0].loc, nblocks));
   }
-  for (int i = 1; i < s; ++i) {  // monomial powers (M⁻¹A with the preconditioner)
-    ST(spmm(ctx, V[i - 1], V[i].loc, t));
-    if (ctx->use_prec) ST(prec_apply(ctx, t, V[i].loc, V[i].loc));
+  if (mpk) {  // matrix-powers kernel: one exchange of s − 1 ghost planes, then local products
+    ST(mpk_powers(ctx, t, s - 1, V));
+  } else {
+    for (int i = 1; i < s; ++i) {  // monomial powers (M⁻¹A with the preconditioner)
+      ST(spmm(ctx, V[i - 1], V[i].loc, t));
+      if (ctx->use_prec) ST(prec_apply(ctx, t, V[i].loc, V[i].loc));
+    }
   }
   if (!Q.empty()) ST(cgs2_stacked(ctx, t, Q, AQ, V, AV));  // AV serves as the pass-1 scratch
   // Gram B (st×st, upper blocks) and g = Vᵀ r_{k−1}: block column j = [V_0..V_{j−1}]ᵀAV_j, then
@@ -1750,6 +1902,11 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   // ---- halo plan (host-only, also exported as eks_plan_halo for the multi-rank CPU tests)
   HaloPlan plan;
   plan_halo(ctx->rank, ctx->nranks, ranges.data(), n, RP, COL, plan);
+  ctx->ranges = ranges;
+  dfree(ctx->mpk_sv);
+  ctx->mpk_sv = nullptr;
+  ctx->mpk_d = 0;
+  ctx->mpk_ok = -1;
   const int64_t old_before = ctx->halo_before, old_after = ctx->halo_after;
   ctx->recvs = plan.recvs;
   ctx->sends.clear();
@@ -2277,6 +2434,7 @@ eks_status eks_solve_ex(eks_ctx* ctx, eks_method method, int s, int t, double to
   const int ring = (method == EKS_SRE_CG) ? (restr ? std::max(3, s + 1) : 3) : (method == EKS_CA_SRE_CG ? 2 * s + 1 : 0);
   ctx->ortho = ortho;
   ctx->use_prec = prec;
+  ctx->mpk_ok = -1;  // the matrix-powers decision depends on the preconditioner option
   // full-basis s-step methods (SRE-CG2, MSDO-CG) keep every W; A·W is cached only with
   // aq_cache = 1 — by default they store Q only (reading R24): the same 4 window sweeps per CGS2, two
   // more SpMMs per block, half the memory per outer iteration
@@ -2658,6 +2816,7 @@ eks_status eks_destroy(eks_ctx* ctx) {
   dfree(ctx->d_lidx);
   dfree(ctx->d_sval);
   dfree(ctx->d_sv);
+  dfree(ctx->mpk_sv);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (auto& p : ctx->prof_pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
@@ -2706,6 +2865,48 @@ eks_status eks_k_spmm(eks_ctx* ctx, int t, const double* X, double* Y, double* G
   }
   CK(cudaStreamSynchronize(ctx->stream));
   return EKS_OK;
+}
+
+eks_status eks_plan_mpk(int nz, int d, int db, int da, int* steps) {
+  if (nz < 1 || d < 1 || db < 0 || da < 0 || db > d || da > d || !steps) return EKS_ERR_INVALID_ARG;
+  std::vector<MpkStep> st(d);
+  mpk_plan(nz, d, db, da, st.data());
+  for (int i = 0; i < d; ++i) {
+    steps[4 * i] = st[i].zlo;
+    steps[4 * i + 1] = st[i].zhi;
+    steps[4 * i + 2] = st[i].gb;
+    steps[4 * i + 3] = st[i].ga;
+  }
+  return EKS_OK;
+}
+
+eks_status eks_k_matrix_powers(eks_ctx* ctx, int t, int s, int z0, int z1, const double* X, double* V) {
+  ST(k_ready(ctx, t));
+  if (!eks::sweep_supported(t) || spmm_path_for(ctx, t) != 4)
+    return fail(ctx, EKS_ERR_INVALID_ARG, "matrix powers need the plane-marching SpMM (stencil operator, t >= 8)");
+  const int nzg = ctx->gplan.nz, d = s - 1;
+  if (d < 1 || z0 < 0 || z1 <= z0 || z1 > nzg || !X || !V) return fail(ctx, EKS_ERR_INVALID_ARG, "bad slab or s");
+  const int64_t plane = (int64_t)ctx->gplan.nx * ctx->gplan.ny;
+  const int VS = (ctx->gplan.w + 1) & ~1;
+  const int nz = z1 - z0, db = std::min(d, z0), da = std::min(d, nzg - z1);
+  const size_t rows = (size_t)(db + nz + da) * plane;
+  double* buf = nullptr;
+  ST(dalloc(ctx, &buf, rows * t * (d + 1)));
+  // every ghost or slab row a power may not read is NaN: a wrong plane range shows up in the slab rows
+  CK(cudaMemsetAsync(buf, 0xFF, sizeof(double) * rows * t * (d + 1), ctx->stream));
+  CK(cudaMemcpyAsync(buf, X + (size_t)(z0 - db) * plane * t, sizeof(double) * rows * t, cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  std::vector<double*> L(d + 1);
+  for (int i = 0; i <= d; ++i) L[i] = buf + (size_t)i * rows * t + (size_t)db * plane * t;
+  eks_status stt = mpk_local(ctx, t, d, nz, db, da, ctx->gplan.sv + (size_t)(z0 - db) * plane * VS, L.data());
+  if (stt == EKS_OK)
+    for (int i = 1; i <= d && stt == EKS_OK; ++i)
+      if (cudaMemcpyAsync(V + (size_t)(i - 1) * nz * plane * t, L[i], sizeof(double) * nz * plane * t,
+                          cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
+        stt = fail(ctx, EKS_ERR_CUDA, "matrix powers: copy failed");
+  cudaStreamSynchronize(ctx->stream);
+  dfree(buf);
+  return stt;
 }
 
 eks_status eks_k_cgs2(eks_ctx* ctx, int t, int nq, const double* const* Q, const double* const* AQ, double* Z,

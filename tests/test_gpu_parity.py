@@ -880,3 +880,48 @@ def test_onesynch_basis_sweep(eks, torch_cuda, oracle_lib, t):
     assert rel(host(W), Wo) <= 1e-9
     Wh = host(W)
     assert np.abs(oracle_lib.xty(Wh, oracle_lib.spmm(A, Wh)) - np.eye(t)).max() <= 1e-10
+
+
+# ------------------------------------------------------------------ §8(f)1 at N > 1: matrix-powers kernel
+@pytest.mark.parametrize("t,s,opname,z0,z1", [
+    (8, 3, "aniso24", 8, 16), (16, 4, "aniso24", 0, 6), (16, 4, "aniso24", 18, 24), (32, 3, "aniso24", 1, 23),
+    (64, 2, "aniso24", 12, 13), (16, 5, "aniso24", 2, 5), (16, 3, "bands96", 30, 60), (8, 6, "bands96", 3, 96)])
+def test_matrix_powers_virtual_slab_bitwise(eks, torch_cuda, oracle_lib, t, s, opname, z0, z1):
+    """Depth-(s−1) ghost-zone matrix powers (reading R37): planes [z0, z1) as a rank's slab —
+    the slab rows of A·X, …, A^(s−1)·X from the shrinking plane-range launches equal the oracle's global
+    powers bitwise (interior slabs, slabs at / near the grid boundary, a one-plane slab)."""
+    torch = torch_cuda
+    A = {"aniso24": lambda: ei.stencil_csr(24, 24, 24, ndim=3, scale=(1.0, 1.0, 1e-2)),
+         "bands96": lambda: ei.stencil_csr(96, 96, ndim=2, kappa=ei.bands_kappa(96, band=8))}[opname]()
+    plane = 24 * 24 if opname == "aniso24" else 96
+    S = eks.Solver(A)
+    X = ei.uniform_pm1(41, A.n * t).reshape(A.n, t)
+    rows = (z1 - z0) * plane
+    V = torch.full((s - 1, rows, t), float("nan"), dtype=torch.float64, device="cuda")
+    eks.eks_k_matrix_powers(S.ctx, t, s, z0, z1, dev(torch, X), V)
+    P = X
+    for i in range(s - 1):
+        P = oracle_lib.spmm(A, P)
+        assert np.array_equal(host(V[i]), P[z0 * plane:z1 * plane]), (i, t, s)
+    S.close()
+
+
+def test_matrix_powers_full_size_sampled(eks, torch_cuda, oracle_lib):
+    """The same at a size whose launches span many units per CTA (128³, t = 16, s = 4, an interior slab of
+    32 planes): the slab rows of the powers equal repeated global eks_k_spmm products bitwise (those are
+    bitwise the oracle's, test_spmm_bitwise_and_gram / test_full_size_spmm_gram_sampled)."""
+    torch = torch_cuda
+    N, t, s, z0, z1 = 128, 16, 4, 48, 80
+    A = ei.stencil_csr(N, N, N, ndim=3, scale=(1.0, 1.0, 1e-2))
+    S = eks.Solver(A)
+    X = dev(torch, ei.uniform_pm1(43, A.n * t).reshape(A.n, t))
+    rows = (z1 - z0) * N * N
+    V = torch.empty(s - 1, rows, t, dtype=torch.float64, device="cuda")
+    eks.eks_k_matrix_powers(S.ctx, t, s, z0, z1, X, V)
+    P = X
+    for i in range(s - 1):
+        Y = torch.empty_like(P)
+        eks.eks_k_spmm(S.ctx, t, P, Y)
+        P = Y
+        assert torch.equal(V[i], P[z0 * N * N:z1 * N * N]), i
+    S.close()

@@ -268,3 +268,121 @@ def test_onesynch_protocol_two_collectives(world, t):
     for rank, ncoll, errs in res:
         assert ncoll == 2, (rank, ncoll)
         assert max(errs) <= 1e-10, (rank, errs)
+
+
+def _mpk_worker(rank, world, port, kind, t, s, q):
+    """Matrix-powers kernel of the CA variants on row slabs (DESIGN reading R37): ONE exchange
+    of d = s − 1 boundary planes of V_0 (and, once per operator, of the stencil values of those planes),
+    then power i = 1..d on the plane ranges of eks_plan_mpk — the slab plus (d − i) ghost planes, redundantly.
+    The slab rows of every power must be BITWISE the global A^i·V_0 (same fma chain per row); rows a power
+    may not read are NaN, so a plan that reads past its valid planes poisons the result."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import paper_1804_10629_b200 as eks
+        A = _matrix(kind)
+        n, d = A.n, s - 1
+        lo, hi = slab(rank, world, n, t)
+        ranges = np.array([v for r in range(world) for v in slab(r, world, n, t)], np.int64)
+        S = A.rows(lo, hi)
+        _, _, geom = eks.eks_plan_halo(rank, world, ranges, S.row_ptr, S.col)
+        g, sv = eks.eks_plan_grid(lo, hi, S.row_ptr, S.col, S.val, geom["halo_before"], geom["halo_after"])
+        plane, nz, w = g["nx"] * g["ny"], g["nz"], g["w"]
+        db, da = (d if rank > 0 else 0), (d if rank < world - 1 else 0)
+        steps = eks.eks_plan_mpk(nz, d, db, da)
+        X = ei.uniform_pm1(31, n * t).reshape(n, t)
+        nbuf = (db + nz + da) * plane
+        nmsg = 0
+
+        def exchange(loc):
+            """rows [db·plane, db·plane + nloc) of `loc` are mine; d planes to / from each neighbour"""
+            nonlocal nmsg
+            reqs, bufs = [], []
+            mine = loc[db * plane:(db + nz) * plane]
+            if rank > 0:
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(mine[:d * plane])), dst=rank - 1))
+                b = torch.empty((d * plane, loc.shape[1]), dtype=torch.float64)
+                reqs.append(dist.irecv(b, src=rank - 1))
+                bufs.append((0, b))
+            if rank < world - 1:
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(mine[-d * plane:])), dst=rank + 1))
+                b = torch.empty((d * plane, loc.shape[1]), dtype=torch.float64)
+                reqs.append(dist.irecv(b, src=rank + 1))
+                bufs.append(((db + nz) * plane, b))
+            for r_ in reqs:
+                r_.wait()
+            for o, b in bufs:
+                loc[o:o + b.shape[0]] = b.numpy()
+            nmsg += 1
+        svx = np.full((nbuf, sv.shape[1]), np.nan)
+        svx[db * plane:(db + nz) * plane] = sv
+        exchange(svx)  # once per operator
+        nmsg = 0
+        V = [np.full((nbuf, t), np.nan) for _ in range(d + 1)]
+        V[0][db * plane:(db + nz) * plane] = X[lo:hi]
+        exchange(V[0])  # the ONE exchange of the outer iteration
+        offs = [-plane, -g["nx"], -1, 0, 1, g["nx"], plane] if w == 7 else [-g["nx"], -1, 0, 1, g["nx"]]
+        plan_ok = True
+        for i in range(1, d + 1):
+            zlo, zhi, gb, ga = (int(v) for v in steps[i - 1])
+            r0, r1 = (zlo + db) * plane, (zhi + db) * plane
+            rows = np.arange(r0, r1)
+            cols = np.empty((rows.size, w), np.int64)
+            for k, o in enumerate(offs):
+                c = rows + o
+                used = svx[r0:r1, k] != 0.0
+                # a used neighbour must lie in the planes this launch may read: [zlo − gb, zhi + ga)
+                inside = (c >= r0 - gb * plane) & (c < r1 + ga * plane)
+                plan_ok &= bool(np.all(inside[used]))
+                cols[:, k] = np.where(used, c, rows)
+            Ag = ei.Csr(rows.size, np.arange(0, rows.size * w + 1, w, dtype=np.int64),
+                        cols.reshape(-1).astype(np.int32), np.ascontiguousarray(svx[r0:r1, :w]).reshape(-1))
+            V[i][r0:r1] = oracle.spmm(Ag, V[i - 1])[:rows.size]
+        P = X
+        bitwise = True
+        for i in range(1, d + 1):
+            P = oracle.spmm(A, P)
+            bitwise &= bool(np.array_equal(V[i][db * plane:(db + nz) * plane], P[lo:hi]))
+        q.put((rank, bitwise, plan_ok, nmsg, steps.tolist()))
+    except Exception as e:
+        q.put((rank, f"error: {e!r}"))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind,t,s", [(2, "aniso3d", 8, 3), (4, "aniso3d", 8, 3), (2, "aniso3d", 4, 4),
+                                            (2, "bands2d", 8, 4), (4, "bands2d", 4, 6)])
+def test_matrix_powers_ghost_zone_protocol(world, kind, t, s):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mpk_worker, args=(r, world, port, kind, t, s, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(not isinstance(r[1], str) for r in res), res
+    for rank, bitwise, plan_ok, nmsg, steps in res:
+        assert bitwise and plan_ok, (rank, steps)
+        assert nmsg == 1  # one ghost-zone exchange per outer iteration instead of s − 1
+
+
+def test_plan_mpk_ranges():
+    """eks_plan_mpk: power i covers the slab plus min(ghost, d − i) planes per side, reads one further
+    plane exactly when one exists, and the last power covers exactly the slab."""
+    import paper_1804_10629_b200 as eks
+    for nz, d, db, da in [(4, 1, 1, 1), (6, 3, 3, 0), (2, 2, 2, 2), (5, 4, 0, 4), (3, 3, 1, 2), (1, 2, 0, 0)]:
+        st = eks.eks_plan_mpk(nz, d, db, da)
+        prev_lo, prev_hi = -db, nz + da  # V_0 is valid on every plane of the buffer
+        for i in range(1, d + 1):
+            zlo, zhi, gb, ga = (int(v) for v in st[i - 1])
+            assert zlo == -min(db, d - i) and zhi == nz + min(da, d - i)
+            assert zlo - gb >= prev_lo and zhi + ga <= prev_hi  # reads only planes the previous power wrote
+            assert gb == (1 if db > -zlo else 0) and ga == (1 if da > zhi - nz else 0)
+            prev_lo, prev_hi = zlo, zhi
+        assert (prev_lo, prev_hi) == (0, nz)
+    with pytest.raises(Exception):
+        eks.eks_plan_mpk(4, 2, 3, 0)
