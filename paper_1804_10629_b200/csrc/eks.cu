@@ -1827,8 +1827,20 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
     RP = rpv.data();
   }
   if (RP[0] != 0) return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr[0] != 0");
-  for (int64_t i = 0; i < n; ++i)
-    if (RP[i + 1] < RP[i]) return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr not monotone at row %lld", (long long)i);
+  {
+    std::atomic<int64_t> bad{INT64_MAX};
+    parallel_rows(n, [&](int64_t lo, int64_t hi) {
+      for (int64_t i = lo; i < hi; ++i)
+        if (RP[i + 1] < RP[i]) {
+          int64_t cur = bad.load();
+          while (i < cur && !bad.compare_exchange_weak(cur, i)) {
+          }
+          break;
+        }
+    });
+    if (bad.load() != INT64_MAX)
+      return fail(ctx, EKS_ERR_BAD_MATRIX, "row_ptr not monotone at row %lld", (long long)bad.load());
+  }
   const int64_t nnz = RP[n];
   if (nnz >= INT_MAX) return fail(ctx, EKS_ERR_INVALID_ARG, "local nnz must be < 2^31");
   const int32_t* COL = col_idx;
@@ -1840,6 +1852,36 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
     CK(cudaMemcpy(valv.data(), vals, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
     COL = colv.data();
     VAL = valv.data();
+  }
+  // One rank, host arrays: the columns and values go to the device as they are, so their copies are
+  // started now and run under the host-side validation (end-to-end setup time; on a validation error
+  // the new buffers are dropped and the context keeps its previous matrix).
+  int* early_col = nullptr;
+  double* early_val = nullptr;
+  struct EarlyGuard {  // any error return before the hand-over frees the early copies
+    eks_ctx* c;
+    int** col;
+    double** val;
+    ~EarlyGuard() {
+      if (*col || *val) {
+        cudaStreamSynchronize(c->stream);
+        dfree(*col);
+        dfree(*val);
+      }
+    }
+  } early_guard{ctx, &early_col, &early_val};
+  if (where == EKS_MEM_HOST && ctx->nranks == 1 && nnz > 0) {
+    if (cudaMalloc((void**)&early_col, sizeof(int) * nnz + 16) != cudaSuccess ||
+        cudaMalloc((void**)&early_val, sizeof(double) * nnz + 16) != cudaSuccess) {
+      cudaGetLastError();
+      dfree(early_col);
+      dfree(early_val);
+      early_col = nullptr;
+      early_val = nullptr;  // not enough room next to the previous matrix: the plain order below
+    } else {
+      CK(cudaMemcpyAsync(early_col, COL, sizeof(int) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(early_val, VAL, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+    }
   }
   // validation (SPEC S:30-33 invariants): sorted unique columns in range, positive diagonal — on all
   // host threads; the first failing row (lowest index) is reported
@@ -1960,11 +2002,19 @@ eks_status eks_setup_csr(eks_ctx* ctx, int64_t n_global, int64_t row_begin, int6
   });
   // +16 bytes of padding: the fused SpMM copies aligned 16-byte chunks that may run past the end
   CK(cudaMalloc((void**)&ctx->d_rp, sizeof(int) * (n + 1) + 16));
-  CK(cudaMalloc((void**)&ctx->d_col, sizeof(int) * nnz + 16));
-  CK(cudaMalloc((void**)&ctx->d_val, sizeof(double) * nnz + 16));
   CK(cudaMemcpy(ctx->d_rp, rp32.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->d_col, ECOL, sizeof(int) * nnz, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->d_val, VAL, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  if (early_col) {  // copied under the validation (one rank: ECOL = COL)
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->d_col = early_col;
+    ctx->d_val = early_val;
+    early_col = nullptr;
+    early_val = nullptr;
+  } else {
+    CK(cudaMalloc((void**)&ctx->d_col, sizeof(int) * nnz + 16));
+    CK(cudaMalloc((void**)&ctx->d_val, sizeof(double) * nnz + 16));
+    CK(cudaMemcpy(ctx->d_col, ECOL, sizeof(int) * nnz, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_val, VAL, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  }
   // ELL copy for the fused SpMM+Gram when every row has ≤ 8 entries (tiles of kEllTR rows,
   // slot-major inside a tile; padding: value 0 and the row's own column)
   // the plane-marching plan first: when it applies (one rank, stencil structure) and no path is

@@ -1446,9 +1446,9 @@ __global__ void __launch_bounds__(256, (T == 16 ? 2 : 1))
 
 // ----------------------------------------------------------------------------
 // The A-CholQR Gram [XᵀY (upper 8×8 tiles, lower mirrored) | Xᵀv] of the t = 64 split SpMM step (R35) with
-// warp-owned rows: warp w owns rows 8w..8w+7 of every 64-row tile and accumulates ALL 36 upper tiles and the
-// 8 v tiles over them (k-steps of 4 rows; each X / Y column-tile fragment loaded once feeds up to 8 DMMAs:
-// 16 shared loads per 44 DMMAs instead of 2 per DMMA); swizzled unpadded rows (aligned cp.async lines,
+// warp-owned rows: warp w owns rows 8w..8w+7 of every 64-row tile and accumulates ALL 36 upper tiles over
+// them, Xᵀv by plain FMAs on the X fragments (k-steps of 4 rows; each X / Y column-tile fragment loaded
+// once feeds up to 8 DMMAs: 16 shared loads per 36 DMMAs instead of 2 per DMMA); swizzled unpadded rows (aligned cp.async lines,
 // conflict-free fragments); 3 stages of 2 tiles = 192 KB → 1 CTA per SM.  The warps' sums are added in warp
 // order (fixed: run-to-run reproducible).
 // ----------------------------------------------------------------------------
@@ -1515,10 +1515,19 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int ni = mi; ni < MT; ++ni, ++u) dmma(acc[u][0], acc[u][1], fx[mi], fy[ni]);
       if constexpr (V) {
-        const double bv = g == 0 ? st[2 * TILE + kr] : 0.0;  // v as column 0 of a tile
+        // Xᵀv on the FMA pipe: the lane's X fragment fx[m] = X[kr][8m+g] times v[kr] (8 DFMA instead of
+        // 8 DMMA with v as column 0 of a tile: a DMMA costs the fp64 pipe ≈ 7 DFMA issue slots)
+        const double bv = st[2 * TILE + kr];
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi) dmma(accv[mi][0], accv[mi][1], fx[mi], bv);
+        for (int mi = 0; mi < MT; ++mi) accv[mi][0] = fma(fx[mi], bv, accv[mi][0]);
       }
+    }
+  }
+  if constexpr (V) {  // rows kr = … + q4: sum the 4 lanes of a group (fixed order)
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi) {
+      accv[mi][0] += __shfl_xor_sync(0xffffffffu, accv[mi][0], 1);
+      accv[mi][0] += __shfl_xor_sync(0xffffffffu, accv[mi][0], 2);
     }
   }
   cp_wait<0>();

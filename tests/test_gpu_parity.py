@@ -481,13 +481,21 @@ def test_cfg4_analog_sre_t64(eks, torch_cuda, oracle_lib):
     assert rel(host(rep["x"]), ref["x"]) <= 1e-6
 
 
-def _oracle_iterations(oracle_lib, p, kmax):
-    """Per-outer-iteration V (n×st), x, r of the oracle's DEFINITION mode (callback of or_solve)."""
+_ORACLE_ITS = {}
+
+
+def _oracle_iterations(oracle_lib, p, kmax, key=None):
+    """Per-outer-iteration V (n×st), x, r of the oracle's DEFINITION mode (callback of or_solve).
+    `key`: the same oracle run serves several tests of one session (the 64³ prefixes take minutes)."""
+    if key is not None and (key, kmax) in _ORACLE_ITS:
+        return _ORACLE_ITS[(key, kmax)]
     its = {}
 
     def cb(k, V, alpha, x, r, rho):
         its[k] = dict(V=V, x=x, r=r, rho=rho)
     ref = oracle_lib.solve(p.A, p.b, p.method, p.s, p.t, 0.0, kmax=kmax, callback=cb)
+    if key is not None:
+        _ORACLE_ITS[(key, kmax)] = (ref, its)
     return ref, its
 
 
@@ -501,7 +509,7 @@ def test_path_size_prefix_vs_definition(eks, torch_cuda, oracle_lib, cfg):
     W, x and the recursive r element-wise within 1e-10 (relative to their max-norm)."""
     torch = torch_cuda
     p = ei.cfg4(N=64) if cfg == "cfg4" else ei.cfg3(N=64)
-    ref, its = _oracle_iterations(oracle_lib, p, kmax=3)
+    ref, its = _oracle_iterations(oracle_lib, p, kmax=3, key=cfg + "-64")
     assert ref["outer_iters"] == 2 and sorted(its) == [1, 2]
     n, t, s_ = p.A.n, p.t, p.s
     S = eks.Solver(p.A)
@@ -852,7 +860,7 @@ def test_onesynch_path_size_prefix(eks, torch_cuda, oracle_lib, cfg):
     max-norm (multi-tile sweeps and plane-marching units at t = 32/64)."""
     torch = torch_cuda
     p = ei.cfg4(N=64) if cfg == "cfg4" else ei.cfg3(N=64)
-    ref, its = _oracle_iterations(oracle_lib, p, kmax=3)
+    ref, its = _oracle_iterations(oracle_lib, p, kmax=3, key=cfg + "-64")
     S = eks.Solver(p.A)
     b = dev(torch, p.b)
     r = torch.empty(p.A.n, dtype=torch.float64, device="cuda")
