@@ -1115,14 +1115,23 @@ eks_status mpk_local(eks_ctx* ctx, int t, int d, int nz, int db, int da, const d
 // SpMM on every rank, no preconditioner (M⁻¹ couples rows of a domain: no ghost rows for it), every
 // slab at least d planes thick (the ghost planes then come from the two neighbour ranks only).  The
 // answer must be the same on all ranks (the exchanges pair up): one MIN allreduce per (t, d), cached.
-// EKS_MPK=0 keeps the one-exchange-per-product path.
+// EKS_MPK=0 keeps the one-exchange-per-product path; EKS_MPK=force also takes the matrix-powers code
+// path on ONE rank (no neighbours: the same products through mpk_powers and the deep-ghost block
+// layout — the integration test of the path on a one-GPU box).
 eks_status mpk_usable(eks_ctx* ctx, int t, int d, bool& on) {
   on = false;
-  if (ctx->nranks == 1 || d < 1) return EKS_OK;
-  static const bool env_on = [] {
+  static const int env_mode = [] {
     const char* e = getenv("EKS_MPK");
-    return !(e && !strcmp(e, "0"));
+    return e && !strcmp(e, "0") ? 0 : (e && !strcmp(e, "force") ? 2 : 1);
   }();
+  const bool env_on = env_mode != 0;
+  if (d < 1) return EKS_OK;
+  if (ctx->nranks == 1) {
+    on = env_mode == 2 && !ctx->use_prec && eks::sweep_supported(t) && spmm_path_for(ctx, t) == 4;
+    if (env_mode == 2 && !on)  // the test switch must not pass silently on the default path
+      return fail(ctx, EKS_ERR_INVALID_ARG, "EKS_MPK=force: the matrix-powers path does not apply (t=%d)", t);
+    return EKS_OK;
+  }
   if (ctx->mpk_ok >= 0 && ctx->mpk_ok_t == t && ctx->mpk_ok_d == d) {
     on = ctx->mpk_ok == 1;
     return EKS_OK;
@@ -1152,6 +1161,7 @@ eks_status mpk_usable(eks_ctx* ctx, int t, int d, bool& on) {
 eks_status mpk_exchange(eks_ctx* ctx, double* loc, int w, int d) {
   const int64_t plane = (int64_t)ctx->gplan.nx * ctx->gplan.ny;
   const size_t cnt = (size_t)d * plane * w;
+  if (ctx->nranks == 1) return EKS_OK;  // no neighbours (EKS_MPK=force)
   KScope k(ctx, EKS_K_COMM);
   CK(cudaEventRecord(ctx->ev_ready, ctx->stream));
   CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_ready, 0));

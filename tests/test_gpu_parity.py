@@ -933,3 +933,46 @@ def test_matrix_powers_full_size_sampled(eks, torch_cuda, oracle_lib):
         P = Y
         assert torch.equal(V[i], P[z0 * N * N:z1 * N * N]), i
     S.close()
+
+
+_MPK_SCRIPT = r"""
+import hashlib, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import eks_inputs as ei
+import paper_1804_10629_b200 as eks
+out = []
+for A in (ei.poisson2d(48), ei.stencil_csr(16, 16, 16, ndim=3)):
+    b = torch.from_numpy(ei.uniform_pm1(51, A.n)).cuda()
+    S = eks.Solver(A)
+    for method, s, t, arn in (("ca-sre-cg", 3, 8, 7), ("ca-sre-cg2", 2, 16, 5), ("ca-msdo-cg", 3, 8, 7)):
+        try:
+            rep = S.solve(b, method, s, t, 1e-8, arnoldi=arn)
+            out.append(f"{method} it={rep['outer_iters']} st={rep['status']} "
+                       + hashlib.sha256(rep['x'].cpu().numpy().tobytes()).hexdigest())
+        except Exception as e:
+            out.append(f"{method} raised {getattr(e, 'status', '?')}")
+    S.close()
+print("|".join(out))
+"""
+
+
+def test_matrix_powers_path_in_ca_solve(eks, torch_cuda):
+    """EKS_MPK=force: the CA outer iteration takes the matrix-powers code path (deep-ghost V blocks,
+    mpk_powers → mpk_local) on one rank, where it issues the same products without neighbours: x, the
+    outer-iteration count and the status of CA SRE-CG / CA SRE-CG2 / CA MSDO-CG solves are bitwise those
+    of the default path (the environment switch is read once per process: two subprocesses)."""
+    import subprocess
+    import sys
+    outs = []
+    for mode in (None, "force"):
+        env = dict(os.environ)
+        env.pop("EKS_MPK", None)
+        if mode:
+            env["EKS_MPK"] = mode
+        r = subprocess.run([sys.executable, "-c", _MPK_SCRIPT, ROOT], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1], outs
+    parts = outs[0].split("|")
+    assert len(parts) == 6 and all(" st=0 " in part for part in parts[:3]), outs[0]  # Poisson2D: converged
