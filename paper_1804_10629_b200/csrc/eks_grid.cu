@@ -338,11 +338,10 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
 #pragma unroll
                       for (int ni = mi; ni < MT; ++ni, ++ut) dmma(acc[ut][0], acc[ut][1], xa[mi], ybv[ni]);
                     if (r != nullptr) {
-                      const double br = (g == 0 && okq)
-                                            ? (rbulk ? Rs[pyq * bx + pxq] : __ldg(r + qrow + (int64_t)pyq * nx + pxq))
+                      const double br = okq ? (rbulk ? Rs[pyq * bx + pxq] : __ldg(r + qrow + (int64_t)pyq * nx + pxq))
                                             : 0.0;
 #pragma unroll
-                      for (int mi = 0; mi < MT; ++mi) dmma(accr[mi][0], accr[mi][1], xa[mi], br);
+                      for (int mi = 0; mi < MT; ++mi) accr[mi][0] = fma(xa[mi], br, accr[mi][0]);
                     }
                   }
                 } else {
@@ -381,10 +380,12 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
                   for (int ni = mi; ni < MT; ++ni, ++ut) dmma(acc[ut][0], acc[ut][1], xa[mi], ybv[ni]);
                 if (r != nullptr) {
                   const int irq = pyq * bx + pxq;
-                  const double br = (g == 0 && okq)
-                                        ? (rbulk ? Rs[irq] : __ldg(r + qrow + (int64_t)pyq * nx + pxq)) : 0.0;
+                  // Xᵀr on the FMA pipe: the lane's X fragment (row q4 of the k-step, column 8·mi + g) times
+                  // that row's r; the 4 lanes of a group are summed once at the end (a DMMA with r as
+                  // column 0 of a tile costs the fp64 pipe ≈ 7 DFMA issue slots)
+                  const double br = okq ? (rbulk ? Rs[irq] : __ldg(r + qrow + (int64_t)pyq * nx + pxq)) : 0.0;
 #pragma unroll
-                  for (int mi = 0; mi < MT; ++mi) dmma(accr[mi][0], accr[mi][1], xa[mi], br);
+                  for (int mi = 0; mi < MT; ++mi) accr[mi][0] = fma(xa[mi], br, accr[mi][0]);
                 }
               }
               }  // !CG
@@ -467,10 +468,9 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
 #pragma unroll
                   for (int ni = mi; ni < MT; ++ni, ++ut) dmma(acc[ut][0], acc[ut][1], xa[mi], yb[ni]);
                 if (r != nullptr) {
-                  const double rv = __shfl_sync(0xffffffffu, vr, rq * G);  // lane rq·G holds row rq's r
-                  const double br = g == 0 ? rv : 0.0;                     // r as column 0 of a tile
+                  const double br = __shfl_sync(0xffffffffu, vr, rq * G);  // lane rq·G holds row rq's r
 #pragma unroll
-                  for (int mi = 0; mi < MT; ++mi) dmma(accr[mi][0], accr[mi][1], xa[mi], br);
+                  for (int mi = 0; mi < MT; ++mi) accr[mi][0] = fma(xa[mi], br, accr[mi][0]);  // FMA pipe (see above)
                 }
               }
             }
@@ -537,6 +537,13 @@ __global__ void __launch_bounds__(GrCfg<T>::NTH, 1)
       }
     }
     __syncthreads();
+  }
+  if constexpr (!K::CG) {  // Xᵀr: rows q4 = 0..3 of every k-step sit in the 4 lanes of a group
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi) {
+      accr[mi][0] += __shfl_xor_sync(0xffffffffu, accr[mi][0], 1);
+      accr[mi][0] += __shfl_xor_sync(0xffffffffu, accr[mi][0], 2);
+    }
   }
   for (int w = 0; w < (K::CG ? 0 : NWC); ++w) {
     if (warp == w) {
